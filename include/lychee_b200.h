@@ -1,0 +1,231 @@
+/* lychee_b200.h -- C ABI of the B200-native LycheeCluster decode-step path.
+ *
+ * Drop-in boundary for the reference's per-decode-step retrieval + sparse
+ * attention + lazy graft (reference: /root/reference/proj, library `tierkv`).
+ * Plain C: opaque handles, plain pointers and sizes, int status codes, no
+ * exceptions and no C++/torch types cross it.  Device pointers are CUDA
+ * device addresses; `stream` is a cudaStream_t passed as void*.
+ *
+ * One handle owns every "slot" resident on one GPU.  A slot is one
+ * (layer, KV head, sequence) triple: its own TokenStore K/V, its own
+ * HierarchicalIndex and its own stream cursor -- the reference's single-head
+ * engine instanced per KV head.  A GQA group of `group` query
+ * heads is scored against its KV head's slot; query head g of slot s is the
+ * reference call retrieve(index[s], q[s][g], budgets, buffer) (retriever.hpp:49).
+ *
+ * Status codes: 0 ok; LC_EINVAL = std::invalid_argument in the reference;
+ * LC_ERUNTIME = std::runtime_error; LC_ECUDA; LC_ENOMEM.  lc_last_error()
+ * returns the thread-local message of the last failure.
+ */
+#ifndef LYCHEE_B200_H
+#define LYCHEE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_OK 0
+#define LC_EINVAL 1
+#define LC_ERUNTIME 2
+#define LC_ECUDA 3
+#define LC_ENOMEM 4
+
+#define LC_MODE_FIXED_CLUSTER_COUNT 0 /* SelectionMode::fixed_cluster_count */
+#define LC_MODE_TOKEN_BUDGET 1        /* SelectionMode::token_budget */
+
+/* retrieve flags */
+#define LC_BUFFER_NONE 0u   /* buffer_ids = {} (retriever.hpp:52 default) */
+#define LC_BUFFER_STREAM 1u /* buffer_ids = StreamState::buffer_ids() = [chunked_end, n) (streamer.cpp:23-27) */
+#define LC_BUFFER_LIST 2u   /* explicit per-slot id lists (see lc_retrieve) */
+
+typedef struct lc_index_s* lc_index_t;
+
+/* Engine shape.  Replaces the reference's per-head objects
+ * (TokenStore types.hpp:25-57, HierarchicalIndex index.hpp:60-73,
+ * StreamerConfig streamer.hpp:19-25) with one HBM-resident SoA arena. */
+typedef struct {
+    uint32_t n_slots;         /* layers x KV heads x sequences */
+    uint32_t dim;             /* head dim d (attention kernel: 64 or 128) */
+    uint32_t group;           /* GQA query heads per slot, 1..8 */
+    uint32_t cap_tokens;      /* per-slot KV capacity (prefix + decode) */
+    uint32_t cap_chunks;      /* per-slot chunk capacity (prefill + grafts) */
+    uint32_t cap_clusters;    /* per-slot fine clusters L (fixed after build) */
+    uint32_t cap_units;       /* per-slot coarse units P (<= 1024) */
+    uint32_t max_candidates;  /* bound on fine candidates per query (0 = auto) */
+    uint32_t splits;          /* attention split-K CTAs per slot (0 = auto) */
+    uint32_t structure_aware; /* StreamerConfig::structure_aware (host chunker) */
+    uint32_t graft_full;      /* StreamerConfig::graft_search == full */
+    uint32_t keep_reps;       /* keep chunk representatives on device (download parity) */
+    uint32_t pooling;         /* IndexConfig::pooling: 0 mean, 1 max (index.hpp:11) */
+    int32_t device;
+} lc_index_desc;
+
+/* tierkv::Budgets (retriever.hpp:13-21) */
+typedef struct {
+    uint32_t unit_topk;
+    uint32_t mode;
+    uint32_t cluster_topk;
+    uint64_t token_budget;
+    uint32_t sink_size;
+} lc_budgets;
+
+/* Host view of one tierkv::HierarchicalIndex in the reference's own numbering
+ * (index.hpp:25-73); member lists as CSR.  Used for upload and download. */
+typedef struct {
+    uint32_t dim, n_chunks, n_clusters, n_units;
+    uint32_t* chunk_span;        /* [n_chunks*4] start, end, kind, level */
+    float* chunk_rep;            /* [n_chunks*dim] (may be NULL on upload) */
+    float* fine_centroid;        /* [n_clusters*dim] */
+    double* fine_radius;         /* [n_clusters] */
+    uint64_t* fine_token_count;  /* [n_clusters] */
+    uint32_t* fine_parent;       /* [n_clusters] */
+    uint32_t* fine_member_off;   /* [n_clusters+1] */
+    uint32_t* fine_members;      /* chunk ids */
+    float* coarse_centroid;      /* [n_units*dim] */
+    double* coarse_radius;       /* [n_units] */
+    uint32_t* coarse_member_off; /* [n_units+1] */
+    uint32_t* coarse_members;    /* fine ids, ascending within a unit */
+    uint32_t* cluster_of_chunk;  /* [n_chunks] */
+} lc_host_index;
+
+/* tierkv::GraftReport (streamer.hpp:27-35) */
+typedef struct {
+    uint32_t chunk_id, cluster_id, unit_id, _pad;
+    double centroid_delta, fine_radius, coarse_radius;
+    uint64_t distance_comps;
+} lc_graft_report;
+
+/* Per query head selection summary (RetrievalResult minus the id lists). */
+typedef struct {
+    uint32_t n_units, n_clusters, degenerate, error;
+    uint64_t scanned_centroids; /* RetrievalResult::scanned_centroids */
+    uint64_t n_active;          /* |active_token_ids| */
+} lc_selection_info;
+
+const char* lc_last_error(void);
+
+/* Allocate every slot's arena on desc->device.  Replaces constructing
+ * H x layers tierkv::StreamState objects (streamer.hpp:49). */
+int lc_index_create(const lc_index_desc* desc, lc_index_t* out);
+void lc_index_destroy(lc_index_t h);
+int lc_index_get_desc(lc_index_t h, lc_index_desc* out);
+
+/* Upload one slot: a HierarchicalIndex produced by build_index (index.hpp:93-95)
+ * plus its TokenStore keys/values as bf16 bit patterns (host memory), n_tokens
+ * rows.  The stream cursor starts at chunked_end = last chunk end
+ * (streamer.cpp:13-21), so tokens past it form the buffer.  Replaces
+ * StreamState::StreamState(TokenStore, HierarchicalIndex, StreamerConfig). */
+int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
+                         const uint16_t* keys_bf16, const uint16_t* values_bf16,
+                         uint32_t n_tokens);
+
+/* Sizes of a slot's current index: dims[0..7] = dim, n_chunks, n_clusters,
+ * n_units, n_tokens, total fine members, total coarse members, chunked_end. */
+int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims);
+
+/* Download a slot's index back into the reference layout, including every
+ * graft applied on the device (for index_to_bytes parity, serialize.cpp:88-125).
+ * Caller allocates every array from lc_index_slot_dims.  Synchronous. */
+int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* out);
+
+/* Append one decoded token's K/V (bf16, device [n_slots][dim] each) to every
+ * slot -- TokenStore::append inside push_token (streamer.cpp:56-58). */
+int lc_kv_append(lc_index_t h, const uint16_t* keys_dev, const uint16_t* values_dev,
+                 void* stream);
+
+/* Batched retrieve() over every query head of every slot (retriever.cpp:161-167):
+ * coarse UB scoring + top-k_g, fine UB scoring, selection (fixed k_c or greedy
+ * token-budget prefix fill), active-set construction and -- when out_dev is
+ * non-NULL -- sparse attention (retriever.cpp:41-50) into out_dev
+ * [n_slots][group][dim] fp32.  q_dev: [n_slots][group][dim] fp32.
+ * flags: LC_BUFFER_*; for LC_BUFFER_LIST, buf_off_dev [n_slots+1] and
+ * buf_ids_dev (sorted, unique, < n_tokens per slot) give each slot's ids.
+ * Asynchronous on `stream`. */
+int lc_retrieve(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
+                const uint32_t* buf_off_dev, const uint32_t* buf_ids_dev, float* out_dev,
+                void* stream);
+
+/* Sparse attention over the active sets of the last lc_retrieve (the second
+ * half of retrieve(), retriever.cpp:165). */
+int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* stream);
+
+/* Lazy incremental update: for every slot with take[slot] > 0, carve the chunk
+ * [chunked_end, chunked_end + take) (flush_buffer, streamer.cpp:29-54; the host
+ * decides `take` with the chunker, kind/level are recorded for download), pool
+ * its representative (index.cpp:20-41) and graft it (graft_chunk,
+ * streamer.cpp:68-143).  take/kind/level: host arrays [n_slots].  reports_dev:
+ * device [n_slots] (entries of slots without a graft are left untouched). */
+int lc_graft(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
+             lc_graft_report* reports_dev, void* stream);
+
+/* One StreamState::decode_step for every slot (streamer.cpp:145-165):
+ * retrieve + attend with buffer_ids = [chunked_end, n), then append the step's
+ * token, then graft where take[slot] > 0.  Stability metrics (jaccard /
+ * window_hit) are host bookkeeping and stay in the caller. */
+int lc_decode_step(lc_index_t h, const float* q_dev, const uint16_t* keys_dev,
+                   const uint16_t* values_dev, const lc_budgets* b, const uint32_t* take,
+                   const uint32_t* kind, const uint32_t* level, float* out_dev,
+                   lc_graft_report* reports_dev, void* stream);
+
+/* End-to-end variant of lc_retrieve over HOST buffers (pinned or pageable):
+ * H2D of q, retrieve + attention, D2H of out; synchronous on `stream`. */
+int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uint32_t flags,
+                     float* out_host, void* stream);
+
+/* Read back the last selection of query head (slot, g): summary, selected
+ * units (rank order), selected clusters (reference ids, rank order) and,
+ * optionally, the sorted unique active token ids.  Synchronous. */
+int lc_selection_download(lc_index_t h, uint32_t slot, uint32_t g, lc_selection_info* info,
+                          uint32_t* units, uint64_t units_cap, uint32_t* clusters,
+                          uint64_t clusters_cap, uint32_t* active, uint64_t active_cap);
+
+/* Bytes read by the last lc_retrieve in algorithmic terms,
+ * computed on the device from the step's own selections: out[0] = union
+ * bytes, out[1] = per-query (non-deduplicated) bytes, out[2] = active tokens
+ * (union over each slot's group), out[3] = fine candidates (union). Synchronous. */
+int lc_step_bytes(lc_index_t h, uint64_t* out);
+
+/* Sticky device-side error bits (lc_common.cuh ErrBits) of every kernel since
+ * the last clear; synchronous. */
+int lc_device_error(lc_index_t h, uint32_t* out, int clear);
+
+/* ---- host chunk-boundary decision (streaming front end) ----------------- */
+
+/* segment() with ChunkPolicy::defaults()'s separator table and the given
+ * min/max lengths (chunker.cpp:103-149).  spans4: start, end, kind
+ * (0 natural, 1 forced, 2 tail), level; up to cap spans. */
+int lc_segment(const char* const* texts, uint32_t n, uint32_t min_len, uint32_t max_len,
+               uint32_t* spans4, uint64_t cap, uint64_t* n_spans);
+
+/* StreamState::flush_buffer's chunk choice (streamer.cpp:29-54) over the n
+ * buffered texts: take = head span length unless it is a tail, else max_len. */
+int lc_flush_take(const char* const* buffer_texts, uint32_t n, uint32_t structure_aware,
+                  uint32_t min_len, uint32_t max_len, uint32_t* take, uint32_t* kind,
+                  uint32_t* level);
+
+/* ---- prefill helpers (GPU index build) ---------- */
+
+/* build_index (index.cpp:155-243) for many slots at once on the device from
+ * the slots' resident keys.  spans: host [n_spans*4] per slot, concatenated,
+ * span_off [n_slots+1]; n_tokens per slot host [n_slots].  Config mirrors
+ * IndexConfig (index.hpp:13-22); seeds[slot] = IndexConfig::seed. */
+int lc_index_build(lc_index_t h, const uint32_t* n_tokens, const uint32_t* spans,
+                   const uint64_t* span_off, double avg_chunks_per_cluster,
+                   uint32_t max_coarse_units, uint32_t kmeans_iters, const uint64_t* seeds);
+
+/* Synthetic clustered K/V written straight into the slots: the reference's
+ * gen_clustered_workload (workload.cpp:110-169) token stream for seed
+ * seeds[slot] (keys/values rounded to bf16 on store), plus texts codes
+ * (0 "", 1 "\n") [n_slots*n_tokens] and queries [n_slots*query_count*dim]
+ * returned to the host. */
+int lc_gen_workload(lc_index_t h, uint32_t n_tokens, uint32_t n_blobs, double concentration,
+                    uint32_t query_count, double query_locality, const uint64_t* seeds,
+                    uint8_t* text_codes_out, float* queries_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LYCHEE_B200_H */

@@ -1,0 +1,625 @@
+// Host side of the C ABI (include/lychee_b200.h): the engine arena, slot
+// upload/download in the reference's numbering, and the stream-ordered
+// launch sequence of every decode-step operation.  No exception crosses the
+// ABI; every entry point returns an LC_* status and records lc_last_error().
+#include "../../include/lychee_b200.h"
+#include "lc_common.cuh"
+
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace lc {
+size_t select_smem_bytes(const Arena& a);
+cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
+                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
+                          cudaStream_t stream);
+cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
+                           const uint32_t* buf_ids, cudaStream_t stream);
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream);
+cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
+cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
+                         cudaStream_t stream);
+}  // namespace lc
+
+using namespace lc;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Status(code, msg); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(LC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return LC_OK;
+    } catch (const Status& s) {
+        g_err = s.what();
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return LC_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LC_ERUNTIME;
+    }
+}
+
+template <typename T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(LC_ENOMEM, std::string("cudaMalloc ") + std::to_string(n * sizeof(T)) + " B: " +
+                            cudaGetErrorString(e));
+    }
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct HostSlot {
+    uint32_t n_tokens = 0, chunked_end = 0, n_chunks = 0, L = 0, P = 0;
+    bool loaded = false;
+    std::vector<uint32_t> kind, level;   // per chunk (host-only fields of ChunkSpan)
+    std::vector<float> rep;              // prefill reps when the device keeps none
+    std::vector<uint32_t> fanout;        // n_u per unit (fixed after build)
+};
+
+struct lc_index_s {
+    lc_index_desc desc{};
+    Arena a{};
+    std::vector<void*> owned;
+    std::vector<HostSlot> hs;
+    float* q_stage = nullptr;    // device staging for lc_retrieve_host
+    float* out_stage = nullptr;
+    uint32_t* take_dev = nullptr;
+    lc_graft_report* rep_scratch = nullptr;
+    uint32_t last_flags = 0;
+    uint32_t last_valid = 0;
+    std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
+
+    ~lc_index_s() {
+        for (void* p : owned) cudaFree(p);
+    }
+    void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
+};
+
+static uint32_t needed_candidates(lc_index_s* h, uint32_t unit_topk) {
+    auto it = h->cand_cache.find(unit_topk);
+    if (it != h->cand_cache.end()) return it->second;
+    uint32_t best = 1;
+    for (const auto& s : h->hs) {
+        if (!s.loaded) continue;
+        std::vector<uint32_t> f = s.fanout;
+        std::sort(f.begin(), f.end(), std::greater<uint32_t>());
+        uint64_t sum = 0;
+        for (size_t i = 0; i < f.size() && i < unit_topk; ++i) sum += f[i];
+        best = std::max<uint32_t>(best, (uint32_t)std::min<uint64_t>(sum, 0xffffffffu));
+    }
+    h->cand_cache[unit_topk] = best;
+    return best;
+}
+
+extern "C" {
+
+const char* lc_last_error(void) { return g_err.c_str(); }
+
+int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
+    return guard([&] {
+        if (!desc || !out) fail(LC_EINVAL, "lc_index_create: null argument");
+        const lc_index_desc& d = *desc;
+        if (d.n_slots == 0 || d.dim == 0 || d.group == 0 || d.group > (uint32_t)kMaxGroup)
+            fail(LC_EINVAL, "lc_index_create: need n_slots >= 1, dim >= 1, 1 <= group <= 8");
+        if (d.dim != 64 && d.dim != 128) fail(LC_EINVAL, "lc_index_create: dim must be 64 or 128");
+        if (d.dim > 256) fail(LC_EINVAL, "lc_index_create: dim > 256");
+        if (d.cap_units == 0 || d.cap_units > 1024) fail(LC_EINVAL, "lc_index_create: 1 <= cap_units <= 1024");
+        if (d.cap_tokens == 0 || d.cap_chunks == 0 || d.cap_clusters == 0)
+            fail(LC_EINVAL, "lc_index_create: zero capacity");
+        if (d.cap_tokens >= (1u << 24)) fail(LC_EINVAL, "lc_index_create: cap_tokens must be < 2^24");
+        auto h = std::make_unique<lc_index_s>();
+        h->desc = d;
+        if (h->desc.splits == 0) h->desc.splits = 8;
+        h->set_device();
+        Arena& a = h->a;
+        a.n_slots = d.n_slots;
+        a.d = d.dim;
+        a.G = d.group;
+        a.cap_tokens = d.cap_tokens;
+        a.cap_chunks = d.cap_chunks;
+        a.cap_clusters = d.cap_clusters;
+        a.cap_units = d.cap_units;
+        a.max_cand = 1;
+        a.splits = h->desc.splits;
+        a.graft_full = d.graft_full;
+        a.keep_reps = d.keep_reps;
+        a.cap_spans = d.cap_chunks + 2 + 1024;
+        const size_t S = d.n_slots, D = d.dim, G = d.group;
+        auto& o = h->owned;
+        a.K = dalloc<__nv_bfloat16>(S * d.cap_tokens * D, o);
+        a.V = dalloc<__nv_bfloat16>(S * d.cap_tokens * D, o);
+        a.chunk_start = dalloc<uint32_t>(S * (d.cap_chunks + 1), o);
+        a.chunk_clu = dalloc<uint32_t>(S * d.cap_chunks, o);
+        a.chunk_rep = d.keep_reps ? dalloc<float>(S * d.cap_chunks * D, o) : nullptr;
+        a.ucent = dalloc<float>(S * d.cap_units * D, o);
+        a.urad = dalloc<double>(S * d.cap_units, o);
+        a.unit_off = dalloc<uint32_t>(S * (d.cap_units + 1), o);
+        a.fcent = dalloc<float>(S * d.cap_clusters * D, o);
+        a.frad = dalloc<double>(S * d.cap_clusters, o);
+        a.ftok = dalloc<uint32_t>(S * d.cap_clusters, o);
+        a.forig = dalloc<uint32_t>(S * d.cap_clusters, o);
+        a.fnmem = dalloc<uint32_t>(S * d.cap_clusters, o);
+        a.funit = dalloc<uint32_t>(S * d.cap_clusters, o);
+        a.state = dalloc<SlotState>(S, o);
+        a.qinfo = dalloc<QInfo>(S * G, o);
+        a.sel_units = dalloc<uint32_t>(S * G * d.cap_units, o);
+        a.sel_clusters = dalloc<uint32_t>(S * G * d.cap_clusters, o);
+        a.sel_bits = dalloc<uint32_t>(S * G * bit_words(d.cap_clusters), o);
+        a.spans = dalloc<Span>(S * a.cap_spans, o);
+        a.span_off = dalloc<uint32_t>(S * (a.cap_spans + 1), o);
+        a.n_spans = dalloc<uint32_t>(S, o);
+        a.step_bytes = dalloc<unsigned long long>(S * 4, o);
+        a.partials = dalloc<float>(S * a.splits * G * (D + 2), o);
+        a.counters = dalloc<uint32_t>(S, o);
+        a.err = dalloc<uint32_t>(1, o);
+        h->q_stage = dalloc<float>(S * G * D, o);
+        h->out_stage = dalloc<float>(S * G * D, o);
+        h->take_dev = dalloc<uint32_t>(S, o);
+        h->rep_scratch = dalloc<lc_graft_report>(S, o);
+        ck(cudaMemset(a.state, 0, S * sizeof(SlotState)), "memset state");
+        ck(cudaMemset(a.counters, 0, S * 4), "memset counters");
+        ck(cudaMemset(a.err, 0, 4), "memset err");
+        ck(cudaMemset(a.n_spans, 0, S * 4), "memset n_spans");
+        ck(cudaMemset(a.span_off, 0, S * (a.cap_spans + 1) * 4), "memset span_off");
+        ck(cudaMemset(a.qinfo, 0, S * G * sizeof(QInfo)), "memset qinfo");
+        h->hs.resize(S);
+        *out = h.release();
+    });
+}
+
+void lc_index_destroy(lc_index_t h) {
+    if (!h) return;
+    cudaSetDevice(h->desc.device);
+    cudaDeviceSynchronize();
+    delete h;
+}
+
+int lc_index_get_desc(lc_index_t h, lc_index_desc* out) {
+    return guard([&] {
+        if (!h || !out) fail(LC_EINVAL, "null argument");
+        *out = h->desc;
+    });
+}
+
+int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
+                         const uint16_t* keys, const uint16_t* values, uint32_t n_tokens) {
+    return guard([&] {
+        if (!h || !ix) fail(LC_EINVAL, "lc_index_upload_slot: null argument");
+        h->set_device();
+        const Arena& a = h->a;
+        if (slot >= a.n_slots) fail(LC_EINVAL, "slot out of range");
+        const uint32_t D = a.d, M = ix->n_chunks, L = ix->n_clusters, P = ix->n_units;
+        if (ix->dim != D) fail(LC_EINVAL, "index dimension mismatch");
+        if (L == 0) fail(LC_EINVAL, "stream state: empty index");  // streamer.cpp:16
+        if (n_tokens > a.cap_tokens || M > a.cap_chunks || L > a.cap_clusters || P > a.cap_units || P == 0)
+            fail(LC_EINVAL, "slot exceeds engine capacity");
+        // chunks must tile [0, chunked_end) (build_index, index.cpp:160-167)
+        uint32_t expect = 0;
+        for (uint32_t j = 0; j < M; ++j) {
+            const uint32_t s = ix->chunk_span[4 * j], e = ix->chunk_span[4 * j + 1];
+            if (s != expect || e <= s) fail(LC_EINVAL, "chunks do not tile the stream");
+            expect = e;
+        }
+        const uint32_t chunked_end = expect;
+        if (chunked_end > n_tokens) fail(LC_EINVAL, "stream state: chunks exceed store");
+        // internal renumbering: coarse members concatenated in unit order
+        std::vector<uint32_t> int_of(L, 0xffffffffu), orig(L), unit_off(P + 1);
+        uint32_t pos = 0;
+        for (uint32_t u = 0; u < P; ++u) {
+            unit_off[u] = pos;
+            for (uint32_t m = ix->coarse_member_off[u]; m < ix->coarse_member_off[u + 1]; ++m) {
+                const uint32_t f = ix->coarse_members[m];
+                if (f >= L || int_of[f] != 0xffffffffu) fail(LC_EINVAL, "coarse members are not a partition");
+                if (ix->fine_parent[f] != u) fail(LC_EINVAL, "fine parent_unit disagrees with coarse members");
+                int_of[f] = pos;
+                orig[pos++] = f;
+            }
+        }
+        unit_off[P] = pos;
+        if (pos != L) fail(LC_EINVAL, "coarse members do not cover every fine cluster");
+        // cluster_of_chunk must agree with the fine member lists
+        std::vector<uint32_t> nmem(L, 0);
+        for (uint32_t f = 0; f < L; ++f)
+            for (uint32_t m = ix->fine_member_off[f]; m < ix->fine_member_off[f + 1]; ++m) {
+                const uint32_t j = ix->fine_members[m];
+                if (j >= M || ix->cluster_of_chunk[j] != f) fail(LC_EINVAL, "fine members disagree with cluster_of_chunk");
+                ++nmem[f];
+            }
+        std::vector<float> fcent((size_t)L * D), ucent((size_t)a.cap_units * D, 0.f);
+        std::vector<double> frad(L), urad(P);
+        std::vector<uint32_t> ftok(L), fn(L), fu(L);
+        for (uint32_t u = 0; u < P; ++u) {
+            const uint32_t base = unit_off[u], nu = unit_off[u + 1] - base;
+            for (uint32_t i = 0; i < nu; ++i) {
+                const uint32_t f = orig[base + i];
+                for (uint32_t j = 0; j < D; ++j)
+                    fcent[(size_t)base * D + (size_t)j * nu + i] = ix->fine_centroid[(size_t)f * D + j];
+            }
+            for (uint32_t j = 0; j < D; ++j) ucent[(size_t)j * a.cap_units + u] = ix->coarse_centroid[(size_t)u * D + j];
+            urad[u] = ix->coarse_radius[u];
+        }
+        for (uint32_t i = 0; i < L; ++i) {
+            const uint32_t f = orig[i];
+            frad[i] = ix->fine_radius[f];
+            if (ix->fine_token_count[f] > 0xffffffffull) fail(LC_EINVAL, "token_count exceeds u32");
+            ftok[i] = (uint32_t)ix->fine_token_count[f];
+            fn[i] = nmem[f];
+            fu[i] = ix->fine_parent[f];
+        }
+        std::vector<uint32_t> cs(M + 1), cc(M);
+        for (uint32_t j = 0; j < M; ++j) {
+            cs[j] = ix->chunk_span[4 * j];
+            cc[j] = int_of[ix->cluster_of_chunk[j]];
+        }
+        cs[M] = chunked_end;
+        const size_t so = slot;
+        auto up = [&](void* dst, const void* src, size_t bytes) {
+            if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
+        };
+        up(a.K + kv_off(a, slot), keys, (size_t)n_tokens * D * 2);
+        up(a.V + kv_off(a, slot), values, (size_t)n_tokens * D * 2);
+        up(a.chunk_start + so * (a.cap_chunks + 1), cs.data(), cs.size() * 4);
+        up(a.chunk_clu + so * a.cap_chunks, cc.data(), cc.size() * 4);
+        up(a.ucent + so * a.cap_units * D, ucent.data(), ucent.size() * 4);
+        up(a.urad + so * a.cap_units, urad.data(), urad.size() * 8);
+        up(a.unit_off + so * (a.cap_units + 1), unit_off.data(), unit_off.size() * 4);
+        up(a.fcent + so * a.cap_clusters * D, fcent.data(), fcent.size() * 4);
+        up(a.frad + so * a.cap_clusters, frad.data(), frad.size() * 8);
+        up(a.ftok + so * a.cap_clusters, ftok.data(), ftok.size() * 4);
+        up(a.forig + so * a.cap_clusters, orig.data(), orig.size() * 4);
+        up(a.fnmem + so * a.cap_clusters, fn.data(), fn.size() * 4);
+        up(a.funit + so * a.cap_clusters, fu.data(), fu.size() * 4);
+        HostSlot& hs = h->hs[slot];
+        hs = HostSlot{};
+        hs.kind.resize(M);
+        hs.level.resize(M);
+        for (uint32_t j = 0; j < M; ++j) {
+            hs.kind[j] = ix->chunk_span[4 * j + 2];
+            hs.level[j] = ix->chunk_span[4 * j + 3];
+        }
+        if (ix->chunk_rep) {
+            if (a.keep_reps) up(a.chunk_rep + so * a.cap_chunks * D, ix->chunk_rep, (size_t)M * D * 4);
+            else hs.rep.assign(ix->chunk_rep, ix->chunk_rep + (size_t)M * D);
+        }
+        SlotState st{};
+        st.n_tokens = n_tokens;
+        st.chunked_end = chunked_end;
+        st.n_chunks = M;
+        st.L = L;
+        st.P = P;
+        up(a.state + slot, &st, sizeof st);
+        hs.n_tokens = n_tokens;
+        hs.chunked_end = chunked_end;
+        hs.n_chunks = M;
+        hs.L = L;
+        hs.P = P;
+        hs.loaded = true;
+        hs.fanout.resize(P);
+        for (uint32_t u = 0; u < P; ++u) hs.fanout[u] = unit_off[u + 1] - unit_off[u];
+        h->cand_cache.clear();
+    });
+}
+
+int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims) {
+    return guard([&] {
+        if (!h || !dims || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_index_slot_dims: bad argument");
+        const HostSlot& s = h->hs[slot];
+        dims[0] = h->a.d;
+        dims[1] = s.n_chunks;
+        dims[2] = s.L;
+        dims[3] = s.P;
+        dims[4] = s.n_tokens;
+        dims[5] = s.n_chunks;  // every chunk belongs to exactly one cluster
+        dims[6] = s.L;         // every cluster belongs to exactly one unit
+        dims[7] = s.chunked_end;
+    });
+}
+
+int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
+    return guard([&] {
+        if (!h || !ix || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_index_download_slot: bad argument");
+        h->set_device();
+        ck(cudaDeviceSynchronize(), "sync");
+        const Arena& a = h->a;
+        const HostSlot& hs = h->hs[slot];
+        const uint32_t D = a.d, M = hs.n_chunks, L = hs.L, P = hs.P;
+        const size_t so = slot;
+        auto down = [&](void* dst, const void* src, size_t bytes) {
+            if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "download");
+        };
+        SlotState st;
+        down(&st, a.state + slot, sizeof st);
+        if (st.n_chunks != M || st.n_tokens != hs.n_tokens || st.chunked_end != hs.chunked_end)
+            fail(LC_ERUNTIME, "device and host stream cursors diverged");
+        std::vector<uint32_t> cs(M + 1), cc(M), unit_off(P + 1), orig(L), ftok(L), fu(L);
+        std::vector<float> fcent((size_t)L * D), ucent((size_t)a.cap_units * D);
+        std::vector<double> frad(L), urad(P);
+        down(cs.data(), a.chunk_start + so * (a.cap_chunks + 1), cs.size() * 4);
+        down(cc.data(), a.chunk_clu + so * a.cap_chunks, cc.size() * 4);
+        down(unit_off.data(), a.unit_off + so * (a.cap_units + 1), unit_off.size() * 4);
+        down(orig.data(), a.forig + so * a.cap_clusters, orig.size() * 4);
+        down(ftok.data(), a.ftok + so * a.cap_clusters, ftok.size() * 4);
+        down(fu.data(), a.funit + so * a.cap_clusters, fu.size() * 4);
+        down(fcent.data(), a.fcent + so * a.cap_clusters * D, fcent.size() * 4);
+        down(ucent.data(), a.ucent + so * a.cap_units * D, ucent.size() * 4);
+        down(frad.data(), a.frad + so * a.cap_clusters, frad.size() * 8);
+        down(urad.data(), a.urad + so * a.cap_units, urad.size() * 8);
+        ix->dim = D;
+        ix->n_chunks = M;
+        ix->n_clusters = L;
+        ix->n_units = P;
+        for (uint32_t j = 0; j < M; ++j) {
+            ix->chunk_span[4 * j] = cs[j];
+            ix->chunk_span[4 * j + 1] = cs[j + 1];
+            ix->chunk_span[4 * j + 2] = hs.kind[j];
+            ix->chunk_span[4 * j + 3] = hs.level[j];
+            ix->cluster_of_chunk[j] = orig[cc[j]];
+        }
+        if (ix->chunk_rep) {
+            if (a.keep_reps) down(ix->chunk_rep, a.chunk_rep + so * a.cap_chunks * D, (size_t)M * D * 4);
+            else if (hs.rep.size() == (size_t)M * D) std::memcpy(ix->chunk_rep, hs.rep.data(), hs.rep.size() * 4);
+            else fail(LC_ERUNTIME, "chunk representatives not kept on device (keep_reps = 0)");
+        }
+        for (uint32_t u = 0; u < P; ++u) {
+            const uint32_t base = unit_off[u], nu = unit_off[u + 1] - base;
+            for (uint32_t i = 0; i < nu; ++i) {
+                const uint32_t f = orig[base + i];
+                for (uint32_t j = 0; j < D; ++j)
+                    ix->fine_centroid[(size_t)f * D + j] = fcent[(size_t)base * D + (size_t)j * nu + i];
+            }
+            for (uint32_t j = 0; j < D; ++j) ix->coarse_centroid[(size_t)u * D + j] = ucent[(size_t)j * a.cap_units + u];
+            ix->coarse_radius[u] = urad[u];
+            ix->coarse_member_off[u] = base;
+            for (uint32_t i = 0; i < nu; ++i) ix->coarse_members[base + i] = orig[base + i];
+        }
+        ix->coarse_member_off[P] = unit_off[P];
+        for (uint32_t i = 0; i < L; ++i) {
+            const uint32_t f = orig[i];
+            ix->fine_radius[f] = frad[i];
+            ix->fine_token_count[f] = ftok[i];
+            ix->fine_parent[f] = fu[i];
+        }
+        // fine member lists: ascending chunk ids per cluster (build order, then grafts)
+        std::vector<uint32_t> cnt(L + 1, 0);
+        for (uint32_t j = 0; j < M; ++j) ++cnt[ix->cluster_of_chunk[j] + 1];
+        for (uint32_t f = 0; f < L; ++f) cnt[f + 1] += cnt[f];
+        for (uint32_t f = 0; f <= L; ++f) ix->fine_member_off[f] = cnt[f];
+        for (uint32_t j = 0; j < M; ++j) ix->fine_members[cnt[ix->cluster_of_chunk[j]]++] = j;
+    });
+}
+
+int lc_kv_append(lc_index_t h, const uint16_t* keys_dev, const uint16_t* values_dev, void* stream) {
+    return guard([&] {
+        if (!h || !keys_dev || !values_dev) fail(LC_EINVAL, "lc_kv_append: null argument");
+        h->set_device();
+        for (auto& s : h->hs) {
+            if (!s.loaded) fail(LC_EINVAL, "lc_kv_append: every slot must be uploaded or built");
+            if (s.n_tokens >= h->a.cap_tokens) fail(LC_ENOMEM, "lc_kv_append: token capacity exhausted");
+        }
+        ck(launch_append(h->a, keys_dev, values_dev, (cudaStream_t)stream), "k_append");
+        for (auto& s : h->hs) s.n_tokens += 1;
+    });
+}
+
+static void validate_budgets(const lc_budgets* b) {
+    if (!b) fail(LC_EINVAL, "null budgets");
+    // Budgets::validate (retriever.cpp:11-17)
+    if (b->unit_topk < 1) fail(LC_EINVAL, "unit_topk must be >= 1");
+    if (b->mode == LC_MODE_FIXED_CLUSTER_COUNT && b->cluster_topk < 1) fail(LC_EINVAL, "cluster_topk must be >= 1");
+    if (b->mode == LC_MODE_TOKEN_BUDGET && b->token_budget < 1) fail(LC_EINVAL, "token_budget must be >= 1");
+    if (b->mode > 1) fail(LC_EINVAL, "unknown selection mode");
+    if (b->unit_topk > 64) fail(LC_EINVAL, "unit_topk > 64 is not supported by the device kernel");
+}
+
+static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
+                          const uint32_t* buf_off, const uint32_t* buf_ids, float* out_dev,
+                          cudaStream_t st) {
+    validate_budgets(b);
+    if (!q_dev) fail(LC_EINVAL, "null q");
+    if (flags > 2) fail(LC_EINVAL, "bad buffer flags");
+    if (flags == LC_BUFFER_LIST && (!buf_off || !buf_ids)) fail(LC_EINVAL, "LC_BUFFER_LIST needs id lists");
+    for (auto& s : h->hs)
+        if (!s.loaded) fail(LC_EINVAL, "retrieve: every slot must be uploaded or built");
+    h->set_device();
+    Arena a = h->a;
+    a.max_cand = needed_candidates(h, std::min<uint32_t>(b->unit_topk, 64));
+    if (select_smem_bytes(a) > 227 * 1024)
+        fail(LC_ENOMEM, "fine candidate set exceeds shared memory (" + std::to_string(a.max_cand) + ")");
+    ck(launch_select(a, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, st),
+       "k_select");
+    ck(launch_compact(a, b->sink_size, flags, buf_off, buf_ids, st), "k_compact");
+    if (out_dev) ck(launch_attend(a, q_dev, out_dev, st), "k_attend");
+    h->last_flags = flags;
+    h->last_valid = 1;
+}
+
+int lc_retrieve(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
+                const uint32_t* buf_off_dev, const uint32_t* buf_ids_dev, float* out_dev, void* stream) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "null handle");
+        retrieve_impl(h, q_dev, b, flags, buf_off_dev, buf_ids_dev, out_dev, (cudaStream_t)stream);
+    });
+}
+
+int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* stream) {
+    return guard([&] {
+        if (!h || !q_dev || !out_dev) fail(LC_EINVAL, "lc_sparse_attention: null argument");
+        if (!h->last_valid) fail(LC_EINVAL, "lc_sparse_attention: no selection yet");
+        h->set_device();
+        ck(launch_attend(h->a, q_dev, out_dev, (cudaStream_t)stream), "k_attend");
+    });
+}
+
+static void graft_impl(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
+                       lc_graft_report* reports_dev, cudaStream_t st) {
+    if (!take) fail(LC_EINVAL, "null take");
+    bool any = false;
+    for (uint32_t s = 0; s < h->a.n_slots; ++s) {
+        const HostSlot& hs = h->hs[s];
+        if (!take[s]) continue;
+        if (!hs.loaded) fail(LC_EINVAL, "graft: slot not loaded");
+        if (take[s] > hs.n_tokens - hs.chunked_end) fail(LC_EINVAL, "graft: take exceeds the buffered tokens");
+        if (hs.n_chunks >= h->a.cap_chunks) fail(LC_ENOMEM, "graft: chunk capacity exhausted");
+        any = true;
+    }
+    if (!any) return;
+    h->set_device();
+    ck(cudaMemcpyAsync(h->take_dev, take, h->a.n_slots * 4, cudaMemcpyHostToDevice, st), "take H2D");
+    ck(launch_graft(h->a, h->take_dev, h->desc.pooling, reports_dev ? (void*)reports_dev : (void*)h->rep_scratch, st),
+       "k_graft");
+    for (uint32_t s = 0; s < h->a.n_slots; ++s) {
+        if (!take[s]) continue;
+        HostSlot& hs = h->hs[s];
+        hs.kind.push_back(kind ? kind[s] : 1u);
+        hs.level.push_back(level ? level[s] : 0u);
+        hs.chunked_end += take[s];
+        hs.n_chunks += 1;
+        if (!hs.rep.empty()) hs.rep.clear();  // prefill reps no longer complete
+    }
+    // take[] is a pageable host array: make the async copy complete before return
+    ck(cudaStreamSynchronize(st), "graft sync");
+}
+
+int lc_graft(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
+             lc_graft_report* reports_dev, void* stream) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "null handle");
+        graft_impl(h, take, kind, level, reports_dev, (cudaStream_t)stream);
+    });
+}
+
+int lc_decode_step(lc_index_t h, const float* q_dev, const uint16_t* keys_dev, const uint16_t* values_dev,
+                   const lc_budgets* b, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
+                   float* out_dev, lc_graft_report* reports_dev, void* stream) {
+    return guard([&] {
+        if (!h || !keys_dev || !values_dev) fail(LC_EINVAL, "lc_decode_step: null argument");
+        cudaStream_t st = (cudaStream_t)stream;
+        retrieve_impl(h, q_dev, b, LC_BUFFER_STREAM, nullptr, nullptr, out_dev, st);
+        for (auto& s : h->hs)
+            if (s.n_tokens >= h->a.cap_tokens) fail(LC_ENOMEM, "decode_step: token capacity exhausted");
+        ck(launch_append(h->a, keys_dev, values_dev, st), "k_append");
+        for (auto& s : h->hs) s.n_tokens += 1;
+        if (take) graft_impl(h, take, kind, level, reports_dev, st);
+    });
+}
+
+int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uint32_t flags,
+                     float* out_host, void* stream) {
+    return guard([&] {
+        if (!h || !q_host || !out_host) fail(LC_EINVAL, "lc_retrieve_host: null argument");
+        if (flags == LC_BUFFER_LIST) fail(LC_EINVAL, "lc_retrieve_host: LC_BUFFER_LIST needs device lists");
+        h->set_device();
+        cudaStream_t st = (cudaStream_t)stream;
+        const size_t bytes = (size_t)h->a.n_slots * h->a.G * h->a.d * 4;
+        ck(cudaMemcpyAsync(h->q_stage, q_host, bytes, cudaMemcpyHostToDevice, st), "q H2D");
+        retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, h->out_stage, st);
+        ck(cudaMemcpyAsync(out_host, h->out_stage, bytes, cudaMemcpyDeviceToHost, st), "out D2H");
+        ck(cudaStreamSynchronize(st), "stream sync");
+    });
+}
+
+int lc_selection_download(lc_index_t h, uint32_t slot, uint32_t g, lc_selection_info* info, uint32_t* units,
+                          uint64_t units_cap, uint32_t* clusters, uint64_t clusters_cap, uint32_t* active,
+                          uint64_t active_cap) {
+    return guard([&] {
+        if (!h || slot >= h->a.n_slots || g >= h->a.G) fail(LC_EINVAL, "lc_selection_download: bad argument");
+        if (!h->last_valid) fail(LC_EINVAL, "no selection yet");
+        h->set_device();
+        ck(cudaDeviceSynchronize(), "sync");
+        const Arena& a = h->a;
+        uint32_t err = 0;
+        ck(cudaMemcpy(&err, a.err, 4, cudaMemcpyDeviceToHost), "err");
+        QInfo qi;
+        ck(cudaMemcpy(&qi, a.qinfo + (size_t)slot * a.G + g, sizeof qi, cudaMemcpyDeviceToHost), "qinfo");
+        if (info) {
+            info->n_units = qi.n_units;
+            info->n_clusters = qi.n_clusters;
+            info->degenerate = qi.degenerate;
+            info->error = qi.error | err;
+            info->scanned_centroids = qi.scanned;
+            info->n_active = qi.n_active;
+        }
+        const HostSlot& hs = h->hs[slot];
+        if (qi.degenerate) {
+            if (units) for (uint64_t i = 0; i < std::min<uint64_t>(units_cap, hs.P); ++i) units[i] = (uint32_t)i;
+            if (clusters) for (uint64_t i = 0; i < std::min<uint64_t>(clusters_cap, hs.L); ++i) clusters[i] = (uint32_t)i;
+        } else {
+            if (units && qi.n_units)
+                ck(cudaMemcpy(units, a.sel_units + ((size_t)slot * a.G + g) * a.cap_units,
+                              std::min<uint64_t>(units_cap, qi.n_units) * 4, cudaMemcpyDeviceToHost), "units");
+            if (clusters && qi.n_clusters)
+                ck(cudaMemcpy(clusters, a.sel_clusters + ((size_t)slot * a.G + g) * a.cap_clusters,
+                              std::min<uint64_t>(clusters_cap, qi.n_clusters) * 4, cudaMemcpyDeviceToHost),
+                   "clusters");
+        }
+        if (active) {
+            uint32_t ns = 0;
+            ck(cudaMemcpy(&ns, a.n_spans + slot, 4, cudaMemcpyDeviceToHost), "n_spans");
+            std::vector<Span> sp(ns);
+            if (ns) ck(cudaMemcpy(sp.data(), a.spans + (size_t)slot * a.cap_spans, ns * sizeof(Span), cudaMemcpyDeviceToHost), "spans");
+            std::vector<uint32_t> ids;
+            for (const Span& s : sp)
+                if ((s.len_mask >> g) & 1u)
+                    for (uint32_t t = 0; t < (s.len_mask >> 8); ++t) ids.push_back(s.start + t);
+            std::sort(ids.begin(), ids.end());
+            ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+            if (info) info->n_active = ids.size();
+            std::memcpy(active, ids.data(), std::min<uint64_t>(active_cap, ids.size()) * 4);
+        }
+    });
+}
+
+int lc_step_bytes(lc_index_t h, uint64_t* out) {
+    return guard([&] {
+        if (!h || !out) fail(LC_EINVAL, "null argument");
+        h->set_device();
+        ck(cudaDeviceSynchronize(), "sync");
+        std::vector<unsigned long long> sb((size_t)h->a.n_slots * 4);
+        ck(cudaMemcpy(sb.data(), h->a.step_bytes, sb.size() * 8, cudaMemcpyDeviceToHost), "step bytes");
+        out[0] = out[1] = out[2] = out[3] = 0;
+        for (uint32_t s = 0; s < h->a.n_slots; ++s)
+            for (int k = 0; k < 4; ++k) out[k] += sb[(size_t)s * 4 + k];
+    });
+}
+
+int lc_device_error(lc_index_t h, uint32_t* out, int clear) {
+    return guard([&] {
+        if (!h || !out) fail(LC_EINVAL, "null argument");
+        h->set_device();
+        ck(cudaDeviceSynchronize(), "sync");
+        ck(cudaMemcpy(out, h->a.err, 4, cudaMemcpyDeviceToHost), "err");
+        if (clear) ck(cudaMemset(h->a.err, 0, 4), "clear err");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,337 @@
+// Gather-based split-K flash-decode over the selected variable-length chunks
+// (north star item 3): kernels::attention (kernels.cpp:108-144) for every query
+// head of a GQA group at once, over the union of the group's active spans.
+//
+// Each KV row of the union is read from HBM exactly once per slot: a 16-token
+// group is loaded straight into mma.sync fragments (16-byte loads, every byte
+// used), QK^T and PV run on the tensor cores with fp32 accumulation, and a
+// per-token query mask removes (query, token) pairs outside that head's own
+// active set.  Precision: q and the softmax weights are split into bf16
+// hi + lo halves (hi in MMA rows 0..G-1, lo in rows 8..8+G-1), so products
+// carry ~16 mantissa bits on top of the exact bf16 K/V; accumulation is fp32.
+// Partials (m, l, o) per CTA are merged with log-sum-exp by the last CTA of
+// each slot.
+//
+// Fragment maps for mma.m16n8k16 (lane = 4r + c):
+//   QK: B = K^T, thread (r, c) holds token r (and 8 + r) dims [c*D/4, c*D/4 + D/4),
+//       k-step s uses dims c*D/4 + 4s + {0,1,2,3} (a dim permutation applied to
+//       both q and k, so the dot product is unchanged).
+//   PV: A = P straight from the QK accumulators (FA2 register reuse);
+//       B = V, n-tile j <-> dim r*D/8 + j, thread (r, c) holds tokens
+//       2c, 2c+1, 8+2c, 9+2c dims [r*D/8, r*D/8 + D/8).
+//   Out: thread (r, c) owns query r dims [c*D/4, c*D/4 + D/4).
+#include "lc_common.cuh"
+
+namespace lc {
+
+struct AttendParams {
+    Arena a;
+    const float* q;  // [slot][G][D]
+    float* out;      // [slot][G][D]
+};
+
+constexpr int kAttThreads = 128;
+constexpr int kWindow = 1024;  // tokens expanded into shared memory at a time
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
+    hi = __bfloat162float(__float2bfloat16_rn(x));
+    lo = x - hi;
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
+    static_assert(D % 64 == 0 && D <= 128, "D must be 64 or 128");
+    constexpr int KS = D / 16;   // k-steps of QK
+    constexpr int KW = D / 32;   // uint4 per thread per K row
+    constexpr int NT = D / 8;    // n-tiles of PV
+    constexpr int VW = D / 64;   // uint4 per thread per V row
+    const Arena& a = p.a;
+    const uint32_t slot = blockIdx.y, split = blockIdx.x, S = gridDim.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
+    const uint32_t G = a.G;
+
+    __shared__ uint32_t s_row[kWindow];
+    __shared__ uint8_t s_msk[kWindow];
+    __shared__ uint32_t s_sstart[kWindow + 1];
+    __shared__ uint32_t s_slm[kWindow + 1];
+    __shared__ uint32_t s_soff[kWindow + 2];
+    __shared__ uint32_t s_lohi[2];
+    __shared__ float s_m[4][kMaxGroup], s_l[4][kMaxGroup];
+    __shared__ float s_o[4][kMaxGroup][D];
+    __shared__ uint32_t s_last;
+
+    const uint32_t ns = a.n_spans[slot];
+    const uint32_t* soff = a.span_off + (size_t)slot * (a.cap_spans + 1);
+    const Span* sp = a.spans + (size_t)slot * a.cap_spans;
+    const uint32_t tot = soff[ns];
+    const uint32_t beg = (uint32_t)(((unsigned long long)tot * split) / S);
+    const uint32_t end = (uint32_t)(((unsigned long long)tot * (split + 1)) / S);
+    const __nv_bfloat16* Ks = a.K + kv_off(a, slot);
+    const __nv_bfloat16* Vs = a.V + kv_off(a, slot);
+
+    // q fragments: softmax scale and log2(e) folded in, bf16 hi (row r) + lo (row r+8)
+    uint32_t qf[KS][4];
+    {
+        const float scale = (float)(1.4426950408889634 / sqrt((double)D));
+        const float* qg = p.q + ((size_t)slot * G + (r < (int)G ? r : 0)) * D + c * (D / 4);
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            float h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) split_bf16(qg[4 * s + e] * scale, h[e], l[e]);
+            const bool on = r < (int)G;
+            qf[s][0] = on ? pack_bf16(h[0], h[1]) : 0u;
+            qf[s][2] = on ? pack_bf16(h[2], h[3]) : 0u;
+            qf[s][1] = on ? pack_bf16(l[0], l[1]) : 0u;
+            qf[s][3] = on ? pack_bf16(l[2], l[3]) : 0u;
+        }
+    }
+    float acc[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    for (uint32_t wb = beg; wb < end; wb += kWindow) {
+        const uint32_t we = min(end, wb + kWindow), wn = we - wb;
+        // spans covering [wb, we): last span with off <= wb .. last span with off < we
+        if (warp == 0) {
+            for (int which = 0; which < 2; ++which) {
+                const uint32_t target = which == 0 ? wb : we - 1;
+                uint32_t lo = 0, hi = ns;  // find last k with soff[k] <= target
+                while (hi - lo > 1) {
+                    // 32-ary search step
+                    const uint32_t step = (hi - lo + 31) / 32;
+                    const uint32_t probe = lo + (uint32_t)lane * step;
+                    const bool ok = probe < hi && soff[probe] <= target;
+                    const unsigned int bal = __ballot_sync(0xffffffffu, ok);
+                    const int last = 31 - __clz(bal);
+                    const uint32_t nlo = lo + (uint32_t)last * step;
+                    hi = min(hi, nlo + step);
+                    lo = nlo;
+                    if (step == 1) break;
+                }
+                if (lane == 0) s_lohi[which] = lo;
+            }
+        }
+        __syncthreads();
+        const uint32_t k0 = s_lohi[0], k1 = s_lohi[1];
+        for (uint32_t k = k0 + tid; k <= k1; k += blockDim.x) {
+            const Span sk = sp[k];
+            s_sstart[k - k0] = sk.start;
+            s_slm[k - k0] = sk.len_mask;
+            s_soff[k - k0] = soff[k];
+        }
+        __syncthreads();
+        const uint32_t nsp = k1 - k0 + 1;
+        for (uint32_t t = tid; t < kWindow; t += blockDim.x) {
+            if (t < wn) {
+                const uint32_t tokpos = wb + t;
+                uint32_t lo = 0, hi = nsp;
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (s_soff[mid] <= tokpos) lo = mid;
+                    else hi = mid;
+                }
+                s_row[t] = s_sstart[lo] + (tokpos - s_soff[lo]);
+                s_msk[t] = (uint8_t)(s_slm[lo] & 0xffu);
+            } else {
+                s_row[t] = 0;
+                s_msk[t] = 0;
+            }
+        }
+        __syncthreads();
+
+        const uint32_t ngrp = (wn + 15) / 16;
+        for (uint32_t grp = warp; grp < ngrp; grp += 4) {
+            const uint32_t t0 = grp * 16;
+            // ---- loads (every byte of the 16 rows is used exactly once) ----
+            uint4 kr[2][KW];
+            uint4 vr[4][VW];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const uint32_t row = s_row[t0 + 8 * nt + r];
+                const uint4* kp = reinterpret_cast<const uint4*>(Ks + (size_t)row * D + c * (D / 4));
+#pragma unroll
+                for (int w = 0; w < KW; ++w) kr[nt][w] = ldg_stream(kp + w);
+            }
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const uint32_t tk = (x >> 1) * 8 + 2 * c + (x & 1);
+                const uint32_t row = s_row[t0 + tk];
+                const uint4* vp = reinterpret_cast<const uint4*>(Vs + (size_t)row * D + r * (D / 8));
+#pragma unroll
+                for (int w = 0; w < VW; ++w) vr[x][w] = ldg_stream(vp + w);
+            }
+            // ---- S = Q K^T (hi rows r, lo rows r+8) ----
+            float sc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+                for (int s = 0; s < KS; ++s) {
+                    const uint4 kv = kr[nt][s >> 1];
+                    const uint32_t b0 = (s & 1) ? kv.z : kv.x;
+                    const uint32_t b1 = (s & 1) ? kv.w : kv.y;
+                    mma16816(sc[nt], qf[s], b0, b1);
+                }
+            }
+            // logits of query r for tokens 2c, 2c+1 (nt 0) and 8+2c, 9+2c (nt 1)
+            float lg[4];
+            bool ok[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int nt = x >> 1, e = x & 1;
+                lg[x] = sc[nt][e] + sc[nt][2 + e];
+                const uint32_t tk = nt * 8 + 2 * c + e;
+                ok[x] = r < (int)G && ((s_msk[t0 + tk] >> r) & 1u);
+            }
+            float mx = -INFINITY;
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+                if (ok[x]) mx = fmaxf(mx, lg[x]);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(m_run, mx);
+            float pr[4];
+            float corr = 1.f;
+            if (m_new == -INFINITY) {
+                pr[0] = pr[1] = pr[2] = pr[3] = 0.f;
+            } else {
+                corr = exp2f(m_run - m_new);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) pr[x] = ok[x] ? exp2f(lg[x] - m_new) : 0.f;
+                m_run = m_new;
+            }
+            l_run = l_run * corr + (pr[0] + pr[1]) + (pr[2] + pr[3]);
+            if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    acc[j][0] *= corr;
+                    acc[j][1] *= corr;
+                    acc[j][2] *= corr;
+                    acc[j][3] *= corr;
+                }
+            }
+            // ---- O += P V ----
+            uint32_t pa[4];
+            {
+                float h[4], l[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) split_bf16(pr[x], h[x], l[x]);
+                pa[0] = pack_bf16(h[0], h[1]);
+                pa[2] = pack_bf16(h[2], h[3]);
+                pa[1] = pack_bf16(l[0], l[1]);
+                pa[3] = pack_bf16(l[2], l[3]);
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int w = j >> 3, word = (j >> 1) & 3;
+                const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
+                auto wd = [&](const uint4& u) -> uint32_t {
+                    return word == 0 ? u.x : word == 1 ? u.y : word == 2 ? u.z : u.w;
+                };
+                const uint32_t b0 = __byte_perm(wd(vr[0][w]), wd(vr[1][w]), sel);
+                const uint32_t b1 = __byte_perm(wd(vr[2][w]), wd(vr[3][w]), sel);
+                mma16816(acc[j], pa, b0, b1);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- warp partial -> CTA partial ----
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    if (r < (int)G) {
+        if (c == 0) {
+            s_m[warp][r] = m_run;
+            s_l[warp][r] = l_run;
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            s_o[warp][r][c * (D / 4) + j] = acc[j][0] + acc[j][2];
+            s_o[warp][r][c * (D / 4) + D / 8 + j] = acc[j][1] + acc[j][3];
+        }
+    }
+    __syncthreads();
+    float* part = a.partials + ((size_t)slot * S + split) * G * (D + 2);
+    for (uint32_t x = tid; x < G * D; x += blockDim.x) {
+        const uint32_t g = x / D, dd = x % D;
+        float M = -INFINITY;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][g]);
+        float o = 0.f, L = 0.f;
+        if (M != -INFINITY)
+            for (int w = 0; w < 4; ++w) {
+                const float f = exp2f(s_m[w][g] - M);
+                o += f * s_o[w][g][dd];
+                L += f * s_l[w][g];
+            }
+        part[g * (D + 2) + 2 + dd] = o;
+        if (dd == 0) {
+            part[g * (D + 2)] = M;
+            part[g * (D + 2) + 1] = L;
+        }
+    }
+    // ---- last CTA of the slot merges the S partials (log-sum-exp) ----
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.counters + slot, 1u) == S - 1 ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float* parts = a.partials + (size_t)slot * S * G * (D + 2);
+    for (uint32_t x = tid; x < G * D; x += blockDim.x) {
+        const uint32_t g = x / D, dd = x % D;
+        float M = -INFINITY;
+        for (uint32_t s = 0; s < S; ++s) M = fmaxf(M, __ldcg(parts + (s * G + g) * (D + 2)));
+        float o = 0.f, L = 0.f;
+        if (M != -INFINITY)
+            for (uint32_t s = 0; s < S; ++s) {
+                const float* ps = parts + (s * G + g) * (D + 2);
+                const float ms = __ldcg(ps);
+                if (ms == -INFINITY) continue;
+                const float f = exp2f(ms - M);
+                o += f * __ldcg(ps + 2 + dd);
+                L += f * __ldcg(ps + 1);
+            }
+        if (L > 0.f) {
+            p.out[((size_t)slot * G + g) * D + dd] = o / L;
+        } else {
+            p.out[((size_t)slot * G + g) * D + dd] = 0.f;
+            if (dd == 0) atomicOr(a.err, kErrEmptyActive);
+        }
+    }
+    if (tid == 0) a.counters[slot] = 0;
+}
+
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream) {
+    AttendParams p{a, q, out};
+    dim3 grid(a.splits, a.n_slots);
+    if (a.d == 128) k_attend<128><<<grid, kAttThreads, 0, stream>>>(p);
+    else if (a.d == 64) k_attend<64><<<grid, kAttThreads, 0, stream>>>(p);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+}  // namespace lc

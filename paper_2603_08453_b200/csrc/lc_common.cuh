@@ -1,0 +1,115 @@
+// Shared device-side definitions for the B200 LycheeCluster decode path.
+//
+// HBM layout (one arena per engine, slot-major; a slot is one
+// (layer, KV head, sequence) single-head engine of the reference):
+//
+//   K, V        bf16 [slot][cap_tokens][d]           TokenStore keys_/values_ (types.hpp:54-56)
+//   chunk_start u32  [slot][cap_chunks+1]            Chunk::span.start; entry M = chunked_end
+//   chunk_clu   u32  [slot][cap_chunks]              cluster_of_chunk (internal cluster id)
+//   chunk_rep   f32  [slot][cap_chunks][d]           Chunk::rep_key (optional, download only)
+//   ucent       f32  [slot][d][cap_units]            CoarseUnit::centroid, dimension-major
+//   urad        f64  [slot][cap_units]               CoarseUnit::radius
+//   unit_off    u32  [slot][cap_units+1]             CoarseUnit::members as a range of
+//                                                    internal fine ids
+//   fcent       f32  [slot][cap_clusters*d]          FineCluster::centroid; the members of
+//                                                    unit u form one block [d][n_u]
+//                                                    (dimension-major) at unit_off[u]*d
+//   frad        f64  [slot][cap_clusters]            FineCluster::radius
+//   ftok        u32  [slot][cap_clusters]            FineCluster::token_count
+//   forig       u32  [slot][cap_clusters]            reference cluster id of internal id
+//   fnmem       u32  [slot][cap_clusters]            FineCluster::members.size()
+//   funit       u32  [slot][cap_clusters]            FineCluster::parent_unit
+//
+// Internal fine ids renumber the reference's clusters so that each coarse
+// unit's members are contiguous, in the unit's stored (ascending id) order
+// (index.cpp:220-241).  All tie-breaks use the reference id (forig).
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace lc {
+
+constexpr int kMaxGroup = 8;
+
+struct SlotState {
+    uint32_t n_tokens;
+    uint32_t chunked_end;
+    uint32_t n_chunks;
+    uint32_t L;
+    uint32_t P;
+    uint32_t pad[3];
+};
+
+struct Span {  // one contiguous run of active tokens and the query heads it serves
+    uint32_t start;
+    uint32_t len_mask;  // len << 8 | group mask
+};
+
+struct QInfo {  // per query head result summary (mirrors lc_selection_info)
+    uint32_t n_units, n_clusters, degenerate, error;
+    unsigned long long scanned;
+    unsigned long long n_active;
+};
+
+struct Arena {
+    // shape
+    uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;
+    uint32_t splits, graft_full, keep_reps, cap_spans;
+    // token store
+    __nv_bfloat16* K;
+    __nv_bfloat16* V;
+    // index
+    uint32_t* chunk_start;
+    uint32_t* chunk_clu;
+    float* chunk_rep;
+    float* ucent;
+    double* urad;
+    uint32_t* unit_off;
+    float* fcent;
+    double* frad;
+    uint32_t* ftok;
+    uint32_t* forig;
+    uint32_t* fnmem;
+    uint32_t* funit;
+    SlotState* state;
+    // per-step selection products
+    QInfo* qinfo;            // [slot][G]
+    uint32_t* sel_units;     // [slot][G][cap_units]
+    uint32_t* sel_clusters;  // [slot][G][cap_clusters] reference ids, rank order
+    uint32_t* sel_bits;      // [slot][G][words(cap_clusters)] internal-id bitmap
+    Span* spans;             // [slot][cap_spans]
+    uint32_t* span_off;      // [slot][cap_spans+1] token prefix offsets
+    uint32_t* n_spans;       // [slot]
+    unsigned long long* step_bytes;  // [slot][4]
+    float* partials;         // [slot][splits][G][d+2]
+    uint32_t* counters;      // [slot]
+    uint32_t* err;           // [1]
+};
+
+__host__ __device__ inline uint32_t bit_words(uint32_t n) { return (n + 31) / 32; }
+
+__host__ __device__ inline size_t kv_off(const Arena& a, uint32_t slot) {
+    return (size_t)slot * a.cap_tokens * a.d;
+}
+
+// Orderable key of a double so that ascending key == descending score.
+__device__ __forceinline__ unsigned long long desc_key(double s) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(s);
+    unsigned long long ord = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    return ~ord;
+}
+
+enum ErrBits : uint32_t {
+    kErrNone = 0,
+    kErrCandOverflow = 1u << 0,   // fine candidates exceed max_candidates
+    kErrEmptyCand = 1u << 1,      // select_topk(k = 0) would throw (retriever.cpp:29)
+    kErrSpanOverflow = 1u << 2,   // active spans exceed cap_spans
+    kErrZeroNorm = 1u << 3,       // chunk_representative zero norm (index.cpp:36-37)
+    kErrChunkCap = 1u << 4,       // graft past cap_chunks
+    kErrTokenCap = 1u << 5,       // append past cap_tokens
+    kErrEmptyActive = 1u << 6,    // sparse_attention over an empty set (retriever.cpp:43)
+};
+
+}  // namespace lc

@@ -1,0 +1,266 @@
+// Lazy incremental update (north star item 4): KV append and the
+// nearest-centroid argmax-and-graft kernel, one CTA per grafting slot.
+//
+// Bit-exact restatement of StreamState::flush_buffer/graft_chunk
+// (streamer.cpp:29-54, 68-143) and chunk_representative (index.cpp:20-41):
+// every fp64 reduction is sequential in the reference's index order, products
+// that are not exact are rounded before the add (__dmul_rn/__dadd_rn), argmax
+// ties keep the first candidate in the reference's scan order.
+#include "lc_common.cuh"
+
+namespace lc {
+
+__global__ void k_append(Arena a, const __nv_bfloat16* keys, const __nv_bfloat16* values) {
+    const uint32_t slot = blockIdx.x;
+    const uint32_t n = a.state[slot].n_tokens;
+    if (n >= a.cap_tokens) {
+        if (threadIdx.x == 0) atomicOr(a.err, kErrTokenCap);
+        return;
+    }
+    __nv_bfloat16* kd = a.K + kv_off(a, slot) + (size_t)n * a.d;
+    __nv_bfloat16* vd = a.V + kv_off(a, slot) + (size_t)n * a.d;
+    for (uint32_t j = threadIdx.x; j < a.d; j += blockDim.x) {
+        kd[j] = keys[(size_t)slot * a.d + j];
+        vd[j] = values[(size_t)slot * a.d + j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) a.state[slot].n_tokens = n + 1;
+}
+
+struct GraftParams {
+    Arena a;
+    const uint32_t* take;   // [n_slots] device
+    uint32_t pooling;
+    void* reports;          // lc_graft_report [n_slots]
+};
+
+struct GraftReportDev {  // layout of lc_graft_report
+    uint32_t chunk_id, cluster_id, unit_id, pad;
+    double centroid_delta, fine_radius, coarse_radius;
+    unsigned long long distance_comps;
+};
+
+constexpr int kGraftThreads = 256;
+
+// block argmax over (score desc, tie key asc)
+__device__ __forceinline__ void argmax_merge(double& s, uint32_t& k, double s2, uint32_t k2) {
+    if (s2 > s || (s2 == s && k2 < k)) {
+        s = s2;
+        k = k2;
+    }
+}
+
+__device__ void block_argmax(double& s, uint32_t& k, double* ws, uint32_t* wk) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const uint32_t k2 = __shfl_xor_sync(0xffffffffu, k, o);
+        argmax_merge(s, k, s2, k2);
+    }
+    if (lane == 0) {
+        ws[warp] = s;
+        wk[warp] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w) argmax_merge(ws[0], wk[0], ws[w], wk[w]);
+    }
+    __syncthreads();
+    s = ws[0];
+    k = wk[0];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
+    const Arena& a = p.a;
+    const uint32_t slot = blockIdx.x, tid = threadIdx.x, d = a.d;
+    const uint32_t take = p.take[slot];
+    if (take == 0) return;
+    __shared__ double s_acc[256];
+    __shared__ float s_rep[256], s_new[256], s_mu[256];
+    __shared__ double s_moved[256];
+    __shared__ double s_norm, s_delta, s_tonew, s_dg;
+    __shared__ double ws[kGraftThreads / 32];
+    __shared__ uint32_t wk[kGraftThreads / 32];
+    SlotState* stp = a.state + slot;
+    const uint32_t start = stp->chunked_end, M = stp->n_chunks, P = stp->P, L = stp->L;
+    if (M >= a.cap_chunks) {
+        if (tid == 0) atomicOr(a.err, kErrChunkCap);
+        return;
+    }
+    // ---- chunk_representative (index.cpp:20-41) over keys [start, start+take) ----
+    const __nv_bfloat16* Ks = a.K + kv_off(a, slot) + (size_t)start * d;
+    for (uint32_t j = tid; j < d; j += blockDim.x) {
+        double acc;
+        if (p.pooling == 0) {
+            acc = 0.0;
+            for (uint32_t i = 0; i < take; ++i) acc = __dadd_rn(acc, (double)__bfloat162float(Ks[(size_t)i * d + j]));
+            acc = __ddiv_rn(acc, (double)take);
+        } else {
+            acc = (double)__bfloat162float(Ks[j]);
+            for (uint32_t i = 1; i < take; ++i) acc = fmax(acc, (double)__bfloat162float(Ks[(size_t)i * d + j]));
+        }
+        s_acc[j] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double n2 = 0.0;  // std::inner_product: n2 + a*a, rounded product
+        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(s_acc[j], s_acc[j]));
+        s_norm = __dsqrt_rn(n2);
+    }
+    __syncthreads();
+    if (s_norm == 0.0) {
+        if (tid == 0) atomicOr(a.err, kErrZeroNorm);
+        return;
+    }
+    for (uint32_t j = tid; j < d; j += blockDim.x) s_rep[j] = (float)__ddiv_rn(s_acc[j], s_norm);
+    __syncthreads();
+
+    // ---- nearest cluster (streamer.cpp:74-106) ----
+    const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
+    const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
+    const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
+    const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
+    unsigned long long comps = 0;
+    bool scoped = !a.graft_full;
+    uint32_t best_c = 0;
+    if (scoped) {
+        double bs = -INFINITY;
+        uint32_t bu = 0xffffffffu;
+        for (uint32_t u = tid; u < P; u += blockDim.x) {
+            double s = 0.0;
+            for (uint32_t j = 0; j < d; ++j)
+                s = __fma_rn((double)s_rep[j], (double)uc[(size_t)j * a.cap_units + u], s);
+            argmax_merge(bs, bu, s, u);
+        }
+        block_argmax(bs, bu, ws, wk);
+        const uint32_t lo = uoff[bu], hi = uoff[bu + 1];
+        comps = P;
+        if (lo == hi) {
+            scoped = false;  // empty unit: fall back to a full scan (streamer.cpp:91)
+        } else {
+            const uint32_t nu = hi - lo;
+            double bs2 = -INFINITY;
+            uint32_t bc = 0xffffffffu;
+            for (uint32_t i = tid; i < nu; i += blockDim.x) {
+                const float* col = fc + (size_t)lo * d + i;
+                double s = 0.0;
+                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)col[(size_t)j * nu], s);
+                argmax_merge(bs2, bc, s, lo + i);  // stored order == internal order
+            }
+            block_argmax(bs2, bc, ws, wk);
+            best_c = bc;
+            comps += nu;
+        }
+    }
+    if (!scoped) {
+        double bs = -INFINITY;
+        uint32_t bo = 0xffffffffu;
+        for (uint32_t u = 0; u < P; ++u) {
+            const uint32_t lo = uoff[u], nu = uoff[u + 1] - lo;
+            for (uint32_t i = tid; i < nu; i += blockDim.x) {
+                const float* col = fc + (size_t)lo * d + i;
+                double s = 0.0;
+                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)col[(size_t)j * nu], s);
+                argmax_merge(bs, bo, s, fo[lo + i]);  // full scan order = reference ids
+            }
+        }
+        block_argmax(bs, bo, ws, wk);
+        // reference id -> internal id
+        for (uint32_t c = tid; c < L; c += blockDim.x)
+            if (fo[c] == bo) s_acc[0] = (double)c;
+        __syncthreads();
+        best_c = (uint32_t)s_acc[0];
+        comps = L;
+        __syncthreads();
+    }
+
+    // ---- update (streamer.cpp:108-134) ----
+    uint32_t* funit = a.funit + (size_t)slot * a.cap_clusters;
+    uint32_t* fnmem = a.fnmem + (size_t)slot * a.cap_clusters;
+    const uint32_t u = funit[best_c];
+    const uint32_t lo = uoff[u], nu = uoff[u + 1] - lo, local = best_c - lo;
+    float* col = a.fcent + (size_t)slot * a.cap_clusters * d + (size_t)lo * d + local;
+    const double n = (double)fnmem[best_c];
+    for (uint32_t j = tid; j < d; j += blockDim.x) {
+        const float mu = col[(size_t)j * nu];
+        s_mu[j] = mu;
+        s_moved[j] = __dadd_rn(__dmul_rn(n, (double)mu), (double)s_rep[j]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double n2 = 0.0;
+        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(s_moved[j], s_moved[j]));
+        s_norm = __dsqrt_rn(n2);
+    }
+    __syncthreads();
+    const double norm = s_norm;
+    for (uint32_t j = tid; j < d; j += blockDim.x)
+        s_new[j] = norm > 0.0 ? (float)__ddiv_rn(s_moved[j], norm) : s_mu[j];
+    __syncthreads();
+    // three sequential l2_dist (kernels.cpp:25-32) on three warps in parallel
+    const float* ucu = uc;  // dimension-major coarse centroid of unit u
+    if (tid == 0 || tid == 32 || tid == 64) {
+        double s = 0.0;
+        for (uint32_t j = 0; j < d; ++j) {
+            double x, y;
+            if (tid == 0) { x = s_new[j]; y = s_mu[j]; }
+            else if (tid == 32) { x = s_rep[j]; y = s_new[j]; }
+            else { x = s_rep[j]; y = ucu[(size_t)j * a.cap_units + u]; }
+            const double diff = __dsub_rn(x, y);
+            s = __dadd_rn(s, __dmul_rn(diff, diff));
+        }
+        const double r = __dsqrt_rn(s);
+        if (tid == 0) s_delta = r;
+        else if (tid == 32) s_tonew = r;
+        else s_dg = r;
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < d; j += blockDim.x) col[(size_t)j * nu] = s_new[j];
+    const uint32_t cid = M;
+    if (a.keep_reps) {
+        float* rp = a.chunk_rep + ((size_t)slot * a.cap_chunks + cid) * d;
+        for (uint32_t j = tid; j < d; j += blockDim.x) rp[j] = s_rep[j];
+    }
+    if (tid == 0) {
+        double* frad = a.frad + (size_t)slot * a.cap_clusters;
+        const double r1 = __dadd_rn(frad[best_c], s_delta);
+        const double rr = r1 < s_tonew ? s_tonew : r1;  // std::max(r + delta, to_new)
+        frad[best_c] = rr;
+        a.ftok[(size_t)slot * a.cap_clusters + best_c] += take;
+        double* ur = a.urad + (size_t)slot * a.cap_units;
+        const double rg = ur[u] < s_dg ? s_dg : ur[u];  // std::max(radius, dist)
+        ur[u] = rg;
+        fnmem[best_c] += 1;
+        uint32_t* cs = a.chunk_start + (size_t)slot * (a.cap_chunks + 1);
+        cs[cid + 1] = start + take;
+        a.chunk_clu[(size_t)slot * a.cap_chunks + cid] = best_c;
+        stp->n_chunks = M + 1;
+        stp->chunked_end = start + take;
+        GraftReportDev* rep = reinterpret_cast<GraftReportDev*>(p.reports) + slot;
+        rep->chunk_id = cid;
+        rep->cluster_id = fo[best_c];
+        rep->unit_id = u;
+        rep->pad = 0;
+        rep->centroid_delta = s_delta;
+        rep->fine_radius = rr;
+        rep->coarse_radius = rg;
+        rep->distance_comps = comps;
+    }
+}
+
+cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream) {
+    k_append<<<a.n_slots, 128, 0, stream>>>(a, static_cast<const __nv_bfloat16*>(keys),
+                                            static_cast<const __nv_bfloat16*>(values));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
+                         cudaStream_t stream) {
+    GraftParams p{a, take_dev, pooling, reports};
+    k_graft<<<a.n_slots, kGraftThreads, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace lc

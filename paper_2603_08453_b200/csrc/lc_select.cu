@@ -1,0 +1,597 @@
+// Fused scoring + pruning + selection (north star item 2) and active-set
+// construction.  One CTA per query head (slot, g).
+//
+// Exactness (bit-identical to the reference's fp64 CPU path):
+//  * kernels::dot (kernels.cpp:13-17) is a sequential fp64 sum of exact
+//    float*float products, so a per-thread sequential DFMA chain over j
+//    reproduces it bit-for-bit; no warp-tree reduction of a dot is used.
+//  * UB = dot + qnorm*r (kernels.cpp:155-159) is __dmul_rn then __dadd_rn
+//    (the reference is compiled without FMA).
+//  * select_topk orders by (score desc, id asc) (retriever.cpp:27-39); the
+//    greedy token-budget fill is a prefix of that order that stops at the
+//    first overflow and always admits one cluster (retriever.cpp:142-154).
+//    We find that prefix with an exact weighted radix select over the
+//    orderable 64-bit image of the fp64 score, resolve exact-score ties by
+//    reference id, and only sort the (small) selected set.
+#include "lc_common.cuh"
+
+namespace lc {
+
+struct SelectParams {
+    Arena a;
+    const float* q;  // [slot][G][d]
+    uint32_t unit_topk, mode, cluster_topk, sink;
+    unsigned long long budget;
+};
+
+constexpr int kSelThreads = 256;
+constexpr int kMaxUnitTopk = 64;
+
+__device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ia,
+                                         unsigned long long kb, uint32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// Dynamic shared memory layout of k_select:
+//   float  qs[d]
+//   u64    ukey[cap_units]
+//   u64    ckey[max_cand]
+//   u32    cw[max_cand]     weight (token_count, or 1 in fixed-k mode)
+//   u32    cid[max_cand]    internal fine id
+//   u32    sel[max_cand]    compacted selected candidate indices
+__global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Arena& a = p.a;
+    const uint32_t slot = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+    const uint32_t d = a.d;
+    const SlotState st = a.state[slot];
+    QInfo* qi = a.qinfo + (size_t)slot * a.G + g;
+    uint32_t* bits = a.sel_bits + ((size_t)slot * a.G + g) * bit_words(a.cap_clusters);
+    const uint32_t nwords = bit_words(st.L);
+
+    // degeneracy (retriever.cpp:86-95): whole store fits the budget, or no chunks
+    const bool degenerate =
+        (p.mode == 1 && (unsigned long long)st.n_tokens <= p.budget) || st.n_chunks == 0;
+    if (degenerate) {
+        if (tid == 0) {
+            qi->n_units = st.P;
+            qi->n_clusters = st.L;
+            qi->degenerate = 1;
+            qi->error = 0;
+            qi->scanned = 0;
+        }
+        return;
+    }
+
+    float* qs = reinterpret_cast<float*>(smem);
+    unsigned long long* ukey =
+        reinterpret_cast<unsigned long long*>(smem + ((d * 4 + 15) & ~15u));
+    unsigned long long* ckey = ukey + a.cap_units;
+    uint32_t* cw = reinterpret_cast<uint32_t*>(ckey + a.max_cand);
+    uint32_t* cid = cw + a.max_cand;
+    uint32_t* sel = cid + a.max_cand;
+
+    __shared__ double s_qnorm;
+    __shared__ uint32_t s_kept[kMaxUnitTopk];
+    __shared__ uint32_t s_pre[kMaxUnitTopk + 1];
+    __shared__ unsigned long long hw[256];
+    __shared__ uint32_t hc[256];
+    __shared__ unsigned long long s_prefix, s_mask, s_wbefore;
+    __shared__ uint32_t s_cbefore, s_state, s_nsel, s_err;
+
+    const float* qg = p.q + ((size_t)slot * a.G + g) * d;
+    for (uint32_t j = tid; j < d; j += blockDim.x) qs[j] = qg[j];
+    for (uint32_t w = tid; w < nwords; w += blockDim.x) bits[w] = 0u;
+    if (tid == 0) s_err = 0;
+    __syncthreads();
+
+    // ||q|| (kernels.cpp:19-23): sequential, exact products -> DFMA chain
+    if (tid == 0) {
+        double s = 0.0;
+        for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)qs[j], (double)qs[j], s);
+        s_qnorm = __dsqrt_rn(s);
+    }
+    // tier 1: coarse units (retriever.cpp:100-112), dimension-major centroids
+    const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
+    const double* ur = a.urad + (size_t)slot * a.cap_units;
+    double udot[4];
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t u = tid + k * blockDim.x;
+        double s = 0.0;
+        if (u < st.P)
+            for (uint32_t j = 0; j < d; ++j)
+                s = __fma_rn((double)qs[j], (double)uc[(size_t)j * a.cap_units + u], s);
+        udot[k] = s;
+    }
+    __syncthreads();
+    const double qnorm = s_qnorm;
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t u = tid + k * blockDim.x;
+        if (u < st.P) ukey[u] = desc_key(__dadd_rn(udot[k], __dmul_rn(qnorm, ur[u])));
+    }
+    __syncthreads();
+    // select_topk(units, unit_topk): rank by counting over (score desc, id asc)
+    const uint32_t kU = min(min(p.unit_topk, st.P), (uint32_t)kMaxUnitTopk);
+    for (uint32_t u = tid; u < st.P; u += blockDim.x) {
+        const unsigned long long ku = ukey[u];
+        uint32_t rank = 0;
+        for (uint32_t v = 0; v < st.P; ++v) rank += key_less(ukey[v], v, ku, u) ? 1u : 0u;
+        if (rank < kU) s_kept[rank] = u;
+    }
+    __syncthreads();
+    const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
+    if (tid == 0) {
+        uint32_t acc = 0;
+        for (uint32_t k = 0; k < kU; ++k) {
+            s_pre[k] = acc;
+            const uint32_t u = s_kept[k];
+            acc += uoff[u + 1] - uoff[u];
+        }
+        s_pre[kU] = acc;
+    }
+    __syncthreads();
+    const uint32_t nc = s_pre[kU];
+    if (nc > a.max_cand || nc == 0) {
+        if (tid == 0) {
+            qi->error = nc == 0 ? kErrEmptyCand : kErrCandOverflow;
+            qi->degenerate = 0;
+            qi->n_units = kU;
+            qi->n_clusters = 0;
+            qi->scanned = st.P + nc;
+            atomicOr(a.err, qi->error);
+        }
+        return;
+    }
+
+    // tier 2: fine clusters of the kept units (retriever.cpp:118-135)
+    const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
+    const double* fr = a.frad + (size_t)slot * a.cap_clusters;
+    const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
+    for (uint32_t i = tid; i < nc; i += blockDim.x) {
+        uint32_t k = 0;
+        while (k + 1 < kU && s_pre[k + 1] <= i) ++k;
+        const uint32_t u = s_kept[k];
+        const uint32_t base = uoff[u], nu = uoff[u + 1] - base, local = i - s_pre[k];
+        const float* col = fc + (size_t)base * d + local;
+        double s = 0.0;
+        uint32_t j = 0;
+        for (; j + 8 <= d; j += 8) {
+            float v[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) v[t] = __ldg(col + (size_t)(j + t) * nu);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) s = __fma_rn((double)qs[j + t], (double)v[t], s);
+        }
+        for (; j < d; ++j) s = __fma_rn((double)qs[j], (double)__ldg(col + (size_t)j * nu), s);
+        const uint32_t c = base + local;
+        ckey[i] = desc_key(__dadd_rn(s, __dmul_rn(qnorm, fr[c])));
+        cw[i] = p.mode == 1 ? ft[c] : 1u;
+        cid[i] = c;
+    }
+    if (tid == 0) {
+        s_prefix = 0;
+        s_mask = 0;
+        s_wbefore = 0;
+        s_cbefore = 0;
+        s_state = 0;
+        s_nsel = 0;
+    }
+    __syncthreads();
+
+    // weighted prefix select: the longest prefix of the (key, id) order whose
+    // weight sum stays <= budget (retriever.cpp:146-153); fixed-k mode is the
+    // same with unit weights and budget = k_c (select_topk, retriever.cpp:141)
+    const unsigned long long budget = p.mode == 1 ? p.budget : (unsigned long long)p.cluster_topk;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (uint32_t b = tid; b < 256; b += blockDim.x) {
+            hw[b] = 0;
+            hc[b] = 0;
+        }
+        __syncthreads();
+        const unsigned long long prefix = s_prefix, mask = s_mask;
+        for (uint32_t i = tid; i < nc; i += blockDim.x) {
+            const unsigned long long k = ckey[i];
+            if ((k & mask) == prefix) {
+                const uint32_t b = (uint32_t)(k >> shift) & 255u;
+                atomicAdd(&hw[b], (unsigned long long)cw[i]);
+                atomicAdd(&hc[b], 1u);
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w8[8];
+            uint32_t c8[8];
+            unsigned long long lw = 0;
+            uint32_t lc = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                w8[t] = hw[lane * 8 + t];
+                c8[t] = hc[lane * 8 + t];
+                lw += w8[t];
+                lc += c8[t];
+            }
+            unsigned long long iw = lw;
+            uint32_t ic = lc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long yw = __shfl_up_sync(0xffffffffu, iw, o);
+                const uint32_t yc = __shfl_up_sync(0xffffffffu, ic, o);
+                if (lane >= o) {
+                    iw += yw;
+                    ic += yc;
+                }
+            }
+            const unsigned long long wbase = s_wbefore + (iw - lw);
+            const uint32_t cbase = ic - lc;
+            // first bin whose inclusive cumulative weight exceeds the budget
+            int found = -1;
+            unsigned long long cum = wbase;
+            uint32_t ccum = cbase;
+            unsigned long long wexcl = 0;
+            uint32_t cexcl = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if (found < 0) {
+                    if (cum + w8[t] > budget) {
+                        found = t;
+                        wexcl = cum;
+                        cexcl = ccum;
+                    } else {
+                        cum += w8[t];
+                        ccum += c8[t];
+                    }
+                }
+            }
+            const unsigned int ballot = __ballot_sync(0xffffffffu, found >= 0);
+            if (ballot == 0) {
+                if (lane == 0) s_state = 2;  // everything matching fits
+            } else {
+                const int first = __ffs(ballot) - 1;
+                if (lane == first) {
+                    const uint32_t b = (uint32_t)(lane * 8 + found);
+                    s_prefix = prefix | ((unsigned long long)b << shift);
+                    s_mask = mask | (255ull << shift);
+                    s_wbefore = wexcl;
+                    s_cbefore += cexcl;
+                    s_state = c8[found] == 1 ? 1u : 0u;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_state != 0) break;
+    }
+    // mark the selection
+    const unsigned long long prefix = s_prefix, mask = s_mask;
+    const uint32_t state = s_state;
+    for (uint32_t i = tid; i < nc; i += blockDim.x) {
+        const unsigned long long k = ckey[i] & mask;
+        bool take = k < prefix;
+        if (k == prefix) {
+            if (state == 2) take = true;                   // whole bucket fits
+            else if (state == 1) take = s_cbefore == 0;    // lone boundary: admit if first
+        }
+        if (take) sel[atomicAdd(&s_nsel, 1u)] = i;
+    }
+    __syncthreads();
+    if (state == 0 && tid == 0) {
+        // bucket of identical fp64 scores: reference-id order (retriever.cpp:33)
+        const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
+        unsigned long long used = s_wbefore;
+        uint32_t admitted = s_cbefore;
+        for (;;) {
+            int best = -1;
+            uint32_t best_id = 0xffffffffu;
+            for (uint32_t i = 0; i < nc; ++i) {
+                if ((ckey[i] & mask) != prefix || cw[i] == 0xffffffffu) continue;
+                const uint32_t oid = fo[cid[i]];
+                if (oid < best_id) {
+                    best_id = oid;
+                    best = (int)i;
+                }
+            }
+            if (best < 0) break;
+            const unsigned long long w = cw[best];
+            if (admitted > 0 && used + w > budget) break;
+            used += w;
+            ++admitted;
+            sel[s_nsel++] = (uint32_t)best;
+            cw[best] = 0xffffffffu;  // consumed
+        }
+    }
+    __syncthreads();
+
+    // rank order of the selected set + outputs
+    const uint32_t nsel = s_nsel;
+    const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
+    uint32_t* out_cl = a.sel_clusters + ((size_t)slot * a.G + g) * a.cap_clusters;
+    for (uint32_t x = tid; x < nsel; x += blockDim.x) {
+        const uint32_t i = sel[x];
+        const unsigned long long ki = ckey[i];
+        const uint32_t ci = cid[i];
+        uint32_t oi = 0xffffffffu;
+        uint32_t rank = 0;
+        for (uint32_t y = 0; y < nsel; ++y) {
+            const unsigned long long ky = ckey[sel[y]];
+            if (ky < ki) {
+                ++rank;
+            } else if (ky == ki && y != x) {
+                if (oi == 0xffffffffu) oi = fo[ci];
+                if (fo[cid[sel[y]]] < oi) ++rank;
+            }
+        }
+        out_cl[rank] = fo[ci];
+        atomicOr(&bits[ci >> 5], 1u << (ci & 31));
+    }
+    uint32_t* out_u = a.sel_units + ((size_t)slot * a.G + g) * a.cap_units;
+    for (uint32_t k = tid; k < kU; k += blockDim.x) out_u[k] = s_kept[k];
+    if (tid == 0) {
+        qi->n_units = kU;
+        qi->n_clusters = nsel;
+        qi->degenerate = 0;
+        qi->error = 0;
+        qi->scanned = (unsigned long long)st.P + nc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Active-set construction (collect_active, retriever.cpp:60-74) for every query
+// head of a slot at once: one pass over the chunk table produces the union of
+// the group's active chunk spans, each tagged with the mask of query heads it
+// serves, in token order.  Sink [0, min(sink, n)) is emitted once for all heads
+// and chunk spans are clipped against it, so the union has no duplicates.
+struct CompactParams {
+    Arena a;
+    uint32_t sink, flags;
+    const uint32_t* buf_off;  // LC_BUFFER_LIST
+    const uint32_t* buf_ids;
+};
+
+constexpr int kCompactThreads = 512;
+
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* warp_tot, T& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        T t = lane < nw ? warp_tot[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const T base = warp > 0 ? warp_tot[warp - 1] : T(0);
+    total = warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
+    extern __shared__ __align__(16) uint32_t sbits[];  // [G][words(L)]
+    const Arena& a = p.a;
+    const uint32_t slot = blockIdx.x, tid = threadIdx.x, G = a.G;
+    const SlotState st = a.state[slot];
+    const uint32_t n = st.n_tokens, M = st.n_chunks, ce = st.chunked_end;
+    const uint32_t all = (1u << G) - 1u;
+    Span* sp = a.spans + (size_t)slot * a.cap_spans;
+    uint32_t* so = a.span_off + (size_t)slot * (a.cap_spans + 1);
+    QInfo* qi = a.qinfo + (size_t)slot * G;
+    unsigned long long* sb = a.step_bytes + (size_t)slot * 4;
+    const unsigned long long d = a.d;
+
+    __shared__ unsigned long long s_cnt[kMaxGroup];
+    __shared__ uint32_t s_nsp[kMaxGroup];
+    __shared__ unsigned long long warp_tot[kCompactThreads / 32];
+    __shared__ uint32_t s_units[32];  // union of kept units (bitset, cap_units <= 1024)
+
+    if (qi[0].degenerate) {
+        if (tid == 0) {
+            sp[0].start = 0;
+            sp[0].len_mask = (n << 8) | all;
+            so[0] = 0;
+            so[1] = n;
+            a.n_spans[slot] = 1;
+            for (uint32_t g = 0; g < G; ++g) qi[g].n_active = n;
+            sb[0] = d * 2 * 2 * n + G * 8 * d;
+            sb[1] = (d * 2 * 2 * n + 8 * d) * G;
+            sb[2] = n;
+            sb[3] = 0;
+        }
+        return;
+    }
+    const uint32_t words = bit_words(st.L);
+    const uint32_t* gbits = a.sel_bits + (size_t)slot * G * bit_words(a.cap_clusters);
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t w = tid; w < words; w += blockDim.x)
+            sbits[g * words + w] = gbits[(size_t)g * bit_words(a.cap_clusters) + w];
+    if (tid < kMaxGroup) {
+        s_cnt[tid] = 0;
+        s_nsp[tid] = 0;
+    }
+    if (tid < 32) s_units[tid] = 0;
+    __syncthreads();
+
+    const uint32_t sink_end = min(p.sink, n);
+    uint32_t out = 0, tok = 0;
+    if (sink_end > 0) {
+        if (tid == 0) {
+            sp[0].start = 0;
+            sp[0].len_mask = (sink_end << 8) | all;
+            so[0] = 0;
+        }
+        out = 1;
+        tok = sink_end;
+    }
+    const uint32_t* cs = a.chunk_start + (size_t)slot * (a.cap_chunks + 1);
+    const uint32_t* cc = a.chunk_clu + (size_t)slot * a.cap_chunks;
+    for (uint32_t base = 0; base < M; base += blockDim.x) {
+        const uint32_t j = base + tid;
+        uint32_t m = 0, s = 0, len = 0;
+        if (j < M) {
+            const uint32_t c = cc[j];
+            for (uint32_t g = 0; g < G; ++g) m |= ((sbits[g * words + (c >> 5)] >> (c & 31)) & 1u) << g;
+            if (m) {
+                s = max(cs[j], sink_end);
+                const uint32_t e = cs[j + 1];
+                if (s >= e) m = 0;
+                else len = e - s;
+            }
+        }
+        const unsigned long long v = m ? ((1ull << 40) | len) : 0ull;
+        unsigned long long total;
+        const unsigned long long ex = block_excl_scan(v, warp_tot, total);
+        if (m) {
+            const uint32_t pos = out + (uint32_t)(ex >> 40);
+            if (pos < a.cap_spans) {
+                sp[pos].start = s;
+                sp[pos].len_mask = (len << 8) | m;
+                so[pos] = tok + (uint32_t)(ex & 0xffffffffffull);
+            }
+            for (uint32_t g = 0; g < G; ++g)
+                if ((m >> g) & 1u) {
+                    atomicAdd(&s_cnt[g], (unsigned long long)len);
+                    atomicAdd(&s_nsp[g], 1u);
+                }
+        }
+        out += (uint32_t)(total >> 40);
+        tok += (uint32_t)(total & 0xffffffffffull);
+    }
+    const uint32_t n_chunk_spans = out - (sink_end > 0 ? 1u : 0u);
+    // buffer ids (collect_active, retriever.cpp:71)
+    if (p.flags == 1u) {  // LC_BUFFER_STREAM: [chunked_end, n), disjoint from chunks
+        const uint32_t b0 = max(ce, sink_end);
+        if (n > b0) {
+            if (tid == 0 && out < a.cap_spans) {
+                sp[out].start = b0;
+                sp[out].len_mask = ((n - b0) << 8) | all;
+                so[out] = tok;
+            }
+            ++out;
+            tok += n - b0;
+        }
+    } else if (p.flags == 2u) {  // explicit sorted unique ids
+        const uint32_t lo = p.buf_off[slot], hi = p.buf_off[slot + 1];
+        for (uint32_t base = lo; base < hi; base += blockDim.x) {
+            const uint32_t i = base + tid;
+            uint32_t resid = 0, id = 0;
+            if (i < hi) {
+                id = p.buf_ids[i];
+                if (id >= sink_end && id < n) {
+                    resid = all;
+                    if (id < ce) {  // inside a chunk: drop the heads that already attend it
+                        uint32_t l = 0, h = M;  // last chunk with start <= id
+                        while (h - l > 1) {
+                            const uint32_t mid = (l + h) >> 1;
+                            if (cs[mid] <= id) l = mid;
+                            else h = mid;
+                        }
+                        const uint32_t c = cc[l];
+                        uint32_t m = 0;
+                        for (uint32_t g = 0; g < G; ++g)
+                            m |= ((sbits[g * words + (c >> 5)] >> (c & 31)) & 1u) << g;
+                        resid = all & ~m;
+                    }
+                }
+            }
+            const unsigned long long v = resid ? ((1ull << 40) | 1ull) : 0ull;
+            unsigned long long total;
+            const unsigned long long ex = block_excl_scan(v, warp_tot, total);
+            if (resid) {
+                const uint32_t pos = out + (uint32_t)(ex >> 40);
+                if (pos < a.cap_spans) {
+                    sp[pos].start = id;
+                    sp[pos].len_mask = (1u << 8) | resid;
+                    so[pos] = tok + (uint32_t)(ex & 0xffffffffffull);
+                }
+                for (uint32_t g = 0; g < G; ++g)
+                    if ((resid >> g) & 1u) atomicAdd(&s_cnt[g], 1ull);
+            }
+            out += (uint32_t)(total >> 40);
+            tok += (uint32_t)(total & 0xffffffffffull);
+        }
+    }
+    // kept-unit union for the byte accounting
+    const uint32_t* su = a.sel_units + (size_t)slot * G * a.cap_units;
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t k = tid; k < qi[g].n_units; k += blockDim.x) {
+            const uint32_t u = su[(size_t)g * a.cap_units + k];
+            if (u < 1024) atomicOr(&s_units[u >> 5], 1u << (u & 31));
+        }
+    __syncthreads();
+    if (tid == 0) {
+        if (out > a.cap_spans) {
+            atomicOr(a.err, kErrSpanOverflow);
+            out = a.cap_spans;
+        }
+        so[out] = tok;
+        a.n_spans[slot] = out;
+        const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
+        unsigned long long nc_union = 0;
+        for (uint32_t u = 0; u < st.P && u < 1024; ++u)
+            if ((s_units[u >> 5] >> (u & 31)) & 1u) nc_union += uoff[u + 1] - uoff[u];
+        const unsigned long long P = st.P;
+        unsigned long long per_q = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const unsigned long long act = s_cnt[g] + sink_end +
+                                           (p.flags == 1u && n > max(ce, sink_end) ? n - max(ce, sink_end) : 0);
+            qi[g].n_active = act;
+            const unsigned long long ncg = qi[g].scanned - P;
+            per_q += P * (4 * d + 8) + ncg * (4 * d + 16) + (unsigned long long)s_nsp[g] * 8 +
+                     act * 2 * d * 2 + 8 * d;
+        }
+        sb[0] = P * (4 * d + 8) + nc_union * (4 * d + 16) + (unsigned long long)n_chunk_spans * 8 +
+                (unsigned long long)tok * 2 * d * 2 + G * 8 * d;
+        sb[1] = per_q;
+        sb[2] = tok;
+        sb[3] = nc_union;
+    }
+}
+
+// launchers ------------------------------------------------------------------
+size_t select_smem_bytes(const Arena& a) {
+    return ((a.d * 4 + 15) & ~15u) + (size_t)a.cap_units * 8 + (size_t)a.max_cand * (8 + 4 + 4 + 4);
+}
+
+cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
+                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
+                          cudaStream_t stream) {
+    SelectParams p{a, q, unit_topk, mode, cluster_topk, sink, budget};
+    const size_t smem = select_smem_bytes(a);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    k_select<<<dim3(a.G, a.n_slots), kSelThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
+                           const uint32_t* buf_ids, cudaStream_t stream) {
+    CompactParams p{a, sink, flags, buf_off, buf_ids};
+    const size_t smem = (size_t)a.G * bit_words(a.cap_clusters) * 4;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    k_compact<<<a.n_slots, kCompactThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace lc
