@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Decode-step throughput of the B200 LycheeCluster path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): Llama-3-8B-shaped cache -- 32 layers x
+8 KV heads (d = 128), GQA 4 (32 query heads), 128K-token context, batch 1,
+2K-token budget.  One step = retrieve() + sparse attention for all 1024
+query heads (32 layers x 32 heads), i.e. one decode step of the model's
+attention path.  Every (layer, KV head) slot has its own synthetic
+clustered KV stream (gen_clustered_workload, seed 1000 + slot, generated on
+the GPU), its own index (build_index, on the GPU, bit-exact to the
+reference) and its own 4 queries.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): the 256 slots are sharded by KV head over the ranks
+(strong scaling of the batch-1 step); the head outputs are all-gathered over
+NCCL once per step.  `--impl reference` times the reference CPU path
+(oracle/_ref, built from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "retrieval+sparse-attn decode steps/s @128K (Llama-3-8B shape); % HBM roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--tokens", type=int, default=131072)
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--kv-heads", type=int, default=8)
+    p.add_argument("--group", type=int, default=4)
+    p.add_argument("--budget", type=int, default=2048)
+    p.add_argument("--batch", type=int, default=1)
+    p.add_argument("--splits", type=int, default=0)
+    p.add_argument("--graph", type=int, default=1)
+    p.add_argument("--cpu-baseline", type=int, default=1)
+    p.add_argument("--seed-base", type=int, default=1000)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(parts)
+            except Exception:
+                pass
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        load = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def build_engine(api, torch, args, slots, device):
+    n = args.tokens
+    S = len(slots)
+    cap_chunks = n // 8 + 64
+    eng = api.Engine(S, 128, args.group, cap_tokens=n + 64, cap_chunks=cap_chunks,
+                     cap_clusters=(cap_chunks + 1) // 2, cap_units=64, splits=args.splits,
+                     keep_reps=False, device=device)
+    seeds = np.array([args.seed_base + s for s in slots], np.uint64)
+    t0 = time.time()
+    codes, qs = eng.gen_workload(n, seeds, query_count=args.group)
+    t1 = time.time()
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+        spans = list(ex.map(lambda s: api.segment_codes(codes[s]), range(S)))
+    t2 = time.time()
+    eng.build_index([n] * S, spans, seeds)
+    torch.cuda.synchronize()
+    t3 = time.time()
+    setup = {"gen_s": round(t1 - t0, 2), "segment_s": round(t2 - t1, 2), "build_s": round(t3 - t2, 2)}
+    return eng, qs, setup
+
+
+def time_loop(torch, fn, steps, stream):
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(steps):
+        fn()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    return ev0.elapsed_time(ev1) / steps  # ms
+
+
+def cpu_baseline_ref(args, n_query_heads, threads=0, reps=None):
+    """The reference's own CPU path (oracle/_ref) on a bounded sample: one
+    reference-built 128K slot, its 4 queries, retrieve() (ids + attention)."""
+    from oracle import refpy as R
+    if not R.available():
+        return None
+    t0 = time.time()
+    w = R.gen_workload(args.tokens, 128, seed=args.seed_base, query_count=args.group)
+    ref = R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base)
+    setup = time.time() - t0
+    nthreads = R.threads() if threads == 0 else threads
+    # mode B (OpenMP over query heads, single-threaded kernels): calls in flight
+    calls = max(nthreads * 4, 64)
+    reps = reps or max(1, calls // args.group)
+    secs, _ = R.time_retrieve([ref], w.queries, token_budget=args.budget, reps=reps, mode=1,
+                              threads=threads)
+    per_call = secs / (reps * args.group)
+    secs_a, _ = R.time_retrieve([ref], w.queries, token_budget=args.budget, reps=1, mode=0,
+                                threads=threads)
+    per_call_a = secs_a / args.group
+    return {"per_call_s": per_call, "per_call_mode_a_s": per_call_a, "threads": nthreads,
+            "calls": reps * args.group, "setup_s": setup, "ref": ref, "w": w,
+            "step_s": per_call * n_query_heads, "step_mode_a_s": per_call_a * n_query_heads}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_qh = args.layers * args.kv_heads * args.group * args.batch
+    base = cpu_baseline_ref(args, n_qh)
+    if base is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    from oracle import refpy as R
+    ref, w = base["ref"], base["w"]
+    # each step: all 1024 query-head retrieve() calls of one decode step, run
+    # against the reference-built slot (its 4 queries cycled), OpenMP over calls
+    qs = np.ascontiguousarray(np.tile(w.queries, (n_qh // args.group, 1)), np.float32)
+    for _ in range(args.warmup):
+        R.time_retrieve([ref], qs[: args.group * 8], token_budget=args.budget, reps=1, mode=1)
+    times = []
+    for _ in range(args.steps):
+        secs, _ = R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1)
+        times.append(secs)
+    step = sum(times) / len(times)
+    v = 1.0 / step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference gen_clustered_workload, seed %d)" % args.seed_base,
+        "config": config_dict(args, 1),
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": base["threads"], "kind": "reference",
+                         "sample": f"1 reference-built {args.tokens}-token slot (build_index on the host), "
+                                   f"{n_qh} retrieve() calls per step (its {args.group} queries cycled), "
+                                   f"OpenMP over calls with {base['threads']} threads"},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def config_dict(args, world):
+    return {"workload": "config2: Llama-3-8B-shaped cache (32 layers x 8 KV heads x d128, GQA 4), "
+                        f"{args.tokens}-token context, batch {args.batch}, {args.budget}-token budget",
+            "layers": args.layers, "kv_heads": args.kv_heads, "group": args.group,
+            "context": args.tokens, "batch": args.batch, "token_budget": args.budget,
+            "unit_topk": 8, "sink": 16, "slots": args.layers * args.kv_heads * args.batch,
+            "parallelism": f"kv-head shard x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (>1 GB of index + KV read per step vs 126 MB L2)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2603_08453_b200 import api
+
+    n_slots_total = args.layers * args.kv_heads * args.batch
+    # KV-head sharding: rank r owns KV heads {h : h*world // kv_heads == r} of every layer/sequence
+    slots = [s for s in range(n_slots_total) if ((s % args.kv_heads) * world) // args.kv_heads == rank]
+    eng, qs, setup = build_engine(api, torch, args, slots, local)
+    stream = torch.cuda.current_stream()
+    q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+    out = torch.zeros_like(q)
+    gathered = torch.zeros((world,) + tuple(q.shape), dtype=q.dtype, device=q.device) if world > 1 else None
+    b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
+
+    def step():
+        eng.retrieve(q, b, out=out)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    err = eng.device_error()
+    if err:
+        raise RuntimeError(f"device error bits 0x{err:x}")
+    graph = None
+    if args.graph and world == 1:
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = time_loop(torch, run, args.steps, stream)
+    clocks = clk.summary()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    step_bytes = eng.step_bytes()  # [union bytes, per-query bytes, union tokens, union candidates]
+    if world > 1:
+        t = torch.tensor(step_bytes, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        step_bytes_all = [float(x) for x in t.tolist()]
+    else:
+        step_bytes_all = [float(x) for x in step_bytes]
+
+    # dominant kernel (sparse attention) and selection timed on their own
+    att_ms = time_loop(torch, lambda: eng.sparse_attention(q, out), args.steps, stream)
+    sel_ms = time_loop(torch, lambda: eng.retrieve(q, b, out=None), args.steps, stream)
+    peak, peak_src = peaks()
+    d = 128
+    att_bytes = step_bytes[2] * 2 * d * 2 + len(slots) * args.group * 2 * 4 * d
+    att_gbs = att_bytes / (att_ms * 1e-3) / 1e9
+    step_gbs = step_bytes[0] / (ms * 1e-3) / 1e9
+
+    # end to end through the public host API (H2D q, retrieve + attention, D2H out)
+    qh = torch.from_numpy(np.ascontiguousarray(qs)).pin_memory()
+    oh = torch.zeros_like(qh).pin_memory()
+    e2e_steps = max(3, args.steps // 2)
+
+    def e2e():
+        eng.retrieve_host(qh.numpy(), b, oh.numpy())
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+
+    for _ in range(2):
+        e2e()
+    e2e_ms = time_loop(torch, e2e, e2e_steps, stream)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    io_bytes = qh.numel() * 4
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        base = cpu_baseline_ref(args, n_slots_total * args.group, reps=None)
+        if base:
+            cpu = {"value": 1.0 / base["step_s"], "unit": "steps/s", "cores": base["threads"],
+                   "kind": "reference",
+                   "sample": f"oracle/_ref (reference built from /root/reference): one reference-built "
+                             f"{args.tokens}-token slot, {base['calls']} retrieve() calls (ids + attention), "
+                             f"OpenMP over calls, {base['threads']} threads; per-call time x "
+                             f"{n_slots_total * args.group} query heads per step. Mode A (reference API as-is, "
+                             f"serial calls, OpenMP kernels): {1.0 / base['step_mode_a_s']:.3f} steps/s"}
+    if rank == 0:
+        value = 1000.0 / ms
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": f"synthetic (gen_clustered_workload streams on the GPU, seeds {args.seed_base}+slot; "
+                    "indexes by GPU build_index, bit-exact to the reference)",
+            "config": config_dict(args, world),
+            "roofline": {"bound": "hbm", "kernel": "k_attend (sparse attention, split-K flash-decode)",
+                         "achieved": att_gbs, "peak": peak, "unit": "GB/s", "frac": att_gbs / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "bytes_per_launch": att_bytes, "ms_per_launch": att_ms},
+            "step_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
+                              "bytes_per_step_union": step_bytes_all[0],
+                              "bytes_per_step_per_query": step_bytes_all[1],
+                              "active_tokens_union": step_bytes_all[2],
+                              "fine_candidates_union": step_bytes_all[3],
+                              "select_ms": sel_ms, "attend_ms": att_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": 1000.0 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes},
+            "gpu_launches": args.steps * 3,
+            "clocks": clocks,
+            "setup": setup,
+            "cuda_graph": graph is not None,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -117,7 +117,9 @@ int lc_index_get_desc(lc_index_t h, lc_index_desc* out);
  * plus its TokenStore keys/values as bf16 bit patterns (host memory), n_tokens
  * rows.  The stream cursor starts at chunked_end = last chunk end
  * (streamer.cpp:13-21), so tokens past it form the buffer.  Replaces
- * StreamState::StreamState(TokenStore, HierarchicalIndex, StreamerConfig). */
+ * StreamState::StreamState(TokenStore, HierarchicalIndex, StreamerConfig).
+ * keys_bf16 == values_bf16 == NULL keeps the K/V already resident in the slot
+ * (e.g. written by lc_gen_workload). */
 int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
                          const uint16_t* keys_bf16, const uint16_t* values_bf16,
                          uint32_t n_tokens);
@@ -130,6 +132,14 @@ int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims);
  * graft applied on the device (for index_to_bytes parity, serialize.cpp:88-125).
  * Caller allocates every array from lc_index_slot_dims.  Synchronous. */
 int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* out);
+
+/* Raw K/V rows of one slot (bf16 bit patterns, host memory): write rows
+ * [0, n_tokens) and set the slot's store size (the index is left as is), or
+ * read them back.  TokenStore::keys_flat/values_flat (types.hpp:48-49). */
+int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const uint16_t* keys_bf16,
+                      const uint16_t* values_bf16, uint32_t n_tokens);
+int lc_kv_download_slot(lc_index_t h, uint32_t slot, uint16_t* keys_bf16, uint16_t* values_bf16,
+                        uint32_t n_tokens);
 
 /* Append one decoded token's K/V (bf16, device [n_slots][dim] each) to every
  * slot -- TokenStore::append inside push_token (streamer.cpp:56-58). */
@@ -199,6 +209,10 @@ int lc_device_error(lc_index_t h, uint32_t* out, int clear);
  * (0 natural, 1 forced, 2 tail), level; up to cap spans. */
 int lc_segment(const char* const* texts, uint32_t n, uint32_t min_len, uint32_t max_len,
                uint32_t* spans4, uint64_t cap, uint64_t* n_spans);
+
+/* lc_segment over packed texts: text i = buf[offs[i], offs[i+1]). */
+int lc_segment_packed(const char* buf, const uint64_t* offs, uint32_t n, uint32_t min_len,
+                      uint32_t max_len, uint32_t* spans4, uint64_t cap, uint64_t* n_spans);
 
 /* StreamState::flush_buffer's chunk choice (streamer.cpp:29-54) over the n
  * buffered texts: take = head span length unless it is a tail, else max_len. */

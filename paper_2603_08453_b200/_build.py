@@ -42,13 +42,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     logs = []
+    procs = []
     for src in CU_SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                                 text=True)))
+    for src, obj, pr in procs:
+        out, _ = pr.communicate()
+        logs.append(f"== {src}\n{out}")
+        if pr.returncode != 0:
+            sys.stderr.write(out)
             raise RuntimeError(f"nvcc failed for {src}")
         objs.append(obj)
     for src in CPP_SOURCES:

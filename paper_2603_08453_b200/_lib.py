@@ -54,8 +54,9 @@ class SelectionInfo_(C.Structure):
 EXPORTS = [
     "lc_last_error", "lc_index_create", "lc_index_destroy", "lc_index_get_desc",
     "lc_index_upload_slot", "lc_index_slot_dims", "lc_index_download_slot", "lc_kv_append",
+    "lc_kv_upload_slot", "lc_kv_download_slot",
     "lc_retrieve", "lc_sparse_attention", "lc_graft", "lc_decode_step", "lc_retrieve_host",
-    "lc_selection_download", "lc_step_bytes", "lc_device_error", "lc_segment", "lc_flush_take",
+    "lc_selection_download", "lc_step_bytes", "lc_device_error", "lc_segment", "lc_segment_packed", "lc_flush_take",
     "lc_index_build", "lc_gen_workload",
 ]
 
@@ -89,6 +90,8 @@ def lib():
         L.lc_index_slot_dims.argtypes = [vp, u32, vp]
         L.lc_index_download_slot.argtypes = [vp, u32, C.POINTER(HostIndex_)]
         L.lc_kv_append.argtypes = [vp, vp, vp, vp]
+        L.lc_kv_upload_slot.argtypes = [vp, u32, vp, vp, u32]
+        L.lc_kv_download_slot.argtypes = [vp, u32, vp, vp, u32]
         L.lc_retrieve.argtypes = [vp, vp, C.POINTER(Budgets_), u32, vp, vp, vp, vp]
         L.lc_sparse_attention.argtypes = [vp, vp, vp, vp]
         L.lc_graft.argtypes = [vp, vp, vp, vp, vp, vp]
@@ -99,6 +102,7 @@ def lib():
         L.lc_step_bytes.argtypes = [vp, vp]
         L.lc_device_error.argtypes = [vp, vp, C.c_int]
         L.lc_segment.argtypes = [vp, u32, u32, u32, vp, u64, C.POINTER(u64)]
+        L.lc_segment_packed.argtypes = [vp, vp, u32, u32, u32, vp, u64, C.POINTER(u64)]
         L.lc_flush_take.argtypes = [vp, u32, u32, u32, u32, C.POINTER(u32), C.POINTER(u32),
                                     C.POINTER(u32)]
         L.lc_index_build.argtypes = [vp, vp, vp, vp, C.c_double, u32, u32, vp]

@@ -235,6 +235,42 @@ class Engine:
         L.check(L.lib().lc_index_upload_slot(self.h, slot, C.byref(s), kb.ctypes.data,
                                              vb.ctypes.data, kb.shape[0]))
 
+    def kv_upload(self, slot: int, keys: np.ndarray, values: np.ndarray):
+        kb = np.ascontiguousarray(keys if keys.dtype == np.uint16 else bf16_bits(keys))
+        vb = np.ascontiguousarray(values if values.dtype == np.uint16 else bf16_bits(values))
+        L.check(L.lib().lc_kv_upload_slot(self.h, slot, kb.ctypes.data, vb.ctypes.data, kb.shape[0]))
+
+    def kv_download(self, slot: int, n: int):
+        k = np.zeros((n, self.dim), np.uint16)
+        v = np.zeros((n, self.dim), np.uint16)
+        L.check(L.lib().lc_kv_download_slot(self.h, slot, k.ctypes.data, v.ctypes.data, n))
+        return k, v
+
+    def gen_workload(self, n_tokens: int, seeds, n_blobs=8, concentration=3.0, query_count=4,
+                     query_locality=0.8):
+        """gen_clustered_workload token streams written straight into every slot
+        (GPU); returns (text codes [S, n], queries [S, query_count, d])."""
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        codes = np.zeros((self.n_slots, n_tokens), np.uint8)
+        qs = np.zeros((self.n_slots, query_count, self.dim), np.float32)
+        L.check(L.lib().lc_gen_workload(self.h, n_tokens, n_blobs, concentration, query_count,
+                                        query_locality, seeds.ctypes.data, codes.ctypes.data,
+                                        qs.ctypes.data))
+        return codes, qs
+
+    def build_index(self, n_tokens, spans_per_slot, seeds, avg_chunks_per_cluster=2.0,
+                    max_coarse_units=64, kmeans_iters=10):
+        """build_index (index.cpp:155-243) for every slot on the GPU from its resident keys."""
+        n_tokens = np.ascontiguousarray(n_tokens, np.uint32)
+        spans = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint32).reshape(-1, 4)
+                                                     for s in spans_per_slot]), np.uint32)
+        off = np.zeros(self.n_slots + 1, np.uint64)
+        off[1:] = np.cumsum([len(s) for s in spans_per_slot])
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        L.check(L.lib().lc_index_build(self.h, n_tokens.ctypes.data, spans.ctypes.data, off.ctypes.data,
+                                       avg_chunks_per_cluster, max_coarse_units, kmeans_iters,
+                                       seeds.ctypes.data))
+
     def slot_dims(self, slot: int):
         out = np.zeros(8, np.uint64)
         L.check(L.lib().lc_index_slot_dims(self.h, slot, out.ctypes.data))
@@ -355,6 +391,21 @@ def segment(texts: Sequence[str], min_len: int = 8, max_len: int = 16) -> np.nda
     n = L.u64()
     L.check(L.lib().lc_segment(arr, len(texts), min_len, max_len, out.ctypes.data, out.shape[0],
                                C.byref(n)))
+    return out[: n.value].copy()
+
+
+def segment_codes(codes: np.ndarray, min_len: int = 8, max_len: int = 16) -> np.ndarray:
+    """segment() over text codes (0 "", 1 "\\n", 2 "}") via packed strings."""
+    codes = np.asarray(codes, np.uint8)
+    table = {0: b"", 1: b"\n", 2: b"}"}
+    lens = np.where(codes == 0, 0, 1).astype(np.uint64)
+    offs = np.zeros(len(codes) + 1, np.uint64)
+    offs[1:] = np.cumsum(lens)
+    buf = np.frombuffer(b"".join(table[int(c)] for c in codes[codes != 0]) + b"\0", np.uint8).copy()
+    out = np.zeros((len(codes) + 1, 4), np.uint32)
+    n = L.u64()
+    L.check(L.lib().lc_segment_packed(buf.ctypes.data, offs.ctypes.data, len(codes), min_len, max_len,
+                                      out.ctypes.data, out.shape[0], C.byref(n)))
     return out[: n.value].copy()
 
 

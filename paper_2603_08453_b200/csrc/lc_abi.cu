@@ -15,95 +15,7 @@
 #include <string>
 #include <vector>
 
-namespace lc {
-size_t select_smem_bytes(const Arena& a);
-cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
-                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
-                          cudaStream_t stream);
-cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
-                           const uint32_t* buf_ids, cudaStream_t stream);
-cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream);
-cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
-cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
-                         cudaStream_t stream);
-}  // namespace lc
-
-using namespace lc;
-
-namespace {
-
-thread_local std::string g_err;
-
-struct Status : std::runtime_error {
-    int code;
-    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-[[noreturn]] void fail(int code, const std::string& msg) { throw Status(code, msg); }
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) fail(LC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-template <typename F>
-int guard(F&& f) {
-    try {
-        f();
-        return LC_OK;
-    } catch (const Status& s) {
-        g_err = s.what();
-        return s.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return LC_ENOMEM;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return LC_ERUNTIME;
-    }
-}
-
-template <typename T>
-T* dalloc(size_t n, std::vector<void*>& owned) {
-    void* p = nullptr;
-    if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        fail(LC_ENOMEM, std::string("cudaMalloc ") + std::to_string(n * sizeof(T)) + " B: " +
-                            cudaGetErrorString(e));
-    }
-    owned.push_back(p);
-    return static_cast<T*>(p);
-}
-
-}  // namespace
-
-struct HostSlot {
-    uint32_t n_tokens = 0, chunked_end = 0, n_chunks = 0, L = 0, P = 0;
-    bool loaded = false;
-    std::vector<uint32_t> kind, level;   // per chunk (host-only fields of ChunkSpan)
-    std::vector<float> rep;              // prefill reps when the device keeps none
-    std::vector<uint32_t> fanout;        // n_u per unit (fixed after build)
-};
-
-struct lc_index_s {
-    lc_index_desc desc{};
-    Arena a{};
-    std::vector<void*> owned;
-    std::vector<HostSlot> hs;
-    float* q_stage = nullptr;    // device staging for lc_retrieve_host
-    float* out_stage = nullptr;
-    uint32_t* take_dev = nullptr;
-    lc_graft_report* rep_scratch = nullptr;
-    uint32_t last_flags = 0;
-    uint32_t last_valid = 0;
-    std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
-
-    ~lc_index_s() {
-        for (void* p : owned) cudaFree(p);
-    }
-    void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
-};
+#include "lc_engine.hpp"
 
 static uint32_t needed_candidates(lc_index_s* h, uint32_t unit_topk) {
     auto it = h->cand_cache.find(unit_topk);
@@ -286,8 +198,8 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         auto up = [&](void* dst, const void* src, size_t bytes) {
             if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
         };
-        up(a.K + kv_off(a, slot), keys, (size_t)n_tokens * D * 2);
-        up(a.V + kv_off(a, slot), values, (size_t)n_tokens * D * 2);
+        if (keys) up(a.K + kv_off(a, slot), keys, (size_t)n_tokens * D * 2);
+        if (values) up(a.V + kv_off(a, slot), values, (size_t)n_tokens * D * 2);
         up(a.chunk_start + so * (a.cap_chunks + 1), cs.data(), cs.size() * 4);
         up(a.chunk_clu + so * a.cap_chunks, cc.data(), cc.size() * 4);
         up(a.ucent + so * a.cap_units * D, ucent.data(), ucent.size() * 4);
@@ -415,6 +327,35 @@ int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
         for (uint32_t f = 0; f < L; ++f) cnt[f + 1] += cnt[f];
         for (uint32_t f = 0; f <= L; ++f) ix->fine_member_off[f] = cnt[f];
         for (uint32_t j = 0; j < M; ++j) ix->fine_members[cnt[ix->cluster_of_chunk[j]]++] = j;
+    });
+}
+
+int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const uint16_t* keys, const uint16_t* values,
+                      uint32_t n_tokens) {
+    return guard([&] {
+        if (!h || !keys || !values || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_kv_upload_slot: bad argument");
+        if (n_tokens > h->a.cap_tokens) fail(LC_EINVAL, "lc_kv_upload_slot: n_tokens exceeds capacity");
+        h->set_device();
+        const Arena& a = h->a;
+        ck(cudaMemcpy(a.K + kv_off(a, slot), keys, (size_t)n_tokens * a.d * 2, cudaMemcpyHostToDevice), "K");
+        ck(cudaMemcpy(a.V + kv_off(a, slot), values, (size_t)n_tokens * a.d * 2, cudaMemcpyHostToDevice), "V");
+        SlotState st;
+        ck(cudaMemcpy(&st, a.state + slot, sizeof st, cudaMemcpyDeviceToHost), "state");
+        st.n_tokens = n_tokens;
+        ck(cudaMemcpy(a.state + slot, &st, sizeof st, cudaMemcpyHostToDevice), "state");
+        h->hs[slot].n_tokens = n_tokens;
+    });
+}
+
+int lc_kv_download_slot(lc_index_t h, uint32_t slot, uint16_t* keys, uint16_t* values, uint32_t n_tokens) {
+    return guard([&] {
+        if (!h || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_kv_download_slot: bad argument");
+        if (n_tokens > h->hs[slot].n_tokens) fail(LC_EINVAL, "lc_kv_download_slot: beyond the store");
+        h->set_device();
+        ck(cudaDeviceSynchronize(), "sync");
+        const Arena& a = h->a;
+        if (keys) ck(cudaMemcpy(keys, a.K + kv_off(a, slot), (size_t)n_tokens * a.d * 2, cudaMemcpyDeviceToHost), "K");
+        if (values) ck(cudaMemcpy(values, a.V + kv_off(a, slot), (size_t)n_tokens * a.d * 2, cudaMemcpyDeviceToHost), "V");
     });
 }
 

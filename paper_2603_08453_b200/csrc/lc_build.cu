@@ -1,15 +1,804 @@
-// GPU prefill helpers: synthetic workload generation
-// and build_index on the device.  (Implemented in a later milestone.)
-#include "../../include/lychee_b200.h"
-#include "lc_common.cuh"
+// GPU prefill helpers:
+//
+//  * lc_gen_workload: the reference's gen_clustered_workload token stream
+//    (workload.cpp:110-169) generated straight into the slots' K/V.  The
+//    splitmix64 generator is counter-based, so the host walks only the
+//    control draws (blob runs, boundary markers) and records each token's
+//    draw offset; the device evaluates the Box-Muller pairs in parallel.
+//    Blob centres and queries are drawn on the host (exact).  CUDA's fp64
+//    log/sin/cos are not glibc's, so a key may differ from the CPU
+//    generator's in the last float bit with probability ~1e-9 per value;
+//    the stream is the same distribution (timing workloads only -- parity
+//    tests use the reference's own generator).
+//
+//  * lc_index_build: build_index (index.cpp:155-243) for every slot at once.
+//    Chunk representatives, spherical k-means (assign_nearest /
+//    group_mean_normalize), radii and the coarse tier run on the device with
+//    the reference's sequential fp64 rules (bit-exact); the seeded sample
+//    init (mt19937_64, index.cpp:46-56) and the rare empty-cluster repair
+//    (index.cpp:68-94) run on the host.
+#include "lc_engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <vector>
+
+namespace {
+
+constexpr uint64_t kGold = 0x9e3779b97f4a7c15ull;
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// host mirror of tierkv::Rng (workload.cpp:21-50), with a draw counter
+struct HRng {
+    uint64_t s0, state, draws = 0;
+    bool has_spare = false;
+    double spare = 0.0;
+    explicit HRng(uint64_t seed) : s0(seed ? seed : kGold), state(seed ? seed : kGold) {}
+    uint64_t next_u64() {
+        ++draws;
+        return mix64(state += kGold);
+    }
+    double next_unit() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+    double next_gaussian() {
+        if (has_spare) {
+            has_spare = false;
+            return spare;
+        }
+        double u1 = next_unit();
+        while (u1 <= 1e-300) u1 = next_unit();
+        const double u2 = next_unit();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double theta = 2.0 * M_PI * u2;
+        spare = r * std::sin(theta);
+        has_spare = true;
+        return r * std::cos(theta);
+    }
+    size_t next_index(size_t n) { return static_cast<size_t>(next_u64() % n); }
+    void skip(uint64_t k) {
+        state += k * kGold;
+        draws += k;
+    }
+};
+
+std::vector<float> unit_gaussian(HRng& rng, size_t d) {  // workload.cpp:54-64
+    std::vector<float> v(d);
+    double n2 = 0.0;
+    for (size_t j = 0; j < d; ++j) {
+        v[j] = static_cast<float>(rng.next_gaussian());
+        n2 += static_cast<double>(v[j]) * v[j];
+    }
+    const double inv = 1.0 / std::sqrt(n2);
+    for (size_t j = 0; j < d; ++j) v[j] = static_cast<float>(v[j] * inv);
+    return v;
+}
+
+std::vector<float> blob_sample(HRng& rng, const float* c, size_t d, double conc) {  // :66-79
+    const double sigma = 1.0 / conc;
+    const double scale = sigma / std::sqrt(static_cast<double>(d));
+    std::vector<float> v(d);
+    double n2 = 0.0;
+    for (size_t j = 0; j < d; ++j) {
+        const double x = c[j] + scale * rng.next_gaussian();
+        v[j] = static_cast<float>(x);
+        n2 += x * x;
+    }
+    const double inv = 1.0 / std::sqrt(n2);
+    for (size_t j = 0; j < d; ++j) v[j] = static_cast<float>(v[j] * inv);
+    return v;
+}
+
+size_t marker_gap(HRng& rng) {  // workload.cpp:92-97
+    const double u = rng.next_unit();
+    if (u < 0.15) return 3 + rng.next_index(5);
+    if (u < 0.85) return 8 + rng.next_index(9);
+    return 17 + rng.next_index(8);
+}
+
+struct TokCtl {
+    unsigned long long draw;  // draws consumed before this token's first gaussian
+    uint32_t blob;
+    uint32_t pad;
+};
+
+__device__ __forceinline__ double unit_of(uint64_t s0, unsigned long long k) {
+    // the (k+1)-th draw of a generator seeded with s0
+    return static_cast<double>(mix64(s0 + (uint64_t)(k + 1) * kGold) >> 11) * 0x1.0p-53;
+}
+
+// one warp per token: 64 key pairs + 64 value pairs (d = 128) of Box-Muller
+__global__ void __launch_bounds__(256) k_gen(Arena a, const TokCtl* ctl, const float* centers,
+                                             const uint64_t* s0s, uint32_t n, uint32_t n_blobs,
+                                             double scale) {
+    const uint32_t slot = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t i = blockIdx.x * 8 + warp;
+    const uint32_t d = a.d;
+    __shared__ double xs[8][256];
+    __shared__ double s_inv[8];
+    if (i >= n) return;
+    const TokCtl t = ctl[(size_t)slot * n + i];
+    const uint64_t s0 = s0s[slot];
+    const float* c = centers + ((size_t)slot * n_blobs + t.blob) * d;
+    for (uint32_t p = lane; p < d; p += 32) {  // p < d/2: key pairs; p >= d/2: value pairs
+        const unsigned long long k = t.draw + 2ull * p;
+        const double u1 = unit_of(s0, k), u2 = unit_of(s0, k + 1);
+        const double r = sqrt(-2.0 * log(u1));
+        const double th = 2.0 * M_PI * u2;
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        const double g0 = r * cs, g1 = r * sn;
+        if (p < d / 2) {
+            const uint32_t j = 2 * p;
+            xs[warp][j] = __dadd_rn((double)c[j], __dmul_rn(scale, g0));
+            xs[warp][j + 1] = __dadd_rn((double)c[j + 1], __dmul_rn(scale, g1));
+        } else {
+            const uint32_t j = 2 * (p - d / 2);
+            __nv_bfloat16* vd = a.V + kv_off(a, slot) + (size_t)i * d;
+            vd[j] = __float2bfloat16_rn((float)g0);
+            vd[j + 1] = __float2bfloat16_rn((float)g1);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double n2 = 0.0;
+        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(xs[warp][j], xs[warp][j]));
+        s_inv[warp] = __ddiv_rn(1.0, __dsqrt_rn(n2));
+    }
+    __syncwarp();
+    const double inv = s_inv[warp];
+    __nv_bfloat16* kd = a.K + kv_off(a, slot) + (size_t)i * d;
+    for (uint32_t j = lane; j < d; j += 32) {
+        const float v = (float)xs[warp][j];
+        kd[j] = __float2bfloat16_rn((float)__dmul_rn((double)v, inv));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// build_index kernels (batched over slots; per-slot offsets into packed arrays)
+
+struct KSlot {             // one k-means problem
+    uint32_t n, k;         // points, clusters
+    uint32_t pt_off;       // first point row in the packed point array
+    uint32_t ct_off;       // first centroid row in the packed centroid array
+};
+
+// chunk_representative (index.cpp:20-41) for every prefill chunk; one warp per chunk
+__global__ void k_reps(Arena a, const uint32_t* cstart, const uint32_t* clen, const uint32_t* cslot,
+                       uint32_t n_chunks, uint32_t pooling, float* reps, uint32_t* err) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t d = a.d;
+    __shared__ double acc_s[8][256];
+    const uint32_t wl = threadIdx.x >> 5;
+    if (w >= n_chunks) return;
+    const uint32_t slot = cslot[w], s = cstart[w], len = clen[w];
+    const __nv_bfloat16* K = a.K + kv_off(a, slot) + (size_t)s * d;
+    for (uint32_t j = lane; j < d; j += 32) {
+        double acc;
+        if (pooling == 0) {
+            acc = 0.0;
+            for (uint32_t i = 0; i < len; ++i) acc = __dadd_rn(acc, (double)__bfloat162float(K[(size_t)i * d + j]));
+            acc = __ddiv_rn(acc, (double)len);
+        } else {
+            acc = (double)__bfloat162float(K[j]);
+            for (uint32_t i = 1; i < len; ++i) acc = fmax(acc, (double)__bfloat162float(K[(size_t)i * d + j]));
+        }
+        acc_s[wl][j] = acc;
+    }
+    __syncwarp();
+    double norm = 0.0;
+    if (lane == 0) {
+        double n2 = 0.0;
+        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(acc_s[wl][j], acc_s[wl][j]));
+        norm = __dsqrt_rn(n2);
+        if (norm == 0.0) atomicOr(err, kErrZeroNorm);
+    }
+    norm = __shfl_sync(0xffffffffu, norm, 0);
+    for (uint32_t j = lane; j < d; j += 32)
+        reps[(size_t)w * d + j] = norm == 0.0 ? 0.f : (float)__ddiv_rn(acc_s[wl][j], norm);
+}
+
+__global__ void k_gather_rows(const float* pts, const uint32_t* idx, const uint32_t* row_dst,
+                              uint32_t n_rows, uint32_t d, float* out) {
+    const uint32_t r = blockIdx.x;
+    if (r >= n_rows) return;
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x)
+        out[(size_t)row_dst[r] * d + j] = pts[(size_t)idx[r] * d + j];
+}
+
+// assign_nearest (kernels.cpp:161-165): argmax_c dot(p, c) in sequential fp64,
+// ties to the smaller c.  64 points x 64 centroids per CTA tile, 4x4 per thread.
+constexpr int kTP = 64, kTC = 64, kTJ = 32;
+__global__ void __launch_bounds__(256) k_assign(const float* pts, const float* cents, const KSlot* ks,
+                                                const uint32_t* tile_slot, const uint32_t* tile_first,
+                                                uint32_t d, uint32_t* assign, double* score) {
+    __shared__ __align__(16) float sp[kTJ][kTP];
+    __shared__ __align__(16) float sc[kTJ][kTC];
+    const uint32_t tile = blockIdx.x;
+    const KSlot K = ks[tile_slot[tile]];
+    const uint32_t p0 = tile_first[tile];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double best[4];
+    uint32_t bidx[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        best[i] = -INFINITY;
+        bidx[i] = 0;
+    }
+    for (uint32_t c0 = 0; c0 < K.k; c0 += kTC) {
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (uint32_t j0 = 0; j0 < d; j0 += kTJ) {
+            __syncthreads();
+            for (uint32_t e = threadIdx.x; e < kTP * kTJ; e += blockDim.x) {
+                const uint32_t row = e / kTJ, jj = e % kTJ;
+                const uint32_t p = p0 + row, c = c0 + row;
+                sp[jj][row] = (p < K.n && j0 + jj < d) ? pts[(size_t)(K.pt_off + p) * d + j0 + jj] : 0.f;
+                sc[jj][row] = (c < K.k && j0 + jj < d) ? cents[(size_t)(K.ct_off + c) * d + j0 + jj] : 0.f;
+            }
+            __syncthreads();
+            const uint32_t jn = min((uint32_t)kTJ, d - j0);
+            for (uint32_t jj = 0; jj < jn; ++jj) {
+                const float4 pv = *reinterpret_cast<const float4*>(&sp[jj][ty * 4]);
+                const float4 cv = *reinterpret_cast<const float4*>(&sc[jj][tx * 4]);
+                const double pd[4] = {(double)pv.x, (double)pv.y, (double)pv.z, (double)pv.w};
+                const double cd[4] = {(double)cv.x, (double)cv.y, (double)cv.z, (double)cv.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(pd[i], cd[j], acc[i][j]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t c = c0 + tx * 4 + j;
+                if (c < K.k && acc[i][j] > best[i]) {
+                    best[i] = acc[i][j];
+                    bidx[i] = c;
+                }
+            }
+    }
+    // merge across the 16 threads sharing these points: (score desc, c asc)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const double s2 = __shfl_xor_sync(0xffffffffu, best[i], o);
+            const uint32_t c2 = __shfl_xor_sync(0xffffffffu, bidx[i], o);
+            if (s2 > best[i] || (s2 == best[i] && c2 < bidx[i])) {
+                best[i] = s2;
+                bidx[i] = c2;
+            }
+        }
+        const uint32_t p = p0 + ty * 4 + i;
+        if (tx == 0 && p < K.n) {
+            assign[K.pt_off + p] = bidx[i];
+            score[K.pt_off + p] = best[i];
+        }
+    }
+}
+
+__global__ void k_count(const KSlot* ks, uint32_t n_slots, const uint32_t* assign, const uint32_t* pt_slot,
+                        uint32_t n_pts, uint32_t* counts) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pts) return;
+    const KSlot K = ks[pt_slot[p]];
+    atomicAdd(&counts[K.ct_off + assign[p]], 1u);
+}
+
+__global__ void k_empties(const uint32_t* counts, const uint32_t* ct_slot, uint32_t n_ct, uint32_t* empties) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < n_ct && counts[c] == 0) atomicAdd(&empties[ct_slot[c]], 1u);
+}
+
+// invert_assignment (index.cpp:58-64): stable CSR of each cluster's points in
+// ascending point order; one CTA per slot, warps take turns per chunk
+__global__ void __launch_bounds__(1024) k_scatter(const KSlot* ks, const uint32_t* assign, const uint32_t* counts,
+                                                  uint32_t* off, uint32_t* members) {
+    const KSlot K = ks[blockIdx.x];
+    extern __shared__ uint32_t cursor[];  // [k]
+    __shared__ uint32_t warp_tot[32];
+    __shared__ uint32_t s_base;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    // exclusive scan of counts -> off / cursor
+    for (uint32_t b = 0; b < K.k; b += blockDim.x) {
+        const uint32_t c = b + tid;
+        const uint32_t v = c < K.k ? counts[K.ct_off + c] : 0u;
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) warp_tot[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t t = warp_tot[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= (uint32_t)o) t += y;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        const uint32_t base = s_base + (warp ? warp_tot[warp - 1] : 0u);
+        if (c < K.k) {
+            cursor[c] = base + x - v;
+            off[K.ct_off + blockIdx.x + c] = base + x - v;
+        }
+        __syncthreads();
+        if (tid == 0) s_base += warp_tot[31];
+        __syncthreads();
+    }
+    if (tid == 0) off[K.ct_off + blockIdx.x + K.k] = s_base;  // off has k+1 rows per slot
+    __syncthreads();
+    for (uint32_t b = 0; b < K.n; b += blockDim.x) {
+        const uint32_t p = b + tid;
+        const bool valid = p < K.n;
+        const uint32_t c = valid ? assign[K.pt_off + p] : 0xffffffffu;
+        const unsigned int same = __match_any_sync(0xffffffffu, c);
+        const uint32_t rank = __popc(same & ((1u << lane) - 1u));
+        const bool leader = rank == 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+            if (warp == w && valid) {
+                const uint32_t pos = cursor[c] + rank;
+                members[K.pt_off + pos] = p;
+                __syncwarp(same);
+                if (leader) cursor[c] += __popc(same);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// group_mean_normalize (kernels.cpp:65-88): one warp per cluster
+__global__ void k_mean(const float* pts, const KSlot* ks, const uint32_t* ct_slot, const uint32_t* off,
+                       const uint32_t* members, uint32_t n_ct, uint32_t d, float* cents) {
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    __shared__ double acc_s[8][256];
+    const uint32_t wl = threadIdx.x >> 5;
+    if (gw >= n_ct) return;
+    const uint32_t slot = ct_slot[gw];
+    const KSlot K = ks[slot];
+    const uint32_t c = gw - K.ct_off;
+    // off is laid out with k+1 entries per slot: row base = ct_off + slot
+    const uint32_t o0 = off[K.ct_off + slot + c], o1 = off[K.ct_off + slot + c + 1];
+    const uint32_t cnt = o1 - o0;
+    if (cnt == 0) return;  // empty group keeps its previous centroid
+    const double inv_n = 1.0 / (double)cnt;
+    for (uint32_t j = lane; j < d; j += 32) {
+        double acc = 0.0;
+        for (uint32_t m = o0; m < o1; ++m)
+            acc = __dadd_rn(acc, (double)pts[(size_t)(K.pt_off + members[K.pt_off + m]) * d + j]);
+        acc_s[wl][j] = __dmul_rn(acc, inv_n);
+    }
+    __syncwarp();
+    double norm = 0.0;
+    if (lane == 0) {
+        double n2 = 0.0;
+        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(acc_s[wl][j], acc_s[wl][j]));
+        norm = __dsqrt_rn(n2);
+    }
+    norm = __shfl_sync(0xffffffffu, norm, 0);
+    if (norm == 0.0) return;
+    for (uint32_t j = lane; j < d; j += 32)
+        cents[(size_t)(K.ct_off + c) * d + j] = (float)__ddiv_rn(acc_s[wl][j], norm);
+}
+
+// group_radius (kernels.cpp:90-96): r_g = max over members of l2_dist(row, c_g)
+// target = second-level assignment (descendant radius) when assign2 != NULL
+__global__ void k_radius(const float* pts, const KSlot* ks, const uint32_t* pt_slot, uint32_t n_pts,
+                         const uint32_t* assign, const KSlot* ks2, const uint32_t* assign2,
+                         const float* cents, uint32_t d, unsigned long long* rad) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pts) return;
+    const uint32_t slot = pt_slot[p];
+    uint32_t c = assign[p];
+    uint32_t crow;
+    if (assign2) {
+        const KSlot K2 = ks2[slot];
+        c = assign2[K2.pt_off + c];
+        crow = K2.ct_off + c;
+    } else {
+        crow = ks[slot].ct_off + c;
+    }
+    const float* x = pts + (size_t)p * d;
+    const float* y = cents + (size_t)crow * d;
+    double s = 0.0;
+    for (uint32_t j = 0; j < d; ++j) {
+        const double diff = __dsub_rn((double)x[j], (double)y[j]);
+        s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+    atomicMax(rad + crow, (unsigned long long)__double_as_longlong(__dsqrt_rn(s)));
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) : n(count) {
+        ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc (build scratch)");
+    }
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    void up(const std::vector<T>& v) {
+        if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    }
+    std::vector<T> down(size_t count, size_t off = 0) const {
+        std::vector<T> v(count);
+        if (count) ck(cudaMemcpy(v.data(), p + off, count * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+        return v;
+    }
+};
+
+// index.cpp:46-56
+std::vector<uint32_t> sample_distinct(size_t n, size_t k, uint64_t seed) {
+    std::vector<uint32_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0u);
+    std::mt19937_64 rng(seed);
+    for (size_t i = 0; i < k; ++i) {
+        size_t j = i + static_cast<size_t>(rng() % (n - i));
+        std::swap(idx[i], idx[j]);
+    }
+    idx.resize(k);
+    return idx;
+}
+
+// batched spherical_kmeans (index.cpp:107-143) over packed points `pts`
+struct KMeans {
+    std::vector<KSlot> ks;
+    size_t n_pts = 0, n_ct = 0;
+    uint32_t d = 0;
+    std::vector<uint32_t> assign;  // host copy of the final assignment
+};
+
+void run_kmeans(KMeans& km, const float* pts, float* cents, uint32_t* assign, double* score,
+                const std::vector<uint64_t>& seeds, uint32_t iters) {
+    const uint32_t S = (uint32_t)km.ks.size(), d = km.d;
+    DBuf<KSlot> ks(S);
+    ks.up(km.ks);
+    std::vector<uint32_t> pt_slot(km.n_pts), ct_slot(km.n_ct), tile_slot, tile_first;
+    for (uint32_t s = 0; s < S; ++s) {
+        const KSlot& K = km.ks[s];
+        for (uint32_t i = 0; i < K.n; ++i) pt_slot[K.pt_off + i] = s;
+        for (uint32_t c = 0; c < K.k; ++c) ct_slot[K.ct_off + c] = s;
+        for (uint32_t p = 0; p < K.n; p += kTP) {
+            tile_slot.push_back(s);
+            tile_first.push_back(p);
+        }
+    }
+    DBuf<uint32_t> d_pt_slot(km.n_pts), d_ct_slot(km.n_ct), d_tile_slot(tile_slot.size()),
+        d_tile_first(tile_first.size()), counts(km.n_ct), off(km.n_ct + S), members(km.n_pts), empties(S);
+    d_pt_slot.up(pt_slot);
+    d_ct_slot.up(ct_slot);
+    d_tile_slot.up(tile_slot);
+    d_tile_first.up(tile_first);
+    // seeded init: centroids = sampled points
+    {
+        std::vector<uint32_t> idx, dst;
+        for (uint32_t s = 0; s < S; ++s) {
+            const KSlot& K = km.ks[s];
+            auto sm = sample_distinct(K.n, K.k, seeds[s]);
+            for (uint32_t c = 0; c < K.k; ++c) {
+                idx.push_back(K.pt_off + sm[c]);
+                dst.push_back(K.ct_off + c);
+            }
+        }
+        DBuf<uint32_t> di(idx.size()), dd(dst.size());
+        di.up(idx);
+        dd.up(dst);
+        k_gather_rows<<<(uint32_t)idx.size(), 128>>>(pts, di.p, dd.p, (uint32_t)idx.size(), d, cents);
+        ck(cudaGetLastError(), "k_gather_rows");
+    }
+    uint32_t max_k = 0;
+    for (const auto& K : km.ks) max_k = std::max(max_k, K.k);
+    const size_t scatter_smem = (size_t)max_k * 4;
+    if (scatter_smem > 48 * 1024)
+        ck(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem),
+           "k_scatter smem");
+    for (uint32_t it = 0; it <= iters; ++it) {
+        const bool final_pass = it == iters;
+        k_assign<<<(uint32_t)tile_slot.size(), 256>>>(pts, cents, ks.p, d_tile_slot.p, d_tile_first.p, d,
+                                                      assign, score);
+        ck(cudaGetLastError(), "k_assign");
+        ck(cudaMemset(counts.p, 0, km.n_ct * 4), "memset");
+        ck(cudaMemset(empties.p, 0, S * 4), "memset");
+        k_count<<<(uint32_t)((km.n_pts + 255) / 256), 256>>>(ks.p, S, assign, d_pt_slot.p, (uint32_t)km.n_pts,
+                                                              counts.p);
+        k_empties<<<(uint32_t)((km.n_ct + 255) / 256), 256>>>(counts.p, d_ct_slot.p, (uint32_t)km.n_ct,
+                                                               empties.p);
+        ck(cudaGetLastError(), "k_count");
+        auto emp = empties.down(S);
+        for (uint32_t s = 0; s < S; ++s) {
+            if (!emp[s]) continue;
+            // repair_empty_clusters (index.cpp:68-94) on the host, exact
+            const KSlot& K = km.ks[s];
+            std::vector<uint32_t> as(K.n);
+            std::vector<double> sc(K.n);
+            ck(cudaMemcpy(as.data(), assign + K.pt_off, K.n * 4, cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(sc.data(), score + K.pt_off, K.n * 8, cudaMemcpyDeviceToHost), "D2H");
+            std::vector<std::vector<uint32_t>> groups(K.k);
+            for (uint32_t p = 0; p < K.n; ++p) groups[as[p]].push_back(p);
+            for (uint32_t c = 0; c < K.k; ++c) {
+                if (!groups[c].empty()) continue;
+                double worst = INFINITY;
+                uint32_t wp = 0;
+                for (uint32_t g = 0; g < K.k; ++g) {
+                    if (groups[g].size() < 2) continue;
+                    for (uint32_t p : groups[g])
+                        if (sc[p] < worst) {
+                            worst = sc[p];
+                            wp = p;
+                        }
+                }
+                auto& donor = groups[as[wp]];
+                donor.erase(std::find(donor.begin(), donor.end(), wp));
+                as[wp] = c;
+                groups[c].push_back(wp);
+                ck(cudaMemcpy(cents + (size_t)(K.ct_off + c) * d, pts + (size_t)(K.pt_off + wp) * d, d * 4,
+                              cudaMemcpyDeviceToDevice), "repair centroid");
+            }
+            ck(cudaMemcpy(assign + K.pt_off, as.data(), K.n * 4, cudaMemcpyHostToDevice), "H2D");
+            // counts of this slot changed
+            std::vector<uint32_t> cnt(K.k);
+            for (uint32_t c = 0; c < K.k; ++c) cnt[c] = (uint32_t)groups[c].size();
+            ck(cudaMemcpy(counts.p + K.ct_off, cnt.data(), K.k * 4, cudaMemcpyHostToDevice), "H2D");
+        }
+        if (final_pass) break;
+        k_scatter<<<S, 1024, scatter_smem>>>(ks.p, assign, counts.p, off.p, members.p);
+        ck(cudaGetLastError(), "k_scatter");
+        k_mean<<<(uint32_t)((km.n_ct * 32 + 255) / 256), 256>>>(pts, ks.p, d_ct_slot.p, off.p, members.p,
+                                                                (uint32_t)km.n_ct, d, cents);
+        ck(cudaGetLastError(), "k_mean");
+    }
+    ck(cudaDeviceSynchronize(), "kmeans");
+}
+
+}  // namespace
 
 extern "C" {
-int lc_index_build(lc_index_t, const uint32_t*, const uint32_t*, const uint64_t*, double, uint32_t,
-                   uint32_t, const uint64_t*) {
-    return LC_ERUNTIME;
+
+int lc_gen_workload(lc_index_t h, uint32_t n_tokens, uint32_t n_blobs, double concentration,
+                    uint32_t query_count, double query_locality, const uint64_t* seeds, uint8_t* text_codes_out,
+                    float* queries_out) {
+    return guard([&] {
+        if (!h || !seeds) fail(LC_EINVAL, "lc_gen_workload: null argument");
+        h->set_device();
+        const Arena& a = h->a;
+        const uint32_t S = a.n_slots, d = a.d;
+        if (n_tokens < 1 || n_tokens > a.cap_tokens) fail(LC_EINVAL, "lc_gen_workload: n_tokens out of range");
+        if (n_blobs < 1 || concentration <= 0.0 || query_locality < 0.0 || query_locality > 1.0)
+            fail(LC_EINVAL, "lc_gen_workload: bad workload spec");  // WorkloadSpec::validate
+        if (d % 2) fail(LC_EINVAL, "lc_gen_workload: odd d");
+        std::vector<TokCtl> ctl((size_t)S * n_tokens);
+        std::vector<float> centers((size_t)S * n_blobs * d);
+        std::vector<uint64_t> s0(S);
+        for (uint32_t s = 0; s < S; ++s) {
+            HRng rng(seeds[s]);
+            s0[s] = rng.s0;
+            for (uint32_t b = 0; b < n_blobs; ++b) {
+                auto c = unit_gaussian(rng, d);
+                std::memcpy(&centers[((size_t)s * n_blobs + b) * d], c.data(), d * 4);
+            }
+            size_t next_marker = marker_gap(rng);
+            size_t blob = rng.next_index(n_blobs);
+            size_t run_left = 12 + rng.next_index(25);
+            for (uint32_t i = 0; i < n_tokens; ++i) {
+                if (run_left == 0) {
+                    blob = rng.next_index(n_blobs);
+                    run_left = 12 + rng.next_index(25);
+                }
+                --run_left;
+                uint8_t code = 0;
+                if (i + 1 == next_marker) {
+                    code = 1;
+                    next_marker += marker_gap(rng);
+                }
+                if (text_codes_out) text_codes_out[(size_t)s * n_tokens + i] = code;
+                ctl[(size_t)s * n_tokens + i] = TokCtl{rng.draws, (uint32_t)blob, 0};
+                rng.skip(2ull * d);  // d key gaussians + d value gaussians, in pairs
+            }
+            for (uint32_t qi = 0; qi < query_count; ++qi) {
+                std::vector<float> q;
+                if (rng.next_unit() < query_locality) {
+                    const size_t b = rng.next_index(n_blobs);
+                    q = blob_sample(rng, &centers[((size_t)s * n_blobs + b) * d], d, concentration);
+                    const double mag = std::sqrt(static_cast<double>(d));
+                    for (uint32_t j = 0; j < d; ++j) q[j] = static_cast<float>(q[j] * mag);
+                } else {
+                    auto dir = unit_gaussian(rng, d);
+                    q.resize(d);
+                    const double mag = std::sqrt(static_cast<double>(d));
+                    for (uint32_t j = 0; j < d; ++j) q[j] = static_cast<float>(dir[j] * mag);
+                }
+                if (queries_out) std::memcpy(queries_out + ((size_t)s * query_count + qi) * d, q.data(), d * 4);
+            }
+        }
+        DBuf<TokCtl> dctl(ctl.size());
+        dctl.up(ctl);
+        DBuf<float> dcent(centers.size());
+        dcent.up(centers);
+        DBuf<uint64_t> ds0(S);
+        ds0.up(s0);
+        const double scale = (1.0 / concentration) / std::sqrt((double)d);
+        k_gen<<<dim3((n_tokens + 7) / 8, S), 256>>>(a, dctl.p, dcent.p, ds0.p, n_tokens, n_blobs, scale);
+        ck(cudaGetLastError(), "k_gen");
+        ck(cudaDeviceSynchronize(), "k_gen sync");
+        std::vector<SlotState> st(S);
+        for (uint32_t s = 0; s < S; ++s) {
+            st[s] = SlotState{};
+            st[s].n_tokens = n_tokens;
+            h->hs[s].n_tokens = n_tokens;
+        }
+        ck(cudaMemcpy(a.state, st.data(), S * sizeof(SlotState), cudaMemcpyHostToDevice), "state");
+    });
 }
-int lc_gen_workload(lc_index_t, uint32_t, uint32_t, double, uint32_t, double, const uint64_t*, uint8_t*,
-                    float*) {
-    return LC_ERUNTIME;
+
+int lc_index_build(lc_index_t h, const uint32_t* n_tokens, const uint32_t* spans, const uint64_t* span_off,
+                   double avg, uint32_t max_units, uint32_t iters, const uint64_t* seeds) {
+    return guard([&] {
+        if (!h || !n_tokens || !spans || !span_off || !seeds) fail(LC_EINVAL, "lc_index_build: null argument");
+        // IndexConfig::validate (index.cpp:13-18)
+        if (avg <= 0.0) fail(LC_EINVAL, "avg_chunks_per_cluster must be positive");
+        if (max_units < 1 || iters < 1) fail(LC_EINVAL, "index config fields must be positive");
+        h->set_device();
+        Arena& a = h->a;
+        const uint32_t S = a.n_slots, d = a.d;
+        KMeans fine, coarse;
+        fine.d = coarse.d = d;
+        std::vector<uint32_t> cstart, clen, cslot;
+        std::vector<uint64_t> fseed(S), cseed(S);
+        for (uint32_t s = 0; s < S; ++s) {
+            const uint64_t b = span_off[s], e = span_off[s + 1];
+            if (e <= b) fail(LC_EINVAL, "build_index: empty spans");
+            uint32_t expect = 0;
+            for (uint64_t i = b; i < e; ++i) {
+                const uint32_t st = spans[4 * i], en = spans[4 * i + 1];
+                if (st != expect || en <= st || en > n_tokens[s]) fail(LC_EINVAL, "build_index: spans do not tile the stream");
+                expect = en;
+                cstart.push_back(st);
+                clen.push_back(en - st);
+                cslot.push_back(s);
+            }
+            if (expect != n_tokens[s]) fail(LC_EINVAL, "build_index: spans do not cover the stream");
+            if (n_tokens[s] > a.cap_tokens) fail(LC_EINVAL, "build_index: n_tokens exceeds capacity");
+            const uint32_t m = (uint32_t)(e - b);
+            // fine_cluster_count / coarse_unit_count (index.cpp:145-153)
+            const uint32_t l = std::max<uint32_t>(1, (uint32_t)std::ceil((double)m / avg));
+            const uint32_t root = (uint32_t)std::ceil(std::sqrt((double)l));
+            const uint32_t p = std::min<uint32_t>(max_units, std::max<uint32_t>(1, root));
+            if (m > a.cap_chunks || l > a.cap_clusters || p > a.cap_units)
+                fail(LC_EINVAL, "build_index: index exceeds engine capacity");
+            if (l > m) fail(LC_EINVAL, "spherical_kmeans: k exceeds point count");
+            fine.ks.push_back(KSlot{m, l, (uint32_t)fine.n_pts, (uint32_t)fine.n_ct});
+            coarse.ks.push_back(KSlot{l, p, (uint32_t)fine.n_ct, (uint32_t)coarse.n_ct});
+            fine.n_pts += m;
+            fine.n_ct += l;
+            coarse.n_pts += l;
+            coarse.n_ct += p;
+            fseed[s] = seeds[s];
+            cseed[s] = seeds[s] + 1;
+        }
+        const uint32_t M = (uint32_t)fine.n_pts;
+        DBuf<uint32_t> dcs(M), dcl(M), dcslot(M), err(1);
+        dcs.up(cstart);
+        dcl.up(clen);
+        dcslot.up(cslot);
+        ck(cudaMemset(err.p, 0, 4), "memset");
+        DBuf<float> reps((size_t)M * d);
+        k_reps<<<(M * 32 + 255) / 256, 256>>>(a, dcs.p, dcl.p, dcslot.p, M, h->desc.pooling, reps.p, err.p);
+        ck(cudaGetLastError(), "k_reps");
+        if (err.down(1)[0]) fail(LC_ERUNTIME, "chunk_representative: pooled key has zero norm");
+        // tier 1: fine clusters over chunk reps
+        DBuf<float> fcent(fine.n_ct * d);
+        DBuf<uint32_t> fassign(M);
+        DBuf<double> fscore(M);
+        run_kmeans(fine, reps.p, fcent.p, fassign.p, fscore.p, fseed, iters);
+        DBuf<uint32_t> fpt_slot(M);
+        fpt_slot.up(cslot);
+        DBuf<unsigned long long> frad(fine.n_ct);
+        ck(cudaMemset(frad.p, 0, fine.n_ct * 8), "memset");
+        DBuf<KSlot> dfks(S), dcks(S);
+        dfks.up(fine.ks);
+        dcks.up(coarse.ks);
+        k_radius<<<(M + 255) / 256, 256>>>(reps.p, dfks.p, fpt_slot.p, M, fassign.p, nullptr, nullptr, fcent.p, d,
+                                           frad.p);
+        ck(cudaGetLastError(), "k_radius");
+        // tier 2: coarse units over fine centroids (seed + 1)
+        DBuf<float> ccent(coarse.n_ct * d);
+        DBuf<uint32_t> cassign(fine.n_ct);
+        DBuf<double> cscore(fine.n_ct);
+        run_kmeans(coarse, fcent.p, ccent.p, cassign.p, cscore.p, cseed, iters);
+        DBuf<unsigned long long> crad(coarse.n_ct);
+        ck(cudaMemset(crad.p, 0, coarse.n_ct * 8), "memset");
+        // coarse radii over descendant chunk reps (index.cpp:222-234)
+        k_radius<<<(M + 255) / 256, 256>>>(reps.p, dfks.p, fpt_slot.p, M, fassign.p, dcks.p, cassign.p, ccent.p, d,
+                                           crad.p);
+        ck(cudaGetLastError(), "k_radius coarse");
+        ck(cudaDeviceSynchronize(), "build");
+        // assemble each slot's HierarchicalIndex and upload it (K/V stay resident)
+        auto h_fa = fassign.down(M);
+        auto h_ca = cassign.down(fine.n_ct);
+        auto h_fc = fcent.down(fine.n_ct * d);
+        auto h_cc = ccent.down(coarse.n_ct * d);
+        auto h_fr = frad.down(fine.n_ct);
+        auto h_cr = crad.down(coarse.n_ct);
+        for (uint32_t s = 0; s < S; ++s) {
+            const KSlot F = fine.ks[s], Cc = coarse.ks[s];
+            const uint32_t m = F.n, l = F.k, p = Cc.k;
+            std::vector<uint32_t> span4((size_t)m * 4), coc(m), fmo(l + 1, 0), fmem(m), fpar(l), cmo(p + 1, 0),
+                cmem(l);
+            std::vector<uint64_t> ftok(l, 0);
+            std::vector<double> frd(l), crd(p);
+            for (uint32_t j = 0; j < m; ++j) {
+                for (int k = 0; k < 4; ++k) span4[4 * j + k] = spans[4 * (span_off[s] + j) + k];
+                coc[j] = h_fa[F.pt_off + j];
+                ftok[coc[j]] += clen[F.pt_off + j];
+                ++fmo[coc[j] + 1];
+            }
+            for (uint32_t c = 0; c < l; ++c) fmo[c + 1] += fmo[c];
+            {
+                std::vector<uint32_t> cur(fmo.begin(), fmo.end() - 1);
+                for (uint32_t j = 0; j < m; ++j) fmem[cur[coc[j]]++] = j;
+            }
+            for (uint32_t c = 0; c < l; ++c) {
+                fpar[c] = h_ca[Cc.pt_off + c];
+                ++cmo[fpar[c] + 1];
+                unsigned long long r = h_fr[F.ct_off + c];
+                std::memcpy(&frd[c], &r, 8);
+            }
+            for (uint32_t u = 0; u < p; ++u) {
+                cmo[u + 1] += cmo[u];
+                unsigned long long r = h_cr[Cc.ct_off + u];
+                std::memcpy(&crd[u], &r, 8);
+            }
+            {
+                std::vector<uint32_t> cur(cmo.begin(), cmo.end() - 1);
+                for (uint32_t c = 0; c < l; ++c) cmem[cur[fpar[c]]++] = c;
+            }
+            lc_host_index ix{};
+            ix.dim = d;
+            ix.n_chunks = m;
+            ix.n_clusters = l;
+            ix.n_units = p;
+            ix.chunk_span = span4.data();
+            ix.chunk_rep = nullptr;
+            ix.fine_centroid = h_fc.data() + (size_t)F.ct_off * d;
+            ix.fine_radius = frd.data();
+            ix.fine_token_count = ftok.data();
+            ix.fine_parent = fpar.data();
+            ix.fine_member_off = fmo.data();
+            ix.fine_members = fmem.data();
+            ix.coarse_centroid = h_cc.data() + (size_t)Cc.ct_off * d;
+            ix.coarse_radius = crd.data();
+            ix.coarse_member_off = cmo.data();
+            ix.coarse_members = cmem.data();
+            ix.cluster_of_chunk = coc.data();
+            const int rc = lc_index_upload_slot(h, s, &ix, nullptr, nullptr, n_tokens[s]);
+            if (rc != LC_OK) fail(rc, std::string("build upload: ") + lc_last_error());
+            if (a.keep_reps)
+                ck(cudaMemcpy(a.chunk_rep + (size_t)s * a.cap_chunks * d, reps.p + (size_t)F.pt_off * d,
+                              (size_t)m * d * 4, cudaMemcpyDeviceToDevice),
+                   "reps D2D");
+        }
+    });
 }
-}
+
+}  // extern "C"

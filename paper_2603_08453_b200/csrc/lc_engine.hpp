@@ -1,0 +1,102 @@
+// Internal engine definition shared by the ABI translation units.
+#pragma once
+
+#include "../../include/lychee_b200.h"
+#include "lc_common.cuh"
+
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace lc {
+size_t select_smem_bytes(const Arena& a);
+cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
+                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
+                          cudaStream_t stream);
+cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
+                           const uint32_t* buf_ids, cudaStream_t stream);
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream);
+cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
+cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
+                         cudaStream_t stream);
+}  // namespace lc
+
+namespace lcx {
+
+inline thread_local std::string g_err;
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Status(code, msg); }
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(LC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return LC_OK;
+    } catch (const Status& s) {
+        g_err = s.what();
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return LC_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LC_ERUNTIME;
+    }
+}
+
+template <typename T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(LC_ENOMEM, std::string("cudaMalloc ") + std::to_string(n * sizeof(T)) + " B: " +
+                            cudaGetErrorString(e));
+    }
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+
+}  // namespace lcx
+
+using namespace lc;
+using namespace lcx;
+
+struct HostSlot {
+    uint32_t n_tokens = 0, chunked_end = 0, n_chunks = 0, L = 0, P = 0;
+    bool loaded = false;
+    std::vector<uint32_t> kind, level;   // per chunk (host-only fields of ChunkSpan)
+    std::vector<float> rep;              // prefill reps when the device keeps none
+    std::vector<uint32_t> fanout;        // n_u per unit (fixed after build)
+};
+
+struct lc_index_s {
+    lc_index_desc desc{};
+    Arena a{};
+    std::vector<void*> owned;
+    std::vector<HostSlot> hs;
+    float* q_stage = nullptr;    // device staging for lc_retrieve_host
+    float* out_stage = nullptr;
+    uint32_t* take_dev = nullptr;
+    lc_graft_report* rep_scratch = nullptr;
+    uint32_t last_flags = 0;
+    uint32_t last_valid = 0;
+    std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
+
+    ~lc_index_s() {
+        for (void* p : owned) cudaFree(p);
+    }
+    void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
+};
+

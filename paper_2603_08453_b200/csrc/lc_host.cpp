@@ -6,6 +6,7 @@
 // grafts the same span on the device.
 #include "../../include/lychee_b200.h"
 
+#include <algorithm>
 #include <cstring>
 #include <optional>
 #include <string>
@@ -123,6 +124,18 @@ int lc_segment(const char* const* texts, uint32_t n, uint32_t min_len, uint32_t 
     *n_spans = v.size() / 4;
     if (spans4) std::memcpy(spans4, v.data(), std::min<uint64_t>(cap * 4, v.size()) * 4);
     return LC_OK;
+}
+
+int lc_segment_packed(const char* buf, const uint64_t* offs, uint32_t n, uint32_t min_len, uint32_t max_len,
+                      uint32_t* spans4, uint64_t cap, uint64_t* n_spans) {
+    if (!buf || !offs || !n_spans) return LC_EINVAL;
+    std::vector<std::string> store(n);
+    std::vector<const char*> ptrs(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        store[i].assign(buf + offs[i], buf + offs[i + 1]);
+        ptrs[i] = store[i].c_str();
+    }
+    return lc_segment(ptrs.data(), n, min_len, max_len, spans4, cap, n_spans);
 }
 
 int lc_flush_take(const char* const* buffer_texts, uint32_t n, uint32_t structure_aware, uint32_t min_len,
