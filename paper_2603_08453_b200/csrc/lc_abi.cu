@@ -44,6 +44,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         if (d.n_slots == 0 || d.dim == 0 || d.group == 0 || d.group > (uint32_t)kMaxGroup)
             fail(LC_EINVAL, "lc_index_create: need n_slots >= 1, dim >= 1, 1 <= group <= 8");
         if (d.dim != 64 && d.dim != 128) fail(LC_EINVAL, "lc_index_create: dim must be 64 or 128");
+        if (d.dim % 4) fail(LC_EINVAL, "lc_index_create: dim must be a multiple of 4");
         if (d.dim > 256) fail(LC_EINVAL, "lc_index_create: dim > 256");
         if (d.cap_units == 0 || d.cap_units > 1024) fail(LC_EINVAL, "lc_index_create: 1 <= cap_units <= 1024");
         if (d.cap_tokens == 0 || d.cap_chunks == 0 || d.cap_clusters == 0)
@@ -175,7 +176,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
             for (uint32_t i = 0; i < nu; ++i) {
                 const uint32_t f = orig[base + i];
                 for (uint32_t j = 0; j < D; ++j)
-                    fcent[(size_t)base * D + (size_t)j * nu + i] = ix->fine_centroid[(size_t)f * D + j];
+                    fcent[fine_at(base, nu, i, j, D)] = ix->fine_centroid[(size_t)f * D + j];
             }
             for (uint32_t j = 0; j < D; ++j) ucent[(size_t)j * a.cap_units + u] = ix->coarse_centroid[(size_t)u * D + j];
             urad[u] = ix->coarse_radius[u];
@@ -307,7 +308,7 @@ int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
             for (uint32_t i = 0; i < nu; ++i) {
                 const uint32_t f = orig[base + i];
                 for (uint32_t j = 0; j < D; ++j)
-                    ix->fine_centroid[(size_t)f * D + j] = fcent[(size_t)base * D + (size_t)j * nu + i];
+                    ix->fine_centroid[(size_t)f * D + j] = fcent[fine_at(base, nu, i, j, D)];
             }
             for (uint32_t j = 0; j < D; ++j) ix->coarse_centroid[(size_t)u * D + j] = ucent[(size_t)j * a.cap_units + u];
             ix->coarse_radius[u] = urad[u];

@@ -2,15 +2,18 @@
 // (north star item 3): kernels::attention (kernels.cpp:108-144) for every query
 // head of a GQA group at once, over the union of the group's active spans.
 //
-// Each KV row of the union is read from HBM exactly once per slot: a 16-token
-// group is loaded straight into mma.sync fragments (16-byte loads, every byte
-// used), QK^T and PV run on the tensor cores with fp32 accumulation, and a
-// per-token query mask removes (query, token) pairs outside that head's own
-// active set.  Precision: q and the softmax weights are split into bf16
-// hi + lo halves (hi in MMA rows 0..G-1, lo in rows 8..8+G-1), so products
-// carry ~16 mantissa bits on top of the exact bf16 K/V; accumulation is fp32.
-// Partials (m, l, o) per CTA are merged with log-sum-exp by the last CTA of
-// each slot.
+// Data movement: each warp streams 16-token groups of gathered K/V rows into
+// a private 3-stage shared-memory ring with cp.async (16-byte requests, every
+// byte used; each KV row of the union is read from HBM exactly once per
+// slot), so two groups are in flight while the third is computed.  The ring
+// is XOR-swizzled so the fragment reads below are bank-conflict free.
+//
+// Math: QK^T and PV on the tensor cores (mma.sync m16n8k16, bf16 in, fp32
+// accumulate) with q and the softmax weights split into bf16 hi + lo halves
+// (hi in MMA rows 0..G-1, lo in rows 8..8+G-1): products carry ~16 mantissa
+// bits over the exact bf16 K/V.  A per-token query mask removes (query, token)
+// pairs outside that head's own active set.  Partials (m, l, o) per CTA are
+// merged with log-sum-exp by the last CTA of each slot.
 //
 // Fragment maps for mma.m16n8k16 (lane = 4r + c):
 //   QK: B = K^T, thread (r, c) holds token r (and 8 + r) dims [c*D/4, c*D/4 + D/4),
@@ -31,7 +34,9 @@ struct AttendParams {
 };
 
 constexpr int kAttThreads = 128;
-constexpr int kWindow = 1024;  // tokens expanded into shared memory at a time
+constexpr int kAttWarps = kAttThreads / 32;
+constexpr int kStages = 3;
+constexpr int kWindow = 512;  // tokens expanded into shared memory at a time
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
@@ -52,34 +57,51 @@ __device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
     lo = x - hi;
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+                 : "r"(saddr));
     return r;
 }
 
+// 16-byte chunk k (0..D/8-1) of staged row `row` -> physical chunk: an XOR
+// swizzle that makes both fragment read patterns conflict-free (D = 128)
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t k) {
+    return k ^ ((k >> 3) << 1) ^ (row & 7) ^ ((row >> 1) & 1);
+}
+
 template <int D>
-__global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
-    static_assert(D % 64 == 0 && D <= 128, "D must be 64 or 128");
-    constexpr int KS = D / 16;   // k-steps of QK
-    constexpr int KW = D / 32;   // uint4 per thread per K row
-    constexpr int NT = D / 8;    // n-tiles of PV
-    constexpr int VW = D / 64;   // uint4 per thread per V row
+__global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
+    static_assert(D == 64 || D == 128, "D must be 64 or 128");
+    constexpr int KS = D / 16;             // k-steps of QK
+    constexpr int KW = D / 32;             // 16-byte chunks per thread per K row
+    constexpr int NT = D / 8;              // n-tiles of PV
+    constexpr int VW = D / 64;             // 16-byte chunks per thread per V row
+    constexpr int ROWB = D * 2;            // bytes per K/V row
+    constexpr int STAGE = 32 * ROWB;       // 16 K rows + 16 V rows
     const Arena& a = p.a;
     const uint32_t slot = blockIdx.y, split = blockIdx.x, S = gridDim.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
     const uint32_t G = a.G;
 
+    extern __shared__ __align__(128) unsigned char dsm[];
+    unsigned char* ring = dsm + (size_t)warp * kStages * STAGE;  // this warp's stages
     __shared__ uint32_t s_row[kWindow];
     __shared__ uint8_t s_msk[kWindow];
     __shared__ uint32_t s_sstart[kWindow + 1];
     __shared__ uint32_t s_slm[kWindow + 1];
     __shared__ uint32_t s_soff[kWindow + 2];
     __shared__ uint32_t s_lohi[2];
-    __shared__ float s_m[4][kMaxGroup], s_l[4][kMaxGroup];
-    __shared__ float s_o[4][kMaxGroup][D];
+    __shared__ float s_m[kAttWarps][kMaxGroup], s_l[kAttWarps][kMaxGroup];
     __shared__ uint32_t s_last;
 
     const uint32_t ns = a.n_spans[slot];
@@ -88,8 +110,9 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
     const uint32_t tot = soff[ns];
     const uint32_t beg = (uint32_t)(((unsigned long long)tot * split) / S);
     const uint32_t end = (uint32_t)(((unsigned long long)tot * (split + 1)) / S);
-    const __nv_bfloat16* Ks = a.K + kv_off(a, slot);
-    const __nv_bfloat16* Vs = a.V + kv_off(a, slot);
+    const unsigned char* Kb = reinterpret_cast<const unsigned char*>(a.K + kv_off(a, slot));
+    const unsigned char* Vb = reinterpret_cast<const unsigned char*>(a.V + kv_off(a, slot));
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
 
     // q fragments: softmax scale and log2(e) folded in, bf16 hi (row r) + lo (row r+8)
     uint32_t qf[KS][4];
@@ -113,15 +136,32 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     float m_run = -INFINITY, l_run = 0.f;
 
+    // cp.async of one 16-token group into stage `st`: each 8-lane quarter-warp
+    // copies one contiguous 128-byte half row, so every request is a full line
+    auto issue = [&](uint32_t t0, uint32_t wn, int st) {
+        const uint32_t sbase = ring_s + (uint32_t)st * STAGE;
+        constexpr int HALVES = ROWB / 128;         // 128-byte segments per row
+        constexpr int SEGS = 16 * HALVES;           // segments per 16 rows
+#pragma unroll
+        for (int e = 0; e < SEGS / 4; ++e) {
+            const uint32_t id = 4u * e + ((uint32_t)lane >> 3);
+            const uint32_t row = id / HALVES, half = id % HALVES;
+            const uint32_t k = half * 8 + ((uint32_t)lane & 7);  // 16-byte chunk of the row
+            const uint32_t tk = t0 + row;
+            const uint32_t src_row = tk < wn ? s_row[tk] : s_row[0];
+            cp_async16(sbase + row * ROWB + swz(row, k) * 16, Kb + (size_t)src_row * ROWB + k * 16);
+            cp_async16(sbase + 16 * ROWB + row * ROWB + swz(row, k) * 16, Vb + (size_t)src_row * ROWB + k * 16);
+        }
+    };
+
     for (uint32_t wb = beg; wb < end; wb += kWindow) {
         const uint32_t we = min(end, wb + kWindow), wn = we - wb;
-        // spans covering [wb, we): last span with off <= wb .. last span with off < we
+        // spans covering [wb, we): last span with off <= wb .. last span with off <= we-1
         if (warp == 0) {
             for (int which = 0; which < 2; ++which) {
                 const uint32_t target = which == 0 ? wb : we - 1;
-                uint32_t lo = 0, hi = ns;  // find last k with soff[k] <= target
+                uint32_t lo = 0, hi = ns;
                 while (hi - lo > 1) {
-                    // 32-ary search step
                     const uint32_t step = (hi - lo + 31) / 32;
                     const uint32_t probe = lo + (uint32_t)lane * step;
                     const bool ok = probe < hi && soff[probe] <= target;
@@ -163,38 +203,35 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
         }
         __syncthreads();
 
+        // this warp's groups: grp = warp, warp + 4, ...
         const uint32_t ngrp = (wn + 15) / 16;
-        for (uint32_t grp = warp; grp < ngrp; grp += 4) {
-            const uint32_t t0 = grp * 16;
-            // ---- loads (every byte of the 16 rows is used exactly once) ----
-            uint4 kr[2][KW];
-            uint4 vr[4][VW];
+        const uint32_t my_n = ngrp > (uint32_t)warp ? (ngrp - warp + kAttWarps - 1) / kAttWarps : 0u;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const uint32_t row = s_row[t0 + 8 * nt + r];
-                const uint4* kp = reinterpret_cast<const uint4*>(Ks + (size_t)row * D + c * (D / 4));
-#pragma unroll
-                for (int w = 0; w < KW; ++w) kr[nt][w] = ldg_stream(kp + w);
+        for (int st = 0; st < kStages - 1; ++st) {
+            if ((uint32_t)st < my_n) issue((warp + st * kAttWarps) * 16, wn, st);
+            cp_commit();
+        }
+        for (uint32_t it = 0; it < my_n; ++it) {
+            {
+                const uint32_t nxt = it + kStages - 1;
+                if (nxt < my_n) issue((warp + nxt * kAttWarps) * 16, wn, (int)(nxt % kStages));
+                cp_commit();
             }
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const uint32_t tk = (x >> 1) * 8 + 2 * c + (x & 1);
-                const uint32_t row = s_row[t0 + tk];
-                const uint4* vp = reinterpret_cast<const uint4*>(Vs + (size_t)row * D + r * (D / 8));
-#pragma unroll
-                for (int w = 0; w < VW; ++w) vr[x][w] = ldg_stream(vp + w);
-            }
+            cp_wait<kStages - 1>();
+            __syncwarp();
+            const uint32_t t0 = (warp + it * kAttWarps) * 16;
+            const uint32_t sb = ring_s + (uint32_t)(it % kStages) * STAGE;
             // ---- S = Q K^T (hi rows r, lo rows r+8) ----
             float sc[2][4];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
                 sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+                const uint32_t row = 8 * nt + r;
 #pragma unroll
-                for (int s = 0; s < KS; ++s) {
-                    const uint4 kv = kr[nt][s >> 1];
-                    const uint32_t b0 = (s & 1) ? kv.z : kv.x;
-                    const uint32_t b1 = (s & 1) ? kv.w : kv.y;
-                    mma16816(sc[nt], qf[s], b0, b1);
+                for (int w = 0; w < KW; ++w) {
+                    const uint4 kv = lds128(sb + row * ROWB + swz(row, c * KW + w) * 16);
+                    mma16816(sc[nt], qf[2 * w], kv.x, kv.y);
+                    mma16816(sc[nt], qf[2 * w + 1], kv.z, kv.w);
                 }
             }
             // logits of query r for tokens 2c, 2c+1 (nt 0) and 8+2c, 9+2c (nt 1)
@@ -245,22 +282,35 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
                 pa[1] = pack_bf16(l[0], l[1]);
                 pa[3] = pack_bf16(l[2], l[3]);
             }
+            const uint32_t vb = sb + 16 * ROWB;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
-                const int w = j >> 3, word = (j >> 1) & 3;
-                const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
-                auto wd = [&](const uint4& u) -> uint32_t {
-                    return word == 0 ? u.x : word == 1 ? u.y : word == 2 ? u.z : u.w;
-                };
-                const uint32_t b0 = __byte_perm(wd(vr[0][w]), wd(vr[1][w]), sel);
-                const uint32_t b1 = __byte_perm(wd(vr[2][w]), wd(vr[3][w]), sel);
-                mma16816(acc[j], pa, b0, b1);
+            for (int w = 0; w < VW; ++w) {
+                uint4 vr[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const uint32_t row = (x >> 1) * 8 + 2 * c + (x & 1);
+                    vr[x] = lds128(vb + row * ROWB + swz(row, r * VW + w) * 16);
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = w * 8 + jj, word = jj >> 1;
+                    const uint32_t sel = (jj & 1) ? 0x7632u : 0x5410u;
+                    auto wd = [&](const uint4& u) -> uint32_t {
+                        return word == 0 ? u.x : word == 1 ? u.y : word == 2 ? u.z : u.w;
+                    };
+                    const uint32_t b0 = __byte_perm(wd(vr[0]), wd(vr[1]), sel);
+                    const uint32_t b1 = __byte_perm(wd(vr[2]), wd(vr[3]), sel);
+                    mma16816(acc[j], pa, b0, b1);
+                }
             }
+            __syncwarp();  // the stage is refilled by the next iteration's issue
         }
+        cp_wait<0>();
         __syncthreads();
     }
 
-    // ---- warp partial -> CTA partial ----
+    // ---- warp partial -> CTA partial (the stage ring is free now) ----
+    float* s_o = reinterpret_cast<float*>(dsm);  // [warps][G][D]
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     if (r < (int)G) {
@@ -268,10 +318,11 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
             s_m[warp][r] = m_run;
             s_l[warp][r] = l_run;
         }
+        float* o = s_o + ((size_t)warp * G + r) * D + c * (D / 4);
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-            s_o[warp][r][c * (D / 4) + j] = acc[j][0] + acc[j][2];
-            s_o[warp][r][c * (D / 4) + D / 8 + j] = acc[j][1] + acc[j][3];
+            o[j] = acc[j][0] + acc[j][2];
+            o[D / 8 + j] = acc[j][1] + acc[j][3];
         }
     }
     __syncthreads();
@@ -279,12 +330,12 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
     for (uint32_t x = tid; x < G * D; x += blockDim.x) {
         const uint32_t g = x / D, dd = x % D;
         float M = -INFINITY;
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][g]);
+        for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, s_m[w][g]);
         float o = 0.f, L = 0.f;
         if (M != -INFINITY)
-            for (int w = 0; w < 4; ++w) {
+            for (int w = 0; w < kAttWarps; ++w) {
                 const float f = exp2f(s_m[w][g] - M);
-                o += f * s_o[w][g][dd];
+                o += f * s_o[((size_t)w * G + g) * D + dd];
                 L += f * s_l[w][g];
             }
         part[g * (D + 2) + 2 + dd] = o;
@@ -325,13 +376,27 @@ __global__ void __launch_bounds__(kAttThreads) k_attend(AttendParams p) {
     if (tid == 0) a.counters[slot] = 0;
 }
 
+template <int D>
+static cudaError_t launch_attend_d(const AttendParams& p, dim3 grid, cudaStream_t stream) {
+    constexpr size_t ring = (size_t)kAttWarps * kStages * 32 * D * 2;
+    constexpr size_t outb = (size_t)kAttWarps * kMaxGroup * D * 4;
+    constexpr size_t smem = ring > outb ? ring : outb;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_attend<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    k_attend<D><<<grid, kAttThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream) {
     AttendParams p{a, q, out};
     dim3 grid(a.splits, a.n_slots);
-    if (a.d == 128) k_attend<128><<<grid, kAttThreads, 0, stream>>>(p);
-    else if (a.d == 64) k_attend<64><<<grid, kAttThreads, 0, stream>>>(p);
-    else return cudaErrorInvalidValue;
-    return cudaGetLastError();
+    if (a.d == 128) return launch_attend_d<128>(p, grid, stream);
+    if (a.d == 64) return launch_attend_d<64>(p, grid, stream);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace lc

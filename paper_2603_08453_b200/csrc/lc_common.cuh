@@ -12,8 +12,10 @@
 //   unit_off    u32  [slot][cap_units+1]             CoarseUnit::members as a range of
 //                                                    internal fine ids
 //   fcent       f32  [slot][cap_clusters*d]          FineCluster::centroid; the members of
-//                                                    unit u form one block [d][n_u]
-//                                                    (dimension-major) at unit_off[u]*d
+//                                                    unit u form one block [d/4][n_u][4]
+//                                                    (dimension-quad-major: a warp reads a
+//                                                    float4 per cluster per step, 512 B
+//                                                    contiguous) at unit_off[u]*d
 //   frad        f64  [slot][cap_clusters]            FineCluster::radius
 //   ftok        u32  [slot][cap_clusters]            FineCluster::token_count
 //   forig       u32  [slot][cap_clusters]            reference cluster id of internal id
@@ -89,6 +91,12 @@ struct Arena {
 };
 
 __host__ __device__ inline uint32_t bit_words(uint32_t n) { return (n + 31) / 32; }
+
+// element (member `local` of the unit block starting at internal id `base` with
+// `nu` members, dimension j) of the fine-centroid array
+__host__ __device__ inline size_t fine_at(uint32_t base, uint32_t nu, uint32_t local, uint32_t j, uint32_t d) {
+    return (size_t)base * d + ((size_t)(j >> 2) * nu + local) * 4 + (j & 3);
+}
 
 __host__ __device__ inline size_t kv_off(const Arena& a, uint32_t slot) {
     return (size_t)slot * a.cap_tokens * a.d;

@@ -144,9 +144,8 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
             double bs2 = -INFINITY;
             uint32_t bc = 0xffffffffu;
             for (uint32_t i = tid; i < nu; i += blockDim.x) {
-                const float* col = fc + (size_t)lo * d + i;
                 double s = 0.0;
-                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)col[(size_t)j * nu], s);
+                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)fc[fine_at(lo, nu, i, j, d)], s);
                 argmax_merge(bs2, bc, s, lo + i);  // stored order == internal order
             }
             block_argmax(bs2, bc, ws, wk);
@@ -160,9 +159,8 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         for (uint32_t u = 0; u < P; ++u) {
             const uint32_t lo = uoff[u], nu = uoff[u + 1] - lo;
             for (uint32_t i = tid; i < nu; i += blockDim.x) {
-                const float* col = fc + (size_t)lo * d + i;
                 double s = 0.0;
-                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)col[(size_t)j * nu], s);
+                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)fc[fine_at(lo, nu, i, j, d)], s);
                 argmax_merge(bs, bo, s, fo[lo + i]);  // full scan order = reference ids
             }
         }
@@ -181,10 +179,10 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     uint32_t* fnmem = a.fnmem + (size_t)slot * a.cap_clusters;
     const uint32_t u = funit[best_c];
     const uint32_t lo = uoff[u], nu = uoff[u + 1] - lo, local = best_c - lo;
-    float* col = a.fcent + (size_t)slot * a.cap_clusters * d + (size_t)lo * d + local;
+    float* fcw = a.fcent + (size_t)slot * a.cap_clusters * d;
     const double n = (double)fnmem[best_c];
     for (uint32_t j = tid; j < d; j += blockDim.x) {
-        const float mu = col[(size_t)j * nu];
+        const float mu = fcw[fine_at(lo, nu, local, j, d)];
         s_mu[j] = mu;
         s_moved[j] = __dadd_rn(__dmul_rn(n, (double)mu), (double)s_rep[j]);
     }
@@ -217,7 +215,7 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         else s_dg = r;
     }
     __syncthreads();
-    for (uint32_t j = tid; j < d; j += blockDim.x) col[(size_t)j * nu] = s_new[j];
+    for (uint32_t j = tid; j < d; j += blockDim.x) fcw[fine_at(lo, nu, local, j, d)] = s_new[j];
     const uint32_t cid = M;
     if (a.keep_reps) {
         float* rp = a.chunk_rep + ((size_t)slot * a.cap_chunks + cid) * d;

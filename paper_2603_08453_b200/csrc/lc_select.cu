@@ -1,5 +1,6 @@
 // Fused scoring + pruning + selection (north star item 2) and active-set
-// construction.  One CTA per query head (slot, g).
+// construction.  k_select: one CTA per query head (slot, g); k_compact: one
+// CTA per slot (all query heads of the GQA group at once).
 //
 // Exactness (bit-identical to the reference's fp64 CPU path):
 //  * kernels::dot (kernels.cpp:13-17) is a sequential fp64 sum of exact
@@ -11,8 +12,10 @@
 //    greedy token-budget fill is a prefix of that order that stops at the
 //    first overflow and always admits one cluster (retriever.cpp:142-154).
 //    We find that prefix with an exact weighted radix select over the
-//    orderable 64-bit image of the fp64 score, resolve exact-score ties by
-//    reference id, and only sort the (small) selected set.
+//    orderable 64-bit image of the fp64 score (starting below the bits every
+//    candidate shares, stopping as soon as the boundary bucket holds one
+//    candidate), resolve exact-score ties by reference id, and sort only the
+//    (small) selected set.
 #include "lc_common.cuh"
 
 namespace lc {
@@ -25,6 +28,7 @@ struct SelectParams {
 };
 
 constexpr int kSelThreads = 256;
+constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kMaxUnitTopk = 64;
 
 __device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ia,
@@ -32,17 +36,17 @@ __device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ia,
     return ka < kb || (ka == kb && ia < ib);
 }
 
-// Dynamic shared memory layout of k_select:
+// Dynamic shared memory of k_select:
 //   float  qs[d]
 //   u64    ukey[cap_units]
-//   u64    ckey[max_cand]
-//   u32    cw[max_cand]     weight (token_count, or 1 in fixed-k mode)
-//   u32    cid[max_cand]    internal fine id
-//   u32    sel[max_cand]    compacted selected candidate indices
+//   u64    ckey[max_cand]     candidate keys (ascending key == descending UB)
+//   u32    cw[max_cand]       weight (token_count, or 1 in fixed-k mode);
+//                             reused as the selected-index list afterwards
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Arena& a = p.a;
     const uint32_t slot = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+    const uint32_t lane = tid & 31, warp = tid >> 5;
     const uint32_t d = a.d;
     const SlotState st = a.state[slot];
     QInfo* qi = a.qinfo + (size_t)slot * a.G + g;
@@ -68,21 +72,20 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         reinterpret_cast<unsigned long long*>(smem + ((d * 4 + 15) & ~15u));
     unsigned long long* ckey = ukey + a.cap_units;
     uint32_t* cw = reinterpret_cast<uint32_t*>(ckey + a.max_cand);
-    uint32_t* cid = cw + a.max_cand;
-    uint32_t* sel = cid + a.max_cand;
 
     __shared__ double s_qnorm;
     __shared__ uint32_t s_kept[kMaxUnitTopk];
     __shared__ uint32_t s_pre[kMaxUnitTopk + 1];
-    __shared__ unsigned long long hw[256];
-    __shared__ uint32_t hc[256];
+    __shared__ uint32_t s_base[kMaxUnitTopk], s_nu[kMaxUnitTopk];
+    __shared__ uint32_t hw[256], hc[256];
+    __shared__ unsigned long long s_min[kSelWarps], s_max[kSelWarps];
     __shared__ unsigned long long s_prefix, s_mask, s_wbefore;
-    __shared__ uint32_t s_cbefore, s_state, s_nsel, s_err;
+    __shared__ uint32_t s_cbefore, s_state, s_nsel;
+    __shared__ int s_shift;
 
     const float* qg = p.q + ((size_t)slot * a.G + g) * d;
     for (uint32_t j = tid; j < d; j += blockDim.x) qs[j] = qg[j];
     for (uint32_t w = tid; w < nwords; w += blockDim.x) bits[w] = 0u;
-    if (tid == 0) s_err = 0;
     __syncthreads();
 
     // ||q|| (kernels.cpp:19-23): sequential, exact products -> DFMA chain
@@ -91,23 +94,27 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)qs[j], (double)qs[j], s);
         s_qnorm = __dsqrt_rn(s);
     }
-    // tier 1: coarse units (retriever.cpp:100-112), dimension-major centroids
+    // tier 1: coarse units (retriever.cpp:100-112), dimension-major centroids;
+    // warp 0 is busy with ||q||, the coarse rows go to warps 1..7
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
     const double* ur = a.urad + (size_t)slot * a.cap_units;
-    double udot[4];
-    for (uint32_t k = 0; k < 4; ++k) {
-        const uint32_t u = tid + k * blockDim.x;
+    double udot[5];
+    const uint32_t ct = tid >= 32 ? tid - 32 : 0xffffffffu;
+#pragma unroll
+    for (uint32_t k = 0; k < 5; ++k) {
+        const uint32_t u = ct + k * (kSelThreads - 32);
         double s = 0.0;
-        if (u < st.P)
+        if (ct != 0xffffffffu && u < st.P)
             for (uint32_t j = 0; j < d; ++j)
-                s = __fma_rn((double)qs[j], (double)uc[(size_t)j * a.cap_units + u], s);
+                s = __fma_rn((double)qs[j], (double)__ldg(uc + (size_t)j * a.cap_units + u), s);
         udot[k] = s;
     }
     __syncthreads();
     const double qnorm = s_qnorm;
-    for (uint32_t k = 0; k < 4; ++k) {
-        const uint32_t u = tid + k * blockDim.x;
-        if (u < st.P) ukey[u] = desc_key(__dadd_rn(udot[k], __dmul_rn(qnorm, ur[u])));
+#pragma unroll
+    for (uint32_t k = 0; k < 5; ++k) {
+        const uint32_t u = ct + k * (kSelThreads - 32);
+        if (ct != 0xffffffffu && u < st.P) ukey[u] = desc_key(__dadd_rn(udot[k], __dmul_rn(qnorm, ur[u])));
     }
     __syncthreads();
     // select_topk(units, unit_topk): rank by counting over (score desc, id asc)
@@ -125,7 +132,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         for (uint32_t k = 0; k < kU; ++k) {
             s_pre[k] = acc;
             const uint32_t u = s_kept[k];
-            acc += uoff[u + 1] - uoff[u];
+            s_base[k] = uoff[u];
+            s_nu[k] = uoff[u + 1] - uoff[u];
+            acc += s_nu[k];
         }
         s_pre[kU] = acc;
     }
@@ -143,34 +152,72 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         return;
     }
 
-    // tier 2: fine clusters of the kept units (retriever.cpp:118-135)
+    // tier 2: fine clusters of the kept units (retriever.cpp:118-135); the
+    // unit blocks are [d/4][n_u][4], one float4 per cluster per step
     const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
     const double* fr = a.frad + (size_t)slot * a.cap_clusters;
     const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
+    const uint32_t dq = d >> 2;
+    unsigned long long kmin = ~0ull, kmax = 0ull;
     for (uint32_t i = tid; i < nc; i += blockDim.x) {
         uint32_t k = 0;
         while (k + 1 < kU && s_pre[k + 1] <= i) ++k;
-        const uint32_t u = s_kept[k];
-        const uint32_t base = uoff[u], nu = uoff[u + 1] - base, local = i - s_pre[k];
-        const float* col = fc + (size_t)base * d + local;
+        const uint32_t base = s_base[k], nu = s_nu[k], local = i - s_pre[k];
+        const float4* col = reinterpret_cast<const float4*>(fc + (size_t)base * d) + local;
         double s = 0.0;
-        uint32_t j = 0;
-        for (; j + 8 <= d; j += 8) {
-            float v[8];
+        uint32_t jq = 0;
+        for (; jq + 4 <= dq; jq += 4) {
+            float4 v[4];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) v[t] = __ldg(col + (size_t)(j + t) * nu);
+            for (int t = 0; t < 4; ++t) v[t] = __ldg(col + (size_t)(jq + t) * nu);
 #pragma unroll
-            for (int t = 0; t < 8; ++t) s = __fma_rn((double)qs[j + t], (double)v[t], s);
+            for (int t = 0; t < 4; ++t) {
+                const float* q4 = qs + 4 * (jq + t);
+                s = __fma_rn((double)q4[0], (double)v[t].x, s);
+                s = __fma_rn((double)q4[1], (double)v[t].y, s);
+                s = __fma_rn((double)q4[2], (double)v[t].z, s);
+                s = __fma_rn((double)q4[3], (double)v[t].w, s);
+            }
         }
-        for (; j < d; ++j) s = __fma_rn((double)qs[j], (double)__ldg(col + (size_t)j * nu), s);
+        for (; jq < dq; ++jq) {
+            const float4 v = __ldg(col + (size_t)jq * nu);
+            const float* q4 = qs + 4 * jq;
+            s = __fma_rn((double)q4[0], (double)v.x, s);
+            s = __fma_rn((double)q4[1], (double)v.y, s);
+            s = __fma_rn((double)q4[2], (double)v.z, s);
+            s = __fma_rn((double)q4[3], (double)v.w, s);
+        }
         const uint32_t c = base + local;
-        ckey[i] = desc_key(__dadd_rn(s, __dmul_rn(qnorm, fr[c])));
+        const unsigned long long key = desc_key(__dadd_rn(s, __dmul_rn(qnorm, fr[c])));
+        ckey[i] = key;
         cw[i] = p.mode == 1 ? ft[c] : 1u;
-        cid[i] = c;
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
     }
+    // the bits every candidate shares are skipped by the radix passes
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) {
+        s_min[warp] = kmin;
+        s_max[warp] = kmax;
+    }
+    __syncthreads();
     if (tid == 0) {
-        s_prefix = 0;
-        s_mask = 0;
+        unsigned long long mn = s_min[0], mx = s_max[0];
+        for (int w = 1; w < kSelWarps; ++w) {
+            mn = min(mn, s_min[w]);
+            mx = max(mx, s_max[w]);
+        }
+        const unsigned long long diff = mn ^ mx;
+        int top = diff ? 63 - __clzll((long long)diff) : 0;  // highest differing bit
+        int shift = (top / 8) * 8;                           // byte holding it
+        unsigned long long mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
+        s_prefix = mn & mask;
+        s_mask = mask;
+        s_shift = shift;
         s_wbefore = 0;
         s_cbefore = 0;
         s_state = 0;
@@ -182,8 +229,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     // weight sum stays <= budget (retriever.cpp:146-153); fixed-k mode is the
     // same with unit weights and budget = k_c (select_topk, retriever.cpp:141)
     const unsigned long long budget = p.mode == 1 ? p.budget : (unsigned long long)p.cluster_topk;
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int shift = s_shift; shift >= 0; shift -= 8) {
         for (uint32_t b = tid; b < 256; b += blockDim.x) {
             hw[b] = 0;
             hc[b] = 0;
@@ -194,14 +240,13 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
             const unsigned long long k = ckey[i];
             if ((k & mask) == prefix) {
                 const uint32_t b = (uint32_t)(k >> shift) & 255u;
-                atomicAdd(&hw[b], (unsigned long long)cw[i]);
+                atomicAdd(&hw[b], cw[i]);
                 atomicAdd(&hc[b], 1u);
             }
         }
         __syncthreads();
         if (warp == 0) {
-            unsigned long long w8[8];
-            uint32_t c8[8];
+            uint32_t w8[8], c8[8];
             unsigned long long lw = 0;
             uint32_t lc = 0;
 #pragma unroll
@@ -217,19 +262,16 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned long long yw = __shfl_up_sync(0xffffffffu, iw, o);
                 const uint32_t yc = __shfl_up_sync(0xffffffffu, ic, o);
-                if (lane >= o) {
+                if (lane >= (uint32_t)o) {
                     iw += yw;
                     ic += yc;
                 }
             }
             const unsigned long long wbase = s_wbefore + (iw - lw);
             const uint32_t cbase = ic - lc;
-            // first bin whose inclusive cumulative weight exceeds the budget
             int found = -1;
-            unsigned long long cum = wbase;
-            uint32_t ccum = cbase;
-            unsigned long long wexcl = 0;
-            uint32_t cexcl = 0;
+            unsigned long long cum = wbase, wexcl = 0;
+            uint32_t ccum = cbase, cexcl = 0;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 if (found < 0) {
@@ -246,81 +288,92 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
             const unsigned int ballot = __ballot_sync(0xffffffffu, found >= 0);
             if (ballot == 0) {
                 if (lane == 0) s_state = 2;  // everything matching fits
-            } else {
-                const int first = __ffs(ballot) - 1;
-                if (lane == first) {
-                    const uint32_t b = (uint32_t)(lane * 8 + found);
-                    s_prefix = prefix | ((unsigned long long)b << shift);
-                    s_mask = mask | (255ull << shift);
-                    s_wbefore = wexcl;
-                    s_cbefore += cexcl;
-                    s_state = c8[found] == 1 ? 1u : 0u;
-                }
+            } else if ((int)lane == __ffs(ballot) - 1) {
+                const uint32_t b = lane * 8 + (uint32_t)found;
+                s_prefix = prefix | ((unsigned long long)b << shift);
+                s_mask = mask | (255ull << shift);
+                s_wbefore = wexcl;
+                s_cbefore += cexcl;
+                s_state = c8[found] == 1 ? 1u : 0u;
             }
         }
         __syncthreads();
         if (s_state != 0) break;
     }
-    // mark the selection
+    // mark the selection (compacted into sel, which reuses the weight array)
     const unsigned long long prefix = s_prefix, mask = s_mask;
     const uint32_t state = s_state;
-    for (uint32_t i = tid; i < nc; i += blockDim.x) {
-        const unsigned long long k = ckey[i] & mask;
-        bool take = k < prefix;
-        if (k == prefix) {
-            if (state == 2) take = true;                   // whole bucket fits
-            else if (state == 1) take = s_cbefore == 0;    // lone boundary: admit if first
+    const uint32_t cbefore = s_cbefore;
+    // (the weights are no longer needed: the tie walk re-reads token counts)
+    for (uint32_t base = 0; base < nc; base += blockDim.x) {
+        const uint32_t i = base + tid;
+        bool take = false;
+        if (i < nc) {
+            const unsigned long long k = ckey[i] & mask;
+            take = k < prefix;
+            if (k == prefix) {
+                if (state == 2) take = true;                 // whole bucket fits
+                else if (state == 1) take = cbefore == 0;    // lone boundary: admit if first
+            }
         }
-        if (take) sel[atomicAdd(&s_nsel, 1u)] = i;
+        const unsigned int bal = __ballot_sync(0xffffffffu, take);
+        uint32_t pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&s_nsel, (uint32_t)__popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        __syncthreads();  // every read of cw[base .. base+blockDim) happened above
+        if (take) cw[pos + __popc(bal & ((1u << lane) - 1u))] = i;
+        __syncthreads();
     }
-    __syncthreads();
+    const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
+    auto cid_of = [&](uint32_t i) -> uint32_t {
+        uint32_t k = 0;
+        while (k + 1 < kU && s_pre[k + 1] <= i) ++k;
+        return s_base[k] + (i - s_pre[k]);
+    };
     if (state == 0 && tid == 0) {
         // bucket of identical fp64 scores: reference-id order (retriever.cpp:33)
-        const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
         unsigned long long used = s_wbefore;
-        uint32_t admitted = s_cbefore;
+        uint32_t admitted = cbefore;
+        uint32_t last_id = 0;
+        bool first = true;
         for (;;) {
             int best = -1;
             uint32_t best_id = 0xffffffffu;
             for (uint32_t i = 0; i < nc; ++i) {
-                if ((ckey[i] & mask) != prefix || cw[i] == 0xffffffffu) continue;
-                const uint32_t oid = fo[cid[i]];
-                if (oid < best_id) {
+                if ((ckey[i] & mask) != prefix) continue;
+                const uint32_t oid = fo[cid_of(i)];
+                if ((first || oid > last_id) && oid < best_id) {
                     best_id = oid;
                     best = (int)i;
                 }
             }
             if (best < 0) break;
-            const unsigned long long w = cw[best];
+            const unsigned long long w = p.mode == 1 ? a.ftok[(size_t)slot * a.cap_clusters + cid_of(best)] : 1ull;
             if (admitted > 0 && used + w > budget) break;
             used += w;
             ++admitted;
-            sel[s_nsel++] = (uint32_t)best;
-            cw[best] = 0xffffffffu;  // consumed
+            cw[s_nsel++] = (uint32_t)best;
+            last_id = best_id;
+            first = false;
         }
     }
     __syncthreads();
 
     // rank order of the selected set + outputs
     const uint32_t nsel = s_nsel;
-    const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
     uint32_t* out_cl = a.sel_clusters + ((size_t)slot * a.G + g) * a.cap_clusters;
     for (uint32_t x = tid; x < nsel; x += blockDim.x) {
-        const uint32_t i = sel[x];
+        const uint32_t i = cw[x];
         const unsigned long long ki = ckey[i];
-        const uint32_t ci = cid[i];
-        uint32_t oi = 0xffffffffu;
+        const uint32_t ci = cid_of(i);
+        const uint32_t oi = fo[ci];
         uint32_t rank = 0;
         for (uint32_t y = 0; y < nsel; ++y) {
-            const unsigned long long ky = ckey[sel[y]];
-            if (ky < ki) {
-                ++rank;
-            } else if (ky == ki && y != x) {
-                if (oi == 0xffffffffu) oi = fo[ci];
-                if (fo[cid[sel[y]]] < oi) ++rank;
-            }
+            const unsigned long long ky = ckey[cw[y]];
+            if (ky < ki) ++rank;
+            else if (ky == ki && y != x && fo[cid_of(cw[y])] < oi) ++rank;
         }
-        out_cl[rank] = fo[ci];
+        out_cl[rank] = oi;
         atomicOr(&bits[ci >> 5], 1u << (ci & 31));
     }
     uint32_t* out_u = a.sel_units + ((size_t)slot * a.G + g) * a.cap_units;
@@ -348,6 +401,7 @@ struct CompactParams {
 };
 
 constexpr int kCompactThreads = 512;
+constexpr int kChunksPerThread = 8;
 
 template <typename T>
 __device__ __forceinline__ T block_excl_scan(T v, T* warp_tot, T& total) {
@@ -380,7 +434,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* warp_tot, T& total) {
 __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     extern __shared__ __align__(16) uint32_t sbits[];  // [G][words(L)]
     const Arena& a = p.a;
-    const uint32_t slot = blockIdx.x, tid = threadIdx.x, G = a.G;
+    const uint32_t slot = blockIdx.x, tid = threadIdx.x, G = a.G, lane = tid & 31;
     const SlotState st = a.state[slot];
     const uint32_t n = st.n_tokens, M = st.n_chunks, ce = st.chunked_end;
     const uint32_t all = (1u << G) - 1u;
@@ -390,7 +444,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     unsigned long long* sb = a.step_bytes + (size_t)slot * 4;
     const unsigned long long d = a.d;
 
-    __shared__ unsigned long long s_cnt[kMaxGroup];
+    __shared__ uint32_t s_cnt[kMaxGroup];
     __shared__ uint32_t s_nsp[kMaxGroup];
     __shared__ unsigned long long warp_tot[kCompactThreads / 32];
     __shared__ uint32_t s_units[32];  // union of kept units (bitset, cap_units <= 1024)
@@ -435,37 +489,69 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     }
     const uint32_t* cs = a.chunk_start + (size_t)slot * (a.cap_chunks + 1);
     const uint32_t* cc = a.chunk_clu + (size_t)slot * a.cap_chunks;
-    for (uint32_t base = 0; base < M; base += blockDim.x) {
-        const uint32_t j = base + tid;
-        uint32_t m = 0, s = 0, len = 0;
-        if (j < M) {
-            const uint32_t c = cc[j];
-            for (uint32_t g = 0; g < G; ++g) m |= ((sbits[g * words + (c >> 5)] >> (c & 31)) & 1u) << g;
-            if (m) {
-                s = max(cs[j], sink_end);
-                const uint32_t e = cs[j + 1];
-                if (s >= e) m = 0;
-                else len = e - s;
+    uint32_t my_cnt[kMaxGroup], my_nsp[kMaxGroup];
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g) my_cnt[g] = my_nsp[g] = 0;
+    constexpr uint32_t kTile = kCompactThreads * kChunksPerThread;
+    for (uint32_t base = 0; base < M; base += kTile) {
+        const uint32_t j0 = base + tid * kChunksPerThread;
+        uint32_t m8[kChunksPerThread], s8[kChunksPerThread], l8[kChunksPerThread];
+        uint32_t cnt = 0, toks = 0;
+#pragma unroll
+        for (int e = 0; e < kChunksPerThread; ++e) {
+            const uint32_t j = j0 + e;
+            uint32_t m = 0, s = 0, len = 0;
+            if (j < M) {
+                const uint32_t c = __ldg(cc + j);
+                for (uint32_t g = 0; g < G; ++g) m |= ((sbits[g * words + (c >> 5)] >> (c & 31)) & 1u) << g;
+                if (m) {
+                    s = max(__ldg(cs + j), sink_end);
+                    const uint32_t e2 = __ldg(cs + j + 1);
+                    if (s >= e2) m = 0;
+                    else len = e2 - s;
+                }
             }
+            m8[e] = m;
+            s8[e] = s;
+            l8[e] = len;
+            cnt += m ? 1u : 0u;
+            toks += len;
+#pragma unroll
+            for (int g = 0; g < kMaxGroup; ++g)
+                if ((m >> g) & 1u) {
+                    my_cnt[g] += len;
+                    my_nsp[g] += 1;
+                }
         }
-        const unsigned long long v = m ? ((1ull << 40) | len) : 0ull;
+        const unsigned long long v = ((unsigned long long)cnt << 40) | toks;
         unsigned long long total;
         const unsigned long long ex = block_excl_scan(v, warp_tot, total);
-        if (m) {
-            const uint32_t pos = out + (uint32_t)(ex >> 40);
-            if (pos < a.cap_spans) {
-                sp[pos].start = s;
-                sp[pos].len_mask = (len << 8) | m;
-                so[pos] = tok + (uint32_t)(ex & 0xffffffffffull);
-            }
-            for (uint32_t g = 0; g < G; ++g)
-                if ((m >> g) & 1u) {
-                    atomicAdd(&s_cnt[g], (unsigned long long)len);
-                    atomicAdd(&s_nsp[g], 1u);
+        uint32_t pos = out + (uint32_t)(ex >> 40);
+        uint32_t tp = tok + (uint32_t)(ex & 0xffffffffffull);
+#pragma unroll
+        for (int e = 0; e < kChunksPerThread; ++e) {
+            if (m8[e]) {
+                if (pos < a.cap_spans) {
+                    sp[pos].start = s8[e];
+                    sp[pos].len_mask = (l8[e] << 8) | m8[e];
+                    so[pos] = tp;
                 }
+                ++pos;
+                tp += l8[e];
+            }
         }
         out += (uint32_t)(total >> 40);
         tok += (uint32_t)(total & 0xffffffffffull);
+    }
+#pragma unroll
+    for (int g = 0; g < kMaxGroup; ++g) {
+        if ((uint32_t)g >= G) break;
+        const uint32_t c1 = __reduce_add_sync(0xffffffffu, my_cnt[g]);
+        const uint32_t c2 = __reduce_add_sync(0xffffffffu, my_nsp[g]);
+        if (lane == 0) {
+            atomicAdd(&s_cnt[g], c1);
+            atomicAdd(&s_nsp[g], c2);
+        }
     }
     const uint32_t n_chunk_spans = out - (sink_end > 0 ? 1u : 0u);
     // buffer ids (collect_active, retriever.cpp:71)
@@ -515,7 +601,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
                     so[pos] = tok + (uint32_t)(ex & 0xffffffffffull);
                 }
                 for (uint32_t g = 0; g < G; ++g)
-                    if ((resid >> g) & 1u) atomicAdd(&s_cnt[g], 1ull);
+                    if ((resid >> g) & 1u) atomicAdd(&s_cnt[g], 1u);
             }
             out += (uint32_t)(total >> 40);
             tok += (uint32_t)(total & 0xffffffffffull);
@@ -542,9 +628,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
             if ((s_units[u >> 5] >> (u & 31)) & 1u) nc_union += uoff[u + 1] - uoff[u];
         const unsigned long long P = st.P;
         unsigned long long per_q = 0;
+        const uint32_t bufl = (p.flags == 1u && n > max(ce, sink_end)) ? n - max(ce, sink_end) : 0u;
         for (uint32_t g = 0; g < G; ++g) {
-            const unsigned long long act = s_cnt[g] + sink_end +
-                                           (p.flags == 1u && n > max(ce, sink_end) ? n - max(ce, sink_end) : 0);
+            const unsigned long long act = (unsigned long long)s_cnt[g] + sink_end + bufl;
             qi[g].n_active = act;
             const unsigned long long ncg = qi[g].scanned - P;
             per_q += P * (4 * d + 8) + ncg * (4 * d + 16) + (unsigned long long)s_nsp[g] * 8 +
@@ -560,7 +646,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
 
 // launchers ------------------------------------------------------------------
 size_t select_smem_bytes(const Arena& a) {
-    return ((a.d * 4 + 15) & ~15u) + (size_t)a.cap_units * 8 + (size_t)a.max_cand * (8 + 4 + 4 + 4);
+    return ((a.d * 4 + 15) & ~15u) + (size_t)a.cap_units * 8 + (size_t)a.max_cand * (8 + 4);
 }
 
 cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
