@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--batch", type=int, default=1)
     p.add_argument("--splits", type=int, default=0)
     p.add_argument("--graph", type=int, default=1)
+    p.add_argument("--slot-groups", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
     p.add_argument("--seed-base", type=int, default=1000)
     return p.parse_args()
@@ -128,7 +129,7 @@ def build_engine(api, torch, args, slots, device):
     cap_chunks = n // 8 + 64
     eng = api.Engine(S, 128, args.group, cap_tokens=n + 64, cap_chunks=cap_chunks,
                      cap_clusters=(cap_chunks + 1) // 2, cap_units=64, splits=args.splits,
-                     keep_reps=False, device=device)
+                     keep_reps=False, device=device, slot_groups=args.slot_groups)
     seeds = np.array([args.seed_base + s for s in slots], np.uint64)
     t0 = time.time()
     codes, qs = eng.gen_workload(n, seeds, query_count=args.group)
@@ -362,6 +363,7 @@ def main():
             "clocks": clocks,
             "setup": setup,
             "cuda_graph": graph is not None,
+            "slot_groups": args.slot_groups,
         }
         print(json.dumps(line))
     if world > 1:

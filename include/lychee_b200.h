@@ -60,6 +60,8 @@ typedef struct {
     uint32_t graft_full;      /* StreamerConfig::graft_search == full */
     uint32_t keep_reps;       /* keep chunk representatives on device (download parity) */
     uint32_t pooling;         /* IndexConfig::pooling: 0 mean, 1 max (index.hpp:11) */
+    uint32_t slot_groups;     /* lc_retrieve runs this many slot groups on forked streams so
+                                 one group's selection overlaps another's attention (0 = 1) */
     int32_t device;
 } lc_index_desc;
 

@@ -23,7 +23,8 @@ class IndexDesc(C.Structure):
     _fields_ = [("n_slots", u32), ("dim", u32), ("group", u32), ("cap_tokens", u32),
                 ("cap_chunks", u32), ("cap_clusters", u32), ("cap_units", u32),
                 ("max_candidates", u32), ("splits", u32), ("structure_aware", u32),
-                ("graft_full", u32), ("keep_reps", u32), ("pooling", u32), ("device", C.c_int32)]
+                ("graft_full", u32), ("keep_reps", u32), ("pooling", u32), ("slot_groups", u32),
+                ("device", C.c_int32)]
 
 
 class Budgets_(C.Structure):

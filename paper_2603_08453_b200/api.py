@@ -199,10 +199,11 @@ class Engine:
     def __init__(self, n_slots: int, dim: int = 128, group: int = 4, cap_tokens: int = 1 << 16,
                  cap_chunks: int = 1 << 13, cap_clusters: int = 1 << 12, cap_units: int = 64,
                  splits: int = 0, structure_aware: bool = True, graft_full: bool = False,
-                 keep_reps: bool = True, pooling: int = 0, device: int = 0, max_candidates: int = 0):
+                 keep_reps: bool = True, pooling: int = 0, device: int = 0, max_candidates: int = 0,
+                 slot_groups: int = 0):
         self.desc = L.IndexDesc(n_slots, dim, group, cap_tokens, cap_chunks, cap_clusters,
                                 cap_units, max_candidates, splits, int(structure_aware),
-                                int(graft_full), int(keep_reps), pooling, device)
+                                int(graft_full), int(keep_reps), pooling, slot_groups, device)
         self.h = C.c_void_p()
         L.check(L.lib().lc_index_create(C.byref(self.desc), C.byref(self.h)))
         got = L.IndexDesc()

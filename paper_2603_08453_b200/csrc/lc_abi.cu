@@ -383,6 +383,19 @@ static void validate_budgets(const lc_budgets* b) {
     if (b->unit_topk > 64) fail(LC_EINVAL, "unit_topk > 64 is not supported by the device kernel");
 }
 
+static void ensure_streams(lc_index_t h, uint32_t groups) {
+    while (h->group_streams.size() < groups) {
+        cudaStream_t s;
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+        h->group_streams.push_back(s);
+    }
+    while (h->group_events.size() < groups + 1) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+        h->group_events.push_back(e);
+    }
+}
+
 static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
                           const uint32_t* buf_off, const uint32_t* buf_ids, float* out_dev,
                           cudaStream_t st) {
@@ -395,12 +408,56 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     h->set_device();
     Arena a = h->a;
     a.max_cand = needed_candidates(h, std::min<uint32_t>(b->unit_topk, 64));
-    if (select_smem_bytes(a) > 227 * 1024)
-        fail(LC_ENOMEM, "fine candidate set exceeds shared memory (" + std::to_string(a.max_cand) + ")");
-    ck(launch_select(a, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, st),
-       "k_select");
-    ck(launch_compact(a, b->sink_size, flags, buf_off, buf_ids, st), "k_compact");
-    if (out_dev) ck(launch_attend(a, q_dev, out_dev, st), "k_attend");
+    // shared-memory candidate area: at least the staged coarse tier [d][P]
+    uint32_t pmax = 1;
+    for (auto& s : h->hs) pmax = std::max(pmax, s.P);
+    const uint32_t stage_c = (uint32_t)(((size_t)a.d * ((pmax + 3) & ~3u) * 4 + 11) / 12);
+    a.smem_cand = std::min<uint32_t>(std::max<uint32_t>(2048, stage_c), std::max<uint32_t>(a.max_cand, stage_c));
+    if (select_smem_bytes(a) > 200 * 1024) a.smem_cand = (uint32_t)((200 * 1024 - a.d * 4 - a.cap_units * 8) / 12);
+    if (a.max_cand > a.smem_cand) {
+        const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
+        if (h->cand_scratch_bytes < need) {
+            if (h->cand_scratch) cudaFree(h->cand_scratch);
+            h->cand_scratch = nullptr;
+            h->cand_scratch_bytes = 0;
+            if (cudaMalloc(&h->cand_scratch, need) != cudaSuccess) {
+                cudaGetLastError();
+                fail(LC_ENOMEM, "candidate scratch allocation failed");
+            }
+            h->cand_scratch_bytes = need;
+        }
+        a.cand_scratch = h->cand_scratch;
+    } else {
+        a.cand_scratch = nullptr;
+    }
+    const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
+    if (groups == 1) {
+        a.slot0 = 0;
+        ck(launch_select(a, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
+                         a.n_slots, st), "k_select");
+        ck(launch_compact(a, b->sink_size, flags, buf_off, buf_ids, a.n_slots, st), "k_compact");
+        if (out_dev) ck(launch_attend(a, q_dev, out_dev, a.n_slots, st), "k_attend");
+    } else {
+        // fork: each slot group runs select -> compact -> attend on its own stream,
+        // so one group's (latency-bound) selection overlaps another's attention
+        ensure_streams(h, groups);
+        ck(cudaEventRecord(h->group_events[0], st), "fork");
+        for (uint32_t gi = 0; gi < groups; ++gi) {
+            const uint32_t s0 = (uint32_t)((uint64_t)a.n_slots * gi / groups);
+            const uint32_t s1 = (uint32_t)((uint64_t)a.n_slots * (gi + 1) / groups);
+            if (s1 == s0) continue;
+            cudaStream_t gs = h->group_streams[gi];
+            ck(cudaStreamWaitEvent(gs, h->group_events[0], 0), "fork wait");
+            Arena ag = a;
+            ag.slot0 = s0;
+            ck(launch_select(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
+                             s1 - s0, gs), "k_select");
+            ck(launch_compact(ag, b->sink_size, flags, buf_off, buf_ids, s1 - s0, gs), "k_compact");
+            if (out_dev) ck(launch_attend(ag, q_dev, out_dev, s1 - s0, gs), "k_attend");
+            ck(cudaEventRecord(h->group_events[gi + 1], gs), "join record");
+            ck(cudaStreamWaitEvent(st, h->group_events[gi + 1], 0), "join");
+        }
+    }
     h->last_flags = flags;
     h->last_valid = 1;
 }
@@ -418,7 +475,9 @@ int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* 
         if (!h || !q_dev || !out_dev) fail(LC_EINVAL, "lc_sparse_attention: null argument");
         if (!h->last_valid) fail(LC_EINVAL, "lc_sparse_attention: no selection yet");
         h->set_device();
-        ck(launch_attend(h->a, q_dev, out_dev, (cudaStream_t)stream), "k_attend");
+        Arena a = h->a;
+        a.slot0 = 0;
+        ck(launch_attend(a, q_dev, out_dev, a.n_slots, (cudaStream_t)stream), "k_attend");
     });
 }
 

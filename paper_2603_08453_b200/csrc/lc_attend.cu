@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     constexpr int ROWB = D * 2;            // bytes per K/V row
     constexpr int STAGE = 32 * ROWB;       // 16 K rows + 16 V rows
     const Arena& a = p.a;
-    const uint32_t slot = blockIdx.y, split = blockIdx.x, S = gridDim.x;
+    const uint32_t slot = a.slot0 + blockIdx.y, split = blockIdx.x, S = gridDim.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
     const uint32_t G = a.G;
 
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
 
 template <int D>
 static cudaError_t launch_attend_d(const AttendParams& p, dim3 grid, cudaStream_t stream) {
+    // (grid.y = number of slots of this launch, starting at p.a.slot0)
     constexpr size_t ring = (size_t)kAttWarps * kStages * 32 * D * 2;
     constexpr size_t outb = (size_t)kAttWarps * kMaxGroup * D * 4;
     constexpr size_t smem = ring > outb ? ring : outb;
@@ -391,9 +392,9 @@ static cudaError_t launch_attend_d(const AttendParams& p, dim3 grid, cudaStream_
     return cudaGetLastError();
 }
 
-cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream) {
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream) {
     AttendParams p{a, q, out};
-    dim3 grid(a.splits, a.n_slots);
+    dim3 grid(a.splits, n_slots);
     if (a.d == 128) return launch_attend_d<128>(p, grid, stream);
     if (a.d == 64) return launch_attend_d<64>(p, grid, stream);
     return cudaErrorInvalidValue;

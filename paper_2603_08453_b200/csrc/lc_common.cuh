@@ -59,6 +59,8 @@ struct Arena {
     // shape
     uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;
     uint32_t splits, graft_full, keep_reps, cap_spans;
+    uint32_t smem_cand;      // candidates kept in shared memory by k_select
+    uint32_t slot0;          // first slot of the launch (slot groups on several streams)
     // token store
     __nv_bfloat16* K;
     __nv_bfloat16* V;
@@ -81,6 +83,7 @@ struct Arena {
     uint32_t* sel_units;     // [slot][G][cap_units]
     uint32_t* sel_clusters;  // [slot][G][cap_clusters] reference ids, rank order
     uint32_t* sel_bits;      // [slot][G][words(cap_clusters)] internal-id bitmap
+    unsigned char* cand_scratch;  // [slot][G][max_cand * 12] overflow of k_select's smem
     Span* spans;             // [slot][cap_spans]
     uint32_t* span_off;      // [slot][cap_spans+1] token prefix offsets
     uint32_t* n_spans;       // [slot]

@@ -13,10 +13,10 @@ namespace lc {
 size_t select_smem_bytes(const Arena& a);
 cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
                           uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
-                          cudaStream_t stream);
+                          uint32_t n_slots, cudaStream_t stream);
 cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
-                           const uint32_t* buf_ids, cudaStream_t stream);
-cudaError_t launch_attend(const Arena& a, const float* q, float* out, cudaStream_t stream);
+                           const uint32_t* buf_ids, uint32_t n_slots, cudaStream_t stream);
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
                          cudaStream_t stream);
@@ -93,9 +93,16 @@ struct lc_index_s {
     uint32_t last_flags = 0;
     uint32_t last_valid = 0;
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
+    unsigned char* cand_scratch = nullptr;     // k_select overflow storage
+    size_t cand_scratch_bytes = 0;
+    std::vector<cudaStream_t> group_streams;   // one per slot group
+    std::vector<cudaEvent_t> group_events;     // fork + one join per group
 
     ~lc_index_s() {
         for (void* p : owned) cudaFree(p);
+        if (cand_scratch) cudaFree(cand_scratch);
+        for (auto s : group_streams) cudaStreamDestroy(s);
+        for (auto e : group_events) cudaEventDestroy(e);
     }
     void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
 };

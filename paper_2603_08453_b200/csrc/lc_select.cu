@@ -37,17 +37,20 @@ __device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ia,
 }
 
 // Dynamic shared memory of k_select:
-//   float  qs[d]
+//   float  qs[D]
 //   u64    ukey[cap_units]
-//   u64    ckey[max_cand]     candidate keys (ascending key == descending UB)
-//   u32    cw[max_cand]       weight (token_count, or 1 in fixed-k mode);
-//                             reused as the selected-index list afterwards
+//   area:  first the coarse centroids [D][Pp] (staged once, coalesced), then
+//          u64 ckey[C] candidate keys (ascending key == descending UB) and
+//          u32 cw[C] weights (token_count, or 1 in fixed-k mode), reused as the
+//          selected-index list.  C = smem_cand; larger candidate sets live in
+//          the per-query-head global scratch (L2 resident) instead.
+template <int D>
 __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Arena& a = p.a;
-    const uint32_t slot = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+    const uint32_t slot = a.slot0 + blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
     const uint32_t lane = tid & 31, warp = tid >> 5;
-    const uint32_t d = a.d;
+    constexpr uint32_t d = D, dq = D / 4;
     const SlotState st = a.state[slot];
     QInfo* qi = a.qinfo + (size_t)slot * a.G + g;
     uint32_t* bits = a.sel_bits + ((size_t)slot * a.G + g) * bit_words(a.cap_clusters);
@@ -68,10 +71,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     }
 
     float* qs = reinterpret_cast<float*>(smem);
-    unsigned long long* ukey =
-        reinterpret_cast<unsigned long long*>(smem + ((d * 4 + 15) & ~15u));
-    unsigned long long* ckey = ukey + a.cap_units;
-    uint32_t* cw = reinterpret_cast<uint32_t*>(ckey + a.max_cand);
+    unsigned long long* ukey = reinterpret_cast<unsigned long long*>(smem + D * 4);
+    unsigned char* area = smem + D * 4 + (size_t)a.cap_units * 8;
+    const uint32_t Pp = (st.P + 3) & ~3u;
+    float* ucs = reinterpret_cast<float*>(area);  // staged coarse centroids [D][Pp]
 
     __shared__ double s_qnorm;
     __shared__ uint32_t s_kept[kMaxUnitTopk];
@@ -86,17 +89,27 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     const float* qg = p.q + ((size_t)slot * a.G + g) * d;
     for (uint32_t j = tid; j < d; j += blockDim.x) qs[j] = qg[j];
     for (uint32_t w = tid; w < nwords; w += blockDim.x) bits[w] = 0u;
+    // stage the coarse tier [D][P] (dimension-major rows of cap_units floats)
+    const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
+    const bool staged = (size_t)D * Pp * 4 <= (size_t)a.smem_cand * 12 && (a.cap_units & 3) == 0;
+    if (staged) {
+        const uint32_t pq = Pp >> 2;
+        for (uint32_t e = tid; e < D * pq; e += blockDim.x) {
+            const uint32_t j = e / pq, u4 = e % pq;
+            reinterpret_cast<float4*>(ucs + (size_t)j * Pp)[u4] =
+                __ldg(reinterpret_cast<const float4*>(uc + (size_t)j * a.cap_units) + u4);
+        }
+    }
     __syncthreads();
 
     // ||q|| (kernels.cpp:19-23): sequential, exact products -> DFMA chain
     if (tid == 0) {
         double s = 0.0;
+#pragma unroll 8
         for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)qs[j], (double)qs[j], s);
         s_qnorm = __dsqrt_rn(s);
     }
-    // tier 1: coarse units (retriever.cpp:100-112), dimension-major centroids;
-    // warp 0 is busy with ||q||, the coarse rows go to warps 1..7
-    const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
+    // tier 1: coarse units (retriever.cpp:100-112); warp 0 is busy with ||q||
     const double* ur = a.urad + (size_t)slot * a.cap_units;
     double udot[5];
     const uint32_t ct = tid >= 32 ? tid - 32 : 0xffffffffu;
@@ -104,9 +117,15 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     for (uint32_t k = 0; k < 5; ++k) {
         const uint32_t u = ct + k * (kSelThreads - 32);
         double s = 0.0;
-        if (ct != 0xffffffffu && u < st.P)
-            for (uint32_t j = 0; j < d; ++j)
-                s = __fma_rn((double)qs[j], (double)__ldg(uc + (size_t)j * a.cap_units + u), s);
+        if (ct != 0xffffffffu && u < st.P) {
+            if (staged) {
+#pragma unroll 8
+                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)qs[j], (double)ucs[j * Pp + u], s);
+            } else {
+                for (uint32_t j = 0; j < d; ++j)
+                    s = __fma_rn((double)qs[j], (double)__ldg(uc + (size_t)j * a.cap_units + u), s);
+            }
+        }
         udot[k] = s;
     }
     __syncthreads();
@@ -140,7 +159,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     }
     __syncthreads();
     const uint32_t nc = s_pre[kU];
-    if (nc > a.max_cand || nc == 0) {
+    if (nc > a.max_cand || nc == 0 || (nc > a.smem_cand && a.cand_scratch == nullptr)) {
         if (tid == 0) {
             qi->error = nc == 0 ? kErrEmptyCand : kErrCandOverflow;
             qi->degenerate = 0;
@@ -151,41 +170,52 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         }
         return;
     }
+    // candidate storage: shared memory, or this query head's global scratch
+    unsigned long long* ckey;
+    uint32_t* cw;
+    if (nc <= a.smem_cand) {
+        ckey = reinterpret_cast<unsigned long long*>(area);
+        cw = reinterpret_cast<uint32_t*>(ckey + a.smem_cand);
+    } else {
+        unsigned char* gs = a.cand_scratch + ((size_t)slot * a.G + g) * (size_t)a.max_cand * 12;
+        ckey = reinterpret_cast<unsigned long long*>(gs);
+        cw = reinterpret_cast<uint32_t*>(ckey + a.max_cand);
+    }
 
     // tier 2: fine clusters of the kept units (retriever.cpp:118-135); the
-    // unit blocks are [d/4][n_u][4], one float4 per cluster per step
+    // unit blocks are [D/4][n_u][4]: one float4 per cluster per step, loads
+    // double-buffered four quads ahead of the sequential DFMA chain
     const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
     const double* fr = a.frad + (size_t)slot * a.cap_clusters;
     const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
-    const uint32_t dq = d >> 2;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     for (uint32_t i = tid; i < nc; i += blockDim.x) {
         uint32_t k = 0;
         while (k + 1 < kU && s_pre[k + 1] <= i) ++k;
         const uint32_t base = s_base[k], nu = s_nu[k], local = i - s_pre[k];
         const float4* col = reinterpret_cast<const float4*>(fc + (size_t)base * d) + local;
-        double s = 0.0;
-        uint32_t jq = 0;
-        for (; jq + 4 <= dq; jq += 4) {
-            float4 v[4];
+        float4 A[4], B[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) v[t] = __ldg(col + (size_t)(jq + t) * nu);
+        for (int t = 0; t < 4; ++t) A[t] = __ldg(col + (size_t)t * nu);
+        double s = 0.0;
+#pragma unroll
+        for (uint32_t jq = 0; jq < dq; jq += 4) {
+            if (jq + 4 < dq) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) B[t] = __ldg(col + (size_t)(jq + 4 + t) * nu);
+            }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const float* q4 = qs + 4 * (jq + t);
-                s = __fma_rn((double)q4[0], (double)v[t].x, s);
-                s = __fma_rn((double)q4[1], (double)v[t].y, s);
-                s = __fma_rn((double)q4[2], (double)v[t].z, s);
-                s = __fma_rn((double)q4[3], (double)v[t].w, s);
+                s = __fma_rn((double)q4[0], (double)A[t].x, s);
+                s = __fma_rn((double)q4[1], (double)A[t].y, s);
+                s = __fma_rn((double)q4[2], (double)A[t].z, s);
+                s = __fma_rn((double)q4[3], (double)A[t].w, s);
             }
-        }
-        for (; jq < dq; ++jq) {
-            const float4 v = __ldg(col + (size_t)jq * nu);
-            const float* q4 = qs + 4 * jq;
-            s = __fma_rn((double)q4[0], (double)v.x, s);
-            s = __fma_rn((double)q4[1], (double)v.y, s);
-            s = __fma_rn((double)q4[2], (double)v.z, s);
-            s = __fma_rn((double)q4[3], (double)v.w, s);
+            if (jq + 4 < dq) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) A[t] = B[t];
+            }
         }
         const uint32_t c = base + local;
         const unsigned long long key = desc_key(__dadd_rn(s, __dmul_rn(qnorm, fr[c])));
@@ -300,11 +330,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         __syncthreads();
         if (s_state != 0) break;
     }
-    // mark the selection (compacted into sel, which reuses the weight array)
+    // mark the selection (compacted into the weight array, no longer needed)
     const unsigned long long prefix = s_prefix, mask = s_mask;
     const uint32_t state = s_state;
     const uint32_t cbefore = s_cbefore;
-    // (the weights are no longer needed: the tie walk re-reads token counts)
     for (uint32_t base = 0; base < nc; base += blockDim.x) {
         const uint32_t i = base + tid;
         bool take = false;
@@ -320,10 +349,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         uint32_t pos = 0;
         if (lane == 0 && bal) pos = atomicAdd(&s_nsel, (uint32_t)__popc(bal));
         pos = __shfl_sync(0xffffffffu, pos, 0);
-        __syncthreads();  // every read of cw[base .. base+blockDim) happened above
         if (take) cw[pos + __popc(bal & ((1u << lane) - 1u))] = i;
-        __syncthreads();
     }
+    __syncthreads();
     const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
     auto cid_of = [&](uint32_t i) -> uint32_t {
         uint32_t k = 0;
@@ -432,9 +460,9 @@ __device__ __forceinline__ T block_excl_scan(T v, T* warp_tot, T& total) {
 }
 
 __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
-    extern __shared__ __align__(16) uint32_t sbits[];  // [G][words(L)]
+    extern __shared__ __align__(16) uint32_t sbits[];  // [G][words(L)] then u8 cmask[L]
     const Arena& a = p.a;
-    const uint32_t slot = blockIdx.x, tid = threadIdx.x, G = a.G, lane = tid & 31;
+    const uint32_t slot = a.slot0 + blockIdx.x, tid = threadIdx.x, G = a.G, lane = tid & 31;
     const SlotState st = a.state[slot];
     const uint32_t n = st.n_tokens, M = st.n_chunks, ce = st.chunked_end;
     const uint32_t all = (1u << G) - 1u;
@@ -475,6 +503,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
     }
     if (tid < 32) s_units[tid] = 0;
     __syncthreads();
+    // per-cluster mask of the query heads that selected it
+    uint8_t* cmask = reinterpret_cast<uint8_t*>(sbits + G * words);
+    for (uint32_t c = tid; c < st.L; c += blockDim.x) {
+        uint32_t m = 0;
+        for (uint32_t g = 0; g < G; ++g) m |= ((sbits[g * words + (c >> 5)] >> (c & 31)) & 1u) << g;
+        cmask[c] = (uint8_t)m;
+    }
+    __syncthreads();
 
     const uint32_t sink_end = min(p.sink, n);
     uint32_t out = 0, tok = 0;
@@ -501,27 +537,27 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
         for (int e = 0; e < kChunksPerThread; ++e) {
             const uint32_t j = j0 + e;
             uint32_t m = 0, s = 0, len = 0;
-            if (j < M) {
-                const uint32_t c = __ldg(cc + j);
-                for (uint32_t g = 0; g < G; ++g) m |= ((sbits[g * words + (c >> 5)] >> (c & 31)) & 1u) << g;
-                if (m) {
-                    s = max(__ldg(cs + j), sink_end);
-                    const uint32_t e2 = __ldg(cs + j + 1);
-                    if (s >= e2) m = 0;
-                    else len = e2 - s;
+            if (j < M) m = cmask[__ldg(cc + j)];
+            if (m) {
+                s = max(__ldg(cs + j), sink_end);
+                const uint32_t e2 = __ldg(cs + j + 1);
+                if (s >= e2) {
+                    m = 0;
+                } else {
+                    len = e2 - s;
+                    cnt += 1;
+                    toks += len;
+#pragma unroll
+                    for (int g = 0; g < kMaxGroup; ++g)
+                        if ((m >> g) & 1u) {
+                            my_cnt[g] += len;
+                            my_nsp[g] += 1;
+                        }
                 }
             }
             m8[e] = m;
             s8[e] = s;
             l8[e] = len;
-            cnt += m ? 1u : 0u;
-            toks += len;
-#pragma unroll
-            for (int g = 0; g < kMaxGroup; ++g)
-                if ((m >> g) & 1u) {
-                    my_cnt[g] += len;
-                    my_nsp[g] += 1;
-                }
         }
         const unsigned long long v = ((unsigned long long)cnt << 40) | toks;
         unsigned long long total;
@@ -646,29 +682,35 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
 
 // launchers ------------------------------------------------------------------
 size_t select_smem_bytes(const Arena& a) {
-    return ((a.d * 4 + 15) & ~15u) + (size_t)a.cap_units * 8 + (size_t)a.max_cand * (8 + 4);
+    return (size_t)a.d * 4 + (size_t)a.cap_units * 8 + (size_t)a.smem_cand * 12;
+}
+
+template <int D>
+static cudaError_t launch_select_d(const SelectParams& p, uint32_t n_slots, size_t smem, cudaStream_t stream) {
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_select<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    k_select<D><<<dim3(p.a.G, n_slots), kSelThreads, smem, stream>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
                           uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
-                          cudaStream_t stream) {
+                          uint32_t n_slots, cudaStream_t stream) {
     SelectParams p{a, q, unit_topk, mode, cluster_topk, sink, budget};
     const size_t smem = select_smem_bytes(a);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
-    k_select<<<dim3(a.G, a.n_slots), kSelThreads, smem, stream>>>(p);
-    return cudaGetLastError();
+    if (a.d == 128) return launch_select_d<128>(p, n_slots, smem, stream);
+    if (a.d == 64) return launch_select_d<64>(p, n_slots, smem, stream);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
-                           const uint32_t* buf_ids, cudaStream_t stream) {
+                           const uint32_t* buf_ids, uint32_t n_slots, cudaStream_t stream) {
     CompactParams p{a, sink, flags, buf_off, buf_ids};
-    const size_t smem = (size_t)a.G * bit_words(a.cap_clusters) * 4;
+    const size_t smem = (size_t)a.G * bit_words(a.cap_clusters) * 4 + a.cap_clusters + 16;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -676,7 +718,7 @@ cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const 
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    k_compact<<<a.n_slots, kCompactThreads, smem, stream>>>(p);
+    k_compact<<<n_slots, kCompactThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

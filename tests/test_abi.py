@@ -37,10 +37,10 @@ def test_no_cpu_fallback_without_device():
 
 
 def test_create_validates_shape():
-    d = _lib.IndexDesc(1, 96, 4, 64, 8, 8, 4, 0, 0, 1, 0, 1, 0, 0)
+    d = _lib.IndexDesc(1, 96, 4, 64, 8, 8, 4, 0, 0, 1, 0, 1, 0, 0, 0)
     h = C.c_void_p()
     assert _lib.lib().lc_index_create(C.byref(d), C.byref(h)) == _lib.LC_EINVAL
-    d = _lib.IndexDesc(1, 128, 9, 64, 8, 8, 4, 0, 0, 1, 0, 1, 0, 0)
+    d = _lib.IndexDesc(1, 128, 9, 64, 8, 8, 4, 0, 0, 1, 0, 1, 0, 0, 0)
     assert _lib.lib().lc_index_create(C.byref(d), C.byref(h)) == _lib.LC_EINVAL
     assert b"group" in _lib.lib().lc_last_error()
 

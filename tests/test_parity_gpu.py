@@ -88,12 +88,14 @@ def test_degenerate_full_attention():
         assert rel_l2(got[g].output, full) < TOL
 
 
-def test_batched_slots_match_per_head_reference():
-    """8 slots (one layer of 8 KV heads), GQA 4: one batched call == 32 reference calls."""
+@pytest.mark.parametrize("slot_groups", [0, 3])
+def test_batched_slots_match_per_head_reference(slot_groups):
+    """8 slots (one layer of 8 KV heads), GQA 4: one batched call == 32 reference calls
+    (also with the slots split into groups on forked streams)."""
     S, G, n = 8, 4, 8192
     b = api.Budgets(token_budget=2048)
     eng = api.Engine(S, 128, G, cap_tokens=n + 64, cap_chunks=n // 8 + 64, cap_clusters=n // 8,
-                     cap_units=64)
+                     cap_units=64, slot_groups=slot_groups)
     refs, ws = [], []
     for s in range(S):
         w = rounded_workload(n, 128, seed=1000 + s, query_count=G)
