@@ -7,6 +7,7 @@
 
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -430,13 +431,42 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     } else {
         a.cand_scratch = nullptr;
     }
+    // fused per-slot selection (k_select_slot) unless the shape needs the
+    // per-query kernels (LC_SELECT=query forces them)
+    const char* env = getenv("LC_SELECT");
+    const uint32_t kU = std::min<uint32_t>(b->unit_topk, 64);
+    bool use_slot = (env && std::string(env) == "slot") && select_slot_supports_group(a.G) && (a.cap_units % 4) == 0 && a.G * pmax <= 1024 &&
+                    (size_t)a.d * ((pmax + 3) & ~3u) * 4 <= 96 * 1024 && select_slot_smem_bytes(a, pmax) <= 200 * 1024;
+    (void)kU;
+    if (use_slot) {
+        const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
+        if (h->slot_scratch_bytes < need) {
+            if (h->slot_scratch) cudaFree(h->slot_scratch);
+            h->slot_scratch = nullptr;
+            h->slot_scratch_bytes = 0;
+            if (cudaMalloc(&h->slot_scratch, need) != cudaSuccess) {
+                cudaGetLastError();
+                fail(LC_ENOMEM, "selection scratch allocation failed");
+            }
+            h->slot_scratch_bytes = need;
+        }
+    }
+    auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs) {
+        if (use_slot) {
+            ck(launch_select_slot(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
+                                  flags, buf_off, buf_ids, h->slot_scratch, a.max_cand, pmax, count, gs),
+               "k_select_slot");
+        } else {
+            ck(launch_select(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
+                             count, gs), "k_select");
+            ck(launch_compact(ag, b->sink_size, flags, buf_off, buf_ids, count, gs), "k_compact");
+        }
+        if (out_dev) ck(launch_attend(ag, q_dev, out_dev, count, gs), "k_attend");
+    };
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
     if (groups == 1) {
         a.slot0 = 0;
-        ck(launch_select(a, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
-                         a.n_slots, st), "k_select");
-        ck(launch_compact(a, b->sink_size, flags, buf_off, buf_ids, a.n_slots, st), "k_compact");
-        if (out_dev) ck(launch_attend(a, q_dev, out_dev, a.n_slots, st), "k_attend");
+        run_group(a, a.n_slots, st);
     } else {
         // fork: each slot group runs select -> compact -> attend on its own stream,
         // so one group's (latency-bound) selection overlaps another's attention
@@ -450,10 +480,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
             ck(cudaStreamWaitEvent(gs, h->group_events[0], 0), "fork wait");
             Arena ag = a;
             ag.slot0 = s0;
-            ck(launch_select(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
-                             s1 - s0, gs), "k_select");
-            ck(launch_compact(ag, b->sink_size, flags, buf_off, buf_ids, s1 - s0, gs), "k_compact");
-            if (out_dev) ck(launch_attend(ag, q_dev, out_dev, s1 - s0, gs), "k_attend");
+            run_group(ag, s1 - s0, gs);
             ck(cudaEventRecord(h->group_events[gi + 1], gs), "join record");
             ck(cudaStreamWaitEvent(st, h->group_events[gi + 1], 0), "join");
         }

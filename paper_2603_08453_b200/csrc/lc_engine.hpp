@@ -17,6 +17,12 @@ cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, ui
 cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, uint32_t n_slots, cudaStream_t stream);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream);
+size_t select_slot_smem_bytes(const Arena& a, uint32_t pmax);
+bool select_slot_supports_group(uint32_t g);
+cudaError_t launch_select_slot(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
+                               unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
+                               const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t pmax,
+                               uint32_t n_slots, cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
                          cudaStream_t stream);
@@ -95,12 +101,15 @@ struct lc_index_s {
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
     unsigned char* cand_scratch = nullptr;     // k_select overflow storage
     size_t cand_scratch_bytes = 0;
+    unsigned char* slot_scratch = nullptr;     // k_select_slot per-query keys + selections
+    size_t slot_scratch_bytes = 0;
     std::vector<cudaStream_t> group_streams;   // one per slot group
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
 
     ~lc_index_s() {
         for (void* p : owned) cudaFree(p);
         if (cand_scratch) cudaFree(cand_scratch);
+        if (slot_scratch) cudaFree(slot_scratch);
         for (auto s : group_streams) cudaStreamDestroy(s);
         for (auto e : group_events) cudaEventDestroy(e);
     }

@@ -18,6 +18,10 @@
 //    (small) selected set.
 #include "lc_common.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 namespace lc {
 
 struct SelectParams {
@@ -25,7 +29,16 @@ struct SelectParams {
     const float* q;  // [slot][G][d]
     uint32_t unit_topk, mode, cluster_topk, sink;
     unsigned long long budget;
+    unsigned long long* prof;  // optional phase timestamps [slot*G + g][8] (LC_PROF=1)
 };
+
+__device__ __forceinline__ unsigned long long gtime_q() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define LC_QMARK(ph) \
+    if (p.prof && threadIdx.x == 0) p.prof[((size_t)slot * a.G + g) * 8 + (ph)] = gtime_q();
 
 constexpr int kSelThreads = 256;
 constexpr int kSelWarps = kSelThreads / 32;
@@ -86,22 +99,33 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     __shared__ uint32_t s_cbefore, s_state, s_nsel;
     __shared__ int s_shift;
 
+    LC_QMARK(0)
     const float* qg = p.q + ((size_t)slot * a.G + g) * d;
     for (uint32_t j = tid; j < d; j += blockDim.x) qs[j] = qg[j];
     for (uint32_t w = tid; w < nwords; w += blockDim.x) bits[w] = 0u;
     // stage the coarse tier [D][P] (dimension-major rows of cap_units floats)
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
     const bool staged = (size_t)D * Pp * 4 <= (size_t)a.smem_cand * 12 && (a.cap_units & 3) == 0;
-    if (staged) {
-        const uint32_t pq = Pp >> 2;
-        for (uint32_t e = tid; e < D * pq; e += blockDim.x) {
-            const uint32_t j = e / pq, u4 = e % pq;
-            reinterpret_cast<float4*>(ucs + (size_t)j * Pp)[u4] =
-                __ldg(reinterpret_cast<const float4*>(uc + (size_t)j * a.cap_units) + u4);
+    if (staged) {  // batched: every thread issues all its loads before any store
+        const uint32_t pq = Pp >> 2, n4 = D * pq;
+        constexpr int kB = 8;
+        for (uint32_t e0 = 0; e0 < n4; e0 += kB * kSelThreads) {
+            float4 v[kB];
+#pragma unroll
+            for (int t = 0; t < kB; ++t) {
+                const uint32_t e = e0 + t * kSelThreads + tid;
+                if (e < n4) v[t] = __ldg(reinterpret_cast<const float4*>(uc + (size_t)(e / pq) * a.cap_units) + e % pq);
+            }
+#pragma unroll
+            for (int t = 0; t < kB; ++t) {
+                const uint32_t e = e0 + t * kSelThreads + tid;
+                if (e < n4) reinterpret_cast<float4*>(ucs + (size_t)(e / pq) * Pp)[e % pq] = v[t];
+            }
         }
     }
     __syncthreads();
 
+    LC_QMARK(1)
     // ||q|| (kernels.cpp:19-23): sequential, exact products -> DFMA chain
     if (tid == 0) {
         double s = 0.0;
@@ -182,6 +206,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         cw = reinterpret_cast<uint32_t*>(ckey + a.max_cand);
     }
 
+    LC_QMARK(2)
     // tier 2: fine clusters of the kept units (retriever.cpp:118-135); the
     // unit blocks are [D/4][n_u][4]: one float4 per cluster per step, loads
     // double-buffered four quads ahead of the sequential DFMA chain
@@ -189,40 +214,74 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     const double* fr = a.frad + (size_t)slot * a.cap_clusters;
     const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
     unsigned long long kmin = ~0ull, kmax = 0ull;
-    for (uint32_t i = tid; i < nc; i += blockDim.x) {
+    // two candidates per thread at a time: two independent DFMA chains and
+    // twice the loads in flight
+    auto locate = [&](uint32_t i, uint32_t& base, uint32_t& nu, uint32_t& local) {
         uint32_t k = 0;
         while (k + 1 < kU && s_pre[k + 1] <= i) ++k;
-        const uint32_t base = s_base[k], nu = s_nu[k], local = i - s_pre[k];
-        const float4* col = reinterpret_cast<const float4*>(fc + (size_t)base * d) + local;
-        float4 A[4], B[4];
+        base = s_base[k];
+        nu = s_nu[k];
+        local = i - s_pre[k];
+    };
+    for (uint32_t i0 = tid; i0 < nc; i0 += 2 * blockDim.x) {
+        const uint32_t i1 = i0 + blockDim.x;
+        const bool has1 = i1 < nc;
+        uint32_t b0, n0, l0, b1 = 0, n1 = 1, l1 = 0;
+        locate(i0, b0, n0, l0);
+        if (has1) locate(i1, b1, n1, l1);
+        const float4* c0 = reinterpret_cast<const float4*>(fc + (size_t)b0 * d) + l0;
+        const float4* c1 = has1 ? reinterpret_cast<const float4*>(fc + (size_t)b1 * d) + l1 : c0;
+        const uint32_t cid0 = b0 + l0, cid1 = has1 ? b1 + l1 : cid0;
+        const double r0 = fr[cid0], r1 = fr[cid1];
+        const uint32_t w0 = p.mode == 1 ? ft[cid0] : 1u, w1 = p.mode == 1 ? ft[cid1] : 1u;
+        float4 A0[4], A1[4], B0[4], B1[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) A[t] = __ldg(col + (size_t)t * nu);
-        double s = 0.0;
+        for (int t = 0; t < 4; ++t) {
+            A0[t] = __ldg(c0 + (size_t)t * n0);
+            A1[t] = __ldg(c1 + (size_t)t * n1);
+        }
+        double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (uint32_t jq = 0; jq < dq; jq += 4) {
             if (jq + 4 < dq) {
 #pragma unroll
-                for (int t = 0; t < 4; ++t) B[t] = __ldg(col + (size_t)(jq + 4 + t) * nu);
+                for (int t = 0; t < 4; ++t) {
+                    B0[t] = __ldg(c0 + (size_t)(jq + 4 + t) * n0);
+                    B1[t] = __ldg(c1 + (size_t)(jq + 4 + t) * n1);
+                }
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                const float* q4 = qs + 4 * (jq + t);
-                s = __fma_rn((double)q4[0], (double)A[t].x, s);
-                s = __fma_rn((double)q4[1], (double)A[t].y, s);
-                s = __fma_rn((double)q4[2], (double)A[t].z, s);
-                s = __fma_rn((double)q4[3], (double)A[t].w, s);
+                const float4 q4 = reinterpret_cast<const float4*>(qs)[jq + t];
+                s0 = __fma_rn((double)q4.x, (double)A0[t].x, s0);
+                s1 = __fma_rn((double)q4.x, (double)A1[t].x, s1);
+                s0 = __fma_rn((double)q4.y, (double)A0[t].y, s0);
+                s1 = __fma_rn((double)q4.y, (double)A1[t].y, s1);
+                s0 = __fma_rn((double)q4.z, (double)A0[t].z, s0);
+                s1 = __fma_rn((double)q4.z, (double)A1[t].z, s1);
+                s0 = __fma_rn((double)q4.w, (double)A0[t].w, s0);
+                s1 = __fma_rn((double)q4.w, (double)A1[t].w, s1);
             }
             if (jq + 4 < dq) {
 #pragma unroll
-                for (int t = 0; t < 4; ++t) A[t] = B[t];
+                for (int t = 0; t < 4; ++t) {
+                    A0[t] = B0[t];
+                    A1[t] = B1[t];
+                }
             }
         }
-        const uint32_t c = base + local;
-        const unsigned long long key = desc_key(__dadd_rn(s, __dmul_rn(qnorm, fr[c])));
-        ckey[i] = key;
-        cw[i] = p.mode == 1 ? ft[c] : 1u;
-        kmin = min(kmin, key);
-        kmax = max(kmax, key);
+        const unsigned long long k0 = desc_key(__dadd_rn(s0, __dmul_rn(qnorm, r0)));
+        ckey[i0] = k0;
+        cw[i0] = w0;
+        kmin = min(kmin, k0);
+        kmax = max(kmax, k0);
+        if (has1) {
+            const unsigned long long k1 = desc_key(__dadd_rn(s1, __dmul_rn(qnorm, r1)));
+            ckey[i1] = k1;
+            cw[i1] = w1;
+            kmin = min(kmin, k1);
+            kmax = max(kmax, k1);
+        }
     }
     // the bits every candidate shares are skipped by the radix passes
 #pragma unroll
@@ -255,6 +314,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     }
     __syncthreads();
 
+    LC_QMARK(3)
     // weighted prefix select: the longest prefix of the (key, id) order whose
     // weight sum stays <= budget (retriever.cpp:146-153); fixed-k mode is the
     // same with unit weights and budget = k_c (select_topk, retriever.cpp:141)
@@ -387,6 +447,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
     }
     __syncthreads();
 
+    LC_QMARK(4)
     // rank order of the selected set + outputs
     const uint32_t nsel = s_nsel;
     uint32_t* out_cl = a.sel_clusters + ((size_t)slot * a.G + g) * a.cap_clusters;
@@ -413,6 +474,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(SelectParams p) {
         qi->error = 0;
         qi->scanned = (unsigned long long)st.P + nc;
     }
+    LC_QMARK(5)
 }
 
 // ---------------------------------------------------------------------------
@@ -533,18 +595,27 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
         const uint32_t j0 = base + tid * kChunksPerThread;
         uint32_t m8[kChunksPerThread], s8[kChunksPerThread], l8[kChunksPerThread];
         uint32_t cnt = 0, toks = 0;
+        uint32_t cl[kChunksPerThread];
+#pragma unroll
+        for (int e = 0; e < kChunksPerThread; ++e) cl[e] = j0 + e < M ? __ldg(cc + j0 + e) : 0u;
+#pragma unroll
+        for (int e = 0; e < kChunksPerThread; ++e) m8[e] = j0 + e < M ? cmask[cl[e]] : 0u;
+        uint32_t e8[kChunksPerThread];
 #pragma unroll
         for (int e = 0; e < kChunksPerThread; ++e) {
-            const uint32_t j = j0 + e;
-            uint32_t m = 0, s = 0, len = 0;
-            if (j < M) m = cmask[__ldg(cc + j)];
+            s8[e] = m8[e] ? __ldg(cs + j0 + e) : 0u;
+            e8[e] = m8[e] ? __ldg(cs + j0 + e + 1) : 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < kChunksPerThread; ++e) {
+            uint32_t m = m8[e], len = 0;
             if (m) {
-                s = max(__ldg(cs + j), sink_end);
-                const uint32_t e2 = __ldg(cs + j + 1);
-                if (s >= e2) {
+                const uint32_t st0 = max(s8[e], sink_end);
+                if (st0 >= e8[e]) {
                     m = 0;
                 } else {
-                    len = e2 - s;
+                    s8[e] = st0;
+                    len = e8[e] - st0;
                     cnt += 1;
                     toks += len;
 #pragma unroll
@@ -556,7 +627,6 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactParams p) {
                 }
             }
             m8[e] = m;
-            s8[e] = s;
             l8[e] = len;
         }
         const unsigned long long v = ((unsigned long long)cnt << 40) | toks;
@@ -700,11 +770,35 @@ static cudaError_t launch_select_d(const SelectParams& p, uint32_t n_slots, size
 cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
                           uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
                           uint32_t n_slots, cudaStream_t stream) {
-    SelectParams p{a, q, unit_topk, mode, cluster_topk, sink, budget};
+    static unsigned long long* prof = nullptr;
+    if (getenv("LC_PROF") && !prof) cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
+    SelectParams p{a, q, unit_topk, mode, cluster_topk, sink, budget, prof};
     const size_t smem = select_smem_bytes(a);
-    if (a.d == 128) return launch_select_d<128>(p, n_slots, smem, stream);
-    if (a.d == 64) return launch_select_d<64>(p, n_slots, smem, stream);
-    return cudaErrorInvalidValue;
+    cudaError_t e = a.d == 128 ? launch_select_d<128>(p, n_slots, smem, stream)
+                  : a.d == 64  ? launch_select_d<64>(p, n_slots, smem, stream)
+                               : cudaErrorInvalidValue;
+    if (prof && e == cudaSuccess) {
+        cudaStreamSynchronize(stream);
+        std::vector<unsigned long long> t((size_t)a.n_slots * a.G * 8);
+        cudaMemcpy(t.data(), prof, t.size() * 8, cudaMemcpyDeviceToHost);
+        double acc[5] = {0, 0, 0, 0, 0};
+        unsigned long long t0 = ~0ull, t1 = 0;
+        size_t cnt = 0;
+        for (uint32_t s = a.slot0; s < a.slot0 + n_slots; ++s)
+            for (uint32_t g = 0; g < a.G; ++g) {
+                const unsigned long long* r = &t[((size_t)s * a.G + g) * 8];
+                if (r[5] < r[0]) continue;
+                for (int k = 0; k < 5; ++k) acc[k] += (double)(r[k + 1] - r[k]);
+                t0 = r[0] < t0 ? r[0] : t0;
+                t1 = r[5] > t1 ? r[5] : t1;
+                ++cnt;
+            }
+        if (cnt)
+            fprintf(stderr, "[LC_PROF] select(query) per-CTA us: setup %.2f coarse %.2f fine %.2f radix %.2f rank %.2f | span %.1f us\n",
+                    acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3, acc[4] / cnt / 1e3,
+                    (t1 - t0) / 1e3);
+    }
+    return e;
 }
 
 cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
