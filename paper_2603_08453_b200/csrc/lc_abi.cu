@@ -53,7 +53,8 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         if (d.cap_tokens >= (1u << 24)) fail(LC_EINVAL, "lc_index_create: cap_tokens must be < 2^24");
         auto h = std::make_unique<lc_index_s>();
         h->desc = d;
-        if (h->desc.splits == 0) h->desc.splits = 8;
+        if (h->desc.splits == 0) h->desc.splits = 4;
+        if (h->desc.splits > 64) fail(LC_EINVAL, "lc_index_create: splits must be <= 64");
         h->set_device();
         Arena& a = h->a;
         a.n_slots = d.n_slots;
@@ -84,6 +85,12 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.forig = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.fnmem = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.funit = dalloc<uint32_t>(S * d.cap_clusters, o);
+        a.fmem_off = dalloc<uint32_t>(S * (d.cap_clusters + 1), o);
+        a.fmem = dalloc<uint32_t>(S * d.cap_chunks, o);
+        a.plan_bytes = (uint32_t)((64 + (size_t)d.cap_units * (4 + d.group) * 4 + 15) & ~15ull);
+        a.plan = dalloc<unsigned char>(S * a.plan_bytes, o);
+        a.chunk_bits = dalloc<uint32_t>(S * G * bit_words(d.cap_chunks), o);
+        a.split_span = dalloc<uint32_t>(S * 64, o);
         a.state = dalloc<SlotState>(S, o);
         a.qinfo = dalloc<QInfo>(S * G, o);
         a.sel_units = dalloc<uint32_t>(S * G * d.cap_units, o);
@@ -196,6 +203,14 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
             cc[j] = int_of[ix->cluster_of_chunk[j]];
         }
         cs[M] = chunked_end;
+        // member CSR by internal cluster id, chunk ids ascending
+        std::vector<uint32_t> moff(L + 1, 0), mem(M);
+        for (uint32_t j = 0; j < M; ++j) ++moff[cc[j] + 1];
+        for (uint32_t c = 0; c < L; ++c) moff[c + 1] += moff[c];
+        {
+            std::vector<uint32_t> cur(moff.begin(), moff.end() - 1);
+            for (uint32_t j = 0; j < M; ++j) mem[cur[cc[j]]++] = j;
+        }
         const size_t so = slot;
         auto up = [&](void* dst, const void* src, size_t bytes) {
             if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
@@ -213,6 +228,8 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         up(a.forig + so * a.cap_clusters, orig.data(), orig.size() * 4);
         up(a.fnmem + so * a.cap_clusters, fn.data(), fn.size() * 4);
         up(a.funit + so * a.cap_clusters, fu.data(), fu.size() * 4);
+        up(a.fmem_off + so * (a.cap_clusters + 1), moff.data(), moff.size() * 4);
+        up(a.fmem + so * a.cap_chunks, mem.data(), mem.size() * 4);
         HostSlot& hs = h->hs[slot];
         hs = HostSlot{};
         hs.kind.resize(M);
@@ -229,6 +246,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         st.n_tokens = n_tokens;
         st.chunked_end = chunked_end;
         st.n_chunks = M;
+        st.m0 = M;
         st.L = L;
         st.P = P;
         up(a.state + slot, &st, sizeof st);
@@ -431,14 +449,16 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     } else {
         a.cand_scratch = nullptr;
     }
-    // fused per-slot selection (k_select_slot) unless the shape needs the
-    // per-query kernels (LC_SELECT=query forces them)
+    // selection pipeline: "three" (k_coarse -> k_fine -> k_pick, default),
+    // "slot" (fused per-slot kernel) or "query" (per-head k_select + k_compact)
     const char* env = getenv("LC_SELECT");
-    const uint32_t kU = std::min<uint32_t>(b->unit_topk, 64);
-    bool use_slot = (env && std::string(env) == "slot") && select_slot_supports_group(a.G) && (a.cap_units % 4) == 0 && a.G * pmax <= 1024 &&
-                    (size_t)a.d * ((pmax + 3) & ~3u) * 4 <= 96 * 1024 && select_slot_smem_bytes(a, pmax) <= 200 * 1024;
-    (void)kU;
-    if (use_slot) {
+    const std::string mode_s = env ? std::string(env) : std::string("three");
+    const bool shape_ok = select_slot_supports_group(a.G) && (a.cap_units % 4) == 0 && a.G * pmax <= 1024 &&
+                          (size_t)a.d * ((pmax + 3) & ~3u) * 4 <= 96 * 1024;
+    const bool use_three = mode_s == "three" && shape_ok && select3_pick_smem(a) <= 200 * 1024;
+    const bool use_slot = mode_s == "slot" && shape_ok && select_slot_smem_bytes(a, pmax) <= 200 * 1024;
+    const uint32_t max_union = needed_candidates(h, std::min<uint32_t>(a.G * std::min<uint32_t>(b->unit_topk, 64), 4096));
+    if (use_slot || use_three) {
         const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
         if (h->slot_scratch_bytes < need) {
             if (h->slot_scratch) cudaFree(h->slot_scratch);
@@ -452,7 +472,12 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         }
     }
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs) {
-        if (use_slot) {
+        if (!use_three) ag.split_span = nullptr;  // only k_spans precomputes the split starts
+        if (use_three) {
+            ck(launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, flags,
+                              buf_off, buf_ids, h->slot_scratch, a.max_cand, max_union, pmax, count, gs),
+               "k_select3");
+        } else if (use_slot) {
             ck(launch_select_slot(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
                                   flags, buf_off, buf_ids, h->slot_scratch, a.max_cand, pmax, count, gs),
                "k_select_slot");
@@ -487,6 +512,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     }
     h->last_flags = flags;
     h->last_valid = 1;
+    h->last_three = use_three;
 }
 
 int lc_retrieve(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
@@ -504,6 +530,7 @@ int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* 
         h->set_device();
         Arena a = h->a;
         a.slot0 = 0;
+        if (!h->last_three) a.split_span = nullptr;
         ck(launch_attend(a, q_dev, out_dev, a.n_slots, (cudaStream_t)stream), "k_attend");
     });
 }

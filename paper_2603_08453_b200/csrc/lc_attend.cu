@@ -25,13 +25,26 @@
 //   Out: thread (r, c) owns query r dims [c*D/4, c*D/4 + D/4).
 #include "lc_common.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 namespace lc {
 
 struct AttendParams {
     Arena a;
     const float* q;  // [slot][G][D]
     float* out;      // [slot][G][D]
+    unsigned long long* prof;  // optional per-CTA phase timestamps (LC_PROF=1)
 };
+
+__device__ __forceinline__ unsigned long long gtime_a() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define LC_AMARK(ph) \
+    if (p.prof && threadIdx.x == 0) p.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ph)] = gtime_a();
 
 constexpr int kAttThreads = 128;
 constexpr int kAttWarps = kAttThreads / 32;
@@ -100,10 +113,11 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     __shared__ uint32_t s_sstart[kWindow + 1];
     __shared__ uint32_t s_slm[kWindow + 1];
     __shared__ uint32_t s_soff[kWindow + 2];
-    __shared__ uint32_t s_lohi[2];
+    __shared__ uint32_t s_lohi[3];
     __shared__ float s_m[kAttWarps][kMaxGroup], s_l[kAttWarps][kMaxGroup];
     __shared__ uint32_t s_last;
 
+    LC_AMARK(0)
     const uint32_t ns = a.n_spans[slot];
     const uint32_t* soff = a.span_off + (size_t)slot * (a.cap_spans + 1);
     const Span* sp = a.spans + (size_t)slot * a.cap_spans;
@@ -135,6 +149,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     float m_run = -INFINITY, l_run = 0.f;
+    LC_AMARK(1)
 
     // cp.async of one 16-token group into stage `st`: each 8-lane quarter-warp
     // copies one contiguous 128-byte half row, so every request is a full line
@@ -154,37 +169,39 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         }
     };
 
+    // first span of this split: precomputed by the span builder (k_spans) or searched
+    if (tid == 0) {
+        uint32_t k0 = 0;
+        if (a.split_span && beg < end) {
+            k0 = a.split_span[(size_t)slot * 64 + split];
+        } else if (beg < end) {
+            uint32_t lo = 0, hi = ns;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (soff[mid] <= beg) lo = mid;
+                else hi = mid;
+            }
+            k0 = lo;
+        }
+        s_lohi[0] = k0;
+        // last span of this split bounds every window's span load
+        s_lohi[2] = (a.split_span && split + 1 < S) ? a.split_span[(size_t)slot * 64 + split + 1] : ns - 1;
+    }
+    __syncthreads();
+    const uint32_t k_last = s_lohi[2];
     for (uint32_t wb = beg; wb < end; wb += kWindow) {
         const uint32_t we = min(end, wb + kWindow), wn = we - wb;
-        // spans covering [wb, we): last span with off <= wb .. last span with off <= we-1
-        if (warp == 0) {
-            for (int which = 0; which < 2; ++which) {
-                const uint32_t target = which == 0 ? wb : we - 1;
-                uint32_t lo = 0, hi = ns;
-                while (hi - lo > 1) {
-                    const uint32_t step = (hi - lo + 31) / 32;
-                    const uint32_t probe = lo + (uint32_t)lane * step;
-                    const bool ok = probe < hi && soff[probe] <= target;
-                    const unsigned int bal = __ballot_sync(0xffffffffu, ok);
-                    const int last = 31 - __clz(bal);
-                    const uint32_t nlo = lo + (uint32_t)last * step;
-                    hi = min(hi, nlo + step);
-                    lo = nlo;
-                    if (step == 1) break;
-                }
-                if (lane == 0) s_lohi[which] = lo;
-            }
+        // every span touching [wb, we) lies in [k0, k0 + wn] (spans hold >= 1 token):
+        // one batched load of those spans, then all lookups in shared memory
+        const uint32_t k0 = s_lohi[0];
+        const uint32_t nsp = min(min(ns - k0, wn + 1), k_last + 1 - k0);
+        for (uint32_t k = tid; k < nsp; k += blockDim.x) {
+            const Span sk = sp[k0 + k];
+            s_sstart[k] = sk.start;
+            s_slm[k] = sk.len_mask;
+            s_soff[k] = soff[k0 + k];
         }
         __syncthreads();
-        const uint32_t k0 = s_lohi[0], k1 = s_lohi[1];
-        for (uint32_t k = k0 + tid; k <= k1; k += blockDim.x) {
-            const Span sk = sp[k];
-            s_sstart[k - k0] = sk.start;
-            s_slm[k - k0] = sk.len_mask;
-            s_soff[k - k0] = soff[k];
-        }
-        __syncthreads();
-        const uint32_t nsp = k1 - k0 + 1;
         for (uint32_t t = tid; t < kWindow; t += blockDim.x) {
             if (t < wn) {
                 const uint32_t tokpos = wb + t;
@@ -196,13 +213,18 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
                 }
                 s_row[t] = s_sstart[lo] + (tokpos - s_soff[lo]);
                 s_msk[t] = (uint8_t)(s_slm[lo] & 0xffu);
+                if (t == wn - 1) {  // the next window starts in the span holding token we
+                    s_lohi[1] = (lo + 1 < nsp && s_soff[lo + 1] <= we) ? k0 + lo + 1 : k0 + lo;
+                }
             } else {
                 s_row[t] = 0;
                 s_msk[t] = 0;
             }
         }
         __syncthreads();
+        if (tid == 0) s_lohi[0] = s_lohi[1];
 
+        if (wb == beg) LC_AMARK(2)
         // this warp's groups: grp = warp, warp + 4, ...
         const uint32_t ngrp = (wn + 15) / 16;
         const uint32_t my_n = ngrp > (uint32_t)warp ? (ngrp - warp + kAttWarps - 1) / kAttWarps : 0u;
@@ -221,19 +243,28 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
             __syncwarp();
             const uint32_t t0 = (warp + it * kAttWarps) * 16;
             const uint32_t sb = ring_s + (uint32_t)(it % kStages) * STAGE;
-            // ---- S = Q K^T (hi rows r, lo rows r+8) ----
-            float sc[2][4];
+            // ---- S = Q K^T (hi rows r, lo rows r+8): even / odd k-steps accumulate
+            // separately so the MMA dependency chains are half as long ----
+            float sc[2][4], sd[2][4];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
                 sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-                const uint32_t row = 8 * nt + r;
+                sd[nt][0] = sd[nt][1] = sd[nt][2] = sd[nt][3] = 0.f;
+            }
 #pragma unroll
-                for (int w = 0; w < KW; ++w) {
+            for (int w = 0; w < KW; ++w) {
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const uint32_t row = 8 * nt + r;
                     const uint4 kv = lds128(sb + row * ROWB + swz(row, c * KW + w) * 16);
                     mma16816(sc[nt], qf[2 * w], kv.x, kv.y);
-                    mma16816(sc[nt], qf[2 * w + 1], kv.z, kv.w);
+                    mma16816(sd[nt], qf[2 * w + 1], kv.z, kv.w);
                 }
             }
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) sc[nt][e] += sd[nt][e];
             // logits of query r for tokens 2c, 2c+1 (nt 0) and 8+2c, 9+2c (nt 1)
             float lg[4];
             bool ok[4];
@@ -309,6 +340,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         __syncthreads();
     }
 
+    LC_AMARK(3)
     // ---- warp partial -> CTA partial (the stage ring is free now) ----
     float* s_o = reinterpret_cast<float*>(dsm);  // [warps][G][D]
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
@@ -349,7 +381,11 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(a.counters + slot, 1u) == S - 1 ? 1u : 0u;
     __syncthreads();
-    if (!s_last) return;
+    LC_AMARK(4)
+    if (!s_last) {
+        LC_AMARK(5)
+        return;
+    }
     __threadfence();
     const float* parts = a.partials + (size_t)slot * S * G * (D + 2);
     for (uint32_t x = tid; x < G * D; x += blockDim.x) {
@@ -374,6 +410,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         }
     }
     if (tid == 0) a.counters[slot] = 0;
+    LC_AMARK(5)
 }
 
 template <int D>
@@ -393,11 +430,31 @@ static cudaError_t launch_attend_d(const AttendParams& p, dim3 grid, cudaStream_
 }
 
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream) {
-    AttendParams p{a, q, out};
+    static unsigned long long* prof = nullptr;
+    const size_t nct = (size_t)a.splits * n_slots;
+    if (getenv("LC_PROF") && !prof) cudaMalloc(&prof, (size_t)a.n_slots * 64 * 8 * 8);
+    AttendParams p{a, q, out, prof};
     dim3 grid(a.splits, n_slots);
-    if (a.d == 128) return launch_attend_d<128>(p, grid, stream);
-    if (a.d == 64) return launch_attend_d<64>(p, grid, stream);
-    return cudaErrorInvalidValue;
+    cudaError_t e = a.d == 128 ? launch_attend_d<128>(p, grid, stream)
+                  : a.d == 64  ? launch_attend_d<64>(p, grid, stream)
+                               : cudaErrorInvalidValue;
+    if (prof && e == cudaSuccess) {
+        cudaStreamSynchronize(stream);
+        std::vector<unsigned long long> t(nct * 8);
+        cudaMemcpy(t.data(), prof, t.size() * 8, cudaMemcpyDeviceToHost);
+        double acc[5] = {0, 0, 0, 0, 0};
+        unsigned long long t0 = ~0ull, t1 = 0;
+        for (size_t c = 0; c < nct; ++c) {
+            const unsigned long long* x = &t[c * 8];
+            for (int k = 0; k < 5; ++k) acc[k] += (double)(x[k + 1] - x[k]);
+            t0 = x[0] < t0 ? x[0] : t0;
+            t1 = x[5] > t1 ? x[5] : t1;
+        }
+        fprintf(stderr, "[LC_PROF] k_attend per-CTA us: q %.2f spans %.2f stream %.2f combine %.2f merge %.2f | span %.1f us\n",
+                acc[0] / nct / 1e3, acc[1] / nct / 1e3, acc[2] / nct / 1e3, acc[3] / nct / 1e3, acc[4] / nct / 1e3,
+                (t1 - t0) / 1e3);
+    }
+    return e;
 }
 
 }  // namespace lc

@@ -41,7 +41,8 @@ struct SlotState {
     uint32_t n_chunks;
     uint32_t L;
     uint32_t P;
-    uint32_t pad[3];
+    uint32_t m0;      // chunks covered by the member CSR (prefill); later ones are grafts
+    uint32_t pad[2];
 };
 
 struct Span {  // one contiguous run of active tokens and the query heads it serves
@@ -77,6 +78,8 @@ struct Arena {
     uint32_t* forig;
     uint32_t* fnmem;
     uint32_t* funit;
+    uint32_t* fmem_off;      // [slot][cap_clusters+1] member CSR of the prefill chunks (internal ids)
+    uint32_t* fmem;          // [slot][cap_chunks] chunk ids, ascending per cluster
     SlotState* state;
     // per-step selection products
     QInfo* qinfo;            // [slot][G]
@@ -84,6 +87,10 @@ struct Arena {
     uint32_t* sel_clusters;  // [slot][G][cap_clusters] reference ids, rank order
     uint32_t* sel_bits;      // [slot][G][words(cap_clusters)] internal-id bitmap
     unsigned char* cand_scratch;  // [slot][G][max_cand * 12] overflow of k_select's smem
+    unsigned char* plan;          // [slot][plan_bytes] coarse-tier plan of the 3-kernel selection
+    uint32_t* chunk_bits;         // [slot][G][words(cap_chunks)] per-head active chunk bitmaps
+    uint32_t* split_span;         // [slot][64] first span of each attention split (k_spans), or null
+    uint32_t plan_bytes;
     Span* spans;             // [slot][cap_spans]
     uint32_t* span_off;      // [slot][cap_spans+1] token prefix offsets
     uint32_t* n_spans;       // [slot]

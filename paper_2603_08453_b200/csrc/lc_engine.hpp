@@ -19,6 +19,11 @@ cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const 
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream);
 size_t select_slot_smem_bytes(const Arena& a, uint32_t pmax);
 bool select_slot_supports_group(uint32_t g);
+size_t select3_pick_smem(const Arena& a);
+cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
+                           unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
+                           const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
+                           uint32_t pmax, uint32_t n_slots, cudaStream_t stream);
 cudaError_t launch_select_slot(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                                unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                                const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t pmax,
@@ -98,6 +103,7 @@ struct lc_index_s {
     lc_graft_report* rep_scratch = nullptr;
     uint32_t last_flags = 0;
     uint32_t last_valid = 0;
+    bool last_three = false;
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
     unsigned char* cand_scratch = nullptr;     // k_select overflow storage
     size_t cand_scratch_bytes = 0;

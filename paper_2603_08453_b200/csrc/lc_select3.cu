@@ -1,0 +1,976 @@
+// Three-kernel selection pipeline (north star item 2), one phase per kernel so
+// that each phase runs with the parallelism it needs:
+//
+//   k_coarse  (one CTA per slot): ||q_g|| and the coarse tier for all G query
+//             heads of the GQA group (retriever.cpp:97-116), per-head top-k_g
+//             units, and the union of the kept units with each head's
+//             candidate offsets -> a small per-slot plan in global memory.
+//   k_fine    (one warp per 32 union candidates, grid over all slots): each lane
+//             loads its candidate's whole centroid (one [d/4][n_u][4] column,
+//             512-byte lines across the warp) into registers, then runs one
+//             sequential fp64 chain per head that kept the unit -- bit-exact
+//             kernels::dot, upper bound dot + ||q||*r (kernels.cpp:155-159).
+//             Pure streaming: every centroid of the union is read once.
+//   k_pick    (one CTA per slot): per head, on its own warps, the exact
+//             weighted radix select of the token-budget prefix / fixed k_c
+//             (retriever.cpp:140-154) and the rank sort of the selection; then
+//             the union active spans from the member lists of the selected
+//             clusters (collect_active, retriever.cpp:60-74).
+#include "lc_common.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+namespace lc {
+
+namespace {
+
+constexpr int kMaxKU3 = 64;
+
+// plan layout (bytes): 0: u32 degenerate, nuu, ncu, kU, nc[8]; 64: u64 kmin[8];
+// 128: u64 kmax[8]; 192: f64 qnorm[8]; 256: units u32 [k][4 + G] =
+// unit, mask, base, n_u, qoff[G]
+struct PlanView {
+    unsigned char* b;
+    __device__ uint32_t* hdr() const { return reinterpret_cast<uint32_t*>(b); }
+    __device__ unsigned long long* kmin() const { return reinterpret_cast<unsigned long long*>(b + 64); }
+    __device__ unsigned long long* kmax() const { return reinterpret_cast<unsigned long long*>(b + 128); }
+    __device__ double* qnorm() const { return reinterpret_cast<double*>(b + 192); }
+    __device__ uint32_t* units() const { return reinterpret_cast<uint32_t*>(b + 256); }
+};
+
+__device__ __forceinline__ void bar_g(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+}  // namespace
+
+struct Sel3Params {
+    Arena a;
+    uint32_t keys_cap;  // per-head candidates staged in k_pickq's shared memory
+    const float* q;  // [slot][G][d]
+    uint32_t unit_topk, mode, cluster_topk, sink, flags;
+    unsigned long long budget;
+    const uint32_t* buf_off;
+    const uint32_t* buf_ids;
+    unsigned char* scratch;  // per slot: keys u64 [G][qcap] + weights/selection u32 [G][qcap]
+    uint32_t qcap;
+    unsigned long long* prof;  // optional k_pick phase timestamps [slot][8] (LC_PROF=1)
+};
+
+__device__ __forceinline__ unsigned long long gtime3() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define LC_PMARK(ph) \
+    if (p.prof && threadIdx.x == 0) p.prof[((size_t)slot * GQ + blockIdx.x) * 8 + (ph)] = gtime3();
+
+// ---------------------------------------------------------------------------
+constexpr int kCoThreads = 256;
+
+template <int D, int GQ>
+__global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Arena& a = p.a;
+    const uint32_t slot = a.slot0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t G = GQ, d = D;
+    const SlotState st = a.state[slot];
+    const uint32_t n = st.n_tokens, P = st.P;
+    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    QInfo* qi = a.qinfo + (size_t)slot * G;
+    const bool degenerate = (p.mode == 1 && (unsigned long long)n <= p.budget) || st.n_chunks == 0;
+    if (degenerate) {
+        if (tid == 0) {
+            pv.hdr()[0] = 1;
+            pv.hdr()[1] = pv.hdr()[2] = 0;
+        }
+        return;
+    }
+    const uint32_t Pp = (P + 3) & ~3u;
+    double* qd = reinterpret_cast<double*>(smem);            // [G][D]
+    float* ucs = reinterpret_cast<float*>(qd + G * D);       // [D][Pp]
+    unsigned long long* ukey = reinterpret_cast<unsigned long long*>(ucs + (size_t)D * Pp);  // [G][P]
+    __shared__ double s_qn[GQ];
+    __shared__ uint32_t s_kept[GQ][kMaxKU3];
+
+    for (uint32_t x = tid; x < G * D; x += blockDim.x) qd[x] = (double)p.q[(size_t)slot * G * D + x];
+    const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
+    {
+        const uint32_t pq = Pp >> 2, n4 = D * pq;
+        constexpr int kB = 8;
+        for (uint32_t e0 = 0; e0 < n4; e0 += kB * kCoThreads) {
+            float4 v[kB];
+#pragma unroll
+            for (int t = 0; t < kB; ++t) {
+                const uint32_t e = e0 + t * kCoThreads + tid;
+                if (e < n4) v[t] = __ldg(reinterpret_cast<const float4*>(uc + (size_t)(e / pq) * a.cap_units) + e % pq);
+            }
+#pragma unroll
+            for (int t = 0; t < kB; ++t) {
+                const uint32_t e = e0 + t * kCoThreads + tid;
+                if (e < n4) reinterpret_cast<float4*>(ucs + (size_t)(e / pq) * Pp)[e % pq] = v[t];
+            }
+        }
+    }
+    __syncthreads();
+    // ||q_g|| (kernels.cpp:19-23) on the last warp; coarse dots on the others
+    if (warp == kCoThreads / 32 - 1) {
+        if (lane < G) {
+            double s = 0.0;
+            const double* qg = qd + lane * D;
+#pragma unroll 8
+            for (uint32_t j = 0; j < d; ++j) s = __fma_rn(qg[j], qg[j], s);
+            s_qn[lane] = __dsqrt_rn(s);
+        }
+    } else {
+        for (uint32_t x = tid; x < G * P; x += kCoThreads - 32) {
+            const uint32_t g = x / P, u = x % P;
+            const double* qg = qd + g * D;
+            double s = 0.0;
+#pragma unroll 8
+            for (uint32_t j = 0; j < d; ++j) s = __fma_rn(qg[j], (double)ucs[j * Pp + u], s);
+            ukey[x] = __double_as_longlong(s);  // raw dot for now
+        }
+    }
+    __syncthreads();
+    const double* ur = a.urad + (size_t)slot * a.cap_units;
+    for (uint32_t x = tid; x < G * P; x += kCoThreads) {
+        const uint32_t g = x / P, u = x % P;
+        ukey[x] = desc_key(__dadd_rn(__longlong_as_double(ukey[x]), __dmul_rn(s_qn[g], ur[u])));
+    }
+    __syncthreads();
+    const uint32_t kU = min(min(p.unit_topk, P), (uint32_t)kMaxKU3);
+    for (uint32_t x = tid; x < G * P; x += kCoThreads) {
+        const uint32_t g = x / P, u = x % P;
+        const unsigned long long* kg = ukey + (size_t)g * P;
+        const unsigned long long ku = kg[u];
+        uint32_t rank = 0;
+        for (uint32_t v = 0; v < P; ++v) rank += (kg[v] < ku || (kg[v] == ku && v < u)) ? 1u : 0u;
+        if (rank < kU) s_kept[g][rank] = u;
+    }
+    __syncthreads();
+    // selected_units (rank order) and the union of kept units in ascending unit order
+    for (uint32_t x = tid; x < G * kU; x += kCoThreads)
+        a.sel_units[((size_t)slot * G + x / kU) * a.cap_units + x % kU] = s_kept[x / kU][x % kU];
+    const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
+    if (warp == 0) {
+        uint32_t* uu = pv.units();
+        const uint32_t stride = 4 + G;
+        uint32_t pos = 0, ncu = 0;
+        uint32_t qacc[GQ];
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) qacc[g] = 0;
+        for (uint32_t u0 = 0; u0 < P; u0 += 32) {
+            const uint32_t u = u0 + lane;
+            uint32_t m = 0;
+            if (u < P)
+#pragma unroll
+                for (int g = 0; g < GQ; ++g)
+                    for (uint32_t k = 0; k < kU; ++k) m |= (s_kept[g][k] == u ? 1u : 0u) << g;
+            const unsigned int bal = __ballot_sync(0xffffffffu, m != 0);
+            const uint32_t nu = m ? uoff[u + 1] - uoff[u] : 0u;
+            const uint32_t idx = pos + __popc(bal & ((1u << lane) - 1u));
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) {
+                const uint32_t mine = ((m >> g) & 1u) ? nu : 0u;
+                uint32_t x = mine;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
+                }
+                if (m) uu[idx * stride + 4 + g] = qacc[g] + x - mine;
+                qacc[g] += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (m) {
+                uu[idx * stride + 0] = u;
+                uu[idx * stride + 1] = m;
+                uu[idx * stride + 2] = uoff[u];
+                uu[idx * stride + 3] = nu;
+            }
+            ncu += __reduce_add_sync(0xffffffffu, nu);
+            pos += __popc(bal);
+        }
+        if (lane == 0) {
+            pv.hdr()[0] = 0;
+            pv.hdr()[1] = pos;
+            pv.hdr()[2] = ncu;
+            pv.hdr()[3] = kU;
+        }
+        if (lane < G) {
+            pv.hdr()[4 + lane] = qacc[lane];
+            pv.kmin()[lane] = ~0ull;
+            pv.kmax()[lane] = 0ull;
+            pv.qnorm()[lane] = s_qn[lane];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kFiThreads = 128;  // 4 warps, one 32-candidate tile each
+
+template <int D, int GQ>
+__global__ void __launch_bounds__(kFiThreads) k_fine(Sel3Params p) {
+    const Arena& a = p.a;
+    const uint32_t slot = a.slot0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t G = GQ, d = D, dq = D / 4;
+    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    __shared__ uint32_t s_hdr[8];
+    __shared__ double s_q[GQ][D];
+    __shared__ double s_qn[GQ];
+    __shared__ uint32_t s_u[kMaxKU3 * GQ][4 + GQ];
+    if (tid < 4) s_hdr[tid] = pv.hdr()[tid];
+    __syncthreads();
+    const uint32_t ncu = s_hdr[2], nuu = s_hdr[1];
+    const uint32_t ntile = (ncu + 31) / 32, nwarps_total = gridDim.x * (kFiThreads / 32);
+    const uint32_t wglobal = blockIdx.x * (kFiThreads / 32) + warp;
+    if (s_hdr[0] || blockIdx.x * (kFiThreads / 32) >= ntile) return;
+    for (uint32_t x = tid; x < G * D; x += blockDim.x) s_q[x / D][x % D] = (double)p.q[(size_t)slot * G * D + x];
+    if (tid < G) s_qn[tid] = pv.qnorm()[tid];
+    for (uint32_t x = tid; x < nuu * (4 + G); x += blockDim.x) s_u[x / (4 + G)][x % (4 + G)] = pv.units()[x];
+    __syncthreads();
+    const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(p.scratch + (size_t)slot * G * p.qcap * 12);
+    uint32_t* wts = reinterpret_cast<uint32_t*>(keys + (size_t)G * p.qcap);
+    unsigned long long wmin[GQ], wmax[GQ];
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) {
+        wmin[g] = ~0ull;
+        wmax[g] = 0ull;
+    }
+    // warps stride over this slot's 32-candidate tiles
+    for (uint32_t tile = wglobal; tile < ntile; tile += nwarps_total) {
+        const uint32_t ci = tile * 32 + lane;
+        const bool active = ci < ncu;
+        uint32_t k = 0, acc = 0;
+        if (active)
+            while (k + 1 < nuu && acc + s_u[k][3] <= ci) {
+                acc += s_u[k][3];
+                ++k;
+            }
+        const uint32_t local = ci - acc, base = s_u[k][2], nu = s_u[k][3], m = active ? s_u[k][1] : 0u;
+        const float4* col = reinterpret_cast<const float4*>(fc + (size_t)base * d) + local;
+        float4 v[dq];
+        if (active) {
+#pragma unroll
+            for (uint32_t jq = 0; jq < dq; ++jq) v[jq] = __ldg(col + (size_t)jq * nu);
+        }
+        const uint32_t cid = base + local;
+        const double r = active ? a.frad[(size_t)slot * a.cap_clusters + cid] : 0.0;
+        const uint32_t w = active ? (p.mode == 1 ? a.ftok[(size_t)slot * a.cap_clusters + cid] : 1u) : 0u;
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) {
+            if ((m >> g) & 1u) {
+                double sacc = 0.0;
+#pragma unroll
+                for (uint32_t jq = 0; jq < dq; ++jq) {
+                    sacc = __fma_rn(s_q[g][4 * jq + 0], (double)v[jq].x, sacc);
+                    sacc = __fma_rn(s_q[g][4 * jq + 1], (double)v[jq].y, sacc);
+                    sacc = __fma_rn(s_q[g][4 * jq + 2], (double)v[jq].z, sacc);
+                    sacc = __fma_rn(s_q[g][4 * jq + 3], (double)v[jq].w, sacc);
+                }
+                const unsigned long long key = desc_key(__dadd_rn(sacc, __dmul_rn(s_qn[g], r)));
+                const size_t at = (size_t)g * p.qcap + s_u[k][4 + g] + local;
+                keys[at] = key;
+                wts[at] = w;
+                wmin[g] = min(wmin[g], key);
+                wmax[g] = max(wmax[g], key);
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) {
+        unsigned long long mn = wmin[g], mx = wmax[g];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0 && mx != 0ull) {
+            atomicMin(pv.kmin() + g, mn);
+            atomicMax(pv.kmax() + g, mx);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kPkThreads = 256;
+constexpr int kPkWarps = kPkThreads / 32;
+constexpr uint32_t kPickStageTotal = 512;
+  // selected clusters ranked from shared memory (all heads)
+
+template <typename T>
+__device__ __forceinline__ T pk_scan(T v, T* wt, T& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wt[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        T t = lane < kPkWarps ? wt[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < kPkWarps) wt[lane] = t;
+    }
+    __syncthreads();
+    const T base = warp > 0 ? wt[warp - 1] : T(0);
+    total = wt[kPkWarps - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+// k_pickq: one CTA per query head (128 threads).  Dynamic smem:
+//   keys u64 [kPickKeysCap], weights / selection u32 [kPickKeysCap] (staged),
+//   cbits u32 [words(cap_chunks)] this head's active-chunk bitmap.
+constexpr int kPqThreads = 128;
+constexpr int kPqWarps = kPqThreads / 32;
+
+template <int GQ>
+__global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
+    extern __shared__ __align__(16) unsigned char qsm[];
+    const Arena& a = p.a;
+    const uint32_t g = blockIdx.x, slot = a.slot0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t G = GQ;
+    const SlotState st = a.state[slot];
+    const uint32_t M = st.n_chunks, P = st.P, L = st.L;
+    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    QInfo* qi = a.qinfo + (size_t)slot * G + g;
+    if (pv.hdr()[0]) return;  // degenerate slot: k_spans writes everything
+    LC_PMARK(0)
+    const uint32_t mwcap = bit_words(a.cap_chunks), mw = bit_words(M);
+    unsigned long long* sk = reinterpret_cast<unsigned long long*>(qsm);
+    uint32_t* sw = reinterpret_cast<uint32_t*>(sk + p.keys_cap);
+    uint32_t* cb = sw + p.keys_cap;
+    __shared__ uint32_t s_gbase[kMaxKU3], s_gpre[kMaxKU3 + 1], s_nc, s_kU;
+    __shared__ uint32_t hw[256], hc[256];
+    __shared__ unsigned long long s_prefix, s_mask, s_wbefore;
+    __shared__ uint32_t s_cbefore, s_state, s_nsel;
+    __shared__ int s_shift;
+    constexpr uint32_t kStage = 512;
+    __shared__ unsigned long long s_sk[kStage];
+    __shared__ uint32_t s_sc[kStage], s_so[kStage];
+    for (uint32_t w = tid; w < mw; w += blockDim.x) cb[w] = 0u;
+    __shared__ uint32_t s_uu[kMaxKU3 * GQ * 3];  // (mask, base, qoff_g) of the union units, staged
+    __shared__ uint32_t s_nuu;
+    if (tid == 0) s_nuu = pv.hdr()[1];
+    __syncthreads();
+    {
+        const uint32_t* uu = pv.units();
+        for (uint32_t k = tid; k < s_nuu; k += blockDim.x) {
+            s_uu[3 * k + 0] = uu[k * (4 + G) + 1];
+            s_uu[3 * k + 1] = uu[k * (4 + G) + 2];
+            s_uu[3 * k + 2] = uu[k * (4 + G) + 4 + g];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t k2 = 0;
+        for (uint32_t k = 0; k < s_nuu; ++k)
+            if ((s_uu[3 * k] >> g) & 1u) {
+                s_gbase[k2] = s_uu[3 * k + 1];
+                s_gpre[k2] = s_uu[3 * k + 2];
+                ++k2;
+            }
+        s_nc = pv.hdr()[4 + g];
+        s_gpre[k2] = s_nc;
+        s_kU = pv.hdr()[3];
+        const unsigned long long mn = pv.kmin()[g], mx = pv.kmax()[g];
+        const unsigned long long diff = mn ^ mx;
+        const int top = diff ? 63 - __clzll((long long)diff) : 0;
+        const int shift = (top / 8) * 8;
+        const unsigned long long mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
+        s_prefix = mn & mask;
+        s_mask = mask;
+        s_shift = shift;
+        s_wbefore = 0;
+        s_cbefore = 0;
+        s_state = 0;
+        s_nsel = 0;
+    }
+    __syncthreads();
+    const uint32_t nc = s_nc, kU = s_kU;
+    if (nc == 0 || nc > p.qcap) {
+        if (tid == 0) {
+            qi->error = nc == 0 ? kErrEmptyCand : kErrCandOverflow;
+            qi->degenerate = 0;
+            qi->n_units = kU;
+            qi->n_clusters = 0;
+            qi->scanned = P + nc;
+            atomicOr(a.err, qi->error);
+        }
+        return;
+    }
+    unsigned long long* kg = reinterpret_cast<unsigned long long*>(p.scratch + (size_t)slot * G * p.qcap * 12) +
+                             (size_t)g * p.qcap;
+    uint32_t* sg = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(
+                       p.scratch + (size_t)slot * G * p.qcap * 12) + (size_t)G * p.qcap) + (size_t)g * p.qcap;
+    if (nc <= p.keys_cap) {  // stage keys and weights (all loads in flight at once)
+        for (uint32_t b0 = 0; b0 < nc; b0 += 8 * kPqThreads) {
+            unsigned long long kv[8];
+            uint32_t wv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t i = b0 + t * kPqThreads + tid;
+                if (i < nc) {
+                    kv[t] = kg[i];
+                    wv[t] = sg[i];
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t i = b0 + t * kPqThreads + tid;
+                if (i < nc) {
+                    sk[i] = kv[t];
+                    sw[i] = wv[t];
+                }
+            }
+        }
+        kg = sk;
+        sg = sw;
+        __syncthreads();
+    }
+    LC_PMARK(1)
+    auto cand = [&](uint32_t i) -> uint32_t {
+        uint32_t k = 0;
+        while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
+        return s_gbase[k] + (i - s_gpre[k]);
+    };
+    const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
+    const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
+    const unsigned long long budget = p.mode == 1 ? p.budget : (unsigned long long)p.cluster_topk;
+    // weighted radix select of the token-budget prefix (retriever.cpp:142-154)
+    for (int shift = s_shift; shift >= 0; shift -= 8) {
+        for (uint32_t b = tid; b < 256; b += blockDim.x) {
+            hw[b] = 0;
+            hc[b] = 0;
+        }
+        __syncthreads();
+        const unsigned long long prefix = s_prefix, mask = s_mask;
+        for (uint32_t b0 = 0; b0 < nc; b0 += 4 * kPqThreads) {
+            unsigned long long kv[4];
+            uint32_t wv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t i = b0 + t * kPqThreads + tid;
+                kv[t] = i < nc ? kg[i] : ~0ull;
+                wv[t] = i < nc ? sg[i] : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t i = b0 + t * kPqThreads + tid;
+                if (i < nc && (kv[t] & mask) == prefix) {
+                    atomicAdd(&hw[(uint32_t)(kv[t] >> shift) & 255u], wv[t]);
+                    atomicAdd(&hc[(uint32_t)(kv[t] >> shift) & 255u], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w8[8], c8[8];
+            unsigned long long lw = 0;
+            uint32_t lc = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                w8[t] = hw[lane * 8 + t];
+                c8[t] = hc[lane * 8 + t];
+                lw += w8[t];
+                lc += c8[t];
+            }
+            unsigned long long iw = lw;
+            uint32_t ic = lc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long yw = __shfl_up_sync(0xffffffffu, iw, o);
+                const uint32_t yc = __shfl_up_sync(0xffffffffu, ic, o);
+                if (lane >= (uint32_t)o) {
+                    iw += yw;
+                    ic += yc;
+                }
+            }
+            int found = -1;
+            unsigned long long cum = s_wbefore + (iw - lw), wexcl = 0;
+            uint32_t ccum = ic - lc, cexcl = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if (found < 0) {
+                    if (cum + w8[t] > budget) {
+                        found = t;
+                        wexcl = cum;
+                        cexcl = ccum;
+                    } else {
+                        cum += w8[t];
+                        ccum += c8[t];
+                    }
+                }
+            }
+            const unsigned int ballot = __ballot_sync(0xffffffffu, found >= 0);
+            if (ballot == 0) {
+                if (lane == 0) s_state = 2;
+            } else if ((int)lane == __ffs(ballot) - 1) {
+                const uint32_t b = lane * 8 + (uint32_t)found;
+                s_prefix = prefix | ((unsigned long long)b << shift);
+                s_mask = mask | (255ull << shift);
+                s_wbefore = wexcl;
+                s_cbefore += cexcl;
+                s_state = c8[found] == 1 ? 1u : 0u;
+            }
+        }
+        __syncthreads();
+        if (s_state != 0) break;
+    }
+    LC_PMARK(2)
+    const unsigned long long prefix = s_prefix, mask = s_mask;
+    const uint32_t state = s_state, cbefore = s_cbefore;
+    for (uint32_t base = 0; base < nc; base += blockDim.x) {
+        const uint32_t i = base + tid;
+        bool take = false;
+        if (i < nc) {
+            const unsigned long long k = kg[i] & mask;
+            take = k < prefix || (k == prefix && (state == 2 || (state == 1 && cbefore == 0)));
+        }
+        const unsigned int bal = __ballot_sync(0xffffffffu, take);
+        uint32_t pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&s_nsel, (uint32_t)__popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        __syncthreads();  // the list overwrites weights that other threads may still read
+        if (take) sg[pos + __popc(bal & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+    }
+    if (state == 0 && tid == 0) {  // identical fp64 scores: reference-id order (retriever.cpp:33)
+        unsigned long long used = s_wbefore;
+        uint32_t admitted = cbefore, last_id = 0;
+        bool first = true;
+        for (;;) {
+            int best = -1;
+            uint32_t best_id = 0xffffffffu;
+            for (uint32_t i = 0; i < nc; ++i) {
+                if ((kg[i] & mask) != prefix) continue;
+                const uint32_t oid = fo[cand(i)];
+                if ((first || oid > last_id) && oid < best_id) {
+                    best_id = oid;
+                    best = (int)i;
+                }
+            }
+            if (best < 0) break;
+            const unsigned long long w = p.mode == 1 ? ft[cand((uint32_t)best)] : 1ull;
+            if (admitted > 0 && used + w > budget) break;
+            used += w;
+            ++admitted;
+            sg[s_nsel++] = (uint32_t)best;
+            last_id = best_id;
+            first = false;
+        }
+    }
+    __syncthreads();
+    LC_PMARK(3)
+    // rank order (select_topk order) + cluster bitmap + member chunks
+    const uint32_t nsel = s_nsel;
+    const bool staged = nsel <= kStage;
+    if (staged) {
+        for (uint32_t x = tid; x < nsel; x += blockDim.x) {
+            const uint32_t i = sg[x], ci = cand(i);
+            s_sk[x] = kg[i];
+            s_sc[x] = ci;
+            s_so[x] = fo[ci];
+        }
+        __syncthreads();
+    }
+    uint32_t* out_cl = a.sel_clusters + ((size_t)slot * G + g) * a.cap_clusters;
+    uint32_t* gbits = a.sel_bits + ((size_t)slot * G + g) * bit_words(a.cap_clusters);
+    for (uint32_t w = tid; w < bit_words(L); w += blockDim.x) gbits[w] = 0u;
+    __syncthreads();
+    const uint32_t* moff = a.fmem_off + (size_t)slot * (a.cap_clusters + 1);
+    const uint32_t* mem = a.fmem + (size_t)slot * a.cap_chunks;
+    for (uint32_t x = tid; x < nsel; x += blockDim.x) {
+        unsigned long long ki;
+        uint32_t ci, oi, rank = 0;
+        if (staged) {
+            ki = s_sk[x];
+            ci = s_sc[x];
+            oi = s_so[x];
+            for (uint32_t y = 0; y < nsel; ++y) {
+                const unsigned long long ky = s_sk[y];
+                rank += (ky < ki || (ky == ki && s_so[y] < oi)) ? 1u : 0u;
+            }
+        } else {
+            const uint32_t i = sg[x];
+            ki = kg[i];
+            ci = cand(i);
+            oi = fo[ci];
+            for (uint32_t y = 0; y < nsel; ++y) {
+                const unsigned long long ky = kg[sg[y]];
+                if (ky < ki) ++rank;
+                else if (ky == ki && y != x && fo[cand(sg[y])] < oi) ++rank;
+            }
+        }
+        out_cl[rank] = oi;
+        atomicOr(&gbits[ci >> 5], 1u << (ci & 31));
+        for (uint32_t t = moff[ci]; t < moff[ci + 1]; ++t) {
+            const uint32_t j = mem[t];
+            atomicOr(&cb[j >> 5], 1u << (j & 31));
+        }
+    }
+    __syncthreads();
+    // grafted chunks [m0, M) are not in the member CSR: test their clusters
+    if (st.m0 < M) {
+        const uint32_t* cc = a.chunk_clu + (size_t)slot * a.cap_chunks;
+        for (uint32_t j = st.m0 + tid; j < M; j += blockDim.x) {
+            const uint32_t c = cc[j];
+            if ((gbits[c >> 5] >> (c & 31)) & 1u) atomicOr(&cb[j >> 5], 1u << (j & 31));
+        }
+        __syncthreads();
+    }
+    LC_PMARK(4)
+    uint32_t* gcb = a.chunk_bits + ((size_t)slot * G + g) * mwcap;
+    for (uint32_t w = tid; w < mw; w += blockDim.x) gcb[w] = cb[w];
+    if (tid == 0) {
+        qi->n_units = kU;
+        qi->n_clusters = nsel;
+        qi->degenerate = 0;
+        qi->error = 0;
+        qi->scanned = (unsigned long long)P + nc;
+    }
+    LC_PMARK(5)
+}
+
+// k_spans: one CTA per slot: union active spans in chunk order with per-head
+// masks (collect_active, retriever.cpp:60-74), sink and buffer spans, counts.
+constexpr int kSpThreads = 256;
+constexpr int kSpWarps = kSpThreads / 32;
+
+template <typename T>
+__device__ __forceinline__ T sp_scan(T v, T* wt, T& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wt[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        T t = lane < kSpWarps ? wt[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < kSpWarps) wt[lane] = t;
+    }
+    __syncthreads();
+    const T base = warp > 0 ? wt[warp - 1] : T(0);
+    total = wt[kSpWarps - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+template <int GQ>
+__global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
+    const Arena& a = p.a;
+    const uint32_t slot = a.slot0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    constexpr uint32_t G = GQ;
+    const SlotState st = a.state[slot];
+    const uint32_t n = st.n_tokens, M = st.n_chunks, ce = st.chunked_end, P = st.P, L = st.L;
+    const uint32_t all = (1u << G) - 1u;
+    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    QInfo* qi = a.qinfo + (size_t)slot * G;
+    Span* sp = a.spans + (size_t)slot * a.cap_spans;
+    uint32_t* so = a.span_off + (size_t)slot * (a.cap_spans + 1);
+    unsigned long long* sb = a.step_bytes + (size_t)slot * 4;
+    const unsigned long long dd = a.d;
+    if (pv.hdr()[0]) {  // degenerate (retriever.cpp:86-95): everything, full attention
+        if (tid < G) {
+            qi[tid].n_units = P;
+            qi[tid].n_clusters = L;
+            qi[tid].degenerate = 1;
+            qi[tid].error = 0;
+            qi[tid].scanned = 0;
+            qi[tid].n_active = n;
+        }
+        if (tid == 0) {
+            sp[0].start = 0;
+            sp[0].len_mask = (n << 8) | all;
+            so[0] = 0;
+            so[1] = n;
+            a.n_spans[slot] = 1;
+            sb[0] = dd * 4 * n + G * 8ull * dd;
+            sb[1] = (dd * 4 * n + 8ull * dd) * G;
+            sb[2] = n;
+            sb[3] = 0;
+        }
+        if (a.split_span && tid < a.splits) a.split_span[(size_t)slot * 64 + tid] = 0;
+        return;
+    }
+    __shared__ unsigned long long wtot[kSpWarps];
+    __shared__ uint32_t s_cnt[GQ], s_nsp[GQ], s_err;
+    if (tid < G) {
+        s_cnt[tid] = 0;
+        s_nsp[tid] = 0;
+    }
+    if (tid == 0) {
+        uint32_t e = 0;
+        for (uint32_t g = 0; g < G; ++g) e |= qi[g].error;
+        s_err = e;
+    }
+    __syncthreads();
+    if (s_err) {
+        if (tid == 0) {
+            a.n_spans[slot] = 0;
+            so[0] = 0;
+        }
+        return;
+    }
+    const uint32_t mwcap = bit_words(a.cap_chunks), mw = bit_words(M);
+    const uint32_t* cbg = a.chunk_bits + (size_t)slot * G * mwcap;
+    const uint32_t sink_end = min(p.sink, n);
+    uint32_t out = 0, tok = 0;
+    if (sink_end > 0) {
+        if (tid == 0) {
+            sp[0].start = 0;
+            sp[0].len_mask = (sink_end << 8) | all;
+            so[0] = 0;
+        }
+        out = 1;
+        tok = sink_end;
+    }
+    const uint32_t* cs = a.chunk_start + (size_t)slot * (a.cap_chunks + 1);
+    uint32_t my_cnt[GQ], my_nsp[GQ];
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) my_cnt[g] = my_nsp[g] = 0;
+    for (uint32_t w0 = 0; w0 < mw; w0 += blockDim.x) {
+        const uint32_t w = w0 + tid;
+        uint32_t wg[GQ], any = 0;
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) {
+            wg[g] = w < mw ? cbg[g * mwcap + w] : 0u;
+            any |= wg[g];
+        }
+        // at most 32 chunks per word; their bounds are loaded together
+        uint32_t cnt = 0, toks = 0;
+        for (uint32_t rem = any; rem; rem &= rem - 1) {
+            const uint32_t j = w * 32 + __ffs(rem) - 1;
+            const uint32_t s0 = max(__ldg(cs + j), sink_end), e0 = __ldg(cs + j + 1);
+            if (s0 < e0) {
+                ++cnt;
+                toks += e0 - s0;
+            }
+        }
+        unsigned long long total;
+        const unsigned long long ex = sp_scan<unsigned long long>(((unsigned long long)cnt << 40) | toks, wtot, total);
+        uint32_t pos = out + (uint32_t)(ex >> 40), tp = tok + (uint32_t)(ex & 0xffffffffffull);
+        for (uint32_t rem = any; rem; rem &= rem - 1) {
+            const uint32_t b = __ffs(rem) - 1, j = w * 32 + b;
+            const uint32_t s0 = max(__ldg(cs + j), sink_end), e0 = __ldg(cs + j + 1);
+            if (s0 >= e0) continue;
+            uint32_t m = 0;
+#pragma unroll
+            for (int g = 0; g < GQ; ++g)
+                if ((wg[g] >> b) & 1u) {
+                    m |= 1u << g;
+                    my_cnt[g] += e0 - s0;
+                    my_nsp[g] += 1;
+                }
+            if (pos < a.cap_spans) {
+                sp[pos].start = s0;
+                sp[pos].len_mask = ((e0 - s0) << 8) | m;
+                so[pos] = tp;
+            }
+            ++pos;
+            tp += e0 - s0;
+        }
+        out += (uint32_t)(total >> 40);
+        tok += (uint32_t)(total & 0xffffffffffull);
+    }
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) {
+        const uint32_t c1 = __reduce_add_sync(0xffffffffu, my_cnt[g]);
+        const uint32_t c2 = __reduce_add_sync(0xffffffffu, my_nsp[g]);
+        if (lane == 0) {
+            atomicAdd(&s_cnt[g], c1);
+            atomicAdd(&s_nsp[g], c2);
+        }
+    }
+    const uint32_t n_chunk_spans = out - (sink_end > 0 ? 1u : 0u);
+    if (p.flags == 1u) {  // buffer_ids = [chunked_end, n), disjoint from the chunks
+        const uint32_t b0 = max(ce, sink_end);
+        if (n > b0) {
+            if (tid == 0 && out < a.cap_spans) {
+                sp[out].start = b0;
+                sp[out].len_mask = ((n - b0) << 8) | all;
+                so[out] = tok;
+            }
+            ++out;
+            tok += n - b0;
+        }
+    } else if (p.flags == 2u) {  // explicit sorted unique ids
+        const uint32_t lo = p.buf_off[slot], hi = p.buf_off[slot + 1];
+        for (uint32_t base = lo; base < hi; base += blockDim.x) {
+            const uint32_t i = base + tid;
+            uint32_t resid = 0, id = 0;
+            if (i < hi) {
+                id = p.buf_ids[i];
+                if (id >= sink_end && id < n) {
+                    resid = all;
+                    if (id < ce) {  // inside a chunk: drop the heads that already attend it
+                        uint32_t l = 0, h = M;
+                        while (h - l > 1) {
+                            const uint32_t mid = (l + h) >> 1;
+                            if (cs[mid] <= id) l = mid;
+                            else h = mid;
+                        }
+                        uint32_t m = 0;
+#pragma unroll
+                        for (int g = 0; g < GQ; ++g) m |= ((cbg[g * mwcap + (l >> 5)] >> (l & 31)) & 1u) << g;
+                        resid = all & ~m;
+                    }
+                }
+            }
+            unsigned long long total;
+            const unsigned long long ex = sp_scan<unsigned long long>(resid ? ((1ull << 40) | 1ull) : 0ull, wtot, total);
+            if (resid) {
+                const uint32_t pos = out + (uint32_t)(ex >> 40);
+                if (pos < a.cap_spans) {
+                    sp[pos].start = id;
+                    sp[pos].len_mask = (1u << 8) | resid;
+                    so[pos] = tok + (uint32_t)(ex & 0xffffffffffull);
+                }
+#pragma unroll
+                for (int g = 0; g < GQ; ++g)
+                    if ((resid >> g) & 1u) atomicAdd(&s_cnt[g], 1u);
+            }
+            out += (uint32_t)(total >> 40);
+            tok += (uint32_t)(total & 0xffffffffffull);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (out > a.cap_spans) {
+            atomicOr(a.err, kErrSpanOverflow);
+            out = a.cap_spans;
+        }
+        so[out] = tok;
+        a.n_spans[slot] = out;
+        const unsigned long long Pl = P;
+        const uint32_t bufl = (p.flags == 1u && n > max(ce, sink_end)) ? n - max(ce, sink_end) : 0u;
+        unsigned long long per_q = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const unsigned long long act = (unsigned long long)s_cnt[g] + sink_end + bufl;
+            qi[g].n_active = act;
+            per_q += Pl * (4 * dd + 8) + (qi[g].scanned - Pl) * (4 * dd + 16) +
+                     (unsigned long long)s_nsp[g] * 8 + act * 2 * dd * 2 + 8 * dd;
+        }
+        const unsigned long long ncu = pv.hdr()[2];
+        sb[0] = Pl * (4 * dd + 8) + ncu * (4 * dd + 16) + (unsigned long long)n_chunk_spans * 8 +
+                (unsigned long long)tok * 2 * dd * 2 + G * 8 * dd;
+        sb[1] = per_q;
+        sb[2] = tok;
+        sb[3] = ncu;
+    }
+    // first span of every attention split (token-balanced, like k_attend's ranges)
+    __syncthreads();
+    if (a.split_span && tid < a.splits) {
+        const uint32_t nsp = out < a.cap_spans ? out : a.cap_spans;
+        const uint32_t beg = (uint32_t)(((unsigned long long)tok * tid) / a.splits);
+        uint32_t lo = 0, hi = nsp;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (so[mid] <= beg) lo = mid;
+            else hi = mid;
+        }
+        a.split_span[(size_t)slot * 64 + tid] = lo;
+    }
+}
+
+size_t select3_pick_smem(const Arena& a);
+
+// ---------------------------------------------------------------------------
+template <int D, int GQ>
+static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t max_union, uint32_t pmax,
+                              cudaStream_t stream) {
+    const size_t co_smem = (size_t)GQ * D * 8 + (size_t)D * ((pmax + 3) & ~3u) * 4 + (size_t)GQ * pmax * 8;
+    const size_t pk_smem = select3_pick_smem(p.a);
+    static size_t co_cfg = 0, pk_cfg = 0;
+    if (co_smem > co_cfg) {
+        cudaError_t e = cudaFuncSetAttribute(k_coarse<D, GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)co_smem);
+        if (e != cudaSuccess) return e;
+        co_cfg = co_smem;
+    }
+    if (pk_smem > pk_cfg) {
+        cudaError_t e = cudaFuncSetAttribute(k_pickq<GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
+        if (e != cudaSuccess) return e;
+        pk_cfg = pk_smem;
+    }
+    k_coarse<D, GQ><<<n_slots, kCoThreads, co_smem, stream>>>(p);
+    const uint32_t tiles = (max_union + 31) / 32;
+    // a few CTAs per slot whose warps stride over the slot's tiles (setup amortized)
+    const uint32_t parts = std::max<uint32_t>(1, std::min<uint32_t>(4, (tiles + 3) / 4));
+    k_fine<D, GQ><<<dim3(parts, n_slots), kFiThreads, 0, stream>>>(p);
+    k_pickq<GQ><<<dim3(GQ, n_slots), kPqThreads, pk_smem, stream>>>(p);
+    k_spans<GQ><<<n_slots, kSpThreads, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch3_d(const Sel3Params& p, uint32_t n_slots, uint32_t max_union, uint32_t pmax,
+                             cudaStream_t stream) {
+    switch (p.a.G) {
+        case 1: return launch3_dg<D, 1>(p, n_slots, max_union, pmax, stream);
+        case 2: return launch3_dg<D, 2>(p, n_slots, max_union, pmax, stream);
+        case 4: return launch3_dg<D, 4>(p, n_slots, max_union, pmax, stream);
+        case 8: return launch3_dg<D, 8>(p, n_slots, max_union, pmax, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+static uint32_t pick_keys_cap(const Arena& a) { return a.max_cand < 1024u ? a.max_cand : 1024u; }
+
+size_t select3_pick_smem(const Arena& a) {
+    return (size_t)pick_keys_cap(a) * 12 + (size_t)bit_words(a.cap_chunks) * 4;
+}
+
+cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
+                           unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
+                           const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
+                           uint32_t pmax, uint32_t n_slots, cudaStream_t stream) {
+    static unsigned long long* prof = nullptr;
+    if (getenv("LC_PROF") && !prof) cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
+    Sel3Params p{a, pick_keys_cap(a), q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof};
+    cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
+                  : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)
+                               : cudaErrorInvalidValue;
+    if (prof && e == cudaSuccess) {
+        cudaStreamSynchronize(stream);
+        std::vector<unsigned long long> t((size_t)a.n_slots * a.G * 8);
+        cudaMemcpy(t.data(), prof, t.size() * 8, cudaMemcpyDeviceToHost);
+        std::vector<double> tot;
+        double acc[5] = {0, 0, 0, 0, 0};
+        unsigned long long t0 = ~0ull, t1 = 0;
+        for (size_t r = (size_t)a.slot0 * a.G; r < (size_t)(a.slot0 + n_slots) * a.G; ++r) {
+            const unsigned long long* x = &t[r * 8];
+            for (int k = 0; k < 5; ++k) acc[k] += (double)(x[k + 1] - x[k]);
+            tot.push_back((double)(x[5] - x[0]));
+            t0 = x[0] < t0 ? x[0] : t0;
+            t1 = x[5] > t1 ? x[5] : t1;
+        }
+        std::sort(tot.begin(), tot.end());
+        const double nq = (double)tot.size();
+        fprintf(stderr, "[LC_PROF] k_pickq per-CTA us: stage %.2f radix %.2f mark %.2f rank+members %.2f out %.2f | "
+                "dur p50 %.2f p99 %.2f max %.2f | first start->last end %.1f us\n",
+                acc[0] / nq / 1e3, acc[1] / nq / 1e3, acc[2] / nq / 1e3, acc[3] / nq / 1e3, acc[4] / nq / 1e3,
+                tot[tot.size() / 2] / 1e3, tot[(size_t)(tot.size() * 0.99)] / 1e3, tot.back() / 1e3, (t1 - t0) / 1e3);
+    }
+    return e;
+}
+
+}  // namespace lc
