@@ -157,9 +157,33 @@ def time_loop(torch, fn, steps, stream):
     return ev0.elapsed_time(ev1) / steps  # ms
 
 
-def cpu_baseline_ref(args, n_query_heads, threads=0, reps=None):
+def verify_outputs(api, torch, eng, q, out, n_tokens, slots):
+    """Plain torch fp64 attention over each checked head's own active set (the
+    engine's selection) vs the kernel output: the bench's correctness guard."""
+    worst = 0.0
+    o = out.cpu().numpy()
+    qn = q.cpu().numpy()
+    for s in slots:
+        kb, vb = eng.kv_download(s, n_tokens)
+        K = torch.from_numpy((kb.astype(np.uint32) << 16).view(np.float32)).cuda().double()
+        V = torch.from_numpy((vb.astype(np.uint32) << 16).view(np.float32)).cuda().double()
+        for g in range(q.shape[1]):
+            ids = torch.from_numpy(eng.selection(s, g).active_token_ids.astype(np.int64)).cuda()
+            qq = torch.from_numpy(qn[s, g].astype(np.float64)).cuda()
+            w = torch.softmax((K[ids] @ qq) / np.sqrt(K.shape[1]), dim=0)
+            ref = (w[:, None] * V[ids]).sum(0).cpu().numpy()
+            err = float(np.linalg.norm(o[s, g] - ref) / max(np.linalg.norm(ref), 1e-30))
+            worst = max(worst, err)
+    return worst
+
+
+def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2):
     """The reference's own CPU path (oracle/_ref) on a bounded sample: one
-    reference-built 128K slot, its 4 queries, retrieve() (ids + attention)."""
+    reference-built slot of the configured context, and per step all
+    n_query_heads retrieve() calls (ids + sparse attention) against it (its
+    queries cycled), OpenMP over calls with every host thread (mode B), after
+    one warm-up step.  Mode A (the reference API as-is: serial calls, OpenMP
+    inside the kernels) is timed on one slot's queries and scaled."""
     from oracle import refpy as R
     if not R.available():
         return None
@@ -168,18 +192,14 @@ def cpu_baseline_ref(args, n_query_heads, threads=0, reps=None):
     ref = R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base)
     setup = time.time() - t0
     nthreads = R.threads() if threads == 0 else threads
-    # mode B (OpenMP over query heads, single-threaded kernels): calls in flight
-    calls = max(nthreads * 4, 64)
-    reps = reps or max(1, calls // args.group)
-    secs, _ = R.time_retrieve([ref], w.queries, token_budget=args.budget, reps=reps, mode=1,
-                              threads=threads)
-    per_call = secs / (reps * args.group)
-    secs_a, _ = R.time_retrieve([ref], w.queries, token_budget=args.budget, reps=1, mode=0,
-                                threads=threads)
-    per_call_a = secs_a / args.group
-    return {"per_call_s": per_call, "per_call_mode_a_s": per_call_a, "threads": nthreads,
-            "calls": reps * args.group, "setup_s": setup, "ref": ref, "w": w,
-            "step_s": per_call * n_query_heads, "step_mode_a_s": per_call_a * n_query_heads}
+    qs = np.ascontiguousarray(np.tile(w.queries, (max(1, n_query_heads // args.group), 1)), np.float32)
+    R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1, threads=threads)  # warm-up
+    times = [R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1, threads=threads)[0]
+             for _ in range(steps)]
+    step_b = sum(times) / len(times)
+    secs_a, _ = R.time_retrieve([ref], w.queries, token_budget=args.budget, reps=1, mode=0, threads=threads)
+    return {"threads": nthreads, "setup_s": setup, "ref": ref, "w": w, "step_s": step_b,
+            "step_mode_a_s": secs_a / args.group * n_query_heads, "calls": qs.shape[0] * steps}
 
 
 def run_reference(args):
@@ -197,7 +217,7 @@ def run_reference(args):
     # against the reference-built slot (its 4 queries cycled), OpenMP over calls
     qs = np.ascontiguousarray(np.tile(w.queries, (n_qh // args.group, 1)), np.float32)
     for _ in range(args.warmup):
-        R.time_retrieve([ref], qs[: args.group * 8], token_budget=args.budget, reps=1, mode=1)
+        R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1)
     times = []
     for _ in range(args.steps):
         secs, _ = R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1)
@@ -243,11 +263,11 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    from paper_2603_08453_b200 import api
+    from paper_2603_08453_b200 import api, shard
 
     n_slots_total = args.layers * args.kv_heads * args.batch
     # KV-head sharding: rank r owns KV heads {h : h*world // kv_heads == r} of every layer/sequence
-    slots = [s for s in range(n_slots_total) if ((s % args.kv_heads) * world) // args.kv_heads == rank]
+    slots = shard.slots_of_rank(rank, world, args.layers, args.kv_heads, args.batch)
     eng, qs, setup = build_engine(api, torch, args, slots, local)
     stream = torch.cuda.current_stream()
     q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
@@ -298,10 +318,19 @@ def main():
     else:
         step_bytes_all = [float(x) for x in step_bytes]
 
+    check_slots = sorted({0, len(slots) // 2, len(slots) - 1})
+    max_err = verify_outputs(api, torch, eng, q, out, args.tokens, check_slots)
+
     # dominant kernel (sparse attention) and selection timed on their own
     att_ms = time_loop(torch, lambda: eng.sparse_attention(q, out), args.steps, stream)
     sel_ms = time_loop(torch, lambda: eng.retrieve(q, b, out=None), args.steps, stream)
     peak, peak_src = peaks()
+    traffic = None
+    try:  # dram bytes of k_attend from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f)["dram_bytes_per_launch"].get("k_attend")
+    except Exception:
+        pass
     d = 128
     att_bytes = step_bytes[2] * 2 * d * 2 + len(slots) * args.group * 2 * 4 * d
     att_gbs = att_bytes / (att_ms * 1e-3) / 1e9
@@ -328,15 +357,15 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline:
-        base = cpu_baseline_ref(args, n_slots_total * args.group, reps=None)
+        base = cpu_baseline_ref(args, n_slots_total * args.group)
         if base:
             cpu = {"value": 1.0 / base["step_s"], "unit": "steps/s", "cores": base["threads"],
                    "kind": "reference",
-                   "sample": f"oracle/_ref (reference built from /root/reference): one reference-built "
-                             f"{args.tokens}-token slot, {base['calls']} retrieve() calls (ids + attention), "
-                             f"OpenMP over calls, {base['threads']} threads; per-call time x "
-                             f"{n_slots_total * args.group} query heads per step. Mode A (reference API as-is, "
-                             f"serial calls, OpenMP kernels): {1.0 / base['step_mode_a_s']:.3f} steps/s"}
+                   "sample": f"oracle/_ref (the reference built from /root/reference): one reference-built "
+                             f"{args.tokens}-token slot; each step = {n_slots_total * args.group} retrieve() calls "
+                             f"(ids + sparse attention) against it, its {args.group} queries cycled, OpenMP over "
+                             f"calls on {base['threads']} threads, 1 warm-up + 2 timed steps. Mode A (reference API "
+                             f"as-is, serial calls, OpenMP kernels): {1.0 / base['step_mode_a_s']:.3f} steps/s"}
     if rank == 0:
         value = 1000.0 / ms
         line = {
@@ -348,7 +377,8 @@ def main():
             "config": config_dict(args, world),
             "roofline": {"bound": "hbm", "kernel": "k_attend (sparse attention, split-K flash-decode)",
                          "achieved": att_gbs, "peak": peak, "unit": "GB/s", "frac": att_gbs / peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)",
+                         "peak_source": peak_src,
                          "bytes_per_launch": att_bytes, "ms_per_launch": att_ms},
             "step_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
                               "bytes_per_step_union": step_bytes_all[0],
@@ -363,6 +393,8 @@ def main():
             "clocks": clocks,
             "setup": setup,
             "cuda_graph": graph is not None,
+            "check": {"max_rel_err_vs_torch_fp64": max_err, "tolerance": 1e-3, "slots": check_slots,
+                      "ok": max_err < 1e-3},
             "slot_groups": args.slot_groups,
         }
         print(json.dumps(line))

@@ -1,0 +1,47 @@
+"""CPU: KV-head sharding and the layer-boundary all-gather over gloo, world size 2."""
+import os
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_08453_b200 import shard
+
+
+def test_slots_partition_all_heads():
+    for world in (1, 2, 4, 8):
+        owned = [shard.slots_of_rank(r, world, 32, 8) for r in range(world)]
+        flat = sorted(s for o in owned for s in o)
+        assert flat == list(range(256))
+        assert all(len(o) == 256 // world for o in owned)
+        # a rank owns whole KV heads across all layers
+        for r, o in enumerate(owned):
+            heads = {s % 8 for s in o}
+            assert len(heads) == 8 // world
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    layers, heads, G, d = 4, 8, 4, 16
+    mine = shard.slots_of_rank(rank, world, layers, heads)
+    local = torch.stack([torch.full((G, d), float(s)) for s in mine])
+    full = shard.gather_outputs(local, rank, world, layers, heads)
+    ok = all(bool((full[s] == float(s)).all()) for s in range(layers * heads))
+    q.put((rank, ok, full.shape[0]))
+    dist.destroy_process_group()
+
+
+def test_allgather_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1]
+    assert all(r[1] for r in res) and all(r[2] == 32 for r in res)
