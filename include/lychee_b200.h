@@ -49,13 +49,13 @@ typedef struct lc_index_s* lc_index_t;
 typedef struct {
     uint32_t n_slots;         /* layers x KV heads x sequences */
     uint32_t dim;             /* head dim d (attention kernel: 64 or 128) */
-    uint32_t group;           /* GQA query heads per slot, 1..8 */
+    uint32_t group;           /* GQA query heads per slot: 1, 2, 4 or 8 */
     uint32_t cap_tokens;      /* per-slot KV capacity (prefix + decode) */
     uint32_t cap_chunks;      /* per-slot chunk capacity (prefill + grafts) */
     uint32_t cap_clusters;    /* per-slot fine clusters L (fixed after build) */
     uint32_t cap_units;       /* per-slot coarse units P (<= 1024) */
     uint32_t max_candidates;  /* bound on fine candidates per query (0 = auto) */
-    uint32_t splits;          /* attention split-K CTAs per slot (0 = auto) */
+    uint32_t splits;          /* unused: the attention grid is persistent and token-balanced */
     uint32_t structure_aware; /* StreamerConfig::structure_aware (host chunker) */
     uint32_t graft_full;      /* StreamerConfig::graft_search == full */
     uint32_t keep_reps;       /* keep chunk representatives on device (download parity) */

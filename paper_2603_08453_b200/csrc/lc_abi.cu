@@ -51,10 +51,15 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         if (d.cap_tokens == 0 || d.cap_chunks == 0 || d.cap_clusters == 0)
             fail(LC_EINVAL, "lc_index_create: zero capacity");
         if (d.cap_tokens >= (1u << 24)) fail(LC_EINVAL, "lc_index_create: cap_tokens must be < 2^24");
+        if (d.group != 1 && d.group != 2 && d.group != 4 && d.group != 8)
+            fail(LC_EINVAL, "lc_index_create: group must be 1, 2, 4 or 8");
+        // k_coarse stages the coarse tier [d][P] and G x P keys in shared memory
+        const uint32_t cu4 = (d.cap_units + 3) & ~3u;
+        if ((size_t)d.dim * cu4 * 4 > 96 * 1024 || (size_t)d.group * cu4 > 1024)
+            fail(LC_EINVAL, "lc_index_create: cap_units too large for the coarse-tier kernel "
+                            "(need dim*cap_units*4 <= 96 KiB and group*cap_units <= 1024)");
         auto h = std::make_unique<lc_index_s>();
         h->desc = d;
-        if (h->desc.splits == 0) h->desc.splits = 4;
-        if (h->desc.splits > 64) fail(LC_EINVAL, "lc_index_create: splits must be <= 64");
         h->set_device();
         Arena& a = h->a;
         a.n_slots = d.n_slots;
@@ -63,9 +68,8 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.cap_tokens = d.cap_tokens;
         a.cap_chunks = d.cap_chunks;
         a.cap_clusters = d.cap_clusters;
-        a.cap_units = d.cap_units;
+        a.cap_units = (d.cap_units + 3) & ~3u;  // float4 rows of the coarse tier
         a.max_cand = 1;
-        a.splits = h->desc.splits;
         a.graft_full = d.graft_full;
         a.keep_reps = d.keep_reps;
         a.cap_spans = d.cap_chunks + 2 + 1024;
@@ -76,9 +80,9 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.chunk_start = dalloc<uint32_t>(S * (d.cap_chunks + 1), o);
         a.chunk_clu = dalloc<uint32_t>(S * d.cap_chunks, o);
         a.chunk_rep = d.keep_reps ? dalloc<float>(S * d.cap_chunks * D, o) : nullptr;
-        a.ucent = dalloc<float>(S * d.cap_units * D, o);
-        a.urad = dalloc<double>(S * d.cap_units, o);
-        a.unit_off = dalloc<uint32_t>(S * (d.cap_units + 1), o);
+        a.ucent = dalloc<float>(S * a.cap_units * D, o);
+        a.urad = dalloc<double>(S * a.cap_units, o);
+        a.unit_off = dalloc<uint32_t>(S * (a.cap_units + 1), o);
         a.fcent = dalloc<float>(S * d.cap_clusters * D, o);
         a.frad = dalloc<double>(S * d.cap_clusters, o);
         a.ftok = dalloc<uint32_t>(S * d.cap_clusters, o);
@@ -87,20 +91,24 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.funit = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.fmem_off = dalloc<uint32_t>(S * (d.cap_clusters + 1), o);
         a.fmem = dalloc<uint32_t>(S * d.cap_chunks, o);
-        a.plan_bytes = (uint32_t)((64 + (size_t)d.cap_units * (4 + d.group) * 4 + 15) & ~15ull);
+        a.plan_bytes = (uint32_t)((256 + (size_t)a.cap_units * (4 + d.group) * 4 + 15) & ~15ull);
         a.plan = dalloc<unsigned char>(S * a.plan_bytes, o);
         a.chunk_bits = dalloc<uint32_t>(S * G * bit_words(d.cap_chunks), o);
-        a.split_span = dalloc<uint32_t>(S * 64, o);
         a.state = dalloc<SlotState>(S, o);
         a.qinfo = dalloc<QInfo>(S * G, o);
-        a.sel_units = dalloc<uint32_t>(S * G * d.cap_units, o);
+        a.sel_units = dalloc<uint32_t>(S * G * a.cap_units, o);
         a.sel_clusters = dalloc<uint32_t>(S * G * d.cap_clusters, o);
         a.sel_bits = dalloc<uint32_t>(S * G * bit_words(d.cap_clusters), o);
         a.spans = dalloc<Span>(S * a.cap_spans, o);
         a.span_off = dalloc<uint32_t>(S * (a.cap_spans + 1), o);
         a.n_spans = dalloc<uint32_t>(S, o);
+        a.rows = dalloc<uint32_t>(S * d.cap_tokens, o);
+        a.slot_tok = dalloc<uint32_t>(S, o);
         a.step_bytes = dalloc<unsigned long long>(S * 4, o);
-        a.partials = dalloc<float>(S * a.splits * G * (D + 2), o);
+        // attention partials + the persistent kernel's pool / barrier counters (zeroed)
+        const size_t part_floats = attend_partials_floats(a.d, a.G, a.n_slots);
+        h->att_part = dalloc<float>(part_floats, o);
+        ck(cudaMemset(h->att_part, 0, part_floats * 4), "memset attention partials");
         a.counters = dalloc<uint32_t>(S, o);
         a.err = dalloc<uint32_t>(1, o);
         h->q_stage = dalloc<float>(S * G * D, o);
@@ -108,9 +116,10 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         h->take_dev = dalloc<uint32_t>(S, o);
         h->rep_scratch = dalloc<lc_graft_report>(S, o);
         ck(cudaMemset(a.state, 0, S * sizeof(SlotState)), "memset state");
-        ck(cudaMemset(a.counters, 0, S * 4), "memset counters");
         ck(cudaMemset(a.err, 0, 4), "memset err");
+        ck(cudaMemset(a.counters, 0, S * 4), "memset counters");
         ck(cudaMemset(a.n_spans, 0, S * 4), "memset n_spans");
+        ck(cudaMemset(a.slot_tok, 0, S * 4), "memset slot_tok");
         ck(cudaMemset(a.span_off, 0, S * (a.cap_spans + 1) * 4), "memset span_off");
         ck(cudaMemset(a.qinfo, 0, S * G * sizeof(QInfo)), "memset qinfo");
         h->hs.resize(S);
@@ -427,74 +436,34 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     h->set_device();
     Arena a = h->a;
     a.max_cand = needed_candidates(h, std::min<uint32_t>(b->unit_topk, 64));
-    // shared-memory candidate area: at least the staged coarse tier [d][P]
     uint32_t pmax = 1;
     for (auto& s : h->hs) pmax = std::max(pmax, s.P);
-    const uint32_t stage_c = (uint32_t)(((size_t)a.d * ((pmax + 3) & ~3u) * 4 + 11) / 12);
-    a.smem_cand = std::min<uint32_t>(std::max<uint32_t>(2048, stage_c), std::max<uint32_t>(a.max_cand, stage_c));
-    if (select_smem_bytes(a) > 200 * 1024) a.smem_cand = (uint32_t)((200 * 1024 - a.d * 4 - a.cap_units * 8) / 12);
-    if (a.max_cand > a.smem_cand) {
-        const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
-        if (h->cand_scratch_bytes < need) {
-            if (h->cand_scratch) cudaFree(h->cand_scratch);
-            h->cand_scratch = nullptr;
-            h->cand_scratch_bytes = 0;
-            if (cudaMalloc(&h->cand_scratch, need) != cudaSuccess) {
-                cudaGetLastError();
-                fail(LC_ENOMEM, "candidate scratch allocation failed");
-            }
-            h->cand_scratch_bytes = need;
-        }
-        a.cand_scratch = h->cand_scratch;
-    } else {
-        a.cand_scratch = nullptr;
-    }
-    // selection pipeline: "three" (k_coarse -> k_fine -> k_pick, default),
-    // "slot" (fused per-slot kernel) or "query" (per-head k_select + k_compact)
-    const char* env = getenv("LC_SELECT");
-    const std::string mode_s = env ? std::string(env) : std::string("three");
-    const bool shape_ok = select_slot_supports_group(a.G) && (a.cap_units % 4) == 0 && a.G * pmax <= 1024 &&
-                          (size_t)a.d * ((pmax + 3) & ~3u) * 4 <= 96 * 1024;
-    const bool use_three = mode_s == "three" && shape_ok && select3_pick_smem(a) <= 200 * 1024;
-    const bool use_slot = mode_s == "slot" && shape_ok && select_slot_smem_bytes(a, pmax) <= 200 * 1024;
+    if (select3_pick_smem(a) > 200 * 1024) fail(LC_EINVAL, "retrieve: chunk capacity too large for k_pickq");
     const uint32_t max_union = needed_candidates(h, std::min<uint32_t>(a.G * std::min<uint32_t>(b->unit_topk, 64), 4096));
-    if (use_slot || use_three) {
-        const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
-        if (h->slot_scratch_bytes < need) {
-            if (h->slot_scratch) cudaFree(h->slot_scratch);
-            h->slot_scratch = nullptr;
-            h->slot_scratch_bytes = 0;
-            if (cudaMalloc(&h->slot_scratch, need) != cudaSuccess) {
-                cudaGetLastError();
-                fail(LC_ENOMEM, "selection scratch allocation failed");
-            }
-            h->slot_scratch_bytes = need;
+    const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
+    if (h->sel_scratch_bytes < need) {
+        if (h->sel_scratch) cudaFree(h->sel_scratch);
+        h->sel_scratch = nullptr;
+        h->sel_scratch_bytes = 0;
+        if (cudaMalloc(&h->sel_scratch, need) != cudaSuccess) {
+            cudaGetLastError();
+            fail(LC_ENOMEM, "selection scratch allocation failed");
         }
+        h->sel_scratch_bytes = need;
     }
+    // k_coarse -> k_fine -> k_pickq -> k_spans (selection, per slot group), then
+    // one persistent k_attend over every slot (its grid barrier needs the whole GPU)
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs) {
-        if (!use_three) ag.split_span = nullptr;  // only k_spans precomputes the split starts
-        if (use_three) {
-            ck(launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, flags,
-                              buf_off, buf_ids, h->slot_scratch, a.max_cand, max_union, pmax, count, gs),
-               "k_select3");
-        } else if (use_slot) {
-            ck(launch_select_slot(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
-                                  flags, buf_off, buf_ids, h->slot_scratch, a.max_cand, pmax, count, gs),
-               "k_select_slot");
-        } else {
-            ck(launch_select(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size,
-                             count, gs), "k_select");
-            ck(launch_compact(ag, b->sink_size, flags, buf_off, buf_ids, count, gs), "k_compact");
-        }
-        if (out_dev) ck(launch_attend(ag, q_dev, out_dev, count, gs), "k_attend");
+        ck(launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, flags,
+                          buf_off, buf_ids, h->sel_scratch, a.max_cand, max_union, pmax, count, gs),
+           "k_select3");
     };
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
     if (groups == 1) {
         a.slot0 = 0;
         run_group(a, a.n_slots, st);
     } else {
-        // fork: each slot group runs select -> compact -> attend on its own stream,
-        // so one group's (latency-bound) selection overlaps another's attention
+        // fork: each slot group's selection runs on its own stream
         ensure_streams(h, groups);
         ck(cudaEventRecord(h->group_events[0], st), "fork");
         for (uint32_t gi = 0; gi < groups; ++gi) {
@@ -510,9 +479,10 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
             ck(cudaStreamWaitEvent(st, h->group_events[gi + 1], 0), "join");
         }
     }
+    a.slot0 = 0;
+    if (out_dev) ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, st), "k_attend");
     h->last_flags = flags;
     h->last_valid = 1;
-    h->last_three = use_three;
 }
 
 int lc_retrieve(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
@@ -530,8 +500,7 @@ int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* 
         h->set_device();
         Arena a = h->a;
         a.slot0 = 0;
-        if (!h->last_three) a.split_span = nullptr;
-        ck(launch_attend(a, q_dev, out_dev, a.n_slots, (cudaStream_t)stream), "k_attend");
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, (cudaStream_t)stream), "k_attend");
     });
 }
 

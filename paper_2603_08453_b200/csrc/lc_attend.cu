@@ -1,19 +1,29 @@
 // Gather-based split-K flash-decode over the selected variable-length chunks
 // (north star item 3): kernels::attention (kernels.cpp:108-144) for every query
-// head of a GQA group at once, over the union of the group's active spans.
+// head of a GQA group at once, over the union of the group's active tokens.
 //
-// Data movement: each warp streams 16-token groups of gathered K/V rows into
-// a private 3-stage shared-memory ring with cp.async (16-byte requests, every
-// byte used; each KV row of the union is read from HBM exactly once per
-// slot), so two groups are in flight while the third is computed.  The ring
-// is XOR-swizzled so the fragment reads below are bank-conflict free.
+// Work partition: a persistent grid (SMs x resident CTAs, 4 warps each).  The
+// union active tokens of all slots of the launch form one global sequence
+// (slot-major; k_spans wrote each slot's row list and total).  Every warp owns
+// an equal contiguous range of that sequence, so the load is balanced to one
+// token group no matter how ragged the per-slot selections are, there are no
+// waves and no per-CTA prologue per slot.  A warp whose range crosses slot
+// boundaries keeps one online-softmax state per slot segment and writes a
+// (m, l, o) partial for each; the warp that completes a slot's token count
+// merges that slot's partials (log-sum-exp) in warp order (deterministic).
+//
+// Data movement: each warp streams 16-token groups of gathered K/V rows into a
+// private 3-stage shared-memory ring with cp.async (16-byte requests, full
+// 128-byte lines; each KV row of the union is read from HBM exactly once).  The
+// row ids of a group come from a 4-entry per-warp descriptor ring, loaded four
+// groups ahead, so the gather addresses are ready two groups before the copy
+// is issued.  The ring is XOR-swizzled so the fragment reads are conflict free.
 //
 // Math: QK^T and PV on the tensor cores (mma.sync m16n8k16, bf16 in, fp32
 // accumulate) with q and the softmax weights split into bf16 hi + lo halves
 // (hi in MMA rows 0..G-1, lo in rows 8..8+G-1): products carry ~16 mantissa
-// bits over the exact bf16 K/V.  A per-token query mask removes (query, token)
-// pairs outside that head's own active set.  Partials (m, l, o) per CTA are
-// merged with log-sum-exp by the last CTA of each slot.
+// bits over the exact bf16 K/V.  A per-token head mask (row list bits 24..31)
+// removes (query, token) pairs outside that head's own active set.
 //
 // Fragment maps for mma.m16n8k16 (lane = 4r + c):
 //   QK: B = K^T, thread (r, c) holds token r (and 8 + r) dims [c*D/4, c*D/4 + D/4),
@@ -25,6 +35,7 @@
 //   Out: thread (r, c) owns query r dims [c*D/4, c*D/4 + D/4).
 #include "lc_common.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -35,7 +46,9 @@ struct AttendParams {
     Arena a;
     const float* q;  // [slot][G][D]
     float* out;      // [slot][G][D]
-    unsigned long long* prof;  // optional per-CTA phase timestamps (LC_PROF=1)
+    uint32_t n;      // slots of this launch, starting at a.slot0
+    float* part;     // [(warps + n)][G][D + 2] per (warp, slot) segment partials
+    unsigned long long* prof;  // optional per-warp [t_start, t_stream_end, t_end, groups | smid << 40] (LC_PROF=1)
 };
 
 __device__ __forceinline__ unsigned long long gtime_a() {
@@ -43,13 +56,12 @@ __device__ __forceinline__ unsigned long long gtime_a() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define LC_AMARK(ph) \
-    if (p.prof && threadIdx.x == 0) p.prof[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ph)] = gtime_a();
 
 constexpr int kAttThreads = 128;
 constexpr int kAttWarps = kAttThreads / 32;
 constexpr int kStages = 3;
-constexpr int kWindow = 512;  // tokens expanded into shared memory at a time
+constexpr int kRing = 8;   // group descriptors per warp (groups it .. it+5 live)
+constexpr int kAhead = 5;  // row lists are fetched this many groups ahead
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
@@ -73,6 +85,9 @@ __device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
 }
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(g));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -92,6 +107,118 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t k) {
     return k ^ ((k >> 3) << 1) ^ (row & 7) ^ ((row >> 1) & 1);
 }
 
+// first global position of warp w's range
+__device__ __forceinline__ uint32_t warp_begin(uint32_t T, uint32_t w, uint32_t NW) {
+    return (uint32_t)(((unsigned long long)T * w) / NW);
+}
+// the warp whose (non-empty) range holds global position pos
+__device__ __forceinline__ uint32_t warp_of(uint32_t T, uint32_t pos, uint32_t NW) {
+    return (uint32_t)((((unsigned long long)pos + 1) * NW - 1) / T);
+}
+
+struct GroupDesc {  // one 16-token group of one slot
+    uint32_t slot;  // local slot index, or ~0u when the warp's work is exhausted
+    uint32_t pos;   // first token's index in the slot's row list
+    uint32_t cnt;   // 1..16
+    uint32_t seg;   // partial index of the (range, slot) segment the group belongs to
+};
+
+// Work split.  Every slot's union token list is cut into a head (the first 3/4)
+// and a tail.  The heads, concatenated, are cut statically into equal
+// contiguous warp ranges; the tails, concatenated, form a pool of at most
+// kPoolPerWarp x warps chunks that warps claim in order as they finish (SMs
+// differ in achieved bandwidth by up to ~30%).  Partial index of a segment:
+// static range w of slot s -> w + s, pool chunk k of slot s -> NW + n + k + s
+// (both injective because range and slot indices grow together).
+constexpr uint32_t kPoolPerWarp = 4;
+__device__ __forceinline__ uint32_t head_of(uint32_t t) { return t - t / 4; }
+struct PoolShape {
+    uint32_t C;  // pool chunk length (multiple of 16)
+    uint32_t K;  // pool chunks
+};
+__device__ __forceinline__ PoolShape pool_shape(uint32_t TP, uint32_t NW) {
+    PoolShape ps;
+    const uint32_t kmax = kPoolPerWarp * NW;
+    uint32_t C = (TP + kmax - 1) / kmax;
+    C = (C + 15) & ~15u;
+    ps.C = C ? C : 16;
+    ps.K = (TP + ps.C - 1) / ps.C;
+    return ps;
+}
+
+// Log-sum-exp combination of head g of slot s from the slot's partials, by one
+// warp, in a fixed order (static head ranges wf.., then pool chunks kf..; a
+// warp with an empty static range wrote nothing and is skipped): lanes load
+// the contributors' (m, l), then every partial row load of a batch is in
+// flight at once.
+template <int D>
+__device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G, uint32_t g, uint32_t n,
+                                           const float* part, uint32_t zero_seg, uint32_t s, uint32_t NW,
+                                           uint32_t TH, uint32_t h0, uint32_t h1, uint32_t t0, uint32_t t1,
+                                           uint32_t C) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t wf = 1, wl = 0, kf = 1, kl = 0;
+    if (h0 < h1) {
+        wf = warp_of(TH, h0, NW);
+        wl = warp_of(TH, h1 - 1, NW);
+    }
+    if (t0 < t1) {
+        kf = t0 / C;
+        kl = (t1 - 1) / C;
+    }
+    const uint32_t nw = wf <= wl ? wl - wf + 1 : 0u, nk = kf <= kl ? kl - kf + 1 : 0u, nc = nw + nk;
+    constexpr int PER = D / 32;
+    float M = -INFINITY, L = 0.f, o[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) o[k] = 0.f;
+    for (uint32_t base = 0; base < nc; base += 32) {
+        // lane j of the batch: contributor base + j's row, max and weight
+        const uint32_t i = base + lane;
+        bool live = false;
+        uint32_t seg = zero_seg;
+        if (i < nc) {
+            if (i < nw) {
+                const uint32_t v = wf + i;
+                live = warp_begin(TH, v, NW) < warp_begin(TH, v + 1, NW);
+                seg = v + s;
+            } else {
+                live = true;
+                seg = NW + n + kf + (i - nw) + s;
+            }
+        }
+        const float* ps = part + ((size_t)seg * G + g) * (D + 2);
+        const float ms = live ? __ldcg(ps) : -INFINITY;
+        const float ls = live ? __ldcg(ps + 1) : 0.f;
+        float bm = ms;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+        const float Mn = fmaxf(M, bm);
+        if (Mn == -INFINITY) continue;
+        const float fo = exp2f(M - Mn);  // rescale what earlier batches accumulated
+        L *= fo;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) o[k] *= fo;
+        M = Mn;
+        const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+        if (f == 0.f) seg = zero_seg;
+        L += f * ls;  // lane-partial, reduced below
+        const uint32_t cnt = min(32u, nc - base);
+#pragma unroll 8
+        for (uint32_t j = 0; j < cnt; ++j) {
+            const float fj = __shfl_sync(0xffffffffu, f, j);
+            const uint32_t sj = __shfl_sync(0xffffffffu, seg, j);
+            const float* pj = part + ((size_t)sj * G + g) * (D + 2) + 2 + lane;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) o[k] += fj * __ldcg(pj + 32 * k);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) out[(size_t)g * D + lane + 32 * k] = L > 0.f ? o[k] / L : 0.f;
+    if (!(L > 0.f) && lane == 0) atomicOr(err, kErrEmptyActive);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     static_assert(D == 64 || D == 128, "D must be 64 or 128");
@@ -102,359 +229,480 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     constexpr int ROWB = D * 2;            // bytes per K/V row
     constexpr int STAGE = 32 * ROWB;       // 16 K rows + 16 V rows
     const Arena& a = p.a;
-    const uint32_t slot = a.slot0 + blockIdx.y, split = blockIdx.x, S = gridDim.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
-    const uint32_t G = a.G;
+    const uint32_t G = a.G, n = p.n;
 
     extern __shared__ __align__(128) unsigned char dsm[];
     unsigned char* ring = dsm + (size_t)warp * kStages * STAGE;  // this warp's stages
-    __shared__ uint32_t s_row[kWindow];
-    __shared__ uint8_t s_msk[kWindow];
-    __shared__ uint32_t s_sstart[kWindow + 1];
-    __shared__ uint32_t s_slm[kWindow + 1];
-    __shared__ uint32_t s_soff[kWindow + 2];
-    __shared__ uint32_t s_lohi[3];
-    __shared__ float s_m[kAttWarps][kMaxGroup], s_l[kAttWarps][kMaxGroup];
-    __shared__ uint32_t s_last;
+    __shared__ uint32_t s_hp[kMaxAttendSlots + 1];  // prefix of the slots' head lengths
+    __shared__ uint32_t s_tp[kMaxAttendSlots + 1];  // prefix of the slots' tail lengths
+    __shared__ uint32_t s_rows[kAttWarps][kRing][16];
+    __shared__ GroupDesc s_gd[kAttWarps][kRing];
+    __shared__ uint32_t s_wsum[2 * kAttWarps];
 
-    LC_AMARK(0)
-    const uint32_t ns = a.n_spans[slot];
-    const uint32_t* soff = a.span_off + (size_t)slot * (a.cap_spans + 1);
-    const Span* sp = a.spans + (size_t)slot * a.cap_spans;
-    const uint32_t tot = soff[ns];
-    const uint32_t beg = (uint32_t)(((unsigned long long)tot * split) / S);
-    const uint32_t end = (uint32_t)(((unsigned long long)tot * (split + 1)) / S);
-    const unsigned char* Kb = reinterpret_cast<const unsigned char*>(a.K + kv_off(a, slot));
-    const unsigned char* Vb = reinterpret_cast<const unsigned char*>(a.V + kv_off(a, slot));
-    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-
-    // q fragments: softmax scale and log2(e) folded in, bf16 hi (row r) + lo (row r+8)
-    uint32_t qf[KS][4];
+    // ---- prefixes of the slots' head and tail lengths (k_spans wrote the totals) ----
     {
-        const float scale = (float)(1.4426950408889634 / sqrt((double)D));
-        const float* qg = p.q + ((size_t)slot * G + (r < (int)G ? r : 0)) * D + c * (D / 4);
+        const uint32_t per = (n + kAttThreads - 1) / kAttThreads, i0 = tid * per;
+        uint32_t lh = 0, lt = 0;
+        for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
+            const uint32_t t = a.slot_tok[a.slot0 + i];
+            lh += head_of(t);
+            lt += t - head_of(t);
+        }
+        uint32_t xh = lh, xt = lt;
 #pragma unroll
-        for (int s = 0; s < KS; ++s) {
-            float h[4], l[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) split_bf16(qg[4 * s + e] * scale, h[e], l[e]);
-            const bool on = r < (int)G;
-            qf[s][0] = on ? pack_bf16(h[0], h[1]) : 0u;
-            qf[s][2] = on ? pack_bf16(h[2], h[3]) : 0u;
-            qf[s][1] = on ? pack_bf16(l[0], l[1]) : 0u;
-            qf[s][3] = on ? pack_bf16(l[2], l[3]) : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yh = __shfl_up_sync(0xffffffffu, xh, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+            if (lane >= o) {
+                xh += yh;
+                xt += yt;
+            }
+        }
+        if (lane == 31) {
+            s_wsum[warp] = xh;
+            s_wsum[kAttWarps + warp] = xt;
+        }
+        __syncthreads();
+        uint32_t bh = 0, bt = 0;
+        for (int w = 0; w < warp; ++w) {
+            bh += s_wsum[w];
+            bt += s_wsum[kAttWarps + w];
+        }
+        uint32_t rh = bh + xh - lh, rt = bt + xt - lt;
+        if (tid == 0) s_hp[0] = s_tp[0] = 0;
+        for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
+            const uint32_t t = a.slot_tok[a.slot0 + i];
+            rh += head_of(t);
+            rt += t - head_of(t);
+            s_hp[i + 1] = rh;
+            s_tp[i + 1] = rt;
+        }
+        __syncthreads();
+    }
+    const uint32_t TH = s_hp[n], TP = s_tp[n];
+    // slots with no active token (reference: sparse_attention throws, retriever.cpp:43)
+    if (blockIdx.x == 0) {
+        for (uint32_t s = warp; s < n; s += kAttWarps) {
+            if (s_hp[s + 1] != s_hp[s] || s_tp[s + 1] != s_tp[s]) continue;
+            for (uint32_t x = lane; x < G * D; x += 32) p.out[(size_t)(a.slot0 + s) * G * D + x] = 0.f;
+            if (lane == 0) atomicOr(a.err, kErrEmptyActive);
         }
     }
-    float acc[NT][4];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-    LC_AMARK(1)
+    const unsigned long long t_start = p.prof ? gtime_a() : 0ull;
+    uint32_t n_groups = 0;
+    if (TH + TP == 0) return;
+    const uint32_t NW = gridDim.x * kAttWarps, w = blockIdx.x * kAttWarps + warp;
+    const PoolShape pool = pool_shape(TP, NW);
+    uint32_t* pool_ctr = reinterpret_cast<uint32_t*>(p.part);  // [0] next pool chunk, [1] barrier, [2] CTAs out
+    float* part = p.part + 16;
 
+    // ---- group producer: warp-uniform cursor over the static range (positions in
+    // the head sequence), then over claimed pool chunks (tail sequence) ----
+    auto slot_of = [&](const uint32_t* pre, uint32_t pos) {  // slot holding pos (skips empty ones)
+        uint32_t lo = 0, hi = n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= pos) lo = mid;
+            else hi = mid;
+        }
+        while (pre[lo + 1] <= pos) ++lo;
+        return lo;
+    };
+    const uint32_t* pre = s_hp;  // active sequence: heads, then tails
+    bool in_pool = false;
+    uint32_t ppos = warp_begin(TH, w, NW), pend = warp_begin(TH, w + 1, NW);
+    uint32_t seg_base = w, ps = ppos < pend ? slot_of(pre, ppos) : 0u;
+    // lane 0 claims the next pool chunk one call before the current range runs
+    // out (the atomic's latency hides behind one group) -- not earlier, so a
+    // slow warp never sits on a chunk a faster one could take
+    uint32_t k_next = 0;
+    if (ppos >= pend && lane == 0) k_next = atomicAdd(pool_ctr, 1u);
+    bool done = false;
+    auto next_group = [&]() -> GroupDesc {
+        GroupDesc gd{~0u, 0u, 0u, 0u};
+        if (done) return gd;
+        if (ppos >= pend) {  // range exhausted: take the claimed pool chunk
+            const uint32_t k = __shfl_sync(0xffffffffu, k_next, 0);
+            if (k >= pool.K) {
+                done = true;
+                return gd;
+            }
+            pre = s_tp;
+            in_pool = true;
+            ppos = k * pool.C;
+            pend = min(TP, ppos + pool.C);
+            seg_base = NW + n + k;
+            ps = slot_of(pre, ppos);
+        }
+        const uint32_t se = pre[ps + 1];
+        const uint32_t lim = se < pend ? se : pend;
+        gd.slot = ps;
+        // row-list index: heads first, the tail after the slot's head
+        gd.pos = ppos - pre[ps] + (in_pool ? s_hp[ps + 1] - s_hp[ps] : 0u);
+        gd.cnt = min(16u, lim - ppos);
+        gd.seg = seg_base + ps;
+        ppos += gd.cnt;
+        if (ppos == se)
+            while (ps + 1 < n && pre[ps + 1] <= ppos) ++ps;
+        if (ppos >= pend && lane == 0) k_next = atomicAdd(pool_ctr, 1u);
+        return gd;
+    };
+    // descriptor + row entries (row | head mask << 24) of a group into ring entry
+    // e: lanes 0..15 cp.async one entry each (padded tokens repeat the last row;
+    // the compute masks them by cnt)
+    auto fetch = [&](int e) {
+        const GroupDesc gd = next_group();
+        if (lane == 0) s_gd[warp][e] = gd;
+        if (gd.slot != ~0u && lane < 16) {
+            const uint32_t* rl = a.rows + (size_t)(a.slot0 + gd.slot) * a.cap_tokens + gd.pos;
+            cp_async4((uint32_t)__cvta_generic_to_shared(&s_rows[warp][e][lane]), rl + min((uint32_t)lane, gd.cnt - 1));
+        }
+    };
+
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     // cp.async of one 16-token group into stage `st`: each 8-lane quarter-warp
-    // copies one contiguous 128-byte half row, so every request is a full line
-    auto issue = [&](uint32_t t0, uint32_t wn, int st) {
+    // copies one contiguous 128-byte line, so every request is a full line
+    auto issue = [&](int e, int st) {
+        const GroupDesc gd = s_gd[warp][e];
+        if (gd.slot == ~0u) return;
+        const unsigned char* Kb = reinterpret_cast<const unsigned char*>(a.K + kv_off(a, a.slot0 + gd.slot));
+        const unsigned char* Vb = reinterpret_cast<const unsigned char*>(a.V + kv_off(a, a.slot0 + gd.slot));
         const uint32_t sbase = ring_s + (uint32_t)st * STAGE;
         constexpr int HALVES = ROWB / 128;         // 128-byte segments per row
         constexpr int SEGS = 16 * HALVES;           // segments per 16 rows
 #pragma unroll
-        for (int e = 0; e < SEGS / 4; ++e) {
-            const uint32_t id = 4u * e + ((uint32_t)lane >> 3);
+        for (int e2 = 0; e2 < SEGS / 4; ++e2) {
+            const uint32_t id = 4u * e2 + ((uint32_t)lane >> 3);
             const uint32_t row = id / HALVES, half = id % HALVES;
             const uint32_t k = half * 8 + ((uint32_t)lane & 7);  // 16-byte chunk of the row
-            const uint32_t tk = t0 + row;
-            const uint32_t src_row = tk < wn ? s_row[tk] : s_row[0];
+            const uint32_t src_row = s_rows[warp][e][row] & 0x00ffffffu;
             cp_async16(sbase + row * ROWB + swz(row, k) * 16, Kb + (size_t)src_row * ROWB + k * 16);
             cp_async16(sbase + 16 * ROWB + row * ROWB + swz(row, k) * 16, Vb + (size_t)src_row * ROWB + k * 16);
         }
     };
 
-    // first span of this split: precomputed by the span builder (k_spans) or searched
-    if (tid == 0) {
-        uint32_t k0 = 0;
-        if (a.split_span && beg < end) {
-            k0 = a.split_span[(size_t)slot * 64 + split];
-        } else if (beg < end) {
-            uint32_t lo = 0, hi = ns;
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (soff[mid] <= beg) lo = mid;
-                else hi = mid;
-            }
-            k0 = lo;
-        }
-        s_lohi[0] = k0;
-        // last span of this split bounds every window's span load
-        s_lohi[2] = (a.split_span && split + 1 < S) ? a.split_span[(size_t)slot * 64 + split + 1] : ns - 1;
+    // prologue: row lists of groups 0 .. kAhead-1, then two groups in flight
+    {
+#pragma unroll
+        for (int e = 0; e < kAhead; ++e) fetch(e);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        issue(0, 0);
+        cp_commit();
+        issue(1, 1);
+        cp_commit();
     }
-    __syncthreads();
-    const uint32_t k_last = s_lohi[2];
-    for (uint32_t wb = beg; wb < end; wb += kWindow) {
-        const uint32_t we = min(end, wb + kWindow), wn = we - wb;
-        // every span touching [wb, we) lies in [k0, k0 + wn] (spans hold >= 1 token):
-        // one batched load of those spans, then all lookups in shared memory
-        const uint32_t k0 = s_lohi[0];
-        const uint32_t nsp = min(min(ns - k0, wn + 1), k_last + 1 - k0);
-        for (uint32_t k = tid; k < nsp; k += blockDim.x) {
-            const Span sk = sp[k0 + k];
-            s_sstart[k] = sk.start;
-            s_slm[k] = sk.len_mask;
-            s_soff[k] = soff[k0 + k];
-        }
-        __syncthreads();
-        for (uint32_t t = tid; t < kWindow; t += blockDim.x) {
-            if (t < wn) {
-                const uint32_t tokpos = wb + t;
-                uint32_t lo = 0, hi = nsp;
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (s_soff[mid] <= tokpos) lo = mid;
-                    else hi = mid;
-                }
-                s_row[t] = s_sstart[lo] + (tokpos - s_soff[lo]);
-                s_msk[t] = (uint8_t)(s_slm[lo] & 0xffu);
-                if (t == wn - 1) {  // the next window starts in the span holding token we
-                    s_lohi[1] = (lo + 1 < nsp && s_soff[lo + 1] <= we) ? k0 + lo + 1 : k0 + lo;
-                }
-            } else {
-                s_row[t] = 0;
-                s_msk[t] = 0;
-            }
-        }
-        __syncthreads();
-        if (tid == 0) s_lohi[0] = s_lohi[1];
 
-        if (wb == beg) LC_AMARK(2)
-        // this warp's groups: grp = warp, warp + 4, ...
-        const uint32_t ngrp = (wn + 15) / 16;
-        const uint32_t my_n = ngrp > (uint32_t)warp ? (ngrp - warp + kAttWarps - 1) / kAttWarps : 0u;
+    uint32_t qf[KS][4];
+    float acc[NT][4];
+    float m_run = -INFINITY, l_run = 0.f;
+    uint32_t cur = ~0u, cur_seg = ~0u;
+    const float scale = (float)(1.4426950408889634 / sqrt((double)D));
+
+    // partial (m, l, o) of this warp's segment of slot s; the warp completing
+    // the slot's token count merges all its partials
+    // partial (m, l, o) of this warp's current segment
+    auto flush = [&](uint32_t seg) {
+        float l = l_run;
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        if (r < (int)G) {
+            float* pr = part + ((size_t)seg * G + r) * (D + 2);
+            if (c == 0) {
+                pr[0] = m_run;
+                pr[1] = l;
+            }
+            float* o = pr + 2 + c * (D / 4);
 #pragma unroll
-        for (int st = 0; st < kStages - 1; ++st) {
-            if ((uint32_t)st < my_n) issue((warp + st * kAttWarps) * 16, wn, st);
-            cp_commit();
+            for (int j = 0; j < NT; ++j) {
+                o[j] = acc[j][0] + acc[j][2];
+                o[D / 8 + j] = acc[j][1] + acc[j][3];
+            }
         }
-        for (uint32_t it = 0; it < my_n; ++it) {
-            {
-                const uint32_t nxt = it + kStages - 1;
-                if (nxt < my_n) issue((warp + nxt * kAttWarps) * 16, wn, (int)(nxt % kStages));
-                cp_commit();
-            }
-            cp_wait<kStages - 1>();
-            __syncwarp();
-            const uint32_t t0 = (warp + it * kAttWarps) * 16;
-            const uint32_t sb = ring_s + (uint32_t)(it % kStages) * STAGE;
-            // ---- S = Q K^T (hi rows r, lo rows r+8): even / odd k-steps accumulate
-            // separately so the MMA dependency chains are half as long ----
-            float sc[2][4], sd[2][4];
+    };
+
+    for (uint32_t it = 0;; ++it) {
+        const int e = (int)(it % kRing);
+        const GroupDesc gd = s_gd[warp][e];
+        if (gd.slot == ~0u) break;
+        ++n_groups;
+        // rows of group it + kAhead ride in this iteration's commit group; the
+        // K/V of group it + 2 (rows fetched three iterations ago) are issued
+        fetch((int)((it + kAhead) % kRing));
+        issue((int)((it + 2) % kRing), (int)((it + 2) % kStages));
+        cp_commit();
+        cp_wait<kStages - 1>();
+        __syncwarp();
+        if (gd.seg != cur_seg) {
+            if (cur_seg != ~0u) flush(cur_seg);
+            cur_seg = gd.seg;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-                sd[nt][0] = sd[nt][1] = sd[nt][2] = sd[nt][3] = 0.f;
-            }
+            for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+            m_run = -INFINITY;
+            l_run = 0.f;
+        }
+        if (gd.slot != cur) {
+            cur = gd.slot;
+            // q fragments: softmax scale and log2(e) folded in, bf16 hi (row r) + lo (row r+8)
+            const float* qg = p.q + ((size_t)(a.slot0 + cur) * G + (r < (int)G ? r : 0)) * D + c * (D / 4);
 #pragma unroll
-            for (int w = 0; w < KW; ++w) {
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    const uint32_t row = 8 * nt + r;
-                    const uint4 kv = lds128(sb + row * ROWB + swz(row, c * KW + w) * 16);
-                    mma16816(sc[nt], qf[2 * w], kv.x, kv.y);
-                    mma16816(sd[nt], qf[2 * w + 1], kv.z, kv.w);
-                }
-            }
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) sc[nt][e] += sd[nt][e];
-            // logits of query r for tokens 2c, 2c+1 (nt 0) and 8+2c, 9+2c (nt 1)
-            float lg[4];
-            bool ok[4];
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int nt = x >> 1, e = x & 1;
-                lg[x] = sc[nt][e] + sc[nt][2 + e];
-                const uint32_t tk = nt * 8 + 2 * c + e;
-                ok[x] = r < (int)G && ((s_msk[t0 + tk] >> r) & 1u);
-            }
-            float mx = -INFINITY;
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-                if (ok[x]) mx = fmaxf(mx, lg[x]);
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float m_new = fmaxf(m_run, mx);
-            float pr[4];
-            float corr = 1.f;
-            if (m_new == -INFINITY) {
-                pr[0] = pr[1] = pr[2] = pr[3] = 0.f;
-            } else {
-                corr = exp2f(m_run - m_new);
-#pragma unroll
-                for (int x = 0; x < 4; ++x) pr[x] = ok[x] ? exp2f(lg[x] - m_new) : 0.f;
-                m_run = m_new;
-            }
-            l_run = l_run * corr + (pr[0] + pr[1]) + (pr[2] + pr[3]);
-            if (__any_sync(0xffffffffu, corr != 1.f)) {
-#pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    acc[j][0] *= corr;
-                    acc[j][1] *= corr;
-                    acc[j][2] *= corr;
-                    acc[j][3] *= corr;
-                }
-            }
-            // ---- O += P V ----
-            uint32_t pa[4];
-            {
+            for (int s = 0; s < KS; ++s) {
+                const float4 qv = __ldg(reinterpret_cast<const float4*>(qg + 4 * s));
+                const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
                 float h[4], l[4];
 #pragma unroll
-                for (int x = 0; x < 4; ++x) split_bf16(pr[x], h[x], l[x]);
-                pa[0] = pack_bf16(h[0], h[1]);
-                pa[2] = pack_bf16(h[2], h[3]);
-                pa[1] = pack_bf16(l[0], l[1]);
-                pa[3] = pack_bf16(l[2], l[3]);
+                for (int x = 0; x < 4; ++x) split_bf16(qq[x] * scale, h[x], l[x]);
+                const bool on = r < (int)G;
+                qf[s][0] = on ? pack_bf16(h[0], h[1]) : 0u;
+                qf[s][2] = on ? pack_bf16(h[2], h[3]) : 0u;
+                qf[s][1] = on ? pack_bf16(l[0], l[1]) : 0u;
+                qf[s][3] = on ? pack_bf16(l[2], l[3]) : 0u;
             }
-            const uint32_t vb = sb + 16 * ROWB;
+        }
+        const uint32_t sb = ring_s + (uint32_t)(it % kStages) * STAGE;
+        // ---- S = Q K^T (hi rows r, lo rows r+8): even / odd k-steps accumulate
+        // separately so the MMA dependency chains are half as long ----
+        float sc[2][4], sd[2][4];
 #pragma unroll
-            for (int w = 0; w < VW; ++w) {
-                uint4 vr[4];
+        for (int nt = 0; nt < 2; ++nt) {
+            sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+            sd[nt][0] = sd[nt][1] = sd[nt][2] = sd[nt][3] = 0.f;
+        }
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const uint32_t row = (x >> 1) * 8 + 2 * c + (x & 1);
-                    vr[x] = lds128(vb + row * ROWB + swz(row, r * VW + w) * 16);
-                }
+        for (int w2 = 0; w2 < KW; ++w2) {
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int j = w * 8 + jj, word = jj >> 1;
-                    const uint32_t sel = (jj & 1) ? 0x7632u : 0x5410u;
-                    auto wd = [&](const uint4& u) -> uint32_t {
-                        return word == 0 ? u.x : word == 1 ? u.y : word == 2 ? u.z : u.w;
-                    };
-                    const uint32_t b0 = __byte_perm(wd(vr[0]), wd(vr[1]), sel);
-                    const uint32_t b1 = __byte_perm(wd(vr[2]), wd(vr[3]), sel);
-                    mma16816(acc[j], pa, b0, b1);
-                }
+            for (int nt = 0; nt < 2; ++nt) {
+                const uint32_t row = 8 * nt + r;
+                const uint4 kv = lds128(sb + row * ROWB + swz(row, c * KW + w2) * 16);
+                mma16816(sc[nt], qf[2 * w2], kv.x, kv.y);
+                mma16816(sd[nt], qf[2 * w2 + 1], kv.z, kv.w);
             }
-            __syncwarp();  // the stage is refilled by the next iteration's issue
         }
-        cp_wait<0>();
-        __syncthreads();
-    }
-
-    LC_AMARK(3)
-    // ---- warp partial -> CTA partial (the stage ring is free now) ----
-    float* s_o = reinterpret_cast<float*>(dsm);  // [warps][G][D]
-    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
-    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    if (r < (int)G) {
-        if (c == 0) {
-            s_m[warp][r] = m_run;
-            s_l[warp][r] = l_run;
-        }
-        float* o = s_o + ((size_t)warp * G + r) * D + c * (D / 4);
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            o[j] = acc[j][0] + acc[j][2];
-            o[D / 8 + j] = acc[j][1] + acc[j][3];
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int x = 0; x < 4; ++x) sc[nt][x] += sd[nt][x];
+        // logits of query r for tokens 2c, 2c+1 (nt 0) and 8+2c, 9+2c (nt 1)
+        float lg[4];
+        bool ok[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const int nt = x >> 1, e2 = x & 1;
+            lg[x] = sc[nt][e2] + sc[nt][2 + e2];
+            const uint32_t tk = nt * 8 + 2 * c + e2;
+            ok[x] = r < (int)G && tk < gd.cnt && ((s_rows[warp][e][tk] >> (24 + r)) & 1u);
         }
-    }
-    __syncthreads();
-    float* part = a.partials + ((size_t)slot * S + split) * G * (D + 2);
-    for (uint32_t x = tid; x < G * D; x += blockDim.x) {
-        const uint32_t g = x / D, dd = x % D;
-        float M = -INFINITY;
-        for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, s_m[w][g]);
-        float o = 0.f, L = 0.f;
-        if (M != -INFINITY)
-            for (int w = 0; w < kAttWarps; ++w) {
-                const float f = exp2f(s_m[w][g] - M);
-                o += f * s_o[((size_t)w * G + g) * D + dd];
-                L += f * s_l[w][g];
-            }
-        part[g * (D + 2) + 2 + dd] = o;
-        if (dd == 0) {
-            part[g * (D + 2)] = M;
-            part[g * (D + 2) + 1] = L;
-        }
-    }
-    // ---- last CTA of the slot merges the S partials (log-sum-exp) ----
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.counters + slot, 1u) == S - 1 ? 1u : 0u;
-    __syncthreads();
-    LC_AMARK(4)
-    if (!s_last) {
-        LC_AMARK(5)
-        return;
-    }
-    __threadfence();
-    const float* parts = a.partials + (size_t)slot * S * G * (D + 2);
-    for (uint32_t x = tid; x < G * D; x += blockDim.x) {
-        const uint32_t g = x / D, dd = x % D;
-        float M = -INFINITY;
-        for (uint32_t s = 0; s < S; ++s) M = fmaxf(M, __ldcg(parts + (s * G + g) * (D + 2)));
-        float o = 0.f, L = 0.f;
-        if (M != -INFINITY)
-            for (uint32_t s = 0; s < S; ++s) {
-                const float* ps = parts + (s * G + g) * (D + 2);
-                const float ms = __ldcg(ps);
-                if (ms == -INFINITY) continue;
-                const float f = exp2f(ms - M);
-                o += f * __ldcg(ps + 2 + dd);
-                L += f * __ldcg(ps + 1);
-            }
-        if (L > 0.f) {
-            p.out[((size_t)slot * G + g) * D + dd] = o / L;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            if (ok[x]) mx = fmaxf(mx, lg[x]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        float pr[4];
+        float corr = 1.f;
+        if (m_new == -INFINITY) {
+            pr[0] = pr[1] = pr[2] = pr[3] = 0.f;
         } else {
-            p.out[((size_t)slot * G + g) * D + dd] = 0.f;
-            if (dd == 0) atomicOr(a.err, kErrEmptyActive);
+            corr = exp2f(m_run - m_new);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) pr[x] = ok[x] ? exp2f(lg[x] - m_new) : 0.f;
+            m_run = m_new;
         }
+        l_run = l_run * corr + (pr[0] + pr[1]) + (pr[2] + pr[3]);
+        if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                acc[j][0] *= corr;
+                acc[j][1] *= corr;
+                acc[j][2] *= corr;
+                acc[j][3] *= corr;
+            }
+        }
+        // ---- O += P V ----
+        uint32_t pa[4];
+        {
+            float h[4], l[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) split_bf16(pr[x], h[x], l[x]);
+            pa[0] = pack_bf16(h[0], h[1]);
+            pa[2] = pack_bf16(h[2], h[3]);
+            pa[1] = pack_bf16(l[0], l[1]);
+            pa[3] = pack_bf16(l[2], l[3]);
+        }
+        const uint32_t vb = sb + 16 * ROWB;
+#pragma unroll
+        for (int w2 = 0; w2 < VW; ++w2) {
+            uint4 vr[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const uint32_t row = (x >> 1) * 8 + 2 * c + (x & 1);
+                vr[x] = lds128(vb + row * ROWB + swz(row, r * VW + w2) * 16);
+            }
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = w2 * 8 + jj, word = jj >> 1;
+                const uint32_t sel = (jj & 1) ? 0x7632u : 0x5410u;
+                auto wd = [&](const uint4& u) -> uint32_t {
+                    return word == 0 ? u.x : word == 1 ? u.y : word == 2 ? u.z : u.w;
+                };
+                const uint32_t b0 = __byte_perm(wd(vr[0]), wd(vr[1]), sel);
+                const uint32_t b1 = __byte_perm(wd(vr[2]), wd(vr[3]), sel);
+                mma16816(acc[j], pa, b0, b1);
+            }
+        }
+        __syncwarp();  // the stage is refilled by a later iteration's issue
     }
-    if (tid == 0) a.counters[slot] = 0;
-    LC_AMARK(5)
+    cp_wait<0>();
+    if (cur_seg != ~0u) flush(cur_seg);
+    const unsigned long long t_merge = p.prof ? gtime_a() : 0ull;
+
+    // ---- grid barrier (the grid is sized to be co-resident), then every warp
+    // merges (slot, head) pairs: the slot's partials in a fixed order ----
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(pool_ctr + 1, 1u);
+        while (*reinterpret_cast<volatile uint32_t*>(pool_ctr + 1) < gridDim.x) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+    for (uint32_t x = w; x < n * G; x += NW) {
+        const uint32_t s = x / G, g = x % G;
+        if (s_hp[s + 1] == s_hp[s] && s_tp[s + 1] == s_tp[s]) continue;  // written by block 0
+        merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, part,
+                      NW + n + kPoolPerWarp * NW + n, s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1],
+                      pool.C);
+    }
+    // the last CTA out resets the pool and the barrier for the next launch
+    __syncthreads();
+    if (tid == 0 && atomicAdd(pool_ctr + 2, 1u) == gridDim.x - 1) {
+        pool_ctr[0] = 0;
+        pool_ctr[1] = 0;
+        pool_ctr[2] = 0;
+    }
+    if (p.prof && lane == 0) {
+        unsigned long long* pw = p.prof + (size_t)w * 4;
+        pw[0] = t_start;
+        pw[1] = t_merge;
+        pw[2] = gtime_a();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        pw[3] = n_groups | ((unsigned long long)smid << 40);
+    }
 }
 
 template <int D>
-static cudaError_t launch_attend_d(const AttendParams& p, dim3 grid, cudaStream_t stream) {
-    // (grid.y = number of slots of this launch, starting at p.a.slot0)
-    constexpr size_t ring = (size_t)kAttWarps * kStages * 32 * D * 2;
-    constexpr size_t outb = (size_t)kAttWarps * kMaxGroup * D * 4;
-    constexpr size_t smem = ring > outb ? ring : outb;
+static constexpr size_t attend_smem() {
+    return (size_t)kAttWarps * kStages * 32 * D * 2;
+}
+
+template <int D>
+static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_attend<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_attend<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)attend_smem<D>());
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    k_attend<D><<<grid, kAttThreads, smem, stream>>>(p);
+    k_attend<D><<<grid, kAttThreads, attend_smem<D>(), stream>>>(p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream) {
-    static unsigned long long* prof = nullptr;
-    const size_t nct = (size_t)a.splits * n_slots;
-    if (getenv("LC_PROF") && !prof) cudaMalloc(&prof, (size_t)a.n_slots * 64 * 8 * 8);
-    AttendParams p{a, q, out, prof};
-    dim3 grid(a.splits, n_slots);
-    cudaError_t e = a.d == 128 ? launch_attend_d<128>(p, grid, stream)
-                  : a.d == 64  ? launch_attend_d<64>(p, grid, stream)
-                               : cudaErrorInvalidValue;
-    if (prof && e == cudaSuccess) {
-        cudaStreamSynchronize(stream);
-        std::vector<unsigned long long> t(nct * 8);
-        cudaMemcpy(t.data(), prof, t.size() * 8, cudaMemcpyDeviceToHost);
-        double acc[5] = {0, 0, 0, 0, 0};
-        unsigned long long t0 = ~0ull, t1 = 0;
-        for (size_t c = 0; c < nct; ++c) {
-            const unsigned long long* x = &t[c * 8];
-            for (int k = 0; k < 5; ++k) acc[k] += (double)(x[k + 1] - x[k]);
-            t0 = x[0] < t0 ? x[0] : t0;
-            t1 = x[5] > t1 ? x[5] : t1;
-        }
-        fprintf(stderr, "[LC_PROF] k_attend per-CTA us: q %.2f spans %.2f stream %.2f combine %.2f merge %.2f | span %.1f us\n",
-                acc[0] / nct / 1e3, acc[1] / nct / 1e3, acc[2] / nct / 1e3, acc[3] / nct / 1e3, acc[4] / nct / 1e3,
-                (t1 - t0) / 1e3);
+// Persistent grid: every SM holds as many CTAs as fit.
+uint32_t attend_grid(uint32_t d) {
+    static uint32_t cached[2] = {0, 0};
+    const int k = d == 128 ? 1 : 0;
+    if (cached[k]) return cached[k];
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (d == 128) {
+        cudaFuncSetAttribute(k_attend<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem<128>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_attend<128>, kAttThreads, attend_smem<128>());
+    } else {
+        cudaFuncSetAttribute(k_attend<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem<64>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_attend<64>, kAttThreads, attend_smem<64>());
     }
-    return e;
+    cudaGetLastError();
+    cached[k] = (uint32_t)(sms > 0 ? sms : 1) * (uint32_t)(per > 0 ? per : 1);
+    return cached[k];
+}
+
+size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots) {
+    const size_t warps = (size_t)attend_grid(d) * kAttWarps, n = std::min<uint32_t>(n_slots, kMaxAttendSlots);
+    return 16 + (warps + n + kPoolPerWarp * warps + n + 1) * G * (d + 2);
+}
+
+// Slots go in launches of at most kMaxAttendSlots whose total token capacity
+// fits the kernel's 32-bit global positions.
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
+                          cudaStream_t stream) {
+    const uint32_t grid = attend_grid(a.d);
+    uint32_t per = kMaxAttendSlots;
+    const unsigned long long cap = a.cap_tokens ? a.cap_tokens : 1;
+    if ((unsigned long long)per * cap > 0xffffffffull) per = (uint32_t)(0xffffffffull / cap);
+    static unsigned long long* prof = nullptr;
+    const bool want_prof = getenv("LC_PROF") != nullptr;
+    if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
+    for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
+        AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr};
+        if (prof) cudaMemset(prof, 0, (size_t)grid * kAttWarps * 4 * 8);
+        p.a.slot0 = a.slot0 + s0;
+        cudaError_t e = a.d == 128 ? launch_attend_d<128>(p, grid, stream)
+                      : a.d == 64  ? launch_attend_d<64>(p, grid, stream)
+                                   : cudaErrorInvalidValue;
+        if (e != cudaSuccess) return e;
+        if (want_prof) {
+            std::vector<unsigned long long> t((size_t)grid * kAttWarps * 4);
+            cudaMemcpy(t.data(), prof, t.size() * 8, cudaMemcpyDeviceToHost);
+            unsigned long long t0 = ~0ull, t1 = 0;
+            std::vector<double> dur, loopd;
+            double pro = 0, grp = 0;
+            for (size_t w = 0; w < (size_t)grid * kAttWarps; ++w) {
+                const unsigned long long* x = &t[w * 4];
+                if (!x[0]) continue;
+                t0 = std::min(t0, x[0]);
+                t1 = std::max(t1, x[2]);
+                dur.push_back((x[2] - x[0]) / 1e3);
+                pro += (x[1] - x[0]) / 1e3;
+                grp += (double)(x[3] & 0xffffffffull);
+            }
+            // spread of warp durations inside a CTA vs across SMs
+            double in_cta = 0, sm_min = 1e30, sm_max = 0;
+            std::vector<double> sm_mean(1024, 0.0), sm_cnt(1024, 0.0);
+            for (size_t b = 0; b < grid; ++b) {
+                double lo = 1e30, hi = 0;
+                for (int k = 0; k < kAttWarps; ++k) {
+                    const unsigned long long* x = &t[(b * kAttWarps + k) * 4];
+                    if (!x[0]) continue;
+                    const double d = (x[2] - x[0]) / 1e3;
+                    lo = std::min(lo, d);
+                    hi = std::max(hi, d);
+                    const uint32_t sm = (uint32_t)(x[3] >> 40) & 1023u;
+                    sm_mean[sm] += d;
+                    sm_cnt[sm] += 1;
+                }
+                if (hi > 0) in_cta += hi - lo;
+            }
+            for (int sm = 0; sm < 1024; ++sm)
+                if (sm_cnt[sm] > 0) {
+                    sm_min = std::min(sm_min, sm_mean[sm] / sm_cnt[sm]);
+                    sm_max = std::max(sm_max, sm_mean[sm] / sm_cnt[sm]);
+                }
+            fprintf(stderr, "[LC_PROF] k_attend mean in-CTA warp spread %.1f us; per-SM mean warp duration %.1f .. %.1f us\n",
+                    in_cta / grid, sm_min, sm_max);
+            std::sort(dur.begin(), dur.end());
+            if (!dur.empty())
+                fprintf(stderr, "[LC_PROF] k_attend warps %zu: dur min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f us | "
+                        "stream %.2f us, groups %.1f per warp | first start -> last end %.1f us\n",
+                        dur.size(), dur[0], dur[dur.size() / 10], dur[dur.size() / 2], dur[dur.size() * 9 / 10],
+                        dur.back(), pro / dur.size(), grp / dur.size(), (t1 - t0) / 1e3);
+        }
+    }
+    return cudaSuccess;
 }
 
 }  // namespace lc

@@ -34,6 +34,7 @@
 namespace lc {
 
 constexpr int kMaxGroup = 8;
+constexpr uint32_t kMaxAttendSlots = 1024;  // slots per attention launch (global prefix in smem)
 
 struct SlotState {
     uint32_t n_tokens;
@@ -59,7 +60,7 @@ struct QInfo {  // per query head result summary (mirrors lc_selection_info)
 struct Arena {
     // shape
     uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;
-    uint32_t splits, graft_full, keep_reps, cap_spans;
+    uint32_t graft_full, keep_reps, cap_spans;
     uint32_t smem_cand;      // candidates kept in shared memory by k_select
     uint32_t slot0;          // first slot of the launch (slot groups on several streams)
     // token store
@@ -89,14 +90,15 @@ struct Arena {
     unsigned char* cand_scratch;  // [slot][G][max_cand * 12] overflow of k_select's smem
     unsigned char* plan;          // [slot][plan_bytes] coarse-tier plan of the 3-kernel selection
     uint32_t* chunk_bits;         // [slot][G][words(cap_chunks)] per-head active chunk bitmaps
-    uint32_t* split_span;         // [slot][64] first span of each attention split (k_spans), or null
     uint32_t plan_bytes;
     Span* spans;             // [slot][cap_spans]
     uint32_t* span_off;      // [slot][cap_spans+1] token prefix offsets
     uint32_t* n_spans;       // [slot]
+    uint32_t* rows;          // [slot][cap_tokens] union active tokens in span order:
+                             //   token row | head mask << 24 (k_spans -> k_attend)
+    uint32_t* slot_tok;      // [slot] union active token count (length of the row list)
     unsigned long long* step_bytes;  // [slot][4]
-    float* partials;         // [slot][splits][G][d+2]
-    uint32_t* counters;      // [slot]
+    uint32_t* counters;      // [slot] k_attend tokens accounted so far (reset by the merging warp)
     uint32_t* err;           // [1]
 };
 

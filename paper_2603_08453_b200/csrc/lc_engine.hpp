@@ -10,24 +10,15 @@
 #include <vector>
 
 namespace lc {
-size_t select_smem_bytes(const Arena& a);
-cudaError_t launch_select(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode,
-                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink,
-                          uint32_t n_slots, cudaStream_t stream);
-cudaError_t launch_compact(const Arena& a, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
-                           const uint32_t* buf_ids, uint32_t n_slots, cudaStream_t stream);
-cudaError_t launch_attend(const Arena& a, const float* q, float* out, uint32_t n_slots, cudaStream_t stream);
-size_t select_slot_smem_bytes(const Arena& a, uint32_t pmax);
-bool select_slot_supports_group(uint32_t g);
 size_t select3_pick_smem(const Arena& a);
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
                            uint32_t pmax, uint32_t n_slots, cudaStream_t stream);
-cudaError_t launch_select_slot(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
-                               unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
-                               const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t pmax,
-                               uint32_t n_slots, cudaStream_t stream);
+uint32_t attend_grid(uint32_t d);
+size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
+cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
+                          cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
                          cudaStream_t stream);
@@ -103,19 +94,16 @@ struct lc_index_s {
     lc_graft_report* rep_scratch = nullptr;
     uint32_t last_flags = 0;
     uint32_t last_valid = 0;
-    bool last_three = false;
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
-    unsigned char* cand_scratch = nullptr;     // k_select overflow storage
-    size_t cand_scratch_bytes = 0;
-    unsigned char* slot_scratch = nullptr;     // k_select_slot per-query keys + selections
-    size_t slot_scratch_bytes = 0;
+    unsigned char* sel_scratch = nullptr;      // per-head candidate keys + weights (k_fine -> k_pickq)
+    size_t sel_scratch_bytes = 0;
+    float* att_part = nullptr;                 // k_attend per-(warp, slot) segment partials + counters
     std::vector<cudaStream_t> group_streams;   // one per slot group
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
 
     ~lc_index_s() {
         for (void* p : owned) cudaFree(p);
-        if (cand_scratch) cudaFree(cand_scratch);
-        if (slot_scratch) cudaFree(slot_scratch);
+        if (sel_scratch) cudaFree(sel_scratch);
         for (auto s : group_streams) cudaStreamDestroy(s);
         for (auto e : group_events) cudaEventDestroy(e);
     }

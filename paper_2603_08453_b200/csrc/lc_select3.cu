@@ -688,6 +688,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     Span* sp = a.spans + (size_t)slot * a.cap_spans;
     uint32_t* so = a.span_off + (size_t)slot * (a.cap_spans + 1);
     unsigned long long* sb = a.step_bytes + (size_t)slot * 4;
+    uint32_t* rows = a.rows + (size_t)slot * a.cap_tokens;
     const unsigned long long dd = a.d;
     if (pv.hdr()[0]) {  // degenerate (retriever.cpp:86-95): everything, full attention
         if (tid < G) {
@@ -708,8 +709,9 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
             sb[1] = (dd * 4 * n + 8ull * dd) * G;
             sb[2] = n;
             sb[3] = 0;
+            a.slot_tok[slot] = n;
         }
-        if (a.split_span && tid < a.splits) a.split_span[(size_t)slot * 64 + tid] = 0;
+        for (uint32_t t = tid; t < n; t += blockDim.x) rows[t] = t | (all << 24);
         return;
     }
     __shared__ unsigned long long wtot[kSpWarps];
@@ -728,6 +730,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         if (tid == 0) {
             a.n_spans[slot] = 0;
             so[0] = 0;
+            a.slot_tok[slot] = 0;
         }
         return;
     }
@@ -743,6 +746,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         }
         out = 1;
         tok = sink_end;
+        for (uint32_t t = tid; t < sink_end; t += blockDim.x) rows[t] = t | (all << 24);
     }
     const uint32_t* cs = a.chunk_start + (size_t)slot * (a.cap_chunks + 1);
     uint32_t my_cnt[GQ], my_nsp[GQ];
@@ -802,6 +806,25 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         }
     }
     const uint32_t n_chunk_spans = out - (sink_end > 0 ? 1u : 0u);
+    __syncthreads();
+    {  // row list of the chunk spans: one warp per 32 spans, coalesced row writes
+        const uint32_t first = sink_end > 0 ? 1u : 0u, warp = tid >> 5;
+        for (uint32_t k0 = first + warp * 32; k0 < out; k0 += kSpWarps * 32) {
+            const uint32_t k = k0 + lane;
+            uint32_t st = 0, lm = 0, off = 0;
+            if (k < out) {
+                st = sp[k].start;
+                lm = sp[k].len_mask;
+                off = so[k];
+            }
+            const uint32_t nk = min(32u, out - k0);
+            for (uint32_t j = 0; j < nk; ++j) {
+                const uint32_t sj = __shfl_sync(0xffffffffu, st, j), lj = __shfl_sync(0xffffffffu, lm, j);
+                const uint32_t oj = __shfl_sync(0xffffffffu, off, j), len = lj >> 8, m = (lj & 0xffu) << 24;
+                for (uint32_t t = lane; t < len; t += 32) rows[oj + t] = (sj + t) | m;
+            }
+        }
+    }
     if (p.flags == 1u) {  // buffer_ids = [chunked_end, n), disjoint from the chunks
         const uint32_t b0 = max(ce, sink_end);
         if (n > b0) {
@@ -810,6 +833,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
                 sp[out].len_mask = ((n - b0) << 8) | all;
                 so[out] = tok;
             }
+            for (uint32_t t = tid; t < n - b0; t += blockDim.x) rows[tok + t] = (b0 + t) | (all << 24);
             ++out;
             tok += n - b0;
         }
@@ -839,6 +863,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
             unsigned long long total;
             const unsigned long long ex = sp_scan<unsigned long long>(resid ? ((1ull << 40) | 1ull) : 0ull, wtot, total);
             if (resid) {
+                rows[tok + (uint32_t)(ex & 0xffffffffffull)] = id | (resid << 24);
                 const uint32_t pos = out + (uint32_t)(ex >> 40);
                 if (pos < a.cap_spans) {
                     sp[pos].start = id;
@@ -861,6 +886,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         }
         so[out] = tok;
         a.n_spans[slot] = out;
+        a.slot_tok[slot] = tok;
         const unsigned long long Pl = P;
         const uint32_t bufl = (p.flags == 1u && n > max(ce, sink_end)) ? n - max(ce, sink_end) : 0u;
         unsigned long long per_q = 0;
@@ -876,19 +902,6 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         sb[1] = per_q;
         sb[2] = tok;
         sb[3] = ncu;
-    }
-    // first span of every attention split (token-balanced, like k_attend's ranges)
-    __syncthreads();
-    if (a.split_span && tid < a.splits) {
-        const uint32_t nsp = out < a.cap_spans ? out : a.cap_spans;
-        const uint32_t beg = (uint32_t)(((unsigned long long)tok * tid) / a.splits);
-        uint32_t lo = 0, hi = nsp;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (so[mid] <= beg) lo = mid;
-            else hi = mid;
-        }
-        a.split_span[(size_t)slot * 64 + tid] = lo;
     }
 }
 
