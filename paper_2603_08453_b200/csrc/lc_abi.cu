@@ -91,7 +91,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.funit = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.fmem_off = dalloc<uint32_t>(S * (d.cap_clusters + 1), o);
         a.fmem = dalloc<uint32_t>(S * d.cap_chunks, o);
-        a.plan_bytes = (uint32_t)((256 + (size_t)a.cap_units * (4 + d.group) * 4 + 15) & ~15ull);
+        a.plan_bytes = plan_layout(a.cap_units, d.group, d.dim, d.cap_clusters, nullptr, nullptr, nullptr);
         a.plan = dalloc<unsigned char>(S * a.plan_bytes, o);
         a.chunk_bits = dalloc<uint32_t>(S * G * bit_words(d.cap_chunks), o);
         a.state = dalloc<SlotState>(S, o);
@@ -109,6 +109,9 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         const size_t part_floats = attend_partials_floats(a.d, a.G, a.n_slots);
         h->att_part = dalloc<float>(part_floats, o);
         ck(cudaMemset(h->att_part, 0, part_floats * 4), "memset attention partials");
+        const size_t groups = std::max<uint32_t>(1, std::min(d.slot_groups, d.n_slots));
+        h->fine_ctr = dalloc<uint32_t>(4 * groups, o);
+        ck(cudaMemset(h->fine_ctr, 0, 4 * groups * 4), "memset k_fine counters");
         a.counters = dalloc<uint32_t>(S, o);
         a.err = dalloc<uint32_t>(1, o);
         h->q_stage = dalloc<float>(S * G * D, o);
@@ -435,12 +438,12 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         if (!s.loaded) fail(LC_EINVAL, "retrieve: every slot must be uploaded or built");
     h->set_device();
     Arena a = h->a;
-    a.max_cand = needed_candidates(h, std::min<uint32_t>(b->unit_topk, 64));
+    a.max_cand = (needed_candidates(h, std::min<uint32_t>(b->unit_topk, 64)) + 1) & ~1u;  // 8-byte key rows
     uint32_t pmax = 1;
     for (auto& s : h->hs) pmax = std::max(pmax, s.P);
     if (select3_pick_smem(a) > 200 * 1024) fail(LC_EINVAL, "retrieve: chunk capacity too large for k_pickq");
     const uint32_t max_union = needed_candidates(h, std::min<uint32_t>(a.G * std::min<uint32_t>(b->unit_topk, 64), 4096));
-    const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 12;
+    const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 20;  // lo key, weight, hi (k_fine)
     if (h->sel_scratch_bytes < need) {
         if (h->sel_scratch) cudaFree(h->sel_scratch);
         h->sel_scratch = nullptr;
@@ -453,15 +456,15 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     }
     // k_coarse -> k_fine -> k_pickq -> k_spans (selection, per slot group), then
     // one persistent k_attend over every slot (its grid barrier needs the whole GPU)
-    auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs) {
+    auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs, uint32_t gi) {
         ck(launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, flags,
-                          buf_off, buf_ids, h->sel_scratch, a.max_cand, max_union, pmax, count, gs),
+                          buf_off, buf_ids, h->sel_scratch, a.max_cand, max_union, pmax, count, h->fine_ctr + 4 * gi, gs),
            "k_select3");
     };
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
     if (groups == 1) {
         a.slot0 = 0;
-        run_group(a, a.n_slots, st);
+        run_group(a, a.n_slots, st, 0);
     } else {
         // fork: each slot group's selection runs on its own stream
         ensure_streams(h, groups);
@@ -474,7 +477,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
             ck(cudaStreamWaitEvent(gs, h->group_events[0], 0), "fork wait");
             Arena ag = a;
             ag.slot0 = s0;
-            run_group(ag, s1 - s0, gs);
+            run_group(ag, s1 - s0, gs, gi);
             ck(cudaEventRecord(h->group_events[gi + 1], gs), "join record");
             ck(cudaStreamWaitEvent(st, h->group_events[gi + 1], 0), "join");
         }

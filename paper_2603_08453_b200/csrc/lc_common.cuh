@@ -104,6 +104,22 @@ struct Arena {
 
 __host__ __device__ inline uint32_t bit_words(uint32_t n) { return (n + 31) / 32; }
 
+// Per-slot selection plan (k_coarse -> k_fine / k_pickq / k_spans): header
+// (256 B), union units u32 [cap_units][4 + G], ucum u32 [cap_units + 1], then
+// q as f64 [G][d] at a 16-byte boundary, then the fine tile table
+// uint4 [ceil(cap_clusters / 32)] = {first union unit, unit-start bit mask,
+// first candidate's index in its unit, 0}.  Returns the total size.
+__host__ __device__ inline uint32_t plan_layout(uint32_t cap_units, uint32_t G, uint32_t d, uint32_t cap_clusters,
+                                                uint32_t* ucum_off, uint32_t* qd_off, uint32_t* tile_off) {
+    const uint32_t u = 256 + cap_units * (4 + G) * 4;
+    const uint32_t q = (u + (cap_units + 1) * 4 + 15) & ~15u;
+    const uint32_t t = q + G * d * 8;
+    if (ucum_off) *ucum_off = u;
+    if (qd_off) *qd_off = q;
+    if (tile_off) *tile_off = t;
+    return t + ((cap_clusters + 31) / 32) * 16;
+}
+
 // element (member `local` of the unit block starting at internal id `base` with
 // `nu` members, dimension j) of the fine-centroid array
 __host__ __device__ inline size_t fine_at(uint32_t base, uint32_t nu, uint32_t local, uint32_t j, uint32_t d) {

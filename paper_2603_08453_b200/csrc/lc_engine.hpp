@@ -14,7 +14,7 @@ size_t select3_pick_smem(const Arena& a);
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
-                           uint32_t pmax, uint32_t n_slots, cudaStream_t stream);
+                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream);
 uint32_t attend_grid(uint32_t d);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
@@ -98,6 +98,7 @@ struct lc_index_s {
     unsigned char* sel_scratch = nullptr;      // per-head candidate keys + weights (k_fine -> k_pickq)
     size_t sel_scratch_bytes = 0;
     float* att_part = nullptr;                 // k_attend per-(warp, slot) segment partials + counters
+    uint32_t* fine_ctr = nullptr;              // k_fine pool counters, 4 per slot group (zeroed)
     std::vector<cudaStream_t> group_streams;   // one per slot group
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
 

@@ -30,16 +30,35 @@ namespace {
 constexpr int kMaxKU3 = 64;
 
 // plan layout (bytes): 0: u32 degenerate, nuu, ncu, kU, nc[8]; 64: u64 kmin[8];
-// 128: u64 kmax[8]; 192: f64 qnorm[8]; 256: units u32 [k][4 + G] =
-// unit, mask, base, n_u, qoff[G]
+// 128: u64 kmax[8]; 192: f64 qnorm[8]; 256: units u32 [cap_units][4 + G] =
+// unit, mask, base, n_u, qoff[G]; then ucum u32 [cap_units + 1] (first union
+// candidate of each union unit); then, 16-byte aligned, q as f64 [G][D]
+// (plan_layout() is the single definition, shared with the host)
 struct PlanView {
     unsigned char* b;
+    uint32_t ucum_off, qd_off, tile_off;
+    __device__ PlanView(unsigned char* base, const Arena& a) : b(base) {
+        plan_layout(a.cap_units, a.G, a.d, a.cap_clusters, &ucum_off, &qd_off, &tile_off);
+    }
     __device__ uint32_t* hdr() const { return reinterpret_cast<uint32_t*>(b); }
     __device__ unsigned long long* kmin() const { return reinterpret_cast<unsigned long long*>(b + 64); }
     __device__ unsigned long long* kmax() const { return reinterpret_cast<unsigned long long*>(b + 128); }
     __device__ double* qnorm() const { return reinterpret_cast<double*>(b + 192); }
     __device__ uint32_t* units() const { return reinterpret_cast<uint32_t*>(b + 256); }
+    __device__ uint32_t* ucum() const { return reinterpret_cast<uint32_t*>(b + ucum_off); }
+    __device__ double* qd() const { return reinterpret_cast<double*>(b + qd_off); }
+    __device__ uint4* tiles() const { return reinterpret_cast<uint4*>(b + tile_off); }
 };
+
+// inverse of desc_key: the score a key stands for
+__device__ __forceinline__ double key_score(unsigned long long key) {
+    const unsigned long long ord = ~key;
+    const unsigned long long b = (ord >> 63) ? (ord & 0x7fffffffffffffffull) : ~ord;
+    return __longlong_as_double((long long)b);
+}
+
+constexpr uint32_t kPickRCap = 256;   // refinement list kept in shared memory
+constexpr uint32_t kPickCols = 8;     // refinement centroids staged per pass
 
 __device__ __forceinline__ void bar_g(uint32_t id, uint32_t n) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -58,6 +77,7 @@ struct Sel3Params {
     unsigned char* scratch;  // per slot: keys u64 [G][qcap] + weights/selection u32 [G][qcap]
     uint32_t qcap;
     unsigned long long* prof;  // optional k_pick phase timestamps [slot][8] (LC_PROF=1)
+    uint32_t* fine_ctr;        // k_fine pool / exit counters (zeroed; reset by k_fine)
 };
 
 __device__ __forceinline__ unsigned long long gtime3() {
@@ -79,7 +99,7 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
     constexpr uint32_t G = GQ, d = D;
     const SlotState st = a.state[slot];
     const uint32_t n = st.n_tokens, P = st.P;
-    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
     QInfo* qi = a.qinfo + (size_t)slot * G;
     const bool degenerate = (p.mode == 1 && (unsigned long long)n <= p.budget) || st.n_chunks == 0;
     if (degenerate) {
@@ -95,8 +115,13 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
     unsigned long long* ukey = reinterpret_cast<unsigned long long*>(ucs + (size_t)D * Pp);  // [G][P]
     __shared__ double s_qn[GQ];
     __shared__ uint32_t s_kept[GQ][kMaxKU3];
+    __shared__ uint32_t s_ucum[1025];
+    __shared__ uint32_t s_nuu;
 
-    for (uint32_t x = tid; x < G * D; x += blockDim.x) qd[x] = (double)p.q[(size_t)slot * G * D + x];
+    for (uint32_t x = tid; x < G * D; x += blockDim.x) {
+        qd[x] = (double)p.q[(size_t)slot * G * D + x];
+        pv.qd()[x] = qd[x];  // k_fine reads q as f64 from the plan (L1-resident)
+    }
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
     {
         const uint32_t pq = Pp >> 2, n4 = D * pq;
@@ -170,8 +195,9 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
 #pragma unroll
                 for (int g = 0; g < GQ; ++g)
                     for (uint32_t k = 0; k < kU; ++k) m |= (s_kept[g][k] == u ? 1u : 0u) << g;
-            const unsigned int bal = __ballot_sync(0xffffffffu, m != 0);
             const uint32_t nu = m ? uoff[u + 1] - uoff[u] : 0u;
+            if (nu == 0) m = 0;  // an empty unit contributes no candidate
+            const unsigned int bal = __ballot_sync(0xffffffffu, m != 0);
             const uint32_t idx = pos + __popc(bal & ((1u << lane) - 1u));
 #pragma unroll
             for (int g = 0; g < GQ; ++g) {
@@ -184,6 +210,18 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
                 }
                 if (m) uu[idx * stride + 4 + g] = qacc[g] + x - mine;
                 qacc[g] += __shfl_sync(0xffffffffu, x, 31);
+            }
+            {
+                uint32_t x = nu;  // nu == 0 for units outside the union
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
+                }
+                if (m) {
+                    pv.ucum()[idx] = ncu + x - nu;
+                    s_ucum[idx] = ncu + x - nu;
+                }
             }
             if (m) {
                 uu[idx * stride + 0] = u;
@@ -199,6 +237,9 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
             pv.hdr()[1] = pos;
             pv.hdr()[2] = ncu;
             pv.hdr()[3] = kU;
+            pv.ucum()[pos] = ncu;
+            s_ucum[pos] = ncu;
+            s_nuu = pos;
         }
         if (lane < G) {
             pv.hdr()[4 + lane] = qacc[lane];
@@ -207,92 +248,245 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
             pv.qnorm()[lane] = s_qn[lane];
         }
     }
+    __syncthreads();
+    // fine tile table: tile t covers union candidates [32t, 32t + 32)
+    {
+        const uint32_t nuu = s_nuu, ncu = s_ucum[nuu], ntiles = (ncu + 31) / 32;
+        for (uint32_t t = tid; t < ntiles; t += kCoThreads) {
+            const uint32_t c0 = t * 32;
+            uint32_t lo = 0, hi = nuu;  // last unit with ucum <= c0
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_ucum[mid] <= c0) lo = mid;
+                else hi = mid;
+            }
+            uint32_t mask = 0;
+            for (uint32_t k = lo + 1; k < nuu && s_ucum[k] < c0 + 32; ++k) mask |= 1u << (s_ucum[k] - c0);
+            pv.tiles()[t] = make_uint4(lo, mask, c0 - s_ucum[lo], 0u);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
-constexpr int kFiThreads = 128;  // 4 warps, one 32-candidate tile each
+// k_fine: persistent fine-tier scoring, as a certified fp32 filter.
+//
+// The union candidates of every slot form one global list of 32-candidate
+// tiles (slot-major; k_coarse planned each slot's union and its tile table).
+// Each warp scores a contiguous static range of tiles, then claims single
+// tiles from a pool (the last kFinePoolPct % of the list) as it finishes, so
+// SMs that see less bandwidth do less work.  In a tile each lane owns one
+// candidate: its 512-byte centroid is loaded into registers in one burst.
+//
+// The reference upper bound UB = fl64(sequential fp64 q.c) + qn*r
+// (kernels.cpp:155-159) is enclosed, not computed: s = fp32 q.c and
+// A = fp32 sum |q_j c_j| give |UB_ref - UB~| <= e with UB~ = s + qn*r and
+// e = 1.01 * 132 * 2^-24 * A + 2^-49 |UB~| (recursive-summation bound for 128
+// products + 3 partial-sum adds in fp32, plus the fp64 dot's and adds'
+// roundings).  k_pickq selects on the lower bounds, then recomputes the exact
+// fp64 chain (bit-exact kernels::dot) only for candidates whose upper bound
+// reaches the selection cut, so every selection stays bit-exact while the
+// bulk of the scoring runs at fp32 speed.
+constexpr int kFiThreads = 128;
+constexpr int kFiWarps = kFiThreads / 32;
+constexpr uint32_t kFinePoolPct = 10;
+constexpr uint32_t kScratchEntry = 20;  // bytes per (head, candidate): lo key u64, weight u32, hi f64
 
 template <int D, int GQ>
-__global__ void __launch_bounds__(kFiThreads) k_fine(Sel3Params p) {
+__global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n) {
     const Arena& a = p.a;
-    const uint32_t slot = a.slot0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr uint32_t G = GQ, d = D, dq = D / 4;
-    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
-    __shared__ uint32_t s_hdr[8];
-    __shared__ double s_q[GQ][D];
-    __shared__ double s_qn[GQ];
-    __shared__ uint32_t s_u[kMaxKU3 * GQ][4 + GQ];
-    if (tid < 4) s_hdr[tid] = pv.hdr()[tid];
-    __syncthreads();
-    const uint32_t ncu = s_hdr[2], nuu = s_hdr[1];
-    const uint32_t ntile = (ncu + 31) / 32, nwarps_total = gridDim.x * (kFiThreads / 32);
-    const uint32_t wglobal = blockIdx.x * (kFiThreads / 32) + warp;
-    if (s_hdr[0] || blockIdx.x * (kFiThreads / 32) >= ntile) return;
-    for (uint32_t x = tid; x < G * D; x += blockDim.x) s_q[x / D][x % D] = (double)p.q[(size_t)slot * G * D + x];
-    if (tid < G) s_qn[tid] = pv.qnorm()[tid];
-    for (uint32_t x = tid; x < nuu * (4 + G); x += blockDim.x) s_u[x / (4 + G)][x % (4 + G)] = pv.units()[x];
-    __syncthreads();
-    const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(p.scratch + (size_t)slot * G * p.qcap * 12);
-    uint32_t* wts = reinterpret_cast<uint32_t*>(keys + (size_t)G * p.qcap);
-    unsigned long long wmin[GQ], wmax[GQ];
-#pragma unroll
-    for (int g = 0; g < GQ; ++g) {
-        wmin[g] = ~0ull;
-        wmax[g] = 0ull;
-    }
-    // warps stride over this slot's 32-candidate tiles
-    for (uint32_t tile = wglobal; tile < ntile; tile += nwarps_total) {
-        const uint32_t ci = tile * 32 + lane;
-        const bool active = ci < ncu;
-        uint32_t k = 0, acc = 0;
-        if (active)
-            while (k + 1 < nuu && acc + s_u[k][3] <= ci) {
-                acc += s_u[k][3];
-                ++k;
-            }
-        const uint32_t local = ci - acc, base = s_u[k][2], nu = s_u[k][3], m = active ? s_u[k][1] : 0u;
-        const float4* col = reinterpret_cast<const float4*>(fc + (size_t)base * d) + local;
-        float4 v[dq];
-        if (active) {
-#pragma unroll
-            for (uint32_t jq = 0; jq < dq; ++jq) v[jq] = __ldg(col + (size_t)jq * nu);
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t G = GQ, V = D / 4;  // float4s per centroid
+    __shared__ uint32_t s_tp[kMaxAttendSlots + 1];  // prefix of the slots' tile counts
+    __shared__ uint32_t s_ws[kFiWarps];
+    __shared__ __align__(16) float s_q[kFiWarps][GQ * D];  // q of the warp's current slot
+    {
+        const uint32_t per = (n + kFiThreads - 1) / kFiThreads, i0 = tid * per;
+        uint32_t loc = 0;
+        for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
+            const uint32_t* h = reinterpret_cast<const uint32_t*>(a.plan + (size_t)(a.slot0 + i) * a.plan_bytes);
+            loc += h[0] ? 0u : (h[2] + 31) / 32;
         }
-        const uint32_t cid = base + local;
-        const double r = active ? a.frad[(size_t)slot * a.cap_clusters + cid] : 0.0;
-        const uint32_t w = active ? (p.mode == 1 ? a.ftok[(size_t)slot * a.cap_clusters + cid] : 1u) : 0u;
+        uint32_t x = loc;
 #pragma unroll
-        for (int g = 0; g < GQ; ++g) {
-            if ((m >> g) & 1u) {
-                double sacc = 0.0;
-#pragma unroll
-                for (uint32_t jq = 0; jq < dq; ++jq) {
-                    sacc = __fma_rn(s_q[g][4 * jq + 0], (double)v[jq].x, sacc);
-                    sacc = __fma_rn(s_q[g][4 * jq + 1], (double)v[jq].y, sacc);
-                    sacc = __fma_rn(s_q[g][4 * jq + 2], (double)v[jq].z, sacc);
-                    sacc = __fma_rn(s_q[g][4 * jq + 3], (double)v[jq].w, sacc);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) s_ws[warp] = x;
+        __syncthreads();
+        uint32_t run = x - loc;
+        for (uint32_t w = 0; w < warp; ++w) run += s_ws[w];
+        if (tid == 0) s_tp[0] = 0;
+        for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
+            const uint32_t* h = reinterpret_cast<const uint32_t*>(a.plan + (size_t)(a.slot0 + i) * a.plan_bytes);
+            run += h[0] ? 0u : (h[2] + 31) / 32;
+            s_tp[i + 1] = run;
+        }
+        __syncthreads();
+    }
+    const uint32_t TT = s_tp[n];
+    uint32_t* ctr = p.fine_ctr;  // [0] next pool tile, [1] CTAs out
+    if (TT > 0) {
+        const uint32_t NW = gridDim.x * kFiWarps, w = blockIdx.x * kFiWarps + warp;
+        const uint32_t TS = TT - (uint32_t)(((unsigned long long)TT * kFinePoolPct) / 100);
+        uint32_t cur_t = (uint32_t)(((unsigned long long)TS * w) / NW);
+        const uint32_t s_end = (uint32_t)(((unsigned long long)TS * (w + 1)) / NW);
+        uint32_t claim = 0;  // lane 0: pool tile claimed one tile before it is needed
+        if (cur_t >= s_end && lane == 0) claim = TS + atomicAdd(ctr, 1u);
+        auto next_tile = [&]() -> uint32_t {
+            if (cur_t < s_end) {
+                const uint32_t t = cur_t++;
+                if (cur_t >= s_end && lane == 0) claim = TS + atomicAdd(ctr, 1u);
+                return t;
+            }
+            const uint32_t t = __shfl_sync(0xffffffffu, claim, 0);
+            if (t >= TT) return ~0u;
+            if (lane == 0) claim = TS + atomicAdd(ctr, 1u);
+            return t;
+        };
+        uint32_t lo = 0;  // slot (local index) of the last described tile
+        struct Desc {
+            uint32_t slot;     // ~0u: no tile
+            uint32_t ti;       // tile index inside the slot
+            uint32_t k, local; // lane's union unit and index inside the unit
+            uint32_t base, nu, valid;
+        };
+        // descriptor of tile t: slot lookup in shared memory, one tile-table
+        // entry, the lane's unit row
+        auto describe = [&](uint32_t t) -> Desc {
+            Desc d;
+            d.slot = ~0u;
+            if (t == ~0u) return d;
+            if (t < s_tp[lo] || t >= s_tp[lo + 1]) {
+                uint32_t l = 0, h = n;
+                while (h - l > 1) {
+                    const uint32_t mid = (l + h) >> 1;
+                    if (s_tp[mid] <= t) l = mid;
+                    else h = mid;
                 }
-                const unsigned long long key = desc_key(__dadd_rn(sacc, __dmul_rn(s_qn[g], r)));
-                const size_t at = (size_t)g * p.qcap + s_u[k][4 + g] + local;
-                keys[at] = key;
-                wts[at] = w;
-                wmin[g] = min(wmin[g], key);
-                wmax[g] = max(wmax[g], key);
+                while (s_tp[l + 1] <= t) ++l;
+                lo = l;
             }
+            d.slot = a.slot0 + lo;
+            const PlanView pv(a.plan + (size_t)d.slot * a.plan_bytes, a);
+            d.ti = t - s_tp[lo];
+            const uint4 te = pv.tiles()[d.ti];  // {first unit, unit starts, first local, -}
+            const uint32_t ncu = __ldg(pv.hdr() + 2);
+            d.valid = d.ti * 32 + lane < ncu;
+            const uint32_t below = te.y & ((2u << lane) - 1u);  // unit starts at positions <= lane
+            const uint32_t nb = __popc(below);
+            d.k = te.x + nb;
+            d.local = d.valid ? (nb ? lane - (31 - __clz(below)) : te.z + lane) : 0u;
+            const uint32_t* u = pv.units() + (size_t)d.k * (4 + G);
+            d.base = __ldg(u + 2);
+            d.nu = __ldg(u + 3);
+            return d;
+        };
+        uint32_t qslot = ~0u;
+        auto load_q = [&](uint32_t slot) {  // the slot's q (fp32) into this warp's buffer
+            for (uint32_t x = lane; x < G * D / 4; x += 32)
+                reinterpret_cast<float4*>(s_q[warp])[x] = __ldg(reinterpret_cast<const float4*>(p.q + (size_t)slot * G * D) + x);
+            __syncwarp();
+            qslot = slot;
+        };
+        uint32_t mslot = ~0u;  // slot whose per-head key range the warp is tracking
+        unsigned long long wmin[GQ], wmax[GQ];
+        auto flush_minmax = [&]() {
+            if (mslot == ~0u) return;
+            PlanView pv(a.plan + (size_t)mslot * a.plan_bytes, a);
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) {
+                unsigned long long mn = wmin[g], mx = wmax[g];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                }
+                if (lane == 0 && mx != 0ull) {
+                    atomicMin(pv.kmin() + g, mn);
+                    atomicMax(pv.kmax() + g, mx);
+                }
+            }
+        };
+
+        Desc d = describe(next_tile());
+        while (d.slot != ~0u) {
+            // the tile's centroids, radius and weight: one burst of loads
+            const float4* col = reinterpret_cast<const float4*>(a.fcent + (size_t)d.slot * a.cap_clusters * D +
+                                                               (size_t)d.base * D) + d.local;
+            float4 v[V];
+            if (d.valid) {
+#pragma unroll
+                for (uint32_t j = 0; j < V; ++j) v[j] = __ldg(col + (size_t)j * d.nu);
+            }
+            const uint32_t cid = d.base + d.local;
+            const double r = d.valid ? __ldg(a.frad + (size_t)d.slot * a.cap_clusters + cid) : 0.0;
+            const uint32_t wt = d.valid ? (p.mode == 1 ? __ldg(a.ftok + (size_t)d.slot * a.cap_clusters + cid) : 1u) : 0u;
+            // next tile's descriptor while this tile's data is in flight
+            const Desc dn = describe(next_tile());
+            if (d.slot != qslot) load_q(d.slot);
+            float s4[GQ][4], a4[GQ][4];
+#pragma unroll
+            for (int g = 0; g < GQ; ++g)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) s4[g][t] = a4[g][t] = 0.f;
+#pragma unroll
+            for (uint32_t j = 0; j < V; ++j) {
+#pragma unroll
+                for (int g = 0; g < GQ; ++g) {
+                    const float4 q4 = reinterpret_cast<const float4*>(s_q[warp] + g * D)[j];
+                    s4[g][0] = fmaf(q4.x, v[j].x, s4[g][0]);
+                    s4[g][1] = fmaf(q4.y, v[j].y, s4[g][1]);
+                    s4[g][2] = fmaf(q4.z, v[j].z, s4[g][2]);
+                    s4[g][3] = fmaf(q4.w, v[j].w, s4[g][3]);
+                    a4[g][0] = fmaf(fabsf(q4.x), fabsf(v[j].x), a4[g][0]);
+                    a4[g][1] = fmaf(fabsf(q4.y), fabsf(v[j].y), a4[g][1]);
+                    a4[g][2] = fmaf(fabsf(q4.z), fabsf(v[j].z), a4[g][2]);
+                    a4[g][3] = fmaf(fabsf(q4.w), fabsf(v[j].w), a4[g][3]);
+                }
+            }
+            if (d.slot != mslot) {
+                flush_minmax();
+                mslot = d.slot;
+#pragma unroll
+                for (int g = 0; g < GQ; ++g) {
+                    wmin[g] = ~0ull;
+                    wmax[g] = 0ull;
+                }
+            }
+            const PlanView pv(a.plan + (size_t)d.slot * a.plan_bytes, a);
+            const uint32_t* u = pv.units() + (size_t)d.k * (4 + G);
+            const uint32_t mask = d.valid ? __ldg(u + 1) : 0u;
+            unsigned char* sc = p.scratch + (size_t)d.slot * G * p.qcap * kScratchEntry;
+            unsigned long long* keys = reinterpret_cast<unsigned long long*>(sc);
+            uint32_t* wts = reinterpret_cast<uint32_t*>(keys + (size_t)G * p.qcap);
+            double* his = reinterpret_cast<double*>(wts + (size_t)G * p.qcap);
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) {
+                if ((mask >> g) & 1u) {
+                    const float sv = (s4[g][0] + s4[g][1]) + (s4[g][2] + s4[g][3]);
+                    const float av = (a4[g][0] + a4[g][1]) + (a4[g][2] + a4[g][3]);
+                    const double ub = __dadd_rn((double)sv, __dmul_rn(__ldg(pv.qnorm() + g), r));
+                    const double e = (double)av * (1.01 * 132.0 / 16777216.0) + fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
+                    const unsigned long long key = desc_key(ub - e);
+                    const size_t at = (size_t)g * p.qcap + __ldg(u + 4 + g) + d.local;
+                    keys[at] = key;
+                    wts[at] = wt;
+                    his[at] = ub + e;
+                    wmin[g] = min(wmin[g], key);
+                    wmax[g] = max(wmax[g], key);
+                }
+            }
+            d = dn;
         }
+        flush_minmax();
     }
-#pragma unroll
-    for (int g = 0; g < GQ; ++g) {
-        unsigned long long mn = wmin[g], mx = wmax[g];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        if (lane == 0 && mx != 0ull) {
-            atomicMin(pv.kmin() + g, mn);
-            atomicMax(pv.kmax() + g, mx);
-        }
+    // the last CTA out resets the pool for the next launch
+    __threadfence();
+    __syncthreads();
+    if (tid == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+        ctr[0] = 0;
+        ctr[1] = 0;
     }
 }
 
@@ -335,15 +529,16 @@ __device__ __forceinline__ T pk_scan(T v, T* wt, T& total) {
 constexpr int kPqThreads = 128;
 constexpr int kPqWarps = kPqThreads / 32;
 
-template <int GQ>
+template <int DQ, int GQ>
 __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
+    constexpr uint32_t D = DQ;
     extern __shared__ __align__(16) unsigned char qsm[];
     const Arena& a = p.a;
     const uint32_t g = blockIdx.x, slot = a.slot0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t G = GQ;
     const SlotState st = a.state[slot];
     const uint32_t M = st.n_chunks, P = st.P, L = st.L;
-    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
     QInfo* qi = a.qinfo + (size_t)slot * G + g;
     if (pv.hdr()[0]) return;  // degenerate slot: k_spans writes everything
     LC_PMARK(0)
@@ -356,9 +551,13 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
     __shared__ unsigned long long s_prefix, s_mask, s_wbefore;
     __shared__ uint32_t s_cbefore, s_state, s_nsel;
     __shared__ int s_shift;
-    constexpr uint32_t kStage = 512;
-    __shared__ unsigned long long s_sk[kStage];
-    __shared__ uint32_t s_sc[kStage], s_so[kStage];
+    constexpr uint32_t kStage = 256;
+    // the rank phase's staging (s_sk, s_sc, s_so) and the refinement's arrays
+    // (s_rk, s_ro, s_rw, s_ri) live in different phases: one buffer
+    __shared__ __align__(16) unsigned char s_ph[kPickRCap * 20 > kStage * 16 ? kPickRCap * 20 : kStage * 16];
+    unsigned long long* s_sk = reinterpret_cast<unsigned long long*>(s_ph);
+    uint32_t* s_sc = reinterpret_cast<uint32_t*>(s_ph + kStage * 8);
+    uint32_t* s_so = reinterpret_cast<uint32_t*>(s_ph + kStage * 12);
     for (uint32_t w = tid; w < mw; w += blockDim.x) cb[w] = 0u;
     __shared__ uint32_t s_uu[kMaxKU3 * GQ * 3];  // (mask, base, qoff_g) of the union units, staged
     __shared__ uint32_t s_nuu;
@@ -410,10 +609,10 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
         }
         return;
     }
-    unsigned long long* kg = reinterpret_cast<unsigned long long*>(p.scratch + (size_t)slot * G * p.qcap * 12) +
+    unsigned long long* kg = reinterpret_cast<unsigned long long*>(p.scratch + (size_t)slot * G * p.qcap * kScratchEntry) +
                              (size_t)g * p.qcap;
     uint32_t* sg = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(
-                       p.scratch + (size_t)slot * G * p.qcap * 12) + (size_t)G * p.qcap) + (size_t)g * p.qcap;
+                       p.scratch + (size_t)slot * G * p.qcap * kScratchEntry) + (size_t)G * p.qcap) + (size_t)g * p.qcap;
     if (nc <= p.keys_cap) {  // stage keys and weights (all loads in flight at once)
         for (uint32_t b0 = 0; b0 < nc; b0 += 8 * kPqThreads) {
             unsigned long long kv[8];
@@ -448,7 +647,10 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
     const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
     const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
     const unsigned long long budget = p.mode == 1 ? p.budget : (unsigned long long)p.cluster_topk;
-    // weighted radix select of the token-budget prefix (retriever.cpp:142-154)
+    // weighted radix select of the token-budget prefix (retriever.cpp:142-154):
+    // the first key (ascending = descending score) at which the running weight
+    // exceeds the budget.  Keys ~0 (candidates ruled out by the filter) are skipped.
+    auto radix_select = [&]() {
     for (int shift = s_shift; shift >= 0; shift -= 8) {
         for (uint32_t b = tid; b < 256; b += blockDim.x) {
             hw[b] = 0;
@@ -468,7 +670,7 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const uint32_t i = b0 + t * kPqThreads + tid;
-                if (i < nc && (kv[t] & mask) == prefix) {
+                if (i < nc && kv[t] != ~0ull && (kv[t] & mask) == prefix) {
                     atomicAdd(&hw[(uint32_t)(kv[t] >> shift) & 255u], wv[t]);
                     atomicAdd(&hc[(uint32_t)(kv[t] >> shift) & 255u], 1u);
                 }
@@ -528,13 +730,212 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
         __syncthreads();
         if (s_state != 0) break;
     }
+    };
+    radix_select();  // on the filter's lower bounds (k_fine)
     LC_PMARK(2)
+    // ---- exact refinement.  Let K* be the boundary key of the lower-bound walk
+    // and x its score: the lower-bound prefix through K* weighs more than the
+    // budget, so the exact walk overflows at or before score x, and every
+    // cluster it admits (and the overflow one) has exact score >= x, hence upper
+    // bound >= x.  Exact fp64 upper bounds (sequential chain, bit-exact
+    // kernels::dot) for exactly those R = {hi >= x}; every other key becomes ~0.
+    __shared__ uint32_t s_fast;
+    {
+        __shared__ unsigned long long s_xkey, s_rmin, s_rmax;
+        __shared__ double s_qd[DQ];
+        __shared__ uint32_t s_rn;
+        __shared__ uint32_t s_r[kPickRCap];
+        __shared__ __align__(16) float4 s_col[kPickCols][DQ / 4];
+        if (tid == 0) {
+            s_xkey = ~0ull;
+            s_rmin = ~0ull;
+            s_rmax = 0ull;
+            s_rn = 0;
+        }
+        for (uint32_t j = tid; j < D; j += blockDim.x) s_qd[j] = (double)p.q[((size_t)slot * G + g) * D + j];
+        __syncthreads();
+        const bool all = s_state == 2;
+        if (!all) {
+            const unsigned long long prefix = s_prefix, mask = s_mask;
+            unsigned long long mn = ~0ull;
+            for (uint32_t i = tid; i < nc; i += blockDim.x)
+                if ((kg[i] & mask) == prefix) mn = min(mn, kg[i]);
+            atomicMin(&s_xkey, mn);
+        }
+        __syncthreads();
+        const double x = all ? -INFINITY : key_score(s_xkey);
+        const double* hg = reinterpret_cast<const double*>(
+                               p.scratch + (size_t)slot * G * p.qcap * kScratchEntry + (size_t)G * p.qcap * 12) +
+                           (size_t)g * p.qcap;
+        // R as a list (ascending i) when it fits, else handled in place
+        for (uint32_t b0 = 0; b0 < nc; b0 += 8 * kPqThreads) {  // eight loads in flight per thread
+            double hv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t i = b0 + t * kPqThreads + tid;
+                hv[t] = i < nc ? hg[i] : -INFINITY;
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t i = b0 + t * kPqThreads + tid;
+                if (i < nc && (all || hv[t] >= x)) {
+                    const uint32_t at = atomicAdd(&s_rn, 1u);
+                    if (at < kPickRCap) s_r[at] = i;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t nr = s_rn;
+        if (p.prof && tid == 0) p.prof[((size_t)slot * GQ + blockIdx.x) * 8 + 7] = nr | ((unsigned long long)nc << 32);
+        const float* fcs = a.fcent + (size_t)slot * a.cap_clusters * D;
+        const double qn = pv.qnorm()[g];
+        auto exact_key = [&](uint32_t i) -> unsigned long long {
+            uint32_t k = 0;
+            while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
+            const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k], ci = s_gbase[k] + local;
+            const float4* col = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local;
+            double sacc = 0.0;
+            for (uint32_t j0 = 0; j0 < D / 4; j0 += 8) {  // 8 loads in flight, then their chain steps
+                float4 v4[8];
+#pragma unroll
+                for (uint32_t t = 0; t < 8; ++t) v4[t] = __ldg(col + (size_t)(j0 + t) * nu);
+#pragma unroll
+                for (uint32_t t = 0; t < 8; ++t) {
+                const uint32_t jq = j0 + t;
+                const float4 v = v4[t];
+                sacc = __fma_rn(s_qd[4 * jq + 0], (double)v.x, sacc);
+                sacc = __fma_rn(s_qd[4 * jq + 1], (double)v.y, sacc);
+                sacc = __fma_rn(s_qd[4 * jq + 2], (double)v.z, sacc);
+                sacc = __fma_rn(s_qd[4 * jq + 3], (double)v.w, sacc);
+                }
+            }
+            return desc_key(__dadd_rn(sacc, __dmul_rn(qn, a.frad[(size_t)slot * a.cap_clusters + ci])));
+        };
+        unsigned long long rmn = ~0ull, rmx = 0ull;
+        if (nr <= kPickRCap) {
+            // R fits: select straight from it.  Rank R by (exact score desc,
+            // reference id asc) -- select_topk's order (retriever.cpp:27-39) --
+            // and admit the rank prefix while the running weight stays within
+            // the budget, the first cluster unconditionally (retriever.cpp:142-154).
+            unsigned long long* s_rk = reinterpret_cast<unsigned long long*>(s_ph);
+            uint32_t* s_ro = reinterpret_cast<uint32_t*>(s_ph + kPickRCap * 8);
+            uint32_t* s_rw = s_ro + kPickRCap;
+            uint32_t* s_ri = s_rw + kPickRCap;
+            for (uint32_t r = tid; r < nr; r += blockDim.x) {
+                const uint32_t i = s_r[r];
+                s_ro[r] = fo[cand(i)];
+                s_rw[r] = sg[i];
+            }
+            // exact upper bounds, kPickCols columns at a time staged by cp.async
+            for (uint32_t b0 = 0; b0 < nr; b0 += kPickCols) {
+                const uint32_t cnt = min(kPickCols, nr - b0);
+                for (uint32_t x = tid; x < cnt * (D / 4); x += blockDim.x) {
+                    const uint32_t i = s_r[b0 + x / (D / 4)], jq = x % (D / 4);
+                    uint32_t k = 0;
+                    while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
+                    const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k];
+                    const float4* src = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local + (size_t)jq * nu;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(&s_col[x / (D / 4)][jq])),
+                                 "l"(src));
+                }
+                asm volatile("cp.async.commit_group;\n" ::);
+                asm volatile("cp.async.wait_group 0;\n" ::);
+                __syncthreads();
+                if (tid < cnt) {
+                    const uint32_t i = s_r[b0 + tid];
+                    uint32_t k = 0;
+                    while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
+                    const uint32_t ci = s_gbase[k] + (i - s_gpre[k]);
+                    double sacc = 0.0;
+#pragma unroll 8
+                    for (uint32_t jq = 0; jq < D / 4; ++jq) {
+                        const float4 v = s_col[tid][jq];
+                        sacc = __fma_rn(s_qd[4 * jq + 0], (double)v.x, sacc);
+                        sacc = __fma_rn(s_qd[4 * jq + 1], (double)v.y, sacc);
+                        sacc = __fma_rn(s_qd[4 * jq + 2], (double)v.z, sacc);
+                        sacc = __fma_rn(s_qd[4 * jq + 3], (double)v.w, sacc);
+                    }
+                    s_rk[b0 + tid] = desc_key(__dadd_rn(sacc, __dmul_rn(qn, a.frad[(size_t)slot * a.cap_clusters + ci])));
+                }
+                __syncthreads();
+            }
+            for (uint32_t r = tid; r < nr; r += blockDim.x) {
+                const unsigned long long kr = s_rk[r];
+                const uint32_t orr = s_ro[r];
+                uint32_t rank = 0;
+                for (uint32_t y = 0; y < nr; ++y) {
+                    const unsigned long long ky = s_rk[y];
+                    rank += (ky < kr || (ky == kr && s_ro[y] < orr)) ? 1u : 0u;
+                }
+                s_ri[rank] = r;
+                kg[s_r[r]] = kr;  // exact key for the rank phase below
+            }
+            __syncthreads();
+            if (warp == 0) {  // walk the ranks: running weight, first overflow ends the prefix
+                unsigned long long run = 0;
+                uint32_t nsel = nr;
+                for (uint32_t b = 0; b < nr; b += 32) {
+                    const uint32_t r = b + lane;
+                    unsigned long long x = r < nr ? (unsigned long long)s_rw[s_ri[r]] : 0ull;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= (uint32_t)o) x += y;
+                    }
+                    const bool over = r < nr && r > 0 && run + x > budget;
+                    const unsigned int bal = __ballot_sync(0xffffffffu, over);
+                    if (bal) {
+                        nsel = b + __ffs(bal) - 1;
+                        break;
+                    }
+                    run += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (lane == 0) s_nsel = nsel;
+            }
+            __syncthreads();
+            for (uint32_t x = tid; x < s_nsel; x += blockDim.x) sg[x] = s_r[s_ri[x]];
+            if (tid == 0) s_fast = 1;
+        } else {
+            if (tid == 0) s_fast = 0;
+            // large R (e.g. everything fits the budget): in place, one candidate per thread
+            __syncthreads();
+            for (uint32_t i = tid; i < nc; i += blockDim.x) {
+                const bool in = all || hg[i] >= x;
+                const unsigned long long k = in ? exact_key(i) : ~0ull;
+                kg[i] = k;
+                if (in) {
+                    rmn = min(rmn, k);
+                    rmx = max(rmx, k);
+                }
+            }
+        }
+        atomicMin(&s_rmin, rmn);
+        atomicMax(&s_rmax, rmx);
+        __syncthreads();
+        if (tid == 0 && !s_fast) {
+            const unsigned long long mn = s_rmin, mx = s_rmax;
+            const unsigned long long diff = mn ^ mx;
+            const int top = diff ? 63 - __clzll((long long)diff) : 0;
+            const int shift = (top / 8) * 8;
+            const unsigned long long mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
+            s_prefix = mn & mask;
+            s_mask = mask;
+            s_shift = shift;
+            s_wbefore = 0;
+            s_cbefore = 0;
+            s_state = 0;
+        }
+        __syncthreads();
+    }
+    if (!s_fast) {
+    radix_select();  // exact keys of R
     const unsigned long long prefix = s_prefix, mask = s_mask;
     const uint32_t state = s_state, cbefore = s_cbefore;
     for (uint32_t base = 0; base < nc; base += blockDim.x) {
         const uint32_t i = base + tid;
         bool take = false;
-        if (i < nc) {
+        if (i < nc && kg[i] != ~0ull) {
             const unsigned long long k = kg[i] & mask;
             take = k < prefix || (k == prefix && (state == 2 || (state == 1 && cbefore == 0)));
         }
@@ -554,7 +955,7 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
             int best = -1;
             uint32_t best_id = 0xffffffffu;
             for (uint32_t i = 0; i < nc; ++i) {
-                if ((kg[i] & mask) != prefix) continue;
+                if (kg[i] == ~0ull || (kg[i] & mask) != prefix) continue;
                 const uint32_t oid = fo[cand(i)];
                 if ((first || oid > last_id) && oid < best_id) {
                     best_id = oid;
@@ -570,6 +971,7 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
             last_id = best_id;
             first = false;
         }
+    }
     }
     __syncthreads();
     LC_PMARK(3)
@@ -683,7 +1085,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     const SlotState st = a.state[slot];
     const uint32_t n = st.n_tokens, M = st.n_chunks, ce = st.chunked_end, P = st.P, L = st.L;
     const uint32_t all = (1u << G) - 1u;
-    PlanView pv{a.plan + (size_t)slot * a.plan_bytes};
+    PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
     QInfo* qi = a.qinfo + (size_t)slot * G;
     Span* sp = a.spans + (size_t)slot * a.cap_spans;
     uint32_t* so = a.span_off + (size_t)slot * (a.cap_spans + 1);
@@ -920,16 +1322,25 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
         co_cfg = co_smem;
     }
     if (pk_smem > pk_cfg) {
-        cudaError_t e = cudaFuncSetAttribute(k_pickq<GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
+        cudaError_t e = cudaFuncSetAttribute(k_pickq<D, GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
         if (e != cudaSuccess) return e;
         pk_cfg = pk_smem;
     }
     k_coarse<D, GQ><<<n_slots, kCoThreads, co_smem, stream>>>(p);
-    const uint32_t tiles = (max_union + 31) / 32;
-    // a few CTAs per slot whose warps stride over the slot's tiles (setup amortized)
-    const uint32_t parts = std::max<uint32_t>(1, std::min<uint32_t>(4, (tiles + 3) / 4));
-    k_fine<D, GQ><<<dim3(parts, n_slots), kFiThreads, 0, stream>>>(p);
-    k_pickq<GQ><<<dim3(GQ, n_slots), kPqThreads, pk_smem, stream>>>(p);
+    static uint32_t fine_grid = 0;
+    if (!fine_grid) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fine<D, GQ>, kFiThreads, 0);
+        fine_grid = (uint32_t)std::max(1, sms) * (uint32_t)std::max(1, per);
+    }
+    for (uint32_t s0 = 0; s0 < n_slots; s0 += kMaxAttendSlots) {
+        Sel3Params q = p;
+        q.a.slot0 = p.a.slot0 + s0;
+        k_fine<D, GQ><<<fine_grid, kFiThreads, 0, stream>>>(q, std::min<uint32_t>(kMaxAttendSlots, n_slots - s0));
+    }
+    k_pickq<D, GQ><<<dim3(GQ, n_slots), kPqThreads, pk_smem, stream>>>(p);
     k_spans<GQ><<<n_slots, kSpThreads, 0, stream>>>(p);
     return cudaGetLastError();
 }
@@ -955,10 +1366,11 @@ size_t select3_pick_smem(const Arena& a) {
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
-                           uint32_t pmax, uint32_t n_slots, cudaStream_t stream) {
+                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream) {
     static unsigned long long* prof = nullptr;
     if (getenv("LC_PROF") && !prof) cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
-    Sel3Params p{a, pick_keys_cap(a), q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof};
+    Sel3Params p{a, pick_keys_cap(a), q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
+                 fine_ctr};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
                   : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)
                                : cudaErrorInvalidValue;
@@ -978,7 +1390,13 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
         }
         std::sort(tot.begin(), tot.end());
         const double nq = (double)tot.size();
-        fprintf(stderr, "[LC_PROF] k_pickq per-CTA us: stage %.2f radix %.2f mark %.2f rank+members %.2f out %.2f | "
+        double rs = 0, ncs = 0;
+        for (size_t r = (size_t)a.slot0 * a.G; r < (size_t)(a.slot0 + n_slots) * a.G; ++r) {
+            rs += (double)(t[r * 8 + 7] & 0xffffffffull);
+            ncs += (double)(t[r * 8 + 7] >> 32);
+        }
+        fprintf(stderr, "[LC_PROF] k_pickq refine set %.1f of %.1f candidates per head\n", rs / nq, ncs / nq);
+        fprintf(stderr, "[LC_PROF] k_pickq per-CTA us: stage %.2f radix(lo) %.2f refine+select %.2f rank+members %.2f out %.2f | "
                 "dur p50 %.2f p99 %.2f max %.2f | first start->last end %.1f us\n",
                 acc[0] / nq / 1e3, acc[1] / nq / 1e3, acc[2] / nq / 1e3, acc[3] / nq / 1e3, acc[4] / nq / 1e3,
                 tot[tot.size() / 2] / 1e3, tot[(size_t)(tot.size() * 0.99)] / 1e3, tot.back() / 1e3, (t1 - t0) / 1e3);
