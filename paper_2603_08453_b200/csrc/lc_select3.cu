@@ -78,6 +78,7 @@ struct Sel3Params {
     uint32_t qcap;
     unsigned long long* prof;  // optional k_pick phase timestamps [slot][8] (LC_PROF=1)
     uint32_t* fine_ctr;        // k_fine pool / exit counters (zeroed; reset by k_fine)
+    unsigned long long* prof_sp;  // optional k_spans phase timestamps [slot][8] (LC_PROF=1)
 };
 
 __device__ __forceinline__ unsigned long long gtime3() {
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
     constexpr uint32_t G = GQ, V = D / 4;  // float4s per centroid
     __shared__ uint32_t s_tp[kMaxAttendSlots + 1];  // prefix of the slots' tile counts
     __shared__ uint32_t s_ws[kFiWarps];
-    __shared__ __align__(16) float s_q[kFiWarps][GQ * D];  // q of the warp's current slot
+    __shared__ __align__(16) float s_q[kFiWarps][2][GQ * D];  // q of the warp's slots (double buffer)
     {
         const uint32_t per = (n + kFiThreads - 1) / kFiThreads, i0 = tid * per;
         uint32_t loc = 0;
@@ -344,19 +345,25 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             if (lane == 0) claim = TS + atomicAdd(ctr, 1u);
             return t;
         };
-        uint32_t lo = 0;  // slot (local index) of the last described tile
-        struct Desc {
-            uint32_t slot;     // ~0u: no tile
-            uint32_t ti;       // tile index inside the slot
-            uint32_t k, local; // lane's union unit and index inside the unit
-            uint32_t base, nu, valid;
+        uint32_t lo = 0;  // slot (local index) of the last looked-up tile
+        // A tile goes through three stages, one loop iteration apart, so no
+        // dependent load sits on the critical path: (A) slot lookup + tile-table
+        // entry load, (B) the lane's unit row loads, (C) the centroid burst and
+        // the fp32 scoring.  The slot's q rides a cp.async into one of two
+        // per-warp buffers one tile ahead of its first use.
+        struct StA {
+            uint32_t slot, ti;  // slot ~0u: no tile
+            uint4 te;           // {first unit, unit starts, first local, -}
+            uint32_t ncu;
         };
-        // descriptor of tile t: slot lookup in shared memory, one tile-table
-        // entry, the lane's unit row
-        auto describe = [&](uint32_t t) -> Desc {
-            Desc d;
-            d.slot = ~0u;
-            if (t == ~0u) return d;
+        struct StB {
+            uint32_t slot, valid, local, base, nu, mask, qb;
+            uint32_t qoff[GQ];
+        };
+        auto stage_a = [&](uint32_t t) -> StA {
+            StA x;
+            x.slot = ~0u;
+            if (t == ~0u) return x;
             if (t < s_tp[lo] || t >= s_tp[lo + 1]) {
                 uint32_t l = 0, h = n;
                 while (h - l > 1) {
@@ -367,27 +374,42 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 while (s_tp[l + 1] <= t) ++l;
                 lo = l;
             }
-            d.slot = a.slot0 + lo;
-            const PlanView pv(a.plan + (size_t)d.slot * a.plan_bytes, a);
-            d.ti = t - s_tp[lo];
-            const uint4 te = pv.tiles()[d.ti];  // {first unit, unit starts, first local, -}
-            const uint32_t ncu = __ldg(pv.hdr() + 2);
-            d.valid = d.ti * 32 + lane < ncu;
-            const uint32_t below = te.y & ((2u << lane) - 1u);  // unit starts at positions <= lane
-            const uint32_t nb = __popc(below);
-            d.k = te.x + nb;
-            d.local = d.valid ? (nb ? lane - (31 - __clz(below)) : te.z + lane) : 0u;
-            const uint32_t* u = pv.units() + (size_t)d.k * (4 + G);
-            d.base = __ldg(u + 2);
-            d.nu = __ldg(u + 3);
-            return d;
+            x.slot = a.slot0 + lo;
+            x.ti = t - s_tp[lo];
+            const PlanView pv(a.plan + (size_t)x.slot * a.plan_bytes, a);
+            x.te = __ldg(pv.tiles() + x.ti);
+            x.ncu = __ldg(pv.hdr() + 2);
+            return x;
         };
-        uint32_t qslot = ~0u;
-        auto load_q = [&](uint32_t slot) {  // the slot's q (fp32) into this warp's buffer
-            for (uint32_t x = lane; x < G * D / 4; x += 32)
-                reinterpret_cast<float4*>(s_q[warp])[x] = __ldg(reinterpret_cast<const float4*>(p.q + (size_t)slot * G * D) + x);
-            __syncwarp();
-            qslot = slot;
+        uint32_t qslot_next = ~0u, qb_next = 1;  // slot whose q was staged last, its buffer
+        auto stage_b = [&](const StA& x) -> StB {
+            StB y;
+            y.slot = x.slot;
+            y.valid = 0;
+            y.mask = 0;
+            if (x.slot == ~0u) return y;
+            const PlanView pv(a.plan + (size_t)x.slot * a.plan_bytes, a);
+            y.valid = x.ti * 32 + lane < x.ncu;
+            const uint32_t below = x.te.y & ((2u << lane) - 1u);  // unit starts at positions <= lane
+            const uint32_t nb = __popc(below);
+            const uint32_t k = x.te.x + nb;
+            y.local = y.valid ? (nb ? lane - (31 - __clz(below)) : x.te.z + lane) : 0u;
+            const uint32_t* u = pv.units() + (size_t)k * (4 + G);
+            y.base = __ldg(u + 2);
+            y.nu = __ldg(u + 3);
+            y.mask = y.valid ? __ldg(u + 1) : 0u;
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) y.qoff[g] = __ldg(u + 4 + g);
+            if (x.slot != qslot_next) {  // stage the slot's q into the other buffer
+                qslot_next = x.slot;
+                qb_next ^= 1u;
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_q[warp][qb_next][0]);
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(p.q + (size_t)x.slot * G * D);
+                for (uint32_t c = lane; c < G * D / 4; c += 32)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst + c * 16), "l"(src + c * 16));
+            }
+            y.qb = qb_next;
+            return y;
         };
         uint32_t mslot = ~0u;  // slot whose per-head key range the warp is tracking
         unsigned long long wmin[GQ], wmax[GQ];
@@ -409,9 +431,12 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             }
         };
 
-        Desc d = describe(next_tile());
+        StA sa = stage_a(next_tile());
+        StB d = stage_b(sa);
+        asm volatile("cp.async.commit_group;\n" ::);
+        sa = stage_a(next_tile());
         while (d.slot != ~0u) {
-            // the tile's centroids, radius and weight: one burst of loads
+            // (C) this tile's centroids, radius and weight: one burst of loads
             const float4* col = reinterpret_cast<const float4*>(a.fcent + (size_t)d.slot * a.cap_clusters * D +
                                                                (size_t)d.base * D) + d.local;
             float4 v[V];
@@ -422,9 +447,13 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             const uint32_t cid = d.base + d.local;
             const double r = d.valid ? __ldg(a.frad + (size_t)d.slot * a.cap_clusters + cid) : 0.0;
             const uint32_t wt = d.valid ? (p.mode == 1 ? __ldg(a.ftok + (size_t)d.slot * a.cap_clusters + cid) : 1u) : 0u;
-            // next tile's descriptor while this tile's data is in flight
-            const Desc dn = describe(next_tile());
-            if (d.slot != qslot) load_q(d.slot);
+            // (B) next tile, (A) the one after
+            const StB dn = stage_b(sa);
+            asm volatile("cp.async.commit_group;\n" ::);
+            sa = stage_a(next_tile());
+            asm volatile("cp.async.wait_group 1;\n" ::);  // this tile's q (staged last iteration)
+            __syncwarp();
+            const float* qs = s_q[warp][d.qb];
             float s4[GQ][4], a4[GQ][4];
 #pragma unroll
             for (int g = 0; g < GQ; ++g)
@@ -434,7 +463,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             for (uint32_t j = 0; j < V; ++j) {
 #pragma unroll
                 for (int g = 0; g < GQ; ++g) {
-                    const float4 q4 = reinterpret_cast<const float4*>(s_q[warp] + g * D)[j];
+                    const float4 q4 = reinterpret_cast<const float4*>(qs + g * D)[j];
                     s4[g][0] = fmaf(q4.x, v[j].x, s4[g][0]);
                     s4[g][1] = fmaf(q4.y, v[j].y, s4[g][1]);
                     s4[g][2] = fmaf(q4.z, v[j].z, s4[g][2]);
@@ -455,21 +484,19 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 }
             }
             const PlanView pv(a.plan + (size_t)d.slot * a.plan_bytes, a);
-            const uint32_t* u = pv.units() + (size_t)d.k * (4 + G);
-            const uint32_t mask = d.valid ? __ldg(u + 1) : 0u;
             unsigned char* sc = p.scratch + (size_t)d.slot * G * p.qcap * kScratchEntry;
             unsigned long long* keys = reinterpret_cast<unsigned long long*>(sc);
             uint32_t* wts = reinterpret_cast<uint32_t*>(keys + (size_t)G * p.qcap);
             double* his = reinterpret_cast<double*>(wts + (size_t)G * p.qcap);
 #pragma unroll
             for (int g = 0; g < GQ; ++g) {
-                if ((mask >> g) & 1u) {
+                if ((d.mask >> g) & 1u) {
                     const float sv = (s4[g][0] + s4[g][1]) + (s4[g][2] + s4[g][3]);
                     const float av = (a4[g][0] + a4[g][1]) + (a4[g][2] + a4[g][3]);
                     const double ub = __dadd_rn((double)sv, __dmul_rn(__ldg(pv.qnorm() + g), r));
                     const double e = (double)av * (1.01 * 132.0 / 16777216.0) + fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
                     const unsigned long long key = desc_key(ub - e);
-                    const size_t at = (size_t)g * p.qcap + __ldg(u + 4 + g) + d.local;
+                    const size_t at = (size_t)g * p.qcap + d.qoff[g] + d.local;
                     keys[at] = key;
                     wts[at] = wt;
                     his[at] = ub + e;
@@ -477,8 +504,10 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                     wmax[g] = max(wmax[g], key);
                 }
             }
+            __syncwarp();  // the q buffer may be restaged two tiles later
             d = dn;
         }
+        asm volatile("cp.async.wait_group 0;\n" ::);
         flush_minmax();
     }
     // the last CTA out resets the pool for the next launch
@@ -530,7 +559,7 @@ constexpr int kPqThreads = 128;
 constexpr int kPqWarps = kPqThreads / 32;
 
 template <int DQ, int GQ>
-__global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
+__device__ __forceinline__ void pick_head(const Sel3Params& p) {
     constexpr uint32_t D = DQ;
     extern __shared__ __align__(16) unsigned char qsm[];
     const Arena& a = p.a;
@@ -540,7 +569,7 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
     const uint32_t M = st.n_chunks, P = st.P, L = st.L;
     PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
     QInfo* qi = a.qinfo + (size_t)slot * G + g;
-    if (pv.hdr()[0]) return;  // degenerate slot: k_spans writes everything
+    if (pv.hdr()[0]) return;  // degenerate slot: build_spans writes everything
     LC_PMARK(0)
     const uint32_t mwcap = bit_words(a.cap_chunks), mw = bit_words(M);
     unsigned long long* sk = reinterpret_cast<unsigned long long*>(qsm);
@@ -1045,13 +1074,14 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
     LC_PMARK(5)
 }
 
-// k_spans: one CTA per slot: union active spans in chunk order with per-head
+// build_spans: for one slot, by the last of its heads' k_pickq CTAs: union
+// active spans in chunk order with per-head
 // masks (collect_active, retriever.cpp:60-74), sink and buffer spans, counts.
-constexpr int kSpThreads = 256;
-constexpr int kSpWarps = kSpThreads / 32;
+constexpr int kSpMaxWarps = 8;
 
 template <typename T>
 __device__ __forceinline__ T sp_scan(T v, T* wt, T& total) {
+    const int kSpWarps = (int)(blockDim.x >> 5);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     T x = v;
 #pragma unroll
@@ -1078,9 +1108,12 @@ __device__ __forceinline__ T sp_scan(T v, T* wt, T& total) {
 }
 
 template <int GQ>
-__global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
+#define LC_SMARK(ph) \
+    if (p.prof_sp && threadIdx.x == 0) p.prof_sp[(size_t)slot * 8 + (ph)] = gtime3();
+__device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) {
+    LC_SMARK(0)
     const Arena& a = p.a;
-    const uint32_t slot = a.slot0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, kSpWarps = blockDim.x >> 5;
     constexpr uint32_t G = GQ;
     const SlotState st = a.state[slot];
     const uint32_t n = st.n_tokens, M = st.n_chunks, ce = st.chunked_end, P = st.P, L = st.L;
@@ -1116,7 +1149,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         for (uint32_t t = tid; t < n; t += blockDim.x) rows[t] = t | (all << 24);
         return;
     }
-    __shared__ unsigned long long wtot[kSpWarps];
+    __shared__ unsigned long long wtot[kSpMaxWarps];
     __shared__ uint32_t s_cnt[GQ], s_nsp[GQ], s_err;
     if (tid < G) {
         s_cnt[tid] = 0;
@@ -1124,7 +1157,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     }
     if (tid == 0) {
         uint32_t e = 0;
-        for (uint32_t g = 0; g < G; ++g) e |= qi[g].error;
+        for (uint32_t g = 0; g < G; ++g) e |= __ldcg(&qi[g].error);  // written by the other heads' CTAs
         s_err = e;
     }
     __syncthreads();
@@ -1154,30 +1187,40 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     uint32_t my_cnt[GQ], my_nsp[GQ];
 #pragma unroll
     for (int g = 0; g < GQ; ++g) my_cnt[g] = my_nsp[g] = 0;
+    LC_SMARK(1)
     for (uint32_t w0 = 0; w0 < mw; w0 += blockDim.x) {
         const uint32_t w = w0 + tid;
         uint32_t wg[GQ], any = 0;
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
-            wg[g] = w < mw ? cbg[g * mwcap + w] : 0u;
+            wg[g] = w < mw ? __ldcg(cbg + g * mwcap + w) : 0u;
             any |= wg[g];
         }
-        // at most 32 chunks per word; their bounds are loaded together
+        // the bounds of the word's set chunks: one batch of independent loads
+        uint32_t bnd[33];
+#pragma unroll
+        for (int b = 0; b <= 32; ++b) {
+            const bool need = (b < 32 && ((any >> b) & 1u)) || (b > 0 && ((any >> (b - 1)) & 1u));
+            bnd[b] = need ? __ldg(cs + w * 32 + b) : 0u;
+        }
         uint32_t cnt = 0, toks = 0;
-        for (uint32_t rem = any; rem; rem &= rem - 1) {
-            const uint32_t j = w * 32 + __ffs(rem) - 1;
-            const uint32_t s0 = max(__ldg(cs + j), sink_end), e0 = __ldg(cs + j + 1);
-            if (s0 < e0) {
-                ++cnt;
-                toks += e0 - s0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            if ((any >> b) & 1u) {
+                const uint32_t s0 = max(bnd[b], sink_end), e0 = bnd[b + 1];
+                if (s0 < e0) {
+                    ++cnt;
+                    toks += e0 - s0;
+                }
             }
         }
         unsigned long long total;
         const unsigned long long ex = sp_scan<unsigned long long>(((unsigned long long)cnt << 40) | toks, wtot, total);
         uint32_t pos = out + (uint32_t)(ex >> 40), tp = tok + (uint32_t)(ex & 0xffffffffffull);
-        for (uint32_t rem = any; rem; rem &= rem - 1) {
-            const uint32_t b = __ffs(rem) - 1, j = w * 32 + b;
-            const uint32_t s0 = max(__ldg(cs + j), sink_end), e0 = __ldg(cs + j + 1);
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            if (!((any >> b) & 1u)) continue;
+            const uint32_t s0 = max(bnd[b], sink_end), e0 = bnd[b + 1];
             if (s0 >= e0) continue;
             uint32_t m = 0;
 #pragma unroll
@@ -1209,6 +1252,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     }
     const uint32_t n_chunk_spans = out - (sink_end > 0 ? 1u : 0u);
     __syncthreads();
+    LC_SMARK(2)
     {  // row list of the chunk spans: one warp per 32 spans, coalesced row writes
         const uint32_t first = sink_end > 0 ? 1u : 0u, warp = tid >> 5;
         for (uint32_t k0 = first + warp * 32; k0 < out; k0 += kSpWarps * 32) {
@@ -1220,13 +1264,25 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
                 off = so[k];
             }
             const uint32_t nk = min(32u, out - k0);
-            for (uint32_t j = 0; j < nk; ++j) {
+            // the batch's tokens [t0, t1), one per lane: each store is a full line
+            const uint32_t t0 = __shfl_sync(0xffffffffu, off, 0);
+            const uint32_t t1 = __shfl_sync(0xffffffffu, off + (lm >> 8), nk - 1);
+            for (uint32_t qb = t0; qb < t1; qb += 32) {  // warp-uniform trip count
+                const uint32_t q = qb + lane;
+                uint32_t j = 0;  // last span of the batch with off <= q
+#pragma unroll
+                for (uint32_t step = 16; step >= 1; step >>= 1) {
+                    const uint32_t c = j + step;
+                    const uint32_t oc = __shfl_sync(0xffffffffu, off, c < nk ? c : nk - 1);
+                    if (c < nk && oc <= q) j = c;
+                }
                 const uint32_t sj = __shfl_sync(0xffffffffu, st, j), lj = __shfl_sync(0xffffffffu, lm, j);
-                const uint32_t oj = __shfl_sync(0xffffffffu, off, j), len = lj >> 8, m = (lj & 0xffu) << 24;
-                for (uint32_t t = lane; t < len; t += 32) rows[oj + t] = (sj + t) | m;
+                const uint32_t oj = __shfl_sync(0xffffffffu, off, j);
+                if (q < t1) rows[q] = (sj + (q - oj)) | ((lj & 0xffu) << 24);
             }
         }
     }
+    LC_SMARK(3)
     if (p.flags == 1u) {  // buffer_ids = [chunked_end, n), disjoint from the chunks
         const uint32_t b0 = max(ce, sink_end);
         if (n > b0) {
@@ -1257,7 +1313,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
                         }
                         uint32_t m = 0;
 #pragma unroll
-                        for (int g = 0; g < GQ; ++g) m |= ((cbg[g * mwcap + (l >> 5)] >> (l & 31)) & 1u) << g;
+                        for (int g = 0; g < GQ; ++g) m |= ((__ldcg(cbg + g * mwcap + (l >> 5)) >> (l & 31)) & 1u) << g;
                         resid = all & ~m;
                     }
                 }
@@ -1295,7 +1351,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         for (uint32_t g = 0; g < G; ++g) {
             const unsigned long long act = (unsigned long long)s_cnt[g] + sink_end + bufl;
             qi[g].n_active = act;
-            per_q += Pl * (4 * dd + 8) + (qi[g].scanned - Pl) * (4 * dd + 16) +
+            per_q += Pl * (4 * dd + 8) + (__ldcg(&qi[g].scanned) - Pl) * (4 * dd + 16) +
                      (unsigned long long)s_nsp[g] * 8 + act * 2 * dd * 2 + 8 * dd;
         }
         const unsigned long long ncu = pv.hdr()[2];
@@ -1305,6 +1361,19 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
         sb[2] = tok;
         sb[3] = ncu;
     }
+    LC_SMARK(4)
+}
+
+// k_pickq: one CTA per (query head, slot); k_spans: one CTA per slot.
+template <int DQ, int GQ>
+__global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
+    pick_head<DQ, GQ>(p);
+}
+
+constexpr int kSpThreads = 256;
+template <int GQ>
+__global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
+    build_spans<GQ>(p, p.a.slot0 + blockIdx.x);
 }
 
 size_t select3_pick_smem(const Arena& a);
@@ -1367,10 +1436,14 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
                            uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream) {
-    static unsigned long long* prof = nullptr;
-    if (getenv("LC_PROF") && !prof) cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
+    static unsigned long long *prof = nullptr, *prof_sp = nullptr;
+    if (getenv("LC_PROF") && !prof) {
+        cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
+        cudaMalloc(&prof_sp, (size_t)a.n_slots * 8 * 8);
+        cudaMemset(prof_sp, 0, (size_t)a.n_slots * 8 * 8);
+    }
     Sel3Params p{a, pick_keys_cap(a), q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
-                 fine_ctr};
+                 fine_ctr, prof_sp};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
                   : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)
                                : cudaErrorInvalidValue;
@@ -1396,6 +1469,24 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
             ncs += (double)(t[r * 8 + 7] >> 32);
         }
         fprintf(stderr, "[LC_PROF] k_pickq refine set %.1f of %.1f candidates per head\n", rs / nq, ncs / nq);
+        {
+            std::vector<unsigned long long> u((size_t)a.n_slots * 8);
+            cudaMemcpy(u.data(), prof_sp, u.size() * 8, cudaMemcpyDeviceToHost);
+            double ph[4] = {0, 0, 0, 0}, cnt = 0, mx = 0;
+            unsigned long long s0 = ~0ull, s1 = 0;
+            for (size_t r = a.slot0; r < (size_t)a.slot0 + n_slots; ++r) {
+                const unsigned long long* x = &u[r * 8];
+                if (!x[4] || !x[0]) continue;
+                for (int k = 0; k < 4; ++k) ph[k] += (double)(x[k + 1] - x[k]);
+                mx = std::max(mx, (double)(x[4] - x[0]));
+                s0 = std::min(s0, x[0]);
+                s1 = std::max(s1, x[4]);
+                cnt += 1;
+            }
+            if (cnt > 0)
+                fprintf(stderr, "[LC_PROF] k_spans per-CTA us: setup %.2f words %.2f rows %.2f buffer+stats %.2f | max %.2f | span %.1f us\n",
+                        ph[0] / cnt / 1e3, ph[1] / cnt / 1e3, ph[2] / cnt / 1e3, ph[3] / cnt / 1e3, mx / 1e3, (s1 - s0) / 1e3);
+        }
         fprintf(stderr, "[LC_PROF] k_pickq per-CTA us: stage %.2f radix(lo) %.2f refine+select %.2f rank+members %.2f out %.2f | "
                 "dur p50 %.2f p99 %.2f max %.2f | first start->last end %.1f us\n",
                 acc[0] / nq / 1e3, acc[1] / nq / 1e3, acc[2] / nq / 1e3, acc[3] / nq / 1e3, acc[4] / nq / 1e3,
