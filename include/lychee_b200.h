@@ -63,6 +63,10 @@ typedef struct {
     uint32_t slot_groups;     /* lc_retrieve runs this many slot groups on forked streams so
                                  one group's selection overlaps another's attention (0 = 1) */
     int32_t device;
+    uint32_t kv_f32;          /* 0: K/V in bf16 (the bench / serving layout; dim 64 or 128);
+                                 1: fp32 K/V exactly as the reference's TokenStore, attention
+                                 in fp64 (reference-exact mode; dim 8/16/32 also allowed for
+                                 group 1 or 4) */
 } lc_index_desc;
 
 /* tierkv::Budgets (retriever.hpp:13-21) */
@@ -116,15 +120,14 @@ void lc_index_destroy(lc_index_t h);
 int lc_index_get_desc(lc_index_t h, lc_index_desc* out);
 
 /* Upload one slot: a HierarchicalIndex produced by build_index (index.hpp:93-95)
- * plus its TokenStore keys/values as bf16 bit patterns (host memory), n_tokens
- * rows.  The stream cursor starts at chunked_end = last chunk end
+ * plus its TokenStore keys/values (host memory, bf16 bit patterns or fp32 as
+ * desc.kv_f32 says), n_tokens rows.  The stream cursor starts at chunked_end = last chunk end
  * (streamer.cpp:13-21), so tokens past it form the buffer.  Replaces
  * StreamState::StreamState(TokenStore, HierarchicalIndex, StreamerConfig).
  * keys_bf16 == values_bf16 == NULL keeps the K/V already resident in the slot
  * (e.g. written by lc_gen_workload). */
 int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
-                         const uint16_t* keys_bf16, const uint16_t* values_bf16,
-                         uint32_t n_tokens);
+                         const void* keys, const void* values, uint32_t n_tokens);
 
 /* Sizes of a slot's current index: dims[0..7] = dim, n_chunks, n_clusters,
  * n_units, n_tokens, total fine members, total coarse members, chunked_end. */
@@ -135,18 +138,17 @@ int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims);
  * Caller allocates every array from lc_index_slot_dims.  Synchronous. */
 int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* out);
 
-/* Raw K/V rows of one slot (bf16 bit patterns, host memory): write rows
+/* Raw K/V rows of one slot (host memory, element type per desc.kv_f32): write rows
  * [0, n_tokens) and set the slot's store size (the index is left as is), or
  * read them back.  TokenStore::keys_flat/values_flat (types.hpp:48-49). */
-int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const uint16_t* keys_bf16,
-                      const uint16_t* values_bf16, uint32_t n_tokens);
-int lc_kv_download_slot(lc_index_t h, uint32_t slot, uint16_t* keys_bf16, uint16_t* values_bf16,
-                        uint32_t n_tokens);
+int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const void* keys, const void* values,
+                      uint32_t n_tokens);
+int lc_kv_download_slot(lc_index_t h, uint32_t slot, void* keys, void* values, uint32_t n_tokens);
 
-/* Append one decoded token's K/V (bf16, device [n_slots][dim] each) to every
- * slot -- TokenStore::append inside push_token (streamer.cpp:56-58). */
-int lc_kv_append(lc_index_t h, const uint16_t* keys_dev, const uint16_t* values_dev,
-                 void* stream);
+/* Append one decoded token's K/V (device [n_slots][dim] each, element type per
+ * desc.kv_f32) to every slot -- TokenStore::append inside push_token
+ * (streamer.cpp:56-58). */
+int lc_kv_append(lc_index_t h, const void* keys_dev, const void* values_dev, void* stream);
 
 /* Batched retrieve() over every query head of every slot (retriever.cpp:161-167):
  * coarse UB scoring + top-k_g, fine UB scoring, selection (fixed k_c or greedy
@@ -177,10 +179,29 @@ int lc_graft(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uin
  * retrieve + attend with buffer_ids = [chunked_end, n), then append the step's
  * token, then graft where take[slot] > 0.  Stability metrics (jaccard /
  * window_hit) are host bookkeeping and stay in the caller. */
-int lc_decode_step(lc_index_t h, const float* q_dev, const uint16_t* keys_dev,
-                   const uint16_t* values_dev, const lc_budgets* b, const uint32_t* take,
+int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev,
+                   const void* values_dev, const lc_budgets* b, const uint32_t* take,
                    const uint32_t* kind, const uint32_t* level, float* out_dev,
                    lc_graft_report* reports_dev, void* stream);
+
+/* graft_chunk(Chunk) (streamer.cpp:68-143) with the chunk's representative
+ * supplied by the caller instead of pooled from the keys: reps_host
+ * [n_slots][dim] fp32 (rows of slots without a graft are ignored). */
+int lc_graft_rep(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
+                 const float* reps_host, lc_graft_report* reports_dev, void* stream);
+
+/* chunk_representative (index.cpp:20-41) of rows [start, start + take) of a
+ * slot's store, pooled with desc.pooling, into rep_host [dim].  A zero norm is
+ * LC_ERUNTIME, as the reference throws std::runtime_error.  Synchronous. */
+int lc_chunk_rep(lc_index_t h, uint32_t slot, uint32_t start, uint32_t take, float* rep_host);
+
+/* sparse_attention(q, store, ids) (retriever.cpp:41-50) for one slot over an
+ * explicit id list (host, each < the slot's token count): q_dev [group][dim]
+ * for the slot's query heads, out_dev [group][dim].  Empty lists are
+ * LC_EINVAL, as the reference throws.  Overwrites the slot's active row list,
+ * so lc_sparse_attention needs a fresh lc_retrieve afterwards.  Synchronous. */
+int lc_sparse_attention_ids(lc_index_t h, uint32_t slot, const float* q_dev, const uint32_t* ids_host,
+                            uint32_t n_ids, float* out_dev, void* stream);
 
 /* End-to-end variant of lc_retrieve over HOST buffers (pinned or pageable):
  * H2D of q, retrieve + attention, D2H of out; synchronous on `stream`. */

@@ -24,7 +24,7 @@ class IndexDesc(C.Structure):
                 ("cap_chunks", u32), ("cap_clusters", u32), ("cap_units", u32),
                 ("max_candidates", u32), ("splits", u32), ("structure_aware", u32),
                 ("graft_full", u32), ("keep_reps", u32), ("pooling", u32), ("slot_groups", u32),
-                ("device", C.c_int32)]
+                ("device", C.c_int32), ("kv_f32", u32)]
 
 
 class Budgets_(C.Structure):
@@ -58,7 +58,7 @@ EXPORTS = [
     "lc_kv_upload_slot", "lc_kv_download_slot",
     "lc_retrieve", "lc_sparse_attention", "lc_graft", "lc_decode_step", "lc_retrieve_host",
     "lc_selection_download", "lc_step_bytes", "lc_device_error", "lc_segment", "lc_segment_packed", "lc_flush_take",
-    "lc_index_build", "lc_gen_workload",
+    "lc_index_build", "lc_gen_workload", "lc_graft_rep", "lc_sparse_attention_ids", "lc_chunk_rep",
 ]
 
 _lib = None
@@ -108,6 +108,9 @@ def lib():
                                     C.POINTER(u32)]
         L.lc_index_build.argtypes = [vp, vp, vp, vp, C.c_double, u32, u32, vp]
         L.lc_gen_workload.argtypes = [vp, u32, u32, C.c_double, u32, C.c_double, vp, vp, vp]
+        L.lc_graft_rep.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.lc_sparse_attention_ids.argtypes = [vp, u32, vp, vp, u32, vp, vp]
+        L.lc_chunk_rep.argtypes = [vp, u32, u32, u32, vp]
         _lib = L
     return _lib
 

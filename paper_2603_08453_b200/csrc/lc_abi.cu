@@ -44,9 +44,13 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         const lc_index_desc& d = *desc;
         if (d.n_slots == 0 || d.dim == 0 || d.group == 0 || d.group > (uint32_t)kMaxGroup)
             fail(LC_EINVAL, "lc_index_create: need n_slots >= 1, dim >= 1, 1 <= group <= 8");
-        if (d.dim != 64 && d.dim != 128) fail(LC_EINVAL, "lc_index_create: dim must be 64 or 128");
-        if (d.dim % 4) fail(LC_EINVAL, "lc_index_create: dim must be a multiple of 4");
-        if (d.dim > 256) fail(LC_EINVAL, "lc_index_create: dim > 256");
+        if (d.kv_f32 > 1) fail(LC_EINVAL, "lc_index_create: kv_f32 must be 0 or 1");
+        // head dims with compiled kernels: 64/128 for every group size; the
+        // reference-exact fp32 mode adds 8/16/32 for single-head and GQA-4 slots
+        const bool big = d.dim == 64 || d.dim == 128;
+        const bool small = (d.dim == 8 || d.dim == 16 || d.dim == 32) && d.kv_f32 && (d.group == 1 || d.group == 4);
+        if (!big && !small)
+            fail(LC_EINVAL, "lc_index_create: dim must be 64 or 128 (or 8/16/32 with kv_f32 and group 1 or 4)");
         if (d.cap_units == 0 || d.cap_units > 1024) fail(LC_EINVAL, "lc_index_create: 1 <= cap_units <= 1024");
         if (d.cap_tokens == 0 || d.cap_chunks == 0 || d.cap_clusters == 0)
             fail(LC_EINVAL, "lc_index_create: zero capacity");
@@ -60,6 +64,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
                             "(need dim*cap_units*4 <= 96 KiB and group*cap_units <= 1024)");
         auto h = std::make_unique<lc_index_s>();
         h->desc = d;
+        h->kv_elem = d.kv_f32 ? 4u : 2u;
         h->set_device();
         Arena& a = h->a;
         a.n_slots = d.n_slots;
@@ -72,11 +77,17 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.max_cand = 1;
         a.graft_full = d.graft_full;
         a.keep_reps = d.keep_reps;
+        a.kv_f32 = d.kv_f32;
         a.cap_spans = d.cap_chunks + 2 + 1024;
         const size_t S = d.n_slots, D = d.dim, G = d.group;
         auto& o = h->owned;
-        a.K = dalloc<__nv_bfloat16>(S * d.cap_tokens * D, o);
-        a.V = dalloc<__nv_bfloat16>(S * d.cap_tokens * D, o);
+        if (d.kv_f32) {
+            a.Kf = dalloc<float>(S * d.cap_tokens * D, o);
+            a.Vf = dalloc<float>(S * d.cap_tokens * D, o);
+        } else {
+            a.K = dalloc<__nv_bfloat16>(S * d.cap_tokens * D, o);
+            a.V = dalloc<__nv_bfloat16>(S * d.cap_tokens * D, o);
+        }
         a.chunk_start = dalloc<uint32_t>(S * (d.cap_chunks + 1), o);
         a.chunk_clu = dalloc<uint32_t>(S * d.cap_chunks, o);
         a.chunk_rep = d.keep_reps ? dalloc<float>(S * d.cap_chunks * D, o) : nullptr;
@@ -118,6 +129,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         h->out_stage = dalloc<float>(S * G * D, o);
         h->take_dev = dalloc<uint32_t>(S, o);
         h->rep_scratch = dalloc<lc_graft_report>(S, o);
+        h->reps_dev = dalloc<float>(S * D, o);
         ck(cudaMemset(a.state, 0, S * sizeof(SlotState)), "memset state");
         ck(cudaMemset(a.err, 0, 4), "memset err");
         ck(cudaMemset(a.counters, 0, S * 4), "memset counters");
@@ -145,7 +157,7 @@ int lc_index_get_desc(lc_index_t h, lc_index_desc* out) {
 }
 
 int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
-                         const uint16_t* keys, const uint16_t* values, uint32_t n_tokens) {
+                         const void* keys, const void* values, uint32_t n_tokens) {
     return guard([&] {
         if (!h || !ix) fail(LC_EINVAL, "lc_index_upload_slot: null argument");
         h->set_device();
@@ -227,8 +239,8 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         auto up = [&](void* dst, const void* src, size_t bytes) {
             if (bytes) ck(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
         };
-        if (keys) up(a.K + kv_off(a, slot), keys, (size_t)n_tokens * D * 2);
-        if (values) up(a.V + kv_off(a, slot), values, (size_t)n_tokens * D * 2);
+        if (keys) up(h->kv_ptr(0, slot), keys, (size_t)n_tokens * D * h->kv_elem);
+        if (values) up(h->kv_ptr(1, slot), values, (size_t)n_tokens * D * h->kv_elem);
         up(a.chunk_start + so * (a.cap_chunks + 1), cs.data(), cs.size() * 4);
         up(a.chunk_clu + so * a.cap_chunks, cc.data(), cc.size() * 4);
         up(a.ucent + so * a.cap_units * D, ucent.data(), ucent.size() * 4);
@@ -362,15 +374,15 @@ int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
     });
 }
 
-int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const uint16_t* keys, const uint16_t* values,
+int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const void* keys, const void* values,
                       uint32_t n_tokens) {
     return guard([&] {
         if (!h || !keys || !values || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_kv_upload_slot: bad argument");
         if (n_tokens > h->a.cap_tokens) fail(LC_EINVAL, "lc_kv_upload_slot: n_tokens exceeds capacity");
         h->set_device();
         const Arena& a = h->a;
-        ck(cudaMemcpy(a.K + kv_off(a, slot), keys, (size_t)n_tokens * a.d * 2, cudaMemcpyHostToDevice), "K");
-        ck(cudaMemcpy(a.V + kv_off(a, slot), values, (size_t)n_tokens * a.d * 2, cudaMemcpyHostToDevice), "V");
+        ck(cudaMemcpy(h->kv_ptr(0, slot), keys, (size_t)n_tokens * a.d * h->kv_elem, cudaMemcpyHostToDevice), "K");
+        ck(cudaMemcpy(h->kv_ptr(1, slot), values, (size_t)n_tokens * a.d * h->kv_elem, cudaMemcpyHostToDevice), "V");
         SlotState st;
         ck(cudaMemcpy(&st, a.state + slot, sizeof st, cudaMemcpyDeviceToHost), "state");
         st.n_tokens = n_tokens;
@@ -379,19 +391,19 @@ int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const uint16_t* keys, const u
     });
 }
 
-int lc_kv_download_slot(lc_index_t h, uint32_t slot, uint16_t* keys, uint16_t* values, uint32_t n_tokens) {
+int lc_kv_download_slot(lc_index_t h, uint32_t slot, void* keys, void* values, uint32_t n_tokens) {
     return guard([&] {
         if (!h || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_kv_download_slot: bad argument");
         if (n_tokens > h->hs[slot].n_tokens) fail(LC_EINVAL, "lc_kv_download_slot: beyond the store");
         h->set_device();
         ck(cudaDeviceSynchronize(), "sync");
         const Arena& a = h->a;
-        if (keys) ck(cudaMemcpy(keys, a.K + kv_off(a, slot), (size_t)n_tokens * a.d * 2, cudaMemcpyDeviceToHost), "K");
-        if (values) ck(cudaMemcpy(values, a.V + kv_off(a, slot), (size_t)n_tokens * a.d * 2, cudaMemcpyDeviceToHost), "V");
+        if (keys) ck(cudaMemcpy(keys, h->kv_ptr(0, slot), (size_t)n_tokens * a.d * h->kv_elem, cudaMemcpyDeviceToHost), "K");
+        if (values) ck(cudaMemcpy(values, h->kv_ptr(1, slot), (size_t)n_tokens * a.d * h->kv_elem, cudaMemcpyDeviceToHost), "V");
     });
 }
 
-int lc_kv_append(lc_index_t h, const uint16_t* keys_dev, const uint16_t* values_dev, void* stream) {
+int lc_kv_append(lc_index_t h, const void* keys_dev, const void* values_dev, void* stream) {
     return guard([&] {
         if (!h || !keys_dev || !values_dev) fail(LC_EINVAL, "lc_kv_append: null argument");
         h->set_device();
@@ -508,7 +520,7 @@ int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* 
 }
 
 static void graft_impl(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
-                       lc_graft_report* reports_dev, cudaStream_t st) {
+                       const float* reps_host, lc_graft_report* reports_dev, cudaStream_t st) {
     if (!take) fail(LC_EINVAL, "null take");
     bool any = false;
     for (uint32_t s = 0; s < h->a.n_slots; ++s) {
@@ -522,7 +534,11 @@ static void graft_impl(lc_index_t h, const uint32_t* take, const uint32_t* kind,
     if (!any) return;
     h->set_device();
     ck(cudaMemcpyAsync(h->take_dev, take, h->a.n_slots * 4, cudaMemcpyHostToDevice, st), "take H2D");
-    ck(launch_graft(h->a, h->take_dev, h->desc.pooling, reports_dev ? (void*)reports_dev : (void*)h->rep_scratch, st),
+    if (reps_host)
+        ck(cudaMemcpyAsync(h->reps_dev, reps_host, (size_t)h->a.n_slots * h->a.d * 4, cudaMemcpyHostToDevice, st),
+           "reps H2D");
+    ck(launch_graft(h->a, h->take_dev, h->desc.pooling, reports_dev ? (void*)reports_dev : (void*)h->rep_scratch,
+                    reps_host ? h->reps_dev : nullptr, st),
        "k_graft");
     for (uint32_t s = 0; s < h->a.n_slots; ++s) {
         if (!take[s]) continue;
@@ -541,11 +557,11 @@ int lc_graft(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uin
              lc_graft_report* reports_dev, void* stream) {
     return guard([&] {
         if (!h) fail(LC_EINVAL, "null handle");
-        graft_impl(h, take, kind, level, reports_dev, (cudaStream_t)stream);
+        graft_impl(h, take, kind, level, nullptr, reports_dev, (cudaStream_t)stream);
     });
 }
 
-int lc_decode_step(lc_index_t h, const float* q_dev, const uint16_t* keys_dev, const uint16_t* values_dev,
+int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev, const void* values_dev,
                    const lc_budgets* b, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
                    float* out_dev, lc_graft_report* reports_dev, void* stream) {
     return guard([&] {
@@ -556,7 +572,60 @@ int lc_decode_step(lc_index_t h, const float* q_dev, const uint16_t* keys_dev, c
             if (s.n_tokens >= h->a.cap_tokens) fail(LC_ENOMEM, "decode_step: token capacity exhausted");
         ck(launch_append(h->a, keys_dev, values_dev, st), "k_append");
         for (auto& s : h->hs) s.n_tokens += 1;
-        if (take) graft_impl(h, take, kind, level, reports_dev, st);
+        if (take) graft_impl(h, take, kind, level, nullptr, reports_dev, st);
+    });
+}
+
+int lc_graft_rep(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
+                 const float* reps_host, lc_graft_report* reports_dev, void* stream) {
+    return guard([&] {
+        if (!h || !reps_host) fail(LC_EINVAL, "lc_graft_rep: null argument");
+        graft_impl(h, take, kind, level, reps_host, reports_dev, (cudaStream_t)stream);
+    });
+}
+
+int lc_chunk_rep(lc_index_t h, uint32_t slot, uint32_t start, uint32_t take, float* rep_host) {
+    return guard([&] {
+        if (!h || !rep_host || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_chunk_rep: bad argument");
+        if (take == 0 || start + take > h->hs[slot].n_tokens) fail(LC_EINVAL, "lc_chunk_rep: rows outside the store");
+        h->set_device();
+        uint32_t err0 = 0;
+        ck(cudaMemcpy(&err0, h->a.err, 4, cudaMemcpyDeviceToHost), "err");
+        ck(launch_chunk_rep(h->a, slot, start, take, h->desc.pooling, h->reps_dev, 0), "k_chunk_rep");
+        ck(cudaMemcpy(rep_host, h->reps_dev, (size_t)h->a.d * 4, cudaMemcpyDeviceToHost), "rep D2H");
+        uint32_t err = 0;
+        ck(cudaMemcpy(&err, h->a.err, 4, cudaMemcpyDeviceToHost), "err");
+        if ((err & ~err0) & kErrZeroNorm) {
+            ck(cudaMemcpy(h->a.err, &err0, 4, cudaMemcpyHostToDevice), "err restore");
+            fail(LC_ERUNTIME, "chunk_representative: zero-norm pooled key");  // index.cpp:36-37
+        }
+    });
+}
+
+int lc_sparse_attention_ids(lc_index_t h, uint32_t slot, const float* q_dev, const uint32_t* ids_host,
+                            uint32_t n_ids, float* out_dev, void* stream) {
+    return guard([&] {
+        if (!h || !q_dev || !out_dev || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_sparse_attention_ids: bad argument");
+        if (n_ids == 0) fail(LC_EINVAL, "sparse_attention: empty active set");  // retriever.cpp:43
+        if (!ids_host) fail(LC_EINVAL, "lc_sparse_attention_ids: null ids");
+        const HostSlot& hs = h->hs[slot];
+        if (n_ids > h->a.cap_tokens) fail(LC_EINVAL, "sparse_attention: more ids than the token capacity");
+        const uint32_t all = (1u << h->a.G) - 1u;
+        std::vector<uint32_t> rows(n_ids);
+        for (uint32_t i = 0; i < n_ids; ++i) {
+            if (ids_host[i] >= hs.n_tokens) fail(LC_EINVAL, "sparse_attention: token id out of range");
+            rows[i] = ids_host[i] | (all << 24);
+        }
+        h->set_device();
+        cudaStream_t st = (cudaStream_t)stream;
+        Arena a = h->a;
+        ck(cudaMemcpyAsync(a.rows + (size_t)slot * a.cap_tokens, rows.data(), (size_t)n_ids * 4, cudaMemcpyHostToDevice, st),
+           "rows H2D");
+        ck(cudaMemcpyAsync(a.slot_tok + slot, &n_ids, 4, cudaMemcpyHostToDevice, st), "count H2D");
+        a.slot0 = slot;
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, 1, st), "k_attend");
+        ck(cudaStreamSynchronize(st), "attention sync");  // host arrays above are pageable
+        h->last_valid = 0;  // the slot's row list no longer matches its selection
     });
 }
 

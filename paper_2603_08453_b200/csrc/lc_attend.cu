@@ -636,10 +636,73 @@ size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots) {
     return 16 + (warps + n + kPoolPerWarp * warps + n + 1) * G * (d + 2);
 }
 
+// Reference-exact mode (fp32 K/V, any head dim): kernels::attention
+// (kernels.cpp:108-144) in fp64 -- logits q.k / sqrt(d), max-subtracted
+// softmax, weighted value sum -- one warp per query head over the slot's row
+// list: per token the lanes split the dims, the logit is a warp sum.
+__global__ void __launch_bounds__(256) k_attend_exact(Arena a, const float* q, float* out) {
+    const uint32_t slot = a.slot0 + blockIdx.x, lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const uint32_t d = a.d, G = a.G;
+    if (g >= G) return;
+    const uint32_t n = a.slot_tok[slot];
+    const uint32_t* rows = a.rows + (size_t)slot * a.cap_tokens;
+    const float* K = a.Kf + kv_off(a, slot);
+    const float* V = a.Vf + kv_off(a, slot);
+    const float* qg = q + ((size_t)slot * G + g) * d;
+    const double scale = 1.0 / sqrt((double)d);
+    auto logit = [&](uint32_t row) -> double {
+        double s = 0.0;
+        for (uint32_t j = lane; j < d; j += 32) s += (double)qg[j] * (double)K[(size_t)row * d + j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s * scale;
+    };
+    double mx = -INFINITY;
+    uint32_t cnt = 0;
+    for (uint32_t t = 0; t < n; ++t) {
+        const uint32_t e = rows[t];
+        if (!((e >> (24 + g)) & 1u)) continue;
+        mx = fmax(mx, logit(e & 0x00ffffffu));
+        ++cnt;
+    }
+    float* og = out + ((size_t)slot * G + g) * d;
+    if (cnt == 0) {  // sparse_attention over an empty set throws (retriever.cpp:43)
+        for (uint32_t j = lane; j < d; j += 32) og[j] = 0.f;
+        if (lane == 0) atomicOr(a.err, kErrEmptyActive);
+        return;
+    }
+    constexpr int kMaxPer = 8;  // d <= 256
+    double acc[kMaxPer];
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) acc[k] = 0.0;
+    double z = 0.0;
+    for (uint32_t t = 0; t < n; ++t) {
+        const uint32_t e = rows[t];
+        if (!((e >> (24 + g)) & 1u)) continue;
+        const uint32_t row = e & 0x00ffffffu;
+        const double w = exp(logit(row) - mx);
+        z += w;
+#pragma unroll
+        for (int k = 0; k < kMaxPer; ++k) {
+            const uint32_t j = lane + 32 * k;
+            if (j < d) acc[k] += w * (double)V[(size_t)row * d + j];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+        const uint32_t j = lane + 32 * k;
+        if (j < d) og[j] = (float)(acc[k] / z);
+    }
+}
+
 // Slots go in launches of at most kMaxAttendSlots whose total token capacity
 // fits the kernel's 32-bit global positions.
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
                           cudaStream_t stream) {
+    if (a.kv_f32) {
+        k_attend_exact<<<n_slots, 32 * a.G, 0, stream>>>(a, q, out);
+        return cudaGetLastError();
+    }
     const uint32_t grid = attend_grid(a.d);
     uint32_t per = kMaxAttendSlots;
     const unsigned long long cap = a.cap_tokens ? a.cap_tokens : 1;

@@ -61,11 +61,14 @@ struct Arena {
     // shape
     uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;
     uint32_t graft_full, keep_reps, cap_spans;
+    uint32_t kv_f32;         // K/V stored as fp32 (Kf, Vf; reference-exact mode) instead of bf16 (K, V)
     uint32_t smem_cand;      // candidates kept in shared memory by k_select
     uint32_t slot0;          // first slot of the launch (slot groups on several streams)
     // token store
     __nv_bfloat16* K;
     __nv_bfloat16* V;
+    float* Kf;
+    float* Vf;
     // index
     uint32_t* chunk_start;
     uint32_t* chunk_clu;

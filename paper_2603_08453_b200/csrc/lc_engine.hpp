@@ -20,8 +20,10 @@ size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
                           cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
+cudaError_t launch_chunk_rep(const Arena& a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling,
+                             float* rep_dev, cudaStream_t stream);
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
-                         cudaStream_t stream);
+                         const float* reps_dev, cudaStream_t stream);
 }  // namespace lc
 
 namespace lcx {
@@ -92,6 +94,13 @@ struct lc_index_s {
     float* out_stage = nullptr;
     uint32_t* take_dev = nullptr;
     lc_graft_report* rep_scratch = nullptr;
+    float* reps_dev = nullptr;     // caller-supplied representatives (lc_graft_rep)
+    uint32_t kv_elem = 2;          // bytes per K/V element (2 bf16, 4 fp32)
+    void* kv_ptr(int which, uint32_t slot) const {
+        const size_t off = kv_off(a, slot);
+        if (a.kv_f32) return (which ? a.Vf : a.Kf) + off;
+        return (which ? a.V : a.K) + off;
+    }
     uint32_t last_flags = 0;
     uint32_t last_valid = 0;
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots

@@ -10,18 +10,27 @@
 
 namespace lc {
 
-__global__ void k_append(Arena a, const __nv_bfloat16* keys, const __nv_bfloat16* values) {
+__global__ void k_append(Arena a, const void* keys, const void* values) {
     const uint32_t slot = blockIdx.x;
     const uint32_t n = a.state[slot].n_tokens;
     if (n >= a.cap_tokens) {
         if (threadIdx.x == 0) atomicOr(a.err, kErrTokenCap);
         return;
     }
-    __nv_bfloat16* kd = a.K + kv_off(a, slot) + (size_t)n * a.d;
-    __nv_bfloat16* vd = a.V + kv_off(a, slot) + (size_t)n * a.d;
-    for (uint32_t j = threadIdx.x; j < a.d; j += blockDim.x) {
-        kd[j] = keys[(size_t)slot * a.d + j];
-        vd[j] = values[(size_t)slot * a.d + j];
+    if (a.kv_f32) {
+        float* kd = a.Kf + kv_off(a, slot) + (size_t)n * a.d;
+        float* vd = a.Vf + kv_off(a, slot) + (size_t)n * a.d;
+        for (uint32_t j = threadIdx.x; j < a.d; j += blockDim.x) {
+            kd[j] = static_cast<const float*>(keys)[(size_t)slot * a.d + j];
+            vd[j] = static_cast<const float*>(values)[(size_t)slot * a.d + j];
+        }
+    } else {
+        __nv_bfloat16* kd = a.K + kv_off(a, slot) + (size_t)n * a.d;
+        __nv_bfloat16* vd = a.V + kv_off(a, slot) + (size_t)n * a.d;
+        for (uint32_t j = threadIdx.x; j < a.d; j += blockDim.x) {
+            kd[j] = static_cast<const __nv_bfloat16*>(keys)[(size_t)slot * a.d + j];
+            vd[j] = static_cast<const __nv_bfloat16*>(values)[(size_t)slot * a.d + j];
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) a.state[slot].n_tokens = n + 1;
@@ -32,6 +41,7 @@ struct GraftParams {
     const uint32_t* take;   // [n_slots] device
     uint32_t pooling;
     void* reports;          // lc_graft_report [n_slots]
+    const float* reps;      // [n_slots][d] caller-supplied representatives (graft_chunk(Chunk)), or null
 };
 
 struct GraftReportDev {  // layout of lc_graft_report
@@ -89,17 +99,24 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         if (tid == 0) atomicOr(a.err, kErrChunkCap);
         return;
     }
+    if (p.reps) {  // graft_chunk(Chunk): the chunk arrives with its representative
+        for (uint32_t j = tid; j < d; j += blockDim.x) s_rep[j] = p.reps[(size_t)slot * d + j];
+        __syncthreads();
+    } else {
     // ---- chunk_representative (index.cpp:20-41) over keys [start, start+take) ----
-    const __nv_bfloat16* Ks = a.K + kv_off(a, slot) + (size_t)start * d;
+    auto key = [&](uint32_t i, uint32_t j) -> double {
+        return a.kv_f32 ? (double)a.Kf[kv_off(a, slot) + (size_t)(start + i) * d + j]
+                        : (double)__bfloat162float(a.K[kv_off(a, slot) + (size_t)(start + i) * d + j]);
+    };
     for (uint32_t j = tid; j < d; j += blockDim.x) {
         double acc;
         if (p.pooling == 0) {
             acc = 0.0;
-            for (uint32_t i = 0; i < take; ++i) acc = __dadd_rn(acc, (double)__bfloat162float(Ks[(size_t)i * d + j]));
+            for (uint32_t i = 0; i < take; ++i) acc = __dadd_rn(acc, key(i, j));
             acc = __ddiv_rn(acc, (double)take);
         } else {
-            acc = (double)__bfloat162float(Ks[j]);
-            for (uint32_t i = 1; i < take; ++i) acc = fmax(acc, (double)__bfloat162float(Ks[(size_t)i * d + j]));
+            acc = key(0, j);
+            for (uint32_t i = 1; i < take; ++i) acc = fmax(acc, key(i, j));
         }
         s_acc[j] = acc;
     }
@@ -116,6 +133,7 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     }
     for (uint32_t j = tid; j < d; j += blockDim.x) s_rep[j] = (float)__ddiv_rn(s_acc[j], s_norm);
     __syncthreads();
+    }
 
     // ---- nearest cluster (streamer.cpp:74-106) ----
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
@@ -248,15 +266,54 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     }
 }
 
+// chunk_representative (index.cpp:20-41) of rows [start, start + take) of one
+// slot, for StreamState::push_token's returned Chunk: per-dim sequential fp64
+// mean (or max), sequential norm, float(acc / norm).
+__global__ void k_chunk_rep(Arena a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling, float* rep) {
+    __shared__ double s_acc[256];
+    __shared__ double s_norm;
+    const uint32_t d = a.d, tid = threadIdx.x;
+    auto key = [&](uint32_t i, uint32_t j) -> double {
+        return a.kv_f32 ? (double)a.Kf[kv_off(a, slot) + (size_t)(start + i) * d + j]
+                        : (double)__bfloat162float(a.K[kv_off(a, slot) + (size_t)(start + i) * d + j]);
+    };
+    for (uint32_t j = tid; j < d; j += blockDim.x) {
+        double acc;
+        if (pooling == 0) {
+            acc = 0.0;
+            for (uint32_t i = 0; i < take; ++i) acc = __dadd_rn(acc, key(i, j));
+            acc = __ddiv_rn(acc, (double)take);
+        } else {
+            acc = key(0, j);
+            for (uint32_t i = 1; i < take; ++i) acc = fmax(acc, key(i, j));
+        }
+        s_acc[j] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double n2 = 0.0;
+        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(s_acc[j], s_acc[j]));
+        s_norm = __dsqrt_rn(n2);
+        if (s_norm == 0.0) atomicOr(a.err, kErrZeroNorm);
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < d; j += blockDim.x) rep[j] = s_norm > 0.0 ? (float)__ddiv_rn(s_acc[j], s_norm) : 0.f;
+}
+
+cudaError_t launch_chunk_rep(const Arena& a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling,
+                             float* rep_dev, cudaStream_t stream) {
+    k_chunk_rep<<<1, 256, 0, stream>>>(a, slot, start, take, pooling, rep_dev);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream) {
-    k_append<<<a.n_slots, 128, 0, stream>>>(a, static_cast<const __nv_bfloat16*>(keys),
-                                            static_cast<const __nv_bfloat16*>(values));
+    k_append<<<a.n_slots, 128, 0, stream>>>(a, keys, values);
     return cudaGetLastError();
 }
 
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
-                         cudaStream_t stream) {
-    GraftParams p{a, take_dev, pooling, reports};
+                         const float* reps_dev, cudaStream_t stream) {
+    GraftParams p{a, take_dev, pooling, reports, reps_dev};
     k_graft<<<a.n_slots, kGraftThreads, 0, stream>>>(p);
     return cudaGetLastError();
 }

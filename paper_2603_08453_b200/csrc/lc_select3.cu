@@ -1419,10 +1419,13 @@ static cudaError_t launch3_d(const Sel3Params& p, uint32_t n_slots, uint32_t max
                              cudaStream_t stream) {
     switch (p.a.G) {
         case 1: return launch3_dg<D, 1>(p, n_slots, max_union, pmax, stream);
-        case 2: return launch3_dg<D, 2>(p, n_slots, max_union, pmax, stream);
         case 4: return launch3_dg<D, 4>(p, n_slots, max_union, pmax, stream);
-        case 8: return launch3_dg<D, 8>(p, n_slots, max_union, pmax, stream);
-        default: return cudaErrorInvalidValue;
+        default:
+            if constexpr (D >= 64) {
+                if (p.a.G == 2) return launch3_dg<D, 2>(p, n_slots, max_union, pmax, stream);
+                if (p.a.G == 8) return launch3_dg<D, 8>(p, n_slots, max_union, pmax, stream);
+            }
+            return cudaErrorInvalidValue;
     }
 }
 
@@ -1446,6 +1449,9 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                  fine_ctr, prof_sp};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
                   : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)
+                  : a.d == 32  ? launch3_d<32>(p, n_slots, max_union, pmax, stream)
+                  : a.d == 16  ? launch3_d<16>(p, n_slots, max_union, pmax, stream)
+                  : a.d == 8   ? launch3_d<8>(p, n_slots, max_union, pmax, stream)
                                : cudaErrorInvalidValue;
     if (prof && e == cudaSuccess) {
         cudaStreamSynchronize(stream);
