@@ -199,7 +199,24 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
     return h;
 }
 
-// content fingerprint of an index and its store: the engine cache key
+// the store's rows, sampled (at most ~32K floats per array hashed) plus its
+// address and size: the store part of the engine cache key
+uint64_t store_key(uint64_t h, const TokenStore& s) {
+    const size_t n = s.size(), d = s.dim();
+    const void* addr = &s;
+    h = fnv(h, &addr, sizeof addr);
+    h = fnv(h, &n, sizeof n);
+    h = fnv(h, &d, sizeof d);
+    for (const auto arr : {s.keys_flat(), s.values_flat()}) {
+        const size_t step = std::max<size_t>(1, arr.size() / 32768);
+        for (size_t i = 0; i < arr.size(); i += step) h = fnv(h, &arr[i], 4);
+        if (!arr.empty()) h = fnv(h, &arr.back(), 4);
+    }
+    return h;
+}
+
+// content fingerprint of an index (every centroid, radius and member list)
+// and its store: the engine cache key
 uint64_t fingerprint(const HierarchicalIndex& ix) {
     uint64_t h = 1469598103934665603ull;
     const size_t d = ix.dim;
@@ -216,23 +233,10 @@ uint64_t fingerprint(const HierarchicalIndex& ix) {
         h = fnv(h, &u.radius, 8);
         h = fnv(h, u.members.data(), u.members.size() * 4);
     }
-    const size_t n = ix.store ? ix.store->size() : 0;
-    h = fnv(h, &n, sizeof n);
-    if (ix.store) {
-        h = fnv(h, ix.store->keys_flat().data(), ix.store->keys_flat().size() * 4);
-        h = fnv(h, ix.store->values_flat().data(), ix.store->values_flat().size() * 4);
-    }
-    return h;
+    return ix.store ? store_key(h, *ix.store) : h;
 }
 
-uint64_t fingerprint(const TokenStore& s) {
-    uint64_t h = 1469598103934665603ull;
-    const size_t n = s.size(), d = s.dim();
-    h = fnv(h, &n, sizeof n);
-    h = fnv(h, &d, sizeof d);
-    h = fnv(h, s.keys_flat().data(), s.keys_flat().size() * 4);
-    return fnv(h, s.values_flat().data(), s.values_flat().size() * 4);
-}
+uint64_t fingerprint(const TokenStore& s) { return store_key(1469598103934665603ull, s); }
 
 // a few engines kept per thread, keyed by content
 struct CacheEntry {
@@ -398,12 +402,27 @@ VecF sparse_attention(std::span<const float> q, const TokenStore& store, std::sp
 struct StreamDevice {
     Engine e;
     size_t dev_end = 0;  // end of the last chunk the device holds
-    StreamDevice(uint32_t d, uint32_t cap_tokens, uint32_t cap_chunks, uint32_t L, uint32_t P, bool full, uint32_t pool)
-        : e(d, cap_tokens, cap_chunks, L, P, full, pool) {}
+    uint32_t cap_chunks = 0;
+    StreamDevice(uint32_t d, uint32_t cap_tokens, uint32_t cap_chunks_, uint32_t L, uint32_t P, bool full, uint32_t pool)
+        : e(d, cap_tokens, cap_chunks_, L, P, full, pool), cap_chunks(cap_chunks_) {}
 };
 
 namespace {
-constexpr uint32_t kStreamGrowth = 1u << 16;  // decode-time token / chunk headroom of a stream engine
+constexpr uint32_t kStreamGrowth = 1u << 14;  // initial decode-time token / chunk headroom of a stream engine
+
+// a fresh engine for the stream's current host mirrors, with room for `extra`
+// more tokens and chunks (the engine is re-created when a stream outgrows it)
+std::unique_ptr<StreamDevice> open_stream(const HierarchicalIndex& ix, const TokenStore& store,
+                                          const StreamerConfig& cfg, uint32_t extra) {
+    auto dev = std::make_unique<StreamDevice>(
+        static_cast<uint32_t>(ix.dim), static_cast<uint32_t>(store.size()) + extra,
+        static_cast<uint32_t>(ix.chunks.size()) + extra, static_cast<uint32_t>(ix.fine.size()),
+        static_cast<uint32_t>(ix.coarse.size()), cfg.graft_search == GraftSearch::full,
+        ix.config.pooling == Pooling::max ? 1u : 0u);
+    dev->e.upload(ix, store);
+    dev->dev_end = ix.chunks.empty() ? 0 : ix.chunks.back().span.end;
+    return dev;
+}
 
 // host mirror <- device slot (after a graft): clusters, units, chunks
 void refresh_mirror(lc_index_t h, HierarchicalIndex& ix) {
@@ -463,13 +482,7 @@ StreamState::StreamState(TokenStore store, HierarchicalIndex index, StreamerConf
     index_.store = &store_;
     chunked_end_ = index_.chunks.empty() ? 0 : index_.chunks.back().span.end;
     if (chunked_end_ > store_.size()) throw std::invalid_argument("stream state: chunks exceed store");
-    dev_ = std::make_unique<StreamDevice>(
-        static_cast<uint32_t>(index_.dim), static_cast<uint32_t>(store_.size()) + kStreamGrowth,
-        static_cast<uint32_t>(index_.chunks.size()) + kStreamGrowth, static_cast<uint32_t>(index_.fine.size()),
-        static_cast<uint32_t>(index_.coarse.size()), cfg_.graft_search == GraftSearch::full,
-        index_.config.pooling == Pooling::max ? 1u : 0u);
-    dev_->e.upload(index_, store_);
-    dev_->dev_end = chunked_end_;
+    dev_ = open_stream(index_, store_, cfg_, kStreamGrowth);
 }
 
 StreamState::~StreamState() = default;
@@ -509,11 +522,17 @@ std::optional<Chunk> StreamState::flush_buffer() {
 
 std::optional<Chunk> StreamState::push_token(const TokenRecord& token) {
     store_.append(token);  // rejects non-sequential ids and dimension mismatches
-    if (store_.size() > dev_->e.cap_tokens) throw std::runtime_error("stream: device token capacity exhausted");
-    const size_t d = store_.dim();
-    cuda_ck(cudaMemcpy(dev_->e.kv_dev, token.key.data(), d * 4, cudaMemcpyHostToDevice), "key H2D");
-    cuda_ck(cudaMemcpy(dev_->e.kv_dev + d, token.value.data(), d * 4, cudaMemcpyHostToDevice), "value H2D");
-    ck(lc_kv_append(dev_->e.h, dev_->e.kv_dev, dev_->e.kv_dev + d, nullptr));
+    if (store_.size() > dev_->e.cap_tokens || index_.chunks.size() + 1 >= dev_->cap_chunks) {
+        // outgrown: a larger engine from the host mirrors (the new token included)
+        const size_t dev_end = dev_->dev_end;
+        dev_ = open_stream(index_, store_, cfg_, std::max<uint32_t>(kStreamGrowth, (uint32_t)store_.size()));
+        dev_->dev_end = dev_end;
+    } else {
+        const size_t d = store_.dim();
+        cuda_ck(cudaMemcpy(dev_->e.kv_dev, token.key.data(), d * 4, cudaMemcpyHostToDevice), "key H2D");
+        cuda_ck(cudaMemcpy(dev_->e.kv_dev + d, token.value.data(), d * 4, cudaMemcpyHostToDevice), "value H2D");
+        ck(lc_kv_append(dev_->e.h, dev_->e.kv_dev, dev_->e.kv_dev + d, nullptr));
+    }
     std::optional<Chunk> emitted;
     if (buffer_size() >= cfg_.policy.max_len) emitted = flush_buffer();
     while (buffer_size() >= cfg_.max_buffer) {  // the reference's hard cap (unreachable under the eager flush)

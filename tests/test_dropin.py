@@ -38,3 +38,16 @@ def test_reference_tests_pass_against_reference_with_shim(name):
 @pytest.mark.parametrize("name", ["test_retriever", "test_streamer"])
 def test_reference_tests_pass_against_b200_dropin(name):
     print(_run(f"b200_{name}", 900))
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_passes_against_b200_dropin():
+    """acceptance.cpp's 12 criteria (UB soundness fuzz, degeneracy, recall
+    monotonicity, streaming stability, graft caps, byte-identical reruns...)
+    with every retrieve() / StreamState call on the B200 drop-in."""
+    path = os.path.join(REF, "b200_acceptance")
+    if not os.path.exists(path):
+        pytest.skip("b200_acceptance not built (needs /root/reference at build time)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=900, cwd=REF)
+    assert r.returncode == 0, r.stdout[-4000:]
+    assert "0 of 12 criteria failed" in r.stdout, r.stdout[-4000:]
