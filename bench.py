@@ -34,6 +34,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "retrieval+sparse-attn decode steps/s @128K (Llama-3-8B shape); % HBM roofline"
+# our kernels per decode step: k_coarse, k_fine, k_pickq, k_spans, k_attend
+KERNELS_PER_STEP = 5
 
 
 def parse():
@@ -375,7 +377,7 @@ def main():
             "data": f"synthetic (gen_clustered_workload streams on the GPU, seeds {args.seed_base}+slot; "
                     "indexes by GPU build_index, bit-exact to the reference)",
             "config": config_dict(args, world),
-            "roofline": {"bound": "hbm", "kernel": "k_attend (sparse attention, split-K flash-decode)",
+            "roofline": {"bound": "hbm", "kernel": "k_attend (persistent token-balanced gather flash-decode)",
                          "achieved": att_gbs, "peak": peak, "unit": "GB/s", "frac": att_gbs / peak,
                          "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)",
                          "peak_source": peak_src,
@@ -389,7 +391,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": 1000.0 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes},
-            "gpu_launches": args.steps * 3,
+            "gpu_launches": args.steps * KERNELS_PER_STEP,
             "clocks": clocks,
             "setup": setup,
             "cuda_graph": graph is not None,

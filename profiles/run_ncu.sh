@@ -4,7 +4,7 @@
 OUT=${1:-gpurun_out}
 mkdir -p $OUT
 BENCH="python bench.py --steps 3 --warmup 3 --graph 0 --cpu-baseline 0"
-KS='k_coarse|k_fine|k_pickq|k_spans|k_attend'
+KS='k_coarse|k_fine|k_pickq|k_spans|k_attend|k_graft|k_append'
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"$KS" --csv --log-file $OUT/launches.csv $BENCH > $OUT/ncu_bench.log 2>&1
 for k in k_coarse k_fine k_pickq k_spans k_attend; do
