@@ -283,6 +283,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         hs.fanout.resize(P);
         for (uint32_t u = 0; u < P; ++u) hs.fanout[u] = unit_off[u + 1] - unit_off[u];
         h->cand_cache.clear();
+        ++h->version;
     });
 }
 
@@ -388,6 +389,7 @@ int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const void* keys, const void*
         st.n_tokens = n_tokens;
         ck(cudaMemcpy(a.state + slot, &st, sizeof st, cudaMemcpyHostToDevice), "state");
         h->hs[slot].n_tokens = n_tokens;
+        ++h->version;
     });
 }
 
@@ -413,6 +415,7 @@ int lc_kv_append(lc_index_t h, const void* keys_dev, const void* values_dev, voi
         }
         ck(launch_append(h->a, keys_dev, values_dev, (cudaStream_t)stream), "k_append");
         for (auto& s : h->hs) s.n_tokens += 1;
+        ++h->version;
     });
 }
 
@@ -547,6 +550,7 @@ static void graft_impl(lc_index_t h, const uint32_t* take, const uint32_t* kind,
         hs.level.push_back(level ? level[s] : 0u);
         hs.chunked_end += take[s];
         hs.n_chunks += 1;
+        ++h->version;
         if (!hs.rep.empty()) hs.rep.clear();  // prefill reps no longer complete
     }
     // take[] is a pageable host array: make the async copy complete before return
@@ -637,10 +641,48 @@ int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uin
         h->set_device();
         cudaStream_t st = (cudaStream_t)stream;
         const size_t bytes = (size_t)h->a.n_slots * h->a.G * h->a.d * 4;
-        ck(cudaMemcpyAsync(h->q_stage, q_host, bytes, cudaMemcpyHostToDevice, st), "q H2D");
-        retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, h->out_stage, st);
-        ck(cudaMemcpyAsync(out_host, h->out_stage, bytes, cudaMemcpyDeviceToHost, st), "out D2H");
-        ck(cudaStreamSynchronize(st), "stream sync");
+        validate_budgets(b);
+        // the decode step's kernels replay as one CUDA graph on the handle's own
+        // stream (captured once per budgets / flags / index version), ordered
+        // after the caller's stream; the copies stay outside the graph because
+        // the host buffers may change from call to call
+        if (!h->host_stream) {
+            ck(cudaStreamCreateWithFlags(&h->host_stream, cudaStreamNonBlocking), "stream create");
+            ck(cudaEventCreateWithFlags(&h->host_event, cudaEventDisableTiming), "event create");
+        }
+        const bool same = h->host_exec && h->host_version == h->version && h->host_flags == flags &&
+                          std::memcmp(&h->host_budgets, b, sizeof *b) == 0;
+        if (!same) {
+            if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
+            h->host_exec = nullptr;
+            // one eager run sizes every scratch buffer, then the capture
+            retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, h->out_stage, h->host_stream);
+            ck(cudaStreamSynchronize(h->host_stream), "warm-up");
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(h->host_stream, cudaStreamCaptureModeThreadLocal), "capture begin");
+            try {
+                retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, h->out_stage, h->host_stream);
+            } catch (...) {
+                cudaStreamEndCapture(h->host_stream, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ck(cudaStreamEndCapture(h->host_stream, &g), "capture end");
+            const cudaError_t e = cudaGraphInstantiate(&h->host_exec, g, 0);
+            cudaGraphDestroy(g);
+            ck(e, "graph instantiate");
+            h->host_version = h->version;
+            h->host_flags = flags;
+            h->host_budgets = *b;
+        }
+        ck(cudaEventRecord(h->host_event, st), "order after caller");
+        ck(cudaStreamWaitEvent(h->host_stream, h->host_event, 0), "order after caller");
+        ck(cudaMemcpyAsync(h->q_stage, q_host, bytes, cudaMemcpyHostToDevice, h->host_stream), "q H2D");
+        ck(cudaGraphLaunch(h->host_exec, h->host_stream), "graph launch");
+        ck(cudaMemcpyAsync(out_host, h->out_stage, bytes, cudaMemcpyDeviceToHost, h->host_stream), "out D2H");
+        ck(cudaStreamSynchronize(h->host_stream), "stream sync");
+        h->last_flags = flags;
+        h->last_valid = 1;
     });
 }
 

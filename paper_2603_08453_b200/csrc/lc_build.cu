@@ -581,6 +581,7 @@ int lc_gen_workload(lc_index_t h, uint32_t n_tokens, uint32_t n_blobs, double co
     return guard([&] {
         if (!h || !seeds) fail(LC_EINVAL, "lc_gen_workload: null argument");
         if (h->a.kv_f32) fail(LC_EINVAL, "lc_gen_workload: the generator writes bf16 K/V (kv_f32 = 0 engines only)");
+        ++h->version;
         h->set_device();
         const Arena& a = h->a;
         const uint32_t S = a.n_slots, d = a.d;
@@ -657,6 +658,7 @@ int lc_index_build(lc_index_t h, const uint32_t* n_tokens, const uint32_t* spans
     return guard([&] {
         if (!h || !n_tokens || !spans || !span_off || !seeds) fail(LC_EINVAL, "lc_index_build: null argument");
         if (h->a.kv_f32) fail(LC_EINVAL, "lc_index_build: the device build reads bf16 keys (kv_f32 = 0 engines only)");
+        ++h->version;
         // IndexConfig::validate (index.cpp:13-18)
         if (avg <= 0.0) fail(LC_EINVAL, "avg_chunks_per_cluster must be positive");
         if (max_units < 1 || iters < 1) fail(LC_EINVAL, "index config fields must be positive");

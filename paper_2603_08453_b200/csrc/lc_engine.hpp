@@ -109,12 +109,22 @@ struct lc_index_s {
     float* att_part = nullptr;                 // k_attend per-(warp, slot) segment partials + counters
     uint32_t* fine_ctr = nullptr;              // k_fine pool counters, 4 per slot group (zeroed)
     std::vector<cudaStream_t> group_streams;   // one per slot group
+    uint64_t version = 0;                      // bumped by every upload / append / graft
+    cudaStream_t host_stream = nullptr;        // lc_retrieve_host's graph replay stream
+    cudaEvent_t host_event = nullptr;
+    cudaGraphExec_t host_exec = nullptr;
+    uint64_t host_version = 0;
+    uint32_t host_flags = 0;
+    lc_budgets host_budgets{};
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
 
     ~lc_index_s() {
         for (void* p : owned) cudaFree(p);
         if (sel_scratch) cudaFree(sel_scratch);
         for (auto s : group_streams) cudaStreamDestroy(s);
+        if (host_exec) cudaGraphExecDestroy(host_exec);
+        if (host_stream) cudaStreamDestroy(host_stream);
+        if (host_event) cudaEventDestroy(host_event);
         for (auto e : group_events) cudaEventDestroy(e);
     }
     void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
