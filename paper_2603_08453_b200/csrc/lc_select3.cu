@@ -279,11 +279,12 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
 // candidate: its 512-byte centroid is loaded into registers in one burst.
 //
 // The reference upper bound UB = fl64(sequential fp64 q.c) + qn*r
-// (kernels.cpp:155-159) is enclosed, not computed: s = fp32 q.c and
-// A = fp32 sum |q_j c_j| give |UB_ref - UB~| <= e with UB~ = s + qn*r and
-// e = 1.01 * 132 * 2^-24 * A + 2^-49 |UB~| (recursive-summation bound for 128
-// products + 3 partial-sum adds in fp32, plus the fp64 dot's and adds'
-// roundings).  k_pickq selects on the lower bounds, then recomputes the exact
+// (kernels.cpp:155-159) is enclosed, not computed: s = fp32 q.c gives
+// |UB_ref - UB~| <= e with UB~ = s + qn*r and
+// e = 1.01 * 132 * 2^-24 * A + 2^-49 |UB~|, A = sum |q_j c_j| <= ||q|| ||c||
+// (recursive-summation bound for 128 products + 3 partial-sum adds in fp32,
+// plus the fp64 dot's and adds' roundings; ||c|| from one fp32 sum of squares
+// shared by every head).  k_pickq selects on the lower bounds, then recomputes the exact
 // fp64 chain (bit-exact kernels::dot) only for candidates whose upper bound
 // reaches the selection cut, so every selection stays bit-exact while the
 // bulk of the scoring runs at fp32 speed.
@@ -454,13 +455,17 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             asm volatile("cp.async.wait_group 1;\n" ::);  // this tile's q (staged last iteration)
             __syncwarp();
             const float* qs = s_q[warp][d.qb];
-            float s4[GQ][4], a4[GQ][4];
+            float s4[GQ][4], c2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int g = 0; g < GQ; ++g)
 #pragma unroll
-                for (int t = 0; t < 4; ++t) s4[g][t] = a4[g][t] = 0.f;
+                for (int t = 0; t < 4; ++t) s4[g][t] = 0.f;
 #pragma unroll
             for (uint32_t j = 0; j < V; ++j) {
+                c2[0] = fmaf(v[j].x, v[j].x, c2[0]);  // ||c||^2, shared by every head
+                c2[1] = fmaf(v[j].y, v[j].y, c2[1]);
+                c2[2] = fmaf(v[j].z, v[j].z, c2[2]);
+                c2[3] = fmaf(v[j].w, v[j].w, c2[3]);
 #pragma unroll
                 for (int g = 0; g < GQ; ++g) {
                     const float4 q4 = reinterpret_cast<const float4*>(qs + g * D)[j];
@@ -468,12 +473,11 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                     s4[g][1] = fmaf(q4.y, v[j].y, s4[g][1]);
                     s4[g][2] = fmaf(q4.z, v[j].z, s4[g][2]);
                     s4[g][3] = fmaf(q4.w, v[j].w, s4[g][3]);
-                    a4[g][0] = fmaf(fabsf(q4.x), fabsf(v[j].x), a4[g][0]);
-                    a4[g][1] = fmaf(fabsf(q4.y), fabsf(v[j].y), a4[g][1]);
-                    a4[g][2] = fmaf(fabsf(q4.z), fabsf(v[j].z), a4[g][2]);
-                    a4[g][3] = fmaf(fabsf(q4.w), fabsf(v[j].w), a4[g][3]);
                 }
             }
+            // Cauchy-Schwarz: sum |q_j c_j| <= ||q|| ||c||; ||c|| from the fp32 sum of
+            // squares (relative error < 132 * 2^-24, covered by the 1.0001 factor)
+            const double cn = sqrt((double)((c2[0] + c2[1]) + (c2[2] + c2[3]))) * 1.0001;
             if (d.slot != mslot) {
                 flush_minmax();
                 mslot = d.slot;
@@ -492,9 +496,9 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             for (int g = 0; g < GQ; ++g) {
                 if ((d.mask >> g) & 1u) {
                     const float sv = (s4[g][0] + s4[g][1]) + (s4[g][2] + s4[g][3]);
-                    const float av = (a4[g][0] + a4[g][1]) + (a4[g][2] + a4[g][3]);
-                    const double ub = __dadd_rn((double)sv, __dmul_rn(__ldg(pv.qnorm() + g), r));
-                    const double e = (double)av * (1.01 * 132.0 / 16777216.0) + fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
+                    const double qn = __ldg(pv.qnorm() + g);
+                    const double ub = __dadd_rn((double)sv, __dmul_rn(qn, r));
+                    const double e = qn * cn * (1.01 * 132.0 / 16777216.0) + fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
                     const unsigned long long key = desc_key(ub - e);
                     const size_t at = (size_t)g * p.qcap + d.qoff[g] + d.local;
                     keys[at] = key;

@@ -4,7 +4,7 @@ OUT=gpurun_out
 timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
 timeout 600 python bench.py --steps 30 --warmup 3 --cpu-baseline 0 > $OUT/bench_q.json 2> $OUT/bench_q.err; tail -3 $OUT/bench_q.err
 python -c "import json;d=json.load(open('$OUT/bench_q.json'));print('steps/s',d['value'],'ms',d['ms_per_step'],'att_frac',d['roofline']['frac'],'sel_ms',d['step_roofline']['select_ms'],'att_ms',d['step_roofline']['attend_ms'],'step_frac',d['step_roofline']['frac'])"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:'k_attend|k_coarse|k_fine|k_pick|k_spans|k_graft|k_append' --csv --log-file $OUT/launches_q.csv python bench.py --steps 3 --warmup 3 --graph 0 --cpu-baseline 0 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:'k_attend|k_coarse|k_fine|k_pick|k_spans|k_select|k_graft|k_append' --csv --log-file $OUT/launches_q.csv python bench.py --steps 3 --warmup 3 --graph 0 --cpu-baseline 0 > /dev/null 2>&1
 python - <<'PY'
 import csv, collections
 rows=list(csv.reader(open('gpurun_out/launches_q.csv')))
