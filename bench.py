@@ -44,6 +44,9 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--mode", default="step", choices=["step", "stream"],
+                   help="step: config 2 retrieval + attention (the headline); stream: config 3 "
+                        "decode steps with KV append and lazy grafts (batch --batch, default 8)")
     p.add_argument("--tokens", type=int, default=131072)
     p.add_argument("--layers", type=int, default=32)
     p.add_argument("--kv-heads", type=int, default=8)
@@ -251,10 +254,97 @@ def config_dict(args, world):
             "l2": "inputs larger than L2 (>1 GB of index + KV read per step vs 126 MB L2)"}
 
 
+def run_stream_mode(args, api, torch):
+    """Config 3: a 128K prefix per slot, then decode steps through lc_decode_step
+    -- retrieve(buffer) + attention, KV append, and the lazy graft whenever the
+    host chunker flushes (streamer.cpp:145-165) -- for every (layer, KV head,
+    sequence) slot at once.  The decoded tokens carry a "\n" marker every 12
+    steps like run_stream (bench.cpp:254-272); all slots of a sequence share
+    that text stream, so a flush grafts one chunk into every slot."""
+    batch = args.batch if args.batch > 1 else 8
+    args.batch = batch
+    n = args.tokens
+    slots = list(range(args.layers * args.kv_heads * batch))
+    S, d, G = len(slots), 128, args.group
+    steps, warm = args.steps, max(args.warmup, 3)
+    cap_chunks = n // 8 + 64 + (steps + warm) // 8 + 8
+    eng = api.Engine(S, d, G, cap_tokens=n + steps + warm + 64, cap_chunks=cap_chunks,
+                     cap_clusters=(n // 8 + 64 + 1) // 2, cap_units=64, keep_reps=False)
+    seeds = np.array([args.seed_base + s for s in slots], np.uint64)
+    t0 = time.time()
+    codes, qs = eng.gen_workload(n, seeds, query_count=G)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+        spans = list(ex.map(lambda s: api.segment_codes(codes[s]), range(S)))
+    eng.build_index([n] * S, spans, seeds)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+    out = torch.zeros_like(q)
+    b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    kv = torch.randn((steps + warm, 2, S, d), device="cuda", generator=gen).to(torch.bfloat16).view(torch.int16)
+    # the buffer starts where the prefix's chunks end (every slot's chunks tile its prefix)
+    buf = []
+    grafts = 0
+
+    def step(i):
+        nonlocal buf, grafts
+        text = "\n" if (i + 1) % 12 == 0 else ""
+        buf.append(text)
+        take = kind = level = None
+        if len(buf) >= 16:  # push_token's flush (streamer.cpp:56-60), decided on the host
+            t, kd, lv = api.flush_take(buf)
+            take = np.full(S, t, np.uint32)
+            kind = np.full(S, kd, np.uint32)
+            level = np.full(S, lv, np.uint32)
+            buf = buf[t:]
+            grafts += 1
+        eng.decode_step(q, kv[i, 0], kv[i, 1], b, take, kind, level, out)
+
+    for i in range(warm):
+        step(i)
+    torch.cuda.synchronize()
+    g0 = grafts
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        ev0.record()
+        for i in range(warm, warm + steps):
+            step(i)
+        ev1.record()
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    ms = ev0.elapsed_time(ev1) / steps
+    err = eng.device_error()
+    if err:
+        raise RuntimeError(f"device error bits 0x{err:x}")
+    line = {
+        "metric": "config3 streaming decode steps/s (retrieve + attend + append + lazy graft, every slot)",
+        "value": 1000.0 / ms, "unit": "steps/s", "n_gpus": 1, "steps": steps, "warmup": warm,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": f"synthetic (gen_clustered_workload prefixes, seeds {args.seed_base}+slot; random decoded K/V; "
+                "a newline marker every 12 decoded tokens)",
+        "config": {"workload": f"config3: {args.layers} layers x {args.kv_heads} KV heads x batch {batch} "
+                               f"(= {S} slots), {n}-token prefix, {args.budget}-token budget, grafts on flush",
+                   "slots": S, "context": n, "batch": batch, "token_budget": args.budget},
+        "grafts_per_slot_timed": grafts - g0, "graft_rate": (grafts - g0) / steps,
+        "gpu_launches_per_step": "7 (5 retrieval kernels + k_append, + k_graft on flush steps)",
+        "clocks": clocks, "setup_s": round(setup_s, 1),
+        "note": "eager launches: each graft step syncs for the host-side flush bookkeeping",
+    }
+    print(json.dumps(line))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.mode == "stream":
+        import torch
+        from paper_2603_08453_b200 import api
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        run_stream_mode(args, api, torch)
         return
     import torch
     import torch.distributed as dist
