@@ -592,29 +592,26 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     uint32_t* s_sc = reinterpret_cast<uint32_t*>(s_ph + kStage * 8);
     uint32_t* s_so = reinterpret_cast<uint32_t*>(s_ph + kStage * 12);
     for (uint32_t w = tid; w < mw; w += blockDim.x) cb[w] = 0u;
-    __shared__ uint32_t s_uu[kMaxKU3 * GQ * 3];  // (mask, base, qoff_g) of the union units, staged
-    __shared__ uint32_t s_nuu;
-    if (tid == 0) s_nuu = pv.hdr()[1];
-    __syncthreads();
-    {
+    if (warp == 0) {  // this head's kept units, in union order (ballot compaction)
+        const uint32_t nuu = pv.hdr()[1];
         const uint32_t* uu = pv.units();
-        for (uint32_t k = tid; k < s_nuu; k += blockDim.x) {
-            s_uu[3 * k + 0] = uu[k * (4 + G) + 1];
-            s_uu[3 * k + 1] = uu[k * (4 + G) + 2];
-            s_uu[3 * k + 2] = uu[k * (4 + G) + 4 + g];
+        uint32_t k2 = 0;
+        for (uint32_t k0 = 0; k0 < nuu; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const bool mine = k < nuu && ((uu[k * (4 + G) + 1] >> g) & 1u);
+            const unsigned int bal = __ballot_sync(0xffffffffu, mine);
+            if (mine) {
+                const uint32_t at = k2 + __popc(bal & ((1u << lane) - 1u));
+                s_gbase[at] = uu[k * (4 + G) + 2];
+                s_gpre[at] = uu[k * (4 + G) + 4 + g];
+            }
+            k2 += __popc(bal);
         }
+        if (lane == 0) s_gpre[k2] = pv.hdr()[4 + g];
     }
     __syncthreads();
     if (tid == 0) {
-        uint32_t k2 = 0;
-        for (uint32_t k = 0; k < s_nuu; ++k)
-            if ((s_uu[3 * k] >> g) & 1u) {
-                s_gbase[k2] = s_uu[3 * k + 1];
-                s_gpre[k2] = s_uu[3 * k + 2];
-                ++k2;
-            }
         s_nc = pv.hdr()[4 + g];
-        s_gpre[k2] = s_nc;
         s_kU = pv.hdr()[3];
         const unsigned long long mn = pv.kmin()[g], mx = pv.kmax()[g];
         const unsigned long long diff = mn ^ mx;
