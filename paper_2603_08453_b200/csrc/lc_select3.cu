@@ -825,12 +825,13 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k], ci = s_gbase[k] + local;
             const float4* col = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local;
             double sacc = 0.0;
-            for (uint32_t j0 = 0; j0 < D / 4; j0 += 8) {  // 8 loads in flight, then their chain steps
-                float4 v4[8];
+            constexpr uint32_t B = D / 4 < 8 ? D / 4 : 8;  // rows per batch (head dims 8 / 16 have fewer)
+            for (uint32_t j0 = 0; j0 < D / 4; j0 += B) {  // B loads in flight, then their chain steps
+                float4 v4[B];
 #pragma unroll
-                for (uint32_t t = 0; t < 8; ++t) v4[t] = __ldg(col + (size_t)(j0 + t) * nu);
+                for (uint32_t t = 0; t < B; ++t) v4[t] = __ldg(col + (size_t)(j0 + t) * nu);
 #pragma unroll
-                for (uint32_t t = 0; t < 8; ++t) {
+                for (uint32_t t = 0; t < B; ++t) {
                 const uint32_t jq = j0 + t;
                 const float4 v = v4[t];
                 sacc = __fma_rn(s_qd[4 * jq + 0], (double)v.x, sacc);
