@@ -200,10 +200,13 @@ class Engine:
                  cap_chunks: int = 1 << 13, cap_clusters: int = 1 << 12, cap_units: int = 64,
                  splits: int = 0, structure_aware: bool = True, graft_full: bool = False,
                  keep_reps: bool = True, pooling: int = 0, device: int = 0, max_candidates: int = 0,
-                 slot_groups: int = 0):
+                 slot_groups: int = 0, kv_f32: bool = False):
+        """kv_f32: keep K/V in fp32 exactly as given, attention in fp64 (the
+        reference-exact mode; head dims 8/16/32 also allowed for group 1 or 4)."""
         self.desc = L.IndexDesc(n_slots, dim, group, cap_tokens, cap_chunks, cap_clusters,
                                 cap_units, max_candidates, splits, int(structure_aware),
-                                int(graft_full), int(keep_reps), pooling, slot_groups, device)
+                                int(graft_full), int(keep_reps), pooling, slot_groups, device, int(kv_f32))
+        self.kv_f32 = bool(kv_f32)
         self.h = C.c_void_p()
         L.check(L.lib().lc_index_create(C.byref(self.desc), C.byref(self.h)))
         got = L.IndexDesc()
@@ -225,11 +228,15 @@ class Engine:
             pass
 
     # ---- slots ----
+    def _kv(self, x: np.ndarray) -> np.ndarray:
+        x = np.asarray(x)
+        if self.kv_f32:
+            return np.ascontiguousarray(x, np.float32)
+        return np.ascontiguousarray(x if x.dtype == np.uint16 else bf16_bits(x))
+
     def upload_slot(self, slot: int, ix: HostIndex, keys: np.ndarray, values: np.ndarray):
-        keys = np.asarray(keys)
-        values = np.asarray(values)
-        kb = keys if keys.dtype == np.uint16 else bf16_bits(keys)
-        vb = values if values.dtype == np.uint16 else bf16_bits(values)
+        kb = self._kv(keys)
+        vb = self._kv(values)
         kb = np.ascontiguousarray(kb)
         vb = np.ascontiguousarray(vb)
         s, keep = ix._c()
@@ -237,13 +244,14 @@ class Engine:
                                              vb.ctypes.data, kb.shape[0]))
 
     def kv_upload(self, slot: int, keys: np.ndarray, values: np.ndarray):
-        kb = np.ascontiguousarray(keys if keys.dtype == np.uint16 else bf16_bits(keys))
-        vb = np.ascontiguousarray(values if values.dtype == np.uint16 else bf16_bits(values))
+        kb = self._kv(keys)
+        vb = self._kv(values)
         L.check(L.lib().lc_kv_upload_slot(self.h, slot, kb.ctypes.data, vb.ctypes.data, kb.shape[0]))
 
     def kv_download(self, slot: int, n: int):
-        k = np.zeros((n, self.dim), np.uint16)
-        v = np.zeros((n, self.dim), np.uint16)
+        dt = np.float32 if self.kv_f32 else np.uint16
+        k = np.zeros((n, self.dim), dt)
+        v = np.zeros((n, self.dim), dt)
         L.check(L.lib().lc_kv_download_slot(self.h, slot, k.ctypes.data, v.ctypes.data, n))
         return k, v
 
@@ -442,12 +450,13 @@ class DeviceIndex:
 
     def __init__(self, ix: HostIndex, keys: np.ndarray, values: np.ndarray, group: int = 1,
                  extra_tokens: int = 0, extra_chunks: int = 0, structure_aware: bool = True,
-                 graft_full: bool = False, device: int = 0, splits: int = 0):
+                 graft_full: bool = False, device: int = 0, splits: int = 0, kv_f32: bool = False):
         n = keys.shape[0]
         self.engine = Engine(1, ix.dim, group, cap_tokens=n + extra_tokens + 1,
                              cap_chunks=ix.n_chunks + extra_chunks + 1,
                              cap_clusters=ix.n_clusters, cap_units=max(ix.n_units, 1), splits=splits,
-                             structure_aware=structure_aware, graft_full=graft_full, device=device)
+                             structure_aware=structure_aware, graft_full=graft_full, device=device,
+                             kv_f32=kv_f32)
         self.engine.upload_slot(0, ix, keys, values)
         self.dim = ix.dim
         self.group = group

@@ -180,3 +180,20 @@ def test_decode_stream_parity(graft_full):
             assert o.graft.coarse_radius == g["coarse_radius"]
     assert grafts >= 15
     assert_same_index(st.engine.download_slot(0), ref.export())
+
+
+@pytest.mark.parametrize("d", [32, 128])
+def test_reference_exact_fp32_mode(d):
+    """kv_f32 engines keep the reference's own fp32 K/V (no bf16 rounding) and
+    attend in fp64: selections bit-exact and outputs at fp64 round-off (the
+    reference's own tests demand 1e-6 / 1e-7, tests/test_dropin.py)."""
+    w = R.gen_workload(4096, d, seed=33, n_blobs=4, query_count=4)
+    ref = ref_engine(w, seed=33)
+    dev = api.DeviceIndex(host_index(ref), w.keys, w.values, group=4, kv_f32=True)
+    for budget in (128, 1024):
+        b = api.Budgets(token_budget=budget)
+        got = dev.retrieve_group(w.queries, b)
+        for g, q in enumerate(w.queries):
+            r = ref.retrieve(q, token_budget=budget)
+            assert_same_selection(got[g], r, (d, budget, g))
+            assert rel_l2(got[g].output, r["output"]) < 1e-6, (d, budget, g)
