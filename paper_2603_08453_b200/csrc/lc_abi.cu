@@ -124,6 +124,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         h->fine_ctr = dalloc<uint32_t>(4 * groups, o);
         ck(cudaMemset(h->fine_ctr, 0, 4 * groups * 4), "memset k_fine counters");
         a.counters = dalloc<uint32_t>(S, o);
+        a.att_sync = dalloc<unsigned long long>(S, o);
         a.err = dalloc<uint32_t>(1, o);
         h->q_stage = dalloc<float>(S * G * D, o);
         h->out_stage = dalloc<float>(S * G * D, o);
@@ -133,6 +134,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         ck(cudaMemset(a.state, 0, S * sizeof(SlotState)), "memset state");
         ck(cudaMemset(a.err, 0, 4), "memset err");
         ck(cudaMemset(a.counters, 0, S * 4), "memset counters");
+        ck(cudaMemset(a.att_sync, 0, S * 8), "memset attention sync");
         ck(cudaMemset(a.n_spans, 0, S * 4), "memset n_spans");
         ck(cudaMemset(a.slot_tok, 0, S * 4), "memset slot_tok");
         ck(cudaMemset(a.span_off, 0, S * (a.cap_spans + 1) * 4), "memset span_off");

@@ -397,13 +397,13 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     uint32_t qf[KS][4];
     float acc[NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t cur = ~0u, cur_seg = ~0u;
+    uint32_t cur = ~0u, cur_seg = ~0u, seg_tok = 0;
     const float scale = (float)(1.4426950408889634 / sqrt((double)D));
 
     // partial (m, l, o) of this warp's segment of slot s; the warp completing
     // the slot's token count merges all its partials
     // partial (m, l, o) of this warp's current segment
-    auto flush = [&](uint32_t seg) {
+    auto flush = [&](uint32_t seg, uint32_t s, uint32_t ntok) {
         float l = l_run;
         l += __shfl_xor_sync(0xffffffffu, l, 1);
         l += __shfl_xor_sync(0xffffffffu, l, 2);
@@ -420,6 +420,10 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
                 o[D / 8 + j] = acc[j][1] + acc[j][3];
             }
         }
+        // publish: the slot's merge waits until every token has been flushed
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(a.att_sync + a.slot0 + s, (unsigned long long)ntok);
     };
 
     for (uint32_t it = 0;; ++it) {
@@ -435,13 +439,15 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         cp_wait<kStages - 1>();
         __syncwarp();
         if (gd.seg != cur_seg) {
-            if (cur_seg != ~0u) flush(cur_seg);
+            if (cur_seg != ~0u) flush(cur_seg, cur, seg_tok);
             cur_seg = gd.seg;
+            seg_tok = 0;
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
             m_run = -INFINITY;
             l_run = 0.f;
         }
+        seg_tok += gd.cnt;
         if (gd.slot != cur) {
             cur = gd.slot;
             // q fragments: softmax scale and log2(e) folded in, bf16 hi (row r) + lo (row r+8)
@@ -555,25 +561,27 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         __syncwarp();  // the stage is refilled by a later iteration's issue
     }
     cp_wait<0>();
-    if (cur_seg != ~0u) flush(cur_seg);
+    if (cur_seg != ~0u) flush(cur_seg, cur, seg_tok);
     const unsigned long long t_merge = p.prof ? gtime_a() : 0ull;
 
-    // ---- grid barrier (the grid is sized to be co-resident), then every warp
-    // merges (slot, head) pairs: the slot's partials in a fixed order ----
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        atomicAdd(pool_ctr + 1, 1u);
-        while (*reinterpret_cast<volatile uint32_t*>(pool_ctr + 1) < gridDim.x) __nanosleep(64);
-        __threadfence();
-    }
-    __syncthreads();
+    // ---- every warp merges (slot, head) pairs, each as soon as all of the
+    // slot's tokens have been flushed (the grid is co-resident, so waiting is
+    // safe): the slot's partials in a fixed order.  The last head to merge a
+    // slot resets its counter for the next launch ----
     for (uint32_t x = w; x < n * G; x += NW) {
         const uint32_t s = x / G, g = x % G;
-        if (s_hp[s + 1] == s_hp[s] && s_tp[s + 1] == s_tp[s]) continue;  // written by block 0
+        const uint32_t tok = s_hp[s + 1] - s_hp[s] + s_tp[s + 1] - s_tp[s];
+        if (tok == 0) continue;  // written by block 0
+        unsigned long long* sync = a.att_sync + a.slot0 + s;
+        if (lane == 0)
+            while ((uint32_t)(*reinterpret_cast<volatile unsigned long long*>(sync)) != tok) __nanosleep(32);
+        __syncwarp();
+        __threadfence();
         merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, part,
                       NW + n + kPoolPerWarp * NW + n, s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1],
                       pool.C);
+        __syncwarp();
+        if (lane == 0 && (atomicAdd(sync, 1ull << 32) >> 32) == G - 1) atomicExch(sync, 0ull);
     }
     // the last CTA out resets the pool and the barrier for the next launch
     __syncthreads();

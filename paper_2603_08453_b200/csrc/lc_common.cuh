@@ -101,7 +101,8 @@ struct Arena {
                              //   token row | head mask << 24 (k_spans -> k_attend)
     uint32_t* slot_tok;      // [slot] union active token count (length of the row list)
     unsigned long long* step_bytes;  // [slot][4]
-    uint32_t* counters;      // [slot] k_attend tokens accounted so far (reset by the merging warp)
+    uint32_t* counters;      // [slot] (unused)
+    unsigned long long* att_sync;  // [slot] k_attend: tokens flushed (low 32) | heads merged (high 32)
     uint32_t* err;           // [1]
 };
 
