@@ -123,22 +123,27 @@ struct GroupDesc {  // one 16-token group of one slot
     uint32_t seg;   // partial index of the (range, slot) segment the group belongs to
 };
 
-// Work split.  Every slot's union token list is cut into a head (the first 3/4)
+// Work split.  Every slot's union token list is cut into a head (the first 7/8)
 // and a tail.  The heads, concatenated, are cut statically into equal
 // contiguous warp ranges; the tails, concatenated, form a pool of at most
 // kPoolPerWarp x warps chunks that warps claim in order as they finish (SMs
 // differ in achieved bandwidth by up to ~30%).  Partial index of a segment:
 // static range w of slot s -> w + s, pool chunk k of slot s -> NW + n + k + s
 // (both injective because range and slot indices grow together).
-constexpr uint32_t kPoolPerWarp = 4;
-__device__ __forceinline__ uint32_t head_of(uint32_t t) { return t - t / 4; }
+constexpr uint32_t kPoolPerWarp = 4;     // pool chunks per warp (upper bound; partial storage)
+// Measured on config 2 (profiles/run_attsweep.sh): a 1/8 tail in one chunk per
+// warp balances the SMs with the fewest partials (tails 1/2..1/32 and 1..8
+// chunks per warp: 156.8 us best vs 166-181 us)
+__device__ uint32_t g_tail_div = 8;       // tail = t / g_tail_div of every slot's tokens (LC_ATT_TAIL_DIV)
+__device__ uint32_t g_pool_per_warp = 1;  // <= kPoolPerWarp (LC_ATT_POOL)
+__device__ __forceinline__ uint32_t head_of(uint32_t t) { return t - t / g_tail_div; }
 struct PoolShape {
     uint32_t C;  // pool chunk length (multiple of 16)
     uint32_t K;  // pool chunks
 };
 __device__ __forceinline__ PoolShape pool_shape(uint32_t TP, uint32_t NW) {
     PoolShape ps;
-    const uint32_t kmax = kPoolPerWarp * NW;
+    const uint32_t kmax = g_pool_per_warp * NW;
     uint32_t C = (TP + kmax - 1) / kmax;
     C = (C + 15) & ~15u;
     ps.C = C ? C : 16;
@@ -715,6 +720,18 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     uint32_t per = kMaxAttendSlots;
     const unsigned long long cap = a.cap_tokens ? a.cap_tokens : 1;
     if ((unsigned long long)per * cap > 0xffffffffull) per = (uint32_t)(0xffffffffull / cap);
+    static bool tuned = false;
+    if (!tuned) {  // experiment knobs: LC_ATT_TAIL_DIV (tail fraction 1/x), LC_ATT_POOL (chunks per warp)
+        tuned = true;
+        if (const char* e = getenv("LC_ATT_TAIL_DIV")) {
+            const uint32_t v = (uint32_t)atoi(e);
+            if (v >= 2) cudaMemcpyToSymbol(g_tail_div, &v, 4);
+        }
+        if (const char* e = getenv("LC_ATT_POOL")) {
+            const uint32_t v = (uint32_t)atoi(e);
+            if (v >= 1 && v <= kPoolPerWarp) cudaMemcpyToSymbol(g_pool_per_warp, &v, 4);
+        }
+    }
     static unsigned long long* prof = nullptr;
     const bool want_prof = getenv("LC_PROF") != nullptr;
     if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
