@@ -226,6 +226,7 @@ __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G
 
 template <int D>
 __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
+    pdl_wait();
     static_assert(D == 64 || D == 128, "D must be 64 or 128");
     constexpr int KS = D / 16;             // k-steps of QK
     constexpr int KW = D / 32;             // 16-byte chunks per thread per K row
@@ -620,8 +621,7 @@ static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStr
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    k_attend<D><<<grid, kAttThreads, attend_smem<D>(), stream>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(k_attend<D>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
 }
 
 // Persistent grid: every SM holds as many CTAs as fit.

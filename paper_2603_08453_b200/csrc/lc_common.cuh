@@ -28,6 +28,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -139,6 +140,28 @@ __device__ __forceinline__ unsigned long long desc_key(double s) {
     unsigned long long b = (unsigned long long)__double_as_longlong(s);
     unsigned long long ord = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
     return ~ord;
+}
+
+// Programmatic dependent launch: the kernel may be scheduled while its stream
+// predecessor drains; it must run pdl_wait() before touching anything the
+// predecessor writes (griddepcontrol.wait returns once the predecessor grid
+// has completed and flushed its memory).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 enum ErrBits : uint32_t {

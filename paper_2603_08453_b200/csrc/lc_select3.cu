@@ -295,6 +295,7 @@ constexpr uint32_t kScratchEntry = 20;  // bytes per (head, candidate): lo key u
 
 template <int D, int GQ>
 __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n) {
+    pdl_wait();
     const Arena& a = p.a;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t G = GQ, V = D / 4;  // float4s per centroid
@@ -1369,12 +1370,14 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
 // k_pickq: one CTA per (query head, slot); k_spans: one CTA per slot.
 template <int DQ, int GQ>
 __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
+    pdl_wait();
     pick_head<DQ, GQ>(p);
 }
 
 constexpr int kSpThreads = 256;
 template <int GQ>
 __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
+    pdl_wait();
     build_spans<GQ>(p, p.a.slot0 + blockIdx.x);
 }
 
@@ -1409,10 +1412,14 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
     for (uint32_t s0 = 0; s0 < n_slots; s0 += kMaxAttendSlots) {
         Sel3Params q = p;
         q.a.slot0 = p.a.slot0 + s0;
-        k_fine<D, GQ><<<fine_grid, kFiThreads, 0, stream>>>(q, std::min<uint32_t>(kMaxAttendSlots, n_slots - s0));
+        cudaError_t e = launch_pdl(k_fine<D, GQ>, dim3(fine_grid), dim3(kFiThreads), 0, stream, q,
+                                   std::min<uint32_t>(kMaxAttendSlots, n_slots - s0));
+        if (e != cudaSuccess) return e;
     }
-    k_pickq<D, GQ><<<dim3(GQ, n_slots), kPqThreads, pk_smem, stream>>>(p);
-    k_spans<GQ><<<n_slots, kSpThreads, 0, stream>>>(p);
+    cudaError_t e2 = launch_pdl(k_pickq<D, GQ>, dim3(GQ, n_slots), dim3(kPqThreads), pk_smem, stream, p);
+    if (e2 != cudaSuccess) return e2;
+    e2 = launch_pdl(k_spans<GQ>, dim3(n_slots), dim3(kSpThreads), 0, stream, p);
+    if (e2 != cudaSuccess) return e2;
     return cudaGetLastError();
 }
 
