@@ -95,6 +95,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.urad = dalloc<double>(S * a.cap_units, o);
         a.unit_off = dalloc<uint32_t>(S * (a.cap_units + 1), o);
         a.fcent = dalloc<float>(S * d.cap_clusters * D, o);
+        a.fcent16 = dalloc<__half>(S * d.cap_clusters * D, o);
         a.frad = dalloc<double>(S * d.cap_clusters, o);
         a.ftok = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.forig = dalloc<uint32_t>(S * d.cap_clusters, o);
@@ -249,6 +250,14 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         up(a.urad + so * a.cap_units, urad.data(), urad.size() * 8);
         up(a.unit_off + so * (a.cap_units + 1), unit_off.data(), unit_off.size() * 4);
         up(a.fcent + so * a.cap_clusters * D, fcent.data(), fcent.size() * 4);
+        {  // fp16 copy for k_fine's filter; its error bound needs finite centroids inside fp16 range
+            std::vector<__half> f16(fcent.size());
+            for (size_t x = 0; x < fcent.size(); ++x) {
+                if (!(std::fabs(fcent[x]) <= 60000.f)) fail(LC_EINVAL, "fine centroids must be finite and |c| <= 6e4");
+                f16[x] = __float2half_rn(fcent[x]);
+            }
+            up(a.fcent16 + so * a.cap_clusters * D, f16.data(), f16.size() * 2);
+        }
         up(a.frad + so * a.cap_clusters, frad.data(), frad.size() * 8);
         up(a.ftok + so * a.cap_clusters, ftok.data(), ftok.size() * 4);
         up(a.forig + so * a.cap_clusters, orig.data(), orig.size() * 4);

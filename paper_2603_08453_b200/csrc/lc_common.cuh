@@ -16,6 +16,8 @@
 //                                                    (dimension-quad-major: a warp reads a
 //                                                    float4 per cluster per step, 512 B
 //                                                    contiguous) at unit_off[u]*d
+//   fcent16     f16  [slot][cap_clusters*d]          fcent rounded to nearest fp16 (k_fine's
+//                                                    certified filter; the exact path reads fcent)
 //   frad        f64  [slot][cap_clusters]            FineCluster::radius
 //   ftok        u32  [slot][cap_clusters]            FineCluster::token_count
 //   forig       u32  [slot][cap_clusters]            reference cluster id of internal id
@@ -30,6 +32,7 @@
 #include <cstdint>
 #include <utility>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace lc {
@@ -78,6 +81,7 @@ struct Arena {
     double* urad;
     uint32_t* unit_off;
     float* fcent;
+    __half* fcent16;         // fcent rounded to fp16, same layout: k_fine's filter reads these
     double* frad;
     uint32_t* ftok;
     uint32_t* forig;

@@ -279,12 +279,13 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
 // candidate: its 512-byte centroid is loaded into registers in one burst.
 //
 // The reference upper bound UB = fl64(sequential fp64 q.c) + qn*r
-// (kernels.cpp:155-159) is enclosed, not computed: s = fp32 q.c gives
+// (kernels.cpp:155-159) is enclosed, not computed, from the fp16 copy of the
+// centroids (half the bytes): with c~ = fp16(c), s = fp32 q.c~ gives
 // |UB_ref - UB~| <= e with UB~ = s + qn*r and
-// e = 1.01 * 132 * 2^-24 * A + 2^-49 |UB~|, A = sum |q_j c_j| <= ||q|| ||c||
-// (recursive-summation bound for 128 products + 3 partial-sum adds in fp32,
-// plus the fp64 dot's and adds' roundings; ||c|| from one fp32 sum of squares
-// shared by every head).  k_pickq selects on the lower bounds, then recomputes the exact
+// e = ||q|| (1.01 * 132 * 2^-24 ||c|| + 2^-11 ||c|| + 2^-25 sqrt(d)) + 2^-49 |UB~|
+// (fp16 rounding of c, recursive-summation bound for 128 products + 3
+// partial-sum adds in fp32, the fp64 dot's and adds' roundings; ||c|| bounded
+// from one fp32 sum of squares of c~ shared by every head).  k_pickq selects on the lower bounds, then recomputes the exact
 // fp64 chain (bit-exact kernels::dot) only for candidates whose upper bound
 // reaches the selection cut, so every selection stays bit-exact while the
 // bulk of the scoring runs at fp32 speed.
@@ -439,12 +440,13 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
         sa = stage_a(next_tile());
         while (d.slot != ~0u) {
             // (C) this tile's centroids, radius and weight: one burst of loads
-            const float4* col = reinterpret_cast<const float4*>(a.fcent + (size_t)d.slot * a.cap_clusters * D +
-                                                               (size_t)d.base * D) + d.local;
-            float4 v[V];
+            // fp16 centroid rows (4 dims = 8 bytes per lane per row)
+            const uint2* col = reinterpret_cast<const uint2*>(a.fcent16 + (size_t)d.slot * a.cap_clusters * D +
+                                                             (size_t)d.base * D) + d.local;
+            uint2 v16[V];
             if (d.valid) {
 #pragma unroll
-                for (uint32_t j = 0; j < V; ++j) v[j] = __ldg(col + (size_t)j * d.nu);
+                for (uint32_t j = 0; j < V; ++j) v16[j] = __ldg(col + (size_t)j * d.nu);
             }
             const uint32_t cid = d.base + d.local;
             const double r = d.valid ? __ldg(a.frad + (size_t)d.slot * a.cap_clusters + cid) : 0.0;
@@ -463,22 +465,29 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 for (int t = 0; t < 4; ++t) s4[g][t] = 0.f;
 #pragma unroll
             for (uint32_t j = 0; j < V; ++j) {
-                c2[0] = fmaf(v[j].x, v[j].x, c2[0]);  // ||c||^2, shared by every head
-                c2[1] = fmaf(v[j].y, v[j].y, c2[1]);
-                c2[2] = fmaf(v[j].z, v[j].z, c2[2]);
-                c2[3] = fmaf(v[j].w, v[j].w, c2[3]);
+                const float2 lo2 = __half22float2(*reinterpret_cast<const __half2*>(&v16[j].x));
+                const float2 hi2 = __half22float2(*reinterpret_cast<const __half2*>(&v16[j].y));
+                const float4 vj = make_float4(lo2.x, lo2.y, hi2.x, hi2.y);
+                c2[0] = fmaf(vj.x, vj.x, c2[0]);  // ||c~||^2, shared by every head
+                c2[1] = fmaf(vj.y, vj.y, c2[1]);
+                c2[2] = fmaf(vj.z, vj.z, c2[2]);
+                c2[3] = fmaf(vj.w, vj.w, c2[3]);
 #pragma unroll
                 for (int g = 0; g < GQ; ++g) {
                     const float4 q4 = reinterpret_cast<const float4*>(qs + g * D)[j];
-                    s4[g][0] = fmaf(q4.x, v[j].x, s4[g][0]);
-                    s4[g][1] = fmaf(q4.y, v[j].y, s4[g][1]);
-                    s4[g][2] = fmaf(q4.z, v[j].z, s4[g][2]);
-                    s4[g][3] = fmaf(q4.w, v[j].w, s4[g][3]);
+                    s4[g][0] = fmaf(q4.x, vj.x, s4[g][0]);
+                    s4[g][1] = fmaf(q4.y, vj.y, s4[g][1]);
+                    s4[g][2] = fmaf(q4.z, vj.z, s4[g][2]);
+                    s4[g][3] = fmaf(q4.w, vj.w, s4[g][3]);
                 }
             }
-            // Cauchy-Schwarz: sum |q_j c_j| <= ||q|| ||c||; ||c|| from the fp32 sum of
-            // squares (relative error < 132 * 2^-24, covered by the 1.0001 factor)
-            const double cn = sqrt((double)((c2[0] + c2[1]) + (c2[2] + c2[3]))) * 1.0001;
+            // the filter reads c~ = fp16(c): |c_j - c~_j| <= 2^-11 |c_j| + 2^-25.  ||c~|| from
+            // an fp32 sum of squares (relative error < 132 * 2^-24, inside the 1.0001 factor);
+            // ||c|| <= (||c~|| + 2^-25 sqrt(d)) / (1 - 2^-11)
+            const double cn16 = sqrt((double)((c2[0] + c2[1]) + (c2[2] + c2[3]))) * 1.0001;
+            const double cn = (cn16 + 2.9802322387695312e-08 * sqrt((double)D)) / (1.0 - 4.8828125e-04);
+            // |q.c - q.c~| <= 2^-11 ||q|| ||c|| + 2^-25 ||q||_1 and ||q||_1 <= sqrt(d) ||q||
+            const double e16 = 4.8828125e-04 * cn + 2.9802322387695312e-08 * sqrt((double)D);
             if (d.slot != mslot) {
                 flush_minmax();
                 mslot = d.slot;
@@ -499,7 +508,8 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                     const float sv = (s4[g][0] + s4[g][1]) + (s4[g][2] + s4[g][3]);
                     const double qn = __ldg(pv.qnorm() + g);
                     const double ub = __dadd_rn((double)sv, __dmul_rn(qn, r));
-                    const double e = qn * cn * (1.01 * 132.0 / 16777216.0) + fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
+                    const double e = qn * (cn * (1.01 * 132.0 / 16777216.0) + e16) * 1.0001 +
+                                     fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
                     const unsigned long long key = desc_key(ub - e);
                     const size_t at = (size_t)g * p.qcap + d.qoff[g] + d.local;
                     keys[at] = key;
