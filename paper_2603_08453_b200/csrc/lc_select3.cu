@@ -57,8 +57,20 @@ __device__ __forceinline__ double key_score(unsigned long long key) {
     return __longlong_as_double((long long)b);
 }
 
-constexpr uint32_t kPickRCap = 256;   // refinement list kept in shared memory
+constexpr uint32_t kPickRCap = 128;   // refinement list kept in shared memory
 constexpr uint32_t kPickCols = 8;     // refinement centroids staged per pass
+constexpr uint32_t kPickBufs = 2;     // ... double-buffered
+constexpr uint32_t kPickStage = 256;  // rank-phase staging entries
+// k_pickq's phase buffer: the radix histograms, the refinement (centroid
+// columns + the per-R arrays) and the rank phase's staging live in different
+// phases of the kernel and share one static buffer.
+template <int DQ>
+struct PickPhase {
+    static constexpr uint32_t refine = kPickBufs * kPickCols * DQ * 4 + kPickRCap * (8 + 8 + 6 * 4);
+    static constexpr uint32_t stage = kPickStage * 16, hist = 2 * 256 * 4;
+    static constexpr uint32_t bytes =
+        refine > stage ? (refine > hist ? refine : hist) : (stage > hist ? stage : hist);
+};
 
 __device__ __forceinline__ void bar_g(uint32_t id, uint32_t n) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -101,7 +113,6 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
     const SlotState st = a.state[slot];
     const uint32_t n = st.n_tokens, P = st.P;
     PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
-    QInfo* qi = a.qinfo + (size_t)slot * G;
     const bool degenerate = (p.mode == 1 && (unsigned long long)n <= p.budget) || st.n_chunks == 0;
     if (degenerate) {
         if (tid == 0) {
@@ -114,58 +125,95 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
     double* qd = reinterpret_cast<double*>(smem);            // [G][D]
     float* ucs = reinterpret_cast<float*>(qd + G * D);       // [D][Pp]
     unsigned long long* ukey = reinterpret_cast<unsigned long long*>(ucs + (size_t)D * Pp);  // [G][P]
+    double* s_urad = reinterpret_cast<double*>(ukey + (size_t)G * P);                         // [P]
+    uint32_t* s_uoff = reinterpret_cast<uint32_t*>(s_urad + P);                              // [P + 1]
+    uint32_t* s_umask = s_uoff + P + 1;                                                      // [P]
     __shared__ double s_qn[GQ];
     __shared__ uint32_t s_kept[GQ][kMaxKU3];
     __shared__ uint32_t s_ucum[1025];
     __shared__ uint32_t s_nuu;
 
-    for (uint32_t x = tid; x < G * D; x += blockDim.x) {
+    // every global input of the kernel is requested up front
+    const double* ur = a.urad + (size_t)slot * a.cap_units;
+    const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
+    for (uint32_t u = tid; u <= P; u += kCoThreads) {
+        s_uoff[u] = uoff[u];
+        if (u < P) {
+            s_urad[u] = ur[u];
+            s_umask[u] = 0;
+        }
+    }
+    for (uint32_t x = tid; x < G * D; x += kCoThreads) {
         qd[x] = (double)p.q[(size_t)slot * G * D + x];
         pv.qd()[x] = qd[x];  // k_fine reads q as f64 from the plan (L1-resident)
     }
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
     {
-        const uint32_t pq = Pp >> 2, n4 = D * pq;
+        // element e = (row j, float4 column c) of the [D][Pp] tile, walked
+        // without a division per element
+        const uint32_t pq = Pp >> 2, n4 = D * pq, sj = kCoThreads / pq, sc = kCoThreads % pq;
+        uint32_t j = tid / pq, c = tid % pq;
         constexpr int kB = 8;
         for (uint32_t e0 = 0; e0 < n4; e0 += kB * kCoThreads) {
             float4 v[kB];
+            uint32_t jj[kB], cc[kB];
 #pragma unroll
             for (int t = 0; t < kB; ++t) {
-                const uint32_t e = e0 + t * kCoThreads + tid;
-                if (e < n4) v[t] = __ldg(reinterpret_cast<const float4*>(uc + (size_t)(e / pq) * a.cap_units) + e % pq);
+                jj[t] = j;
+                cc[t] = c;
+                if (e0 + t * kCoThreads + tid < n4)
+                    v[t] = __ldg(reinterpret_cast<const float4*>(uc + (size_t)j * a.cap_units) + c);
+                j += sj;
+                c += sc;
+                if (c >= pq) {
+                    c -= pq;
+                    ++j;
+                }
             }
 #pragma unroll
-            for (int t = 0; t < kB; ++t) {
-                const uint32_t e = e0 + t * kCoThreads + tid;
-                if (e < n4) reinterpret_cast<float4*>(ucs + (size_t)(e / pq) * Pp)[e % pq] = v[t];
-            }
+            for (int t = 0; t < kB; ++t)
+                if (e0 + t * kCoThreads + tid < n4) reinterpret_cast<float4*>(ucs + (size_t)jj[t] * Pp)[cc[t]] = v[t];
         }
     }
     __syncthreads();
-    // ||q_g|| (kernels.cpp:19-23) on the last warp; coarse dots on the others
-    if (warp == kCoThreads / 32 - 1) {
+    // one thread per unit runs the G coarse dots as independent chains (one
+    // fp32->fp64 conversion of the centroid element feeds all of them);
+    // ||q_g|| (kernels.cpp:19-23) runs on the last warp when it holds no unit
+    const bool qn_apart = P <= kCoThreads - 32;
+    if (qn_apart && warp == kCoThreads / 32 - 1) {
         if (lane < G) {
-            double s = 0.0;
-            const double* qg = qd + lane * D;
+            double n2 = 0.0;
 #pragma unroll 8
-            for (uint32_t j = 0; j < d; ++j) s = __fma_rn(qg[j], qg[j], s);
-            s_qn[lane] = __dsqrt_rn(s);
+            for (uint32_t j = 0; j < d; ++j) n2 = __fma_rn(qd[lane * D + j], qd[lane * D + j], n2);
+            s_qn[lane] = __dsqrt_rn(n2);
         }
     } else {
-        for (uint32_t x = tid; x < G * P; x += kCoThreads - 32) {
-            const uint32_t g = x / P, u = x % P;
-            const double* qg = qd + g * D;
-            double s = 0.0;
-#pragma unroll 8
-            for (uint32_t j = 0; j < d; ++j) s = __fma_rn(qg[j], (double)ucs[j * Pp + u], s);
-            ukey[x] = __double_as_longlong(s);  // raw dot for now
+        for (uint32_t u = tid; u < P; u += kCoThreads) {
+            double s[GQ];
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) s[g] = 0.0;
+#pragma unroll 4
+            for (uint32_t j = 0; j < d; ++j) {
+                const double c = (double)ucs[j * Pp + u];
+#pragma unroll
+                for (int g = 0; g < GQ; ++g) s[g] = __fma_rn(qd[g * D + j], c, s[g]);
+            }
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) ukey[g * P + u] = __double_as_longlong(s[g]);  // raw dot for now
+        }
+    }
+    if (!qn_apart) {
+        __syncthreads();
+        if (tid < G) {
+            double n2 = 0.0;
+            for (uint32_t j = 0; j < d; ++j) n2 = __fma_rn(qd[tid * D + j], qd[tid * D + j], n2);
+            s_qn[tid] = __dsqrt_rn(n2);
         }
     }
     __syncthreads();
-    const double* ur = a.urad + (size_t)slot * a.cap_units;
     for (uint32_t x = tid; x < G * P; x += kCoThreads) {
         const uint32_t g = x / P, u = x % P;
-        ukey[x] = desc_key(__dadd_rn(__longlong_as_double(ukey[x]), __dmul_rn(s_qn[g], ur[u])));
+        ukey[x] = desc_key(__dadd_rn(__longlong_as_double(ukey[x]), __dmul_rn(s_qn[g], s_urad[u])));
     }
     __syncthreads();
     const uint32_t kU = min(min(p.unit_topk, P), (uint32_t)kMaxKU3);
@@ -175,13 +223,15 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
         const unsigned long long ku = kg[u];
         uint32_t rank = 0;
         for (uint32_t v = 0; v < P; ++v) rank += (kg[v] < ku || (kg[v] == ku && v < u)) ? 1u : 0u;
-        if (rank < kU) s_kept[g][rank] = u;
+        if (rank < kU) {
+            s_kept[g][rank] = u;
+            atomicOr(s_umask + u, 1u << g);
+        }
     }
     __syncthreads();
     // selected_units (rank order) and the union of kept units in ascending unit order
     for (uint32_t x = tid; x < G * kU; x += kCoThreads)
         a.sel_units[((size_t)slot * G + x / kU) * a.cap_units + x % kU] = s_kept[x / kU][x % kU];
-    const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
     if (warp == 0) {
         uint32_t* uu = pv.units();
         const uint32_t stride = 4 + G;
@@ -191,12 +241,8 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
         for (int g = 0; g < GQ; ++g) qacc[g] = 0;
         for (uint32_t u0 = 0; u0 < P; u0 += 32) {
             const uint32_t u = u0 + lane;
-            uint32_t m = 0;
-            if (u < P)
-#pragma unroll
-                for (int g = 0; g < GQ; ++g)
-                    for (uint32_t k = 0; k < kU; ++k) m |= (s_kept[g][k] == u ? 1u : 0u) << g;
-            const uint32_t nu = m ? uoff[u + 1] - uoff[u] : 0u;
+            uint32_t m = u < P ? s_umask[u] : 0u;
+            const uint32_t nu = m ? s_uoff[u + 1] - s_uoff[u] : 0u;
             if (nu == 0) m = 0;  // an empty unit contributes no candidate
             const unsigned int bal = __ballot_sync(0xffffffffu, m != 0);
             const uint32_t idx = pos + __popc(bal & ((1u << lane) - 1u));
@@ -227,7 +273,7 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
             if (m) {
                 uu[idx * stride + 0] = u;
                 uu[idx * stride + 1] = m;
-                uu[idx * stride + 2] = uoff[u];
+                uu[idx * stride + 2] = s_uoff[u];
                 uu[idx * stride + 3] = nu;
             }
             ncu += __reduce_add_sync(0xffffffffu, nu);
@@ -591,14 +637,13 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     uint32_t* sw = reinterpret_cast<uint32_t*>(sk + p.keys_cap);
     uint32_t* cb = sw + p.keys_cap;
     __shared__ uint32_t s_gbase[kMaxKU3], s_gpre[kMaxKU3 + 1], s_nc, s_kU;
-    __shared__ uint32_t hw[256], hc[256];
+    __shared__ __align__(16) unsigned char s_ph[PickPhase<DQ>::bytes];
+    uint32_t* hw = reinterpret_cast<uint32_t*>(s_ph);  // radix histograms (weights, counts)
+    uint32_t* hc = hw + 256;
     __shared__ unsigned long long s_prefix, s_mask, s_wbefore;
     __shared__ uint32_t s_cbefore, s_state, s_nsel;
     __shared__ int s_shift;
-    constexpr uint32_t kStage = 256;
-    // the rank phase's staging (s_sk, s_sc, s_so) and the refinement's arrays
-    // (s_rk, s_ro, s_rw, s_ri) live in different phases: one buffer
-    __shared__ __align__(16) unsigned char s_ph[kPickRCap * 20 > kStage * 16 ? kPickRCap * 20 : kStage * 16];
+    constexpr uint32_t kStage = kPickStage;
     unsigned long long* s_sk = reinterpret_cast<unsigned long long*>(s_ph);
     uint32_t* s_sc = reinterpret_cast<uint32_t*>(s_ph + kStage * 8);
     uint32_t* s_so = reinterpret_cast<uint32_t*>(s_ph + kStage * 12);
@@ -687,6 +732,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     };
     const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
     const uint32_t* ft = a.ftok + (size_t)slot * a.cap_clusters;
+    const uint32_t* moff_g = a.fmem_off + (size_t)slot * (a.cap_clusters + 1);
     const unsigned long long budget = p.mode == 1 ? p.budget : (unsigned long long)p.cluster_topk;
     // weighted radix select of the token-budget prefix (retriever.cpp:142-154):
     // the first key (ascending = descending score) at which the running weight
@@ -786,7 +832,6 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
         __shared__ double s_qd[DQ];
         __shared__ uint32_t s_rn;
         __shared__ uint32_t s_r[kPickRCap];
-        __shared__ __align__(16) float4 s_col[kPickCols][DQ / 4];
         if (tid == 0) {
             s_xkey = ~0ull;
             s_rmin = ~0ull;
@@ -859,18 +904,20 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             // reference id asc) -- select_topk's order (retriever.cpp:27-39) --
             // and admit the rank prefix while the running weight stays within
             // the budget, the first cluster unconditionally (retriever.cpp:142-154).
-            unsigned long long* s_rk = reinterpret_cast<unsigned long long*>(s_ph);
-            uint32_t* s_ro = reinterpret_cast<uint32_t*>(s_ph + kPickRCap * 8);
+            float4* s_col = reinterpret_cast<float4*>(s_ph);  // [kPickBufs * kPickCols][D / 4]
+            unsigned long long* s_rk = reinterpret_cast<unsigned long long*>(s_ph + kPickBufs * kPickCols * D * 4);
+            double* s_rf = reinterpret_cast<double*>(s_rk + kPickRCap);
+            uint32_t* s_ro = reinterpret_cast<uint32_t*>(s_rf + kPickRCap);
             uint32_t* s_rw = s_ro + kPickRCap;
             uint32_t* s_ri = s_rw + kPickRCap;
-            for (uint32_t r = tid; r < nr; r += blockDim.x) {
-                const uint32_t i = s_r[r];
-                s_ro[r] = fo[cand(i)];
-                s_rw[r] = sg[i];
-            }
-            // exact upper bounds, kPickCols columns at a time staged by cp.async
-            for (uint32_t b0 = 0; b0 < nr; b0 += kPickCols) {
-                const uint32_t cnt = min(kPickCols, nr - b0);
+            uint32_t* s_rci = s_ri + kPickRCap;
+            uint32_t* s_rmo = s_rci + kPickRCap;
+            uint32_t* s_rmn = s_rmo + kPickRCap;
+            // centroid columns of R, kPickCols at a time into a double buffer (cp.async)
+            const uint32_t nb = (nr + kPickCols - 1) / kPickCols;
+            auto issue = [&](uint32_t b) {
+                const uint32_t b0 = b * kPickCols, cnt = min(kPickCols, nr - b0);
+                float4* dst = s_col + (size_t)(b % kPickBufs) * kPickCols * (D / 4);
                 for (uint32_t x = tid; x < cnt * (D / 4); x += blockDim.x) {
                     const uint32_t i = s_r[b0 + x / (D / 4)], jq = x % (D / 4);
                     uint32_t k = 0;
@@ -878,29 +925,43 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                     const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k];
                     const float4* src = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local + (size_t)jq * nu;
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
-                                     (uint32_t)__cvta_generic_to_shared(&s_col[x / (D / 4)][jq])),
+                                     (uint32_t)__cvta_generic_to_shared(dst + x)),
                                  "l"(src));
                 }
                 asm volatile("cp.async.commit_group;\n" ::);
-                asm volatile("cp.async.wait_group 0;\n" ::);
+            };
+            issue(0);
+            if (nb > 1) issue(1);
+            // every per-cluster field R needs, in one round of independent loads
+            for (uint32_t r = tid; r < nr; r += blockDim.x) {
+                const uint32_t i = s_r[r], ci = cand(i);
+                s_rci[r] = ci;
+                s_ro[r] = fo[ci];
+                s_rw[r] = sg[i];
+                s_rf[r] = a.frad[(size_t)slot * a.cap_clusters + ci];
+                s_rmo[r] = moff_g[ci];
+                s_rmn[r] = moff_g[ci + 1];
+            }
+            for (uint32_t b = 0; b < nb; ++b) {
+                if (b + 1 < nb) asm volatile("cp.async.wait_group 1;\n" ::);
+                else asm volatile("cp.async.wait_group 0;\n" ::);
                 __syncthreads();
+                const uint32_t b0 = b * kPickCols, cnt = min(kPickCols, nr - b0);
                 if (tid < cnt) {
-                    const uint32_t i = s_r[b0 + tid];
-                    uint32_t k = 0;
-                    while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
-                    const uint32_t ci = s_gbase[k] + (i - s_gpre[k]);
+                    const float4* col = s_col + ((size_t)(b % kPickBufs) * kPickCols + tid) * (D / 4);
                     double sacc = 0.0;
 #pragma unroll 8
                     for (uint32_t jq = 0; jq < D / 4; ++jq) {
-                        const float4 v = s_col[tid][jq];
+                        const float4 v = col[jq];
                         sacc = __fma_rn(s_qd[4 * jq + 0], (double)v.x, sacc);
                         sacc = __fma_rn(s_qd[4 * jq + 1], (double)v.y, sacc);
                         sacc = __fma_rn(s_qd[4 * jq + 2], (double)v.z, sacc);
                         sacc = __fma_rn(s_qd[4 * jq + 3], (double)v.w, sacc);
                     }
-                    s_rk[b0 + tid] = desc_key(__dadd_rn(sacc, __dmul_rn(qn, a.frad[(size_t)slot * a.cap_clusters + ci])));
+                    s_rk[b0 + tid] = desc_key(__dadd_rn(sacc, __dmul_rn(qn, s_rf[b0 + tid])));
                 }
-                __syncthreads();
+                __syncthreads();  // the buffer is free again
+                if (b + 2 < nb) issue(b + 2);
             }
             for (uint32_t r = tid; r < nr; r += blockDim.x) {
                 const unsigned long long kr = s_rk[r];
@@ -911,7 +972,6 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                     rank += (ky < kr || (ky == kr && s_ro[y] < orr)) ? 1u : 0u;
                 }
                 s_ri[rank] = r;
-                kg[s_r[r]] = kr;  // exact key for the rank phase below
             }
             __syncthreads();
             if (warp == 0) {  // walk the ranks: running weight, first overflow ends the prefix
@@ -935,8 +995,6 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                 }
                 if (lane == 0) s_nsel = nsel;
             }
-            __syncthreads();
-            for (uint32_t x = tid; x < s_nsel; x += blockDim.x) sg[x] = s_r[s_ri[x]];
             if (tid == 0) s_fast = 1;
         } else {
             if (tid == 0) s_fast = 0;
@@ -1019,7 +1077,8 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     LC_PMARK(3)
     // rank order (select_topk order) + cluster bitmap + member chunks
     const uint32_t nsel = s_nsel;
-    const bool staged = nsel <= kStage;
+    const bool fast = s_fast != 0;  // R's arrays (rank order, ids, member ranges) are still in s_ph
+    const bool staged = !fast && nsel <= kStage;
     if (staged) {
         for (uint32_t x = tid; x < nsel; x += blockDim.x) {
             const uint32_t i = sg[x], ci = cand(i);
@@ -1033,8 +1092,29 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     uint32_t* gbits = a.sel_bits + ((size_t)slot * G + g) * bit_words(a.cap_clusters);
     for (uint32_t w = tid; w < bit_words(L); w += blockDim.x) gbits[w] = 0u;
     __syncthreads();
-    const uint32_t* moff = a.fmem_off + (size_t)slot * (a.cap_clusters + 1);
+    const uint32_t* moff = moff_g;
     const uint32_t* mem = a.fmem + (size_t)slot * a.cap_chunks;
+    if (fast) {
+        // the walk's rank order is select_topk's order; one warp per cluster
+        // spreads its member chunks over the lanes
+        const unsigned long long* s_rk = reinterpret_cast<const unsigned long long*>(s_ph + kPickBufs * kPickCols * D * 4);
+        const uint32_t* s_ro = reinterpret_cast<const uint32_t*>(s_rk + 2 * kPickRCap);
+        const uint32_t* s_ri = s_ro + 2 * kPickRCap;
+        const uint32_t* s_rci = s_ri + kPickRCap;
+        const uint32_t* s_rmo = s_rci + kPickRCap;
+        const uint32_t* s_rmn = s_rmo + kPickRCap;
+        for (uint32_t x = warp; x < nsel; x += kPqWarps) {
+            const uint32_t r = s_ri[x], ci = s_rci[r];
+            if (lane == 0) {
+                out_cl[x] = s_ro[r];
+                atomicOr(&gbits[ci >> 5], 1u << (ci & 31));
+            }
+            for (uint32_t t = s_rmo[r] + lane; t < s_rmn[r]; t += 32) {
+                const uint32_t j = mem[t];
+                atomicOr(&cb[j >> 5], 1u << (j & 31));
+            }
+        }
+    } else
     for (uint32_t x = tid; x < nsel; x += blockDim.x) {
         unsigned long long ki;
         uint32_t ci, oi, rank = 0;
@@ -1397,7 +1477,8 @@ size_t select3_pick_smem(const Arena& a);
 template <int D, int GQ>
 static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t max_union, uint32_t pmax,
                               cudaStream_t stream) {
-    const size_t co_smem = (size_t)GQ * D * 8 + (size_t)D * ((pmax + 3) & ~3u) * 4 + (size_t)GQ * pmax * 8;
+    const size_t co_smem = (size_t)GQ * D * 8 + (size_t)D * ((pmax + 3) & ~3u) * 4 + (size_t)GQ * pmax * 8 +
+                           (size_t)pmax * 16 + 4;  // urad, unit_off, union mask
     const size_t pk_smem = select3_pick_smem(p.a);
     static size_t co_cfg = 0, pk_cfg = 0;
     if (co_smem > co_cfg) {
