@@ -873,6 +873,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
         __syncthreads();
         const uint32_t nr = s_rn;
         if (p.prof && tid == 0) p.prof[((size_t)slot * GQ + blockIdx.x) * 8 + 7] = nr | ((unsigned long long)nc << 32);
+        LC_PMARK(6)
         const float* fcs = a.fcent + (size_t)slot * a.cap_clusters * D;
         const double qn = pv.qnorm()[g];
         auto exact_key = [&](uint32_t i) -> unsigned long long {
@@ -914,24 +915,28 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             uint32_t* s_rmo = s_rci + kPickRCap;
             uint32_t* s_rmn = s_rmo + kPickRCap;
             // centroid columns of R, kPickCols at a time into a double buffer (cp.async)
-            const uint32_t nb = (nr + kPickCols - 1) / kPickCols;
-            auto issue = [&](uint32_t b) {
-                const uint32_t b0 = b * kPickCols, cnt = min(kPickCols, nr - b0);
-                float4* dst = s_col + (size_t)(b % kPickBufs) * kPickCols * (D / 4);
-                for (uint32_t x = tid; x < cnt * (D / 4); x += blockDim.x) {
-                    const uint32_t i = s_r[b0 + x / (D / 4)], jq = x % (D / 4);
+            // centroid columns of R by cp.async into column slots: the static
+            // buffer, plus the staged keys / weights region once R's own fields
+            // are read (nothing after this point reads it) -- usually all of R
+            // in one round
+            const uint32_t nst = kPickBufs * kPickCols;
+            const uint32_t nslots = nst + (uint32_t)((p.keys_cap * 12u) / (D * 4u));
+            auto slot_col = [&](uint32_t k) -> float4* {
+                return k < nst ? s_col + (size_t)k * (D / 4) : reinterpret_cast<float4*>(qsm) + (size_t)(k - nst) * (D / 4);
+            };
+            auto issue = [&](uint32_t r0, uint32_t r1, uint32_t k0) {  // R entries [r0, r1) into slots k0..
+                for (uint32_t x = tid; x < (r1 - r0) * (D / 4); x += blockDim.x) {
+                    const uint32_t i = s_r[r0 + x / (D / 4)], jq = x % (D / 4);
                     uint32_t k = 0;
                     while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
                     const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k];
                     const float4* src = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local + (size_t)jq * nu;
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
-                                     (uint32_t)__cvta_generic_to_shared(dst + x)),
+                                     (uint32_t)__cvta_generic_to_shared(slot_col(k0 + x / (D / 4)) + jq)),
                                  "l"(src));
                 }
-                asm volatile("cp.async.commit_group;\n" ::);
             };
-            issue(0);
-            if (nb > 1) issue(1);
+            issue(0, min(nr, nst), 0);
             // every per-cluster field R needs, in one round of independent loads
             for (uint32_t r = tid; r < nr; r += blockDim.x) {
                 const uint32_t i = s_r[r], ci = cand(i);
@@ -942,13 +947,19 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                 s_rmo[r] = moff_g[ci];
                 s_rmn[r] = moff_g[ci + 1];
             }
-            for (uint32_t b = 0; b < nb; ++b) {
-                if (b + 1 < nb) asm volatile("cp.async.wait_group 1;\n" ::);
-                else asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();  // the keys / weights region is free
+            if (nr > nst) issue(nst, min(nr, nslots), nst);
+            asm volatile("cp.async.commit_group;\n" ::);
+            for (uint32_t base = 0; base < nr; base += nslots) {
+                if (base > 0) {
+                    issue(base, min(nr, base + nslots), 0);
+                    asm volatile("cp.async.commit_group;\n" ::);
+                }
+                asm volatile("cp.async.wait_group 0;\n" ::);
                 __syncthreads();
-                const uint32_t b0 = b * kPickCols, cnt = min(kPickCols, nr - b0);
-                if (tid < cnt) {
-                    const float4* col = s_col + ((size_t)(b % kPickBufs) * kPickCols + tid) * (D / 4);
+                const uint32_t cnt = min(nslots, nr - base);
+                for (uint32_t t = tid; t < cnt; t += blockDim.x) {
+                    const float4* col = slot_col(t);
                     double sacc = 0.0;
 #pragma unroll 8
                     for (uint32_t jq = 0; jq < D / 4; ++jq) {
@@ -958,10 +969,9 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                         sacc = __fma_rn(s_qd[4 * jq + 2], (double)v.z, sacc);
                         sacc = __fma_rn(s_qd[4 * jq + 3], (double)v.w, sacc);
                     }
-                    s_rk[b0 + tid] = desc_key(__dadd_rn(sacc, __dmul_rn(qn, s_rf[b0 + tid])));
+                    s_rk[base + t] = desc_key(__dadd_rn(sacc, __dmul_rn(qn, s_rf[base + t])));
                 }
-                __syncthreads();  // the buffer is free again
-                if (b + 2 < nb) issue(b + 2);
+                __syncthreads();  // the slots are free again
             }
             for (uint32_t r = tid; r < nr; r += blockDim.x) {
                 const unsigned long long kr = s_rk[r];
@@ -1171,6 +1181,9 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
 // active spans in chunk order with per-head
 // masks (collect_active, retriever.cpp:60-74), sink and buffer spans, counts.
 constexpr int kSpMaxWarps = 8;
+constexpr int kSpThreads = 256;
+constexpr int kSpThreadsMax = kSpThreads;
+constexpr uint32_t kSpCache = 1024;  // chunk spans kept in shared memory for the row-list pass
 
 template <typename T>
 __device__ __forceinline__ T sp_scan(T v, T* wt, T& total) {
@@ -1244,6 +1257,8 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
     }
     __shared__ unsigned long long wtot[kSpMaxWarps];
     __shared__ uint32_t s_cnt[GQ], s_nsp[GQ], s_err;
+    __shared__ uint32_t s_sst[kSpCache], s_slm[kSpCache], s_soff[kSpCache];
+    __shared__ uint32_t s_bnd[33][kSpThreadsMax];  // each thread's word: its chunks' bounds
     if (tid < G) {
         s_cnt[tid] = 0;
         s_nsp[tid] = 0;
@@ -1289,31 +1304,34 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
             wg[g] = w < mw ? __ldcg(cbg + g * mwcap + w) : 0u;
             any |= wg[g];
         }
-        // the bounds of the word's set chunks: one batch of independent loads
-        uint32_t bnd[33];
+        // the bounds of the word's set chunks: one batch of independent loads,
+        // parked in the thread's own shared column so the loops below visit
+        // only the set bits
+        {
+            uint32_t bnd[33];
 #pragma unroll
-        for (int b = 0; b <= 32; ++b) {
-            const bool need = (b < 32 && ((any >> b) & 1u)) || (b > 0 && ((any >> (b - 1)) & 1u));
-            bnd[b] = need ? __ldg(cs + w * 32 + b) : 0u;
+            for (int b = 0; b <= 32; ++b) {
+                const bool need = (b < 32 && ((any >> b) & 1u)) || (b > 0 && ((any >> (b - 1)) & 1u));
+                bnd[b] = need ? __ldg(cs + w * 32 + b) : 0u;
+            }
+#pragma unroll
+            for (int b = 0; b <= 32; ++b) s_bnd[b][tid] = bnd[b];
         }
         uint32_t cnt = 0, toks = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            if ((any >> b) & 1u) {
-                const uint32_t s0 = max(bnd[b], sink_end), e0 = bnd[b + 1];
-                if (s0 < e0) {
-                    ++cnt;
-                    toks += e0 - s0;
-                }
+        for (uint32_t bits = any; bits; bits &= bits - 1u) {
+            const uint32_t b = __ffs(bits) - 1;
+            const uint32_t s0 = max(s_bnd[b][tid], sink_end), e0 = s_bnd[b + 1][tid];
+            if (s0 < e0) {
+                ++cnt;
+                toks += e0 - s0;
             }
         }
         unsigned long long total;
         const unsigned long long ex = sp_scan<unsigned long long>(((unsigned long long)cnt << 40) | toks, wtot, total);
         uint32_t pos = out + (uint32_t)(ex >> 40), tp = tok + (uint32_t)(ex & 0xffffffffffull);
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            if (!((any >> b) & 1u)) continue;
-            const uint32_t s0 = max(bnd[b], sink_end), e0 = bnd[b + 1];
+        for (uint32_t bits = any; bits; bits &= bits - 1u) {
+            const uint32_t b = __ffs(bits) - 1;
+            const uint32_t s0 = max(s_bnd[b][tid], sink_end), e0 = s_bnd[b + 1][tid];
             if (s0 >= e0) continue;
             uint32_t m = 0;
 #pragma unroll
@@ -1327,6 +1345,11 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
                 sp[pos].start = s0;
                 sp[pos].len_mask = ((e0 - s0) << 8) | m;
                 so[pos] = tp;
+            }
+            if (pos < kSpCache) {
+                s_sst[pos] = s0;
+                s_slm[pos] = ((e0 - s0) << 8) | m;
+                s_soff[pos] = tp;
             }
             ++pos;
             tp += e0 - s0;
@@ -1346,33 +1369,21 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
     const uint32_t n_chunk_spans = out - (sink_end > 0 ? 1u : 0u);
     __syncthreads();
     LC_SMARK(2)
-    {  // row list of the chunk spans: one warp per 32 spans, coalesced row writes
-        const uint32_t first = sink_end > 0 ? 1u : 0u, warp = tid >> 5;
-        for (uint32_t k0 = first + warp * 32; k0 < out; k0 += kSpWarps * 32) {
-            const uint32_t k = k0 + lane;
-            uint32_t st = 0, lm = 0, off = 0;
-            if (k < out) {
+    {  // row list of the chunk spans: one thread per span writes its rows
+        const uint32_t first = sink_end > 0 ? 1u : 0u, lim = min(out, a.cap_spans);
+        for (uint32_t k = first + tid; k < lim; k += blockDim.x) {
+            uint32_t st, lm, off;
+            if (k < kSpCache) {
+                st = s_sst[k];
+                lm = s_slm[k];
+                off = s_soff[k];
+            } else {
                 st = sp[k].start;
                 lm = sp[k].len_mask;
                 off = so[k];
             }
-            const uint32_t nk = min(32u, out - k0);
-            // the batch's tokens [t0, t1), one per lane: each store is a full line
-            const uint32_t t0 = __shfl_sync(0xffffffffu, off, 0);
-            const uint32_t t1 = __shfl_sync(0xffffffffu, off + (lm >> 8), nk - 1);
-            for (uint32_t qb = t0; qb < t1; qb += 32) {  // warp-uniform trip count
-                const uint32_t q = qb + lane;
-                uint32_t j = 0;  // last span of the batch with off <= q
-#pragma unroll
-                for (uint32_t step = 16; step >= 1; step >>= 1) {
-                    const uint32_t c = j + step;
-                    const uint32_t oc = __shfl_sync(0xffffffffu, off, c < nk ? c : nk - 1);
-                    if (c < nk && oc <= q) j = c;
-                }
-                const uint32_t sj = __shfl_sync(0xffffffffu, st, j), lj = __shfl_sync(0xffffffffu, lm, j);
-                const uint32_t oj = __shfl_sync(0xffffffffu, off, j);
-                if (q < t1) rows[q] = (sj + (q - oj)) | ((lj & 0xffu) << 24);
-            }
+            const uint32_t len = lm >> 8, hm = (lm & 0xffu) << 24;
+            for (uint32_t t = 0; t < len; ++t) rows[off + t] = (st + t) | hm;
         }
     }
     LC_SMARK(3)
@@ -1464,7 +1475,6 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
     pick_head<DQ, GQ>(p);
 }
 
-constexpr int kSpThreads = 256;
 template <int GQ>
 __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     pdl_wait();
@@ -1574,7 +1584,10 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
             rs += (double)(t[r * 8 + 7] & 0xffffffffull);
             ncs += (double)(t[r * 8 + 7] >> 32);
         }
-        fprintf(stderr, "[LC_PROF] k_pickq refine set %.1f of %.1f candidates per head\n", rs / nq, ncs / nq);
+        double pre = 0;
+        for (size_t r = (size_t)a.slot0 * a.G; r < (size_t)(a.slot0 + n_slots) * a.G; ++r) pre += (double)(t[r * 8 + 6] - t[r * 8 + 2]);
+        fprintf(stderr, "[LC_PROF] k_pickq refine set %.1f of %.1f candidates per head; x + R list %.2f us of refine\n", rs / nq,
+                ncs / nq, pre / nq / 1e3);
         {
             std::vector<unsigned long long> u((size_t)a.n_slots * 8);
             cudaMemcpy(u.data(), prof_sp, u.size() * 8, cudaMemcpyDeviceToHost);
