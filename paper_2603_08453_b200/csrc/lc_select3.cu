@@ -66,7 +66,7 @@ constexpr uint32_t kPickStage = 256;  // rank-phase staging entries
 // phases of the kernel and share one static buffer.
 template <int DQ>
 struct PickPhase {
-    static constexpr uint32_t refine = kPickBufs * kPickCols * DQ * 4 + kPickRCap * (8 + 8 + 6 * 4);
+    static constexpr uint32_t refine = kPickBufs * kPickCols * (DQ + 4) * 4 + kPickRCap * (8 + 8 + 6 * 4);
     static constexpr uint32_t stage = kPickStage * 16, hist = 2 * 256 * 4;
     static constexpr uint32_t bytes =
         refine > stage ? (refine > hist ? refine : hist) : (stage > hist ? stage : hist);
@@ -647,6 +647,8 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     unsigned long long* s_sk = reinterpret_cast<unsigned long long*>(s_ph);
     uint32_t* s_sc = reinterpret_cast<uint32_t*>(s_ph + kStage * 8);
     uint32_t* s_so = reinterpret_cast<uint32_t*>(s_ph + kStage * 12);
+    __shared__ double s_qd[DQ];  // q (f64) for the refinement's exact chains
+    for (uint32_t j = tid; j < D; j += blockDim.x) s_qd[j] = (double)p.q[((size_t)slot * G + g) * D + j];
     for (uint32_t w = tid; w < mw; w += blockDim.x) cb[w] = 0u;
     if (warp == 0) {  // this head's kept units, in union order (ballot compaction)
         const uint32_t nuu = pv.hdr()[1];
@@ -699,6 +701,18 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                              (size_t)g * p.qcap;
     uint32_t* sg = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(
                        p.scratch + (size_t)slot * G * p.qcap * kScratchEntry) + (size_t)G * p.qcap) + (size_t)g * p.qcap;
+    // the filter's upper bounds, requested now: the refinement reads them after the select
+    const double* hg = reinterpret_cast<const double*>(
+                           p.scratch + (size_t)slot * G * p.qcap * kScratchEntry + (size_t)G * p.qcap * 12) +
+                       (size_t)g * p.qcap;
+    constexpr int kHPre = 8;
+    const bool hpre_ok = nc <= kHPre * kPqThreads;
+    double hpre[kHPre];
+#pragma unroll
+    for (int t = 0; t < kHPre; ++t) {
+        const uint32_t i = t * kPqThreads + tid;
+        hpre[t] = hpre_ok && i < nc ? hg[i] : -INFINITY;
+    }
     if (nc <= p.keys_cap) {  // stage keys and weights (all loads in flight at once)
         for (uint32_t b0 = 0; b0 < nc; b0 += 8 * kPqThreads) {
             unsigned long long kv[8];
@@ -829,7 +843,6 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     __shared__ uint32_t s_fast;
     {
         __shared__ unsigned long long s_xkey, s_rmin, s_rmax;
-        __shared__ double s_qd[DQ];
         __shared__ uint32_t s_rn;
         __shared__ uint32_t s_r[kPickRCap];
         if (tid == 0) {
@@ -838,7 +851,6 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             s_rmax = 0ull;
             s_rn = 0;
         }
-        for (uint32_t j = tid; j < D; j += blockDim.x) s_qd[j] = (double)p.q[((size_t)slot * G + g) * D + j];
         __syncthreads();
         const bool all = s_state == 2;
         if (!all) {
@@ -850,23 +862,34 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
         }
         __syncthreads();
         const double x = all ? -INFINITY : key_score(s_xkey);
-        const double* hg = reinterpret_cast<const double*>(
-                               p.scratch + (size_t)slot * G * p.qcap * kScratchEntry + (size_t)G * p.qcap * 12) +
-                           (size_t)g * p.qcap;
+        // R's arrays (fast path) follow the column slots in the phase buffer;
+        // R's weights are read here, while the staged weights are live
+        float4* s_col = reinterpret_cast<float4*>(s_ph);  // [kPickBufs * kPickCols][D / 4 + 1]
+        unsigned long long* s_rk = reinterpret_cast<unsigned long long*>(s_ph + kPickBufs * kPickCols * (D + 4) * 4);
+        double* s_rf = reinterpret_cast<double*>(s_rk + kPickRCap);
+        uint32_t* s_ro = reinterpret_cast<uint32_t*>(s_rf + kPickRCap);
+        uint32_t* s_rw = s_ro + kPickRCap;
+        uint32_t* s_ri = s_rw + kPickRCap;
+        uint32_t* s_rci = s_ri + kPickRCap;
+        uint32_t* s_rmo = s_rci + kPickRCap;
+        uint32_t* s_rmn = s_rmo + kPickRCap;
         // R as a list (ascending i) when it fits, else handled in place
         for (uint32_t b0 = 0; b0 < nc; b0 += 8 * kPqThreads) {  // eight loads in flight per thread
             double hv[8];
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const uint32_t i = b0 + t * kPqThreads + tid;
-                hv[t] = i < nc ? hg[i] : -INFINITY;
+                hv[t] = hpre_ok ? hpre[t] : (i < nc ? hg[i] : -INFINITY);
             }
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const uint32_t i = b0 + t * kPqThreads + tid;
                 if (i < nc && (all || hv[t] >= x)) {
                     const uint32_t at = atomicAdd(&s_rn, 1u);
-                    if (at < kPickRCap) s_r[at] = i;
+                    if (at < kPickRCap) {
+                        s_r[at] = i;
+                        s_rw[at] = sg[i];
+                    }
                 }
             }
         }
@@ -905,24 +928,16 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             // reference id asc) -- select_topk's order (retriever.cpp:27-39) --
             // and admit the rank prefix while the running weight stays within
             // the budget, the first cluster unconditionally (retriever.cpp:142-154).
-            float4* s_col = reinterpret_cast<float4*>(s_ph);  // [kPickBufs * kPickCols][D / 4]
-            unsigned long long* s_rk = reinterpret_cast<unsigned long long*>(s_ph + kPickBufs * kPickCols * D * 4);
-            double* s_rf = reinterpret_cast<double*>(s_rk + kPickRCap);
-            uint32_t* s_ro = reinterpret_cast<uint32_t*>(s_rf + kPickRCap);
-            uint32_t* s_rw = s_ro + kPickRCap;
-            uint32_t* s_ri = s_rw + kPickRCap;
-            uint32_t* s_rci = s_ri + kPickRCap;
-            uint32_t* s_rmo = s_rci + kPickRCap;
-            uint32_t* s_rmn = s_rmo + kPickRCap;
-            // centroid columns of R, kPickCols at a time into a double buffer (cp.async)
             // centroid columns of R by cp.async into column slots: the static
             // buffer, plus the staged keys / weights region once R's own fields
             // are read (nothing after this point reads it) -- usually all of R
             // in one round
+            // (slots are D/4 + 1 float4s apart: the chains' column reads spread over the banks)
             const uint32_t nst = kPickBufs * kPickCols;
-            const uint32_t nslots = nst + (uint32_t)((p.keys_cap * 12u) / (D * 4u));
+            const uint32_t nslots = nst + (uint32_t)((p.keys_cap * 12u) / (D * 4u + 16u));
             auto slot_col = [&](uint32_t k) -> float4* {
-                return k < nst ? s_col + (size_t)k * (D / 4) : reinterpret_cast<float4*>(qsm) + (size_t)(k - nst) * (D / 4);
+                return k < nst ? s_col + (size_t)k * (D / 4 + 1)
+                               : reinterpret_cast<float4*>(qsm) + (size_t)(k - nst) * (D / 4 + 1);
             };
             auto issue = [&](uint32_t r0, uint32_t r1, uint32_t k0) {  // R entries [r0, r1) into slots k0..
                 for (uint32_t x = tid; x < (r1 - r0) * (D / 4); x += blockDim.x) {
@@ -936,20 +951,17 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                                  "l"(src));
                 }
             };
-            issue(0, min(nr, nst), 0);
-            // every per-cluster field R needs, in one round of independent loads
+            issue(0, min(nr, nslots), 0);  // the keys / weights region is dead: R's weights are in s_rw
+            asm volatile("cp.async.commit_group;\n" ::);
+            // every other per-cluster field R needs, in one round of independent loads
             for (uint32_t r = tid; r < nr; r += blockDim.x) {
                 const uint32_t i = s_r[r], ci = cand(i);
                 s_rci[r] = ci;
                 s_ro[r] = fo[ci];
-                s_rw[r] = sg[i];
                 s_rf[r] = a.frad[(size_t)slot * a.cap_clusters + ci];
                 s_rmo[r] = moff_g[ci];
                 s_rmn[r] = moff_g[ci + 1];
             }
-            __syncthreads();  // the keys / weights region is free
-            if (nr > nst) issue(nst, min(nr, nslots), nst);
-            asm volatile("cp.async.commit_group;\n" ::);
             for (uint32_t base = 0; base < nr; base += nslots) {
                 if (base > 0) {
                     issue(base, min(nr, base + nslots), 0);
@@ -1107,7 +1119,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     if (fast) {
         // the walk's rank order is select_topk's order; one warp per cluster
         // spreads its member chunks over the lanes
-        const unsigned long long* s_rk = reinterpret_cast<const unsigned long long*>(s_ph + kPickBufs * kPickCols * D * 4);
+        const unsigned long long* s_rk = reinterpret_cast<const unsigned long long*>(s_ph + kPickBufs * kPickCols * (D + 4) * 4);
         const uint32_t* s_ro = reinterpret_cast<const uint32_t*>(s_rk + 2 * kPickRCap);
         const uint32_t* s_ri = s_ro + 2 * kPickRCap;
         const uint32_t* s_rci = s_ri + kPickRCap;
