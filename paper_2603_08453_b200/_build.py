@@ -19,6 +19,7 @@ CPP_SOURCES = ["lc_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ccbin", "/usr/bin/g++",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("LC_NVCC_EXTRA", "").split()  # experiment switches (e.g. -DLC_FINE_CPASYNC)
 
 
 def _deps():

@@ -204,14 +204,19 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
                 ++nmem[f];
             }
         std::vector<float> fcent((size_t)L * D), ucent((size_t)a.cap_units * D, 0.f);
+        std::vector<__half> f16((size_t)L * D);  // k_fine's filter copy; its error bound needs |c| <= 6e4
         std::vector<double> frad(L), urad(P);
         std::vector<uint32_t> ftok(L), fn(L), fu(L);
         for (uint32_t u = 0; u < P; ++u) {
             const uint32_t base = unit_off[u], nu = unit_off[u + 1] - base;
             for (uint32_t i = 0; i < nu; ++i) {
                 const uint32_t f = orig[base + i];
-                for (uint32_t j = 0; j < D; ++j)
-                    fcent[fine_at(base, nu, i, j, D)] = ix->fine_centroid[(size_t)f * D + j];
+                for (uint32_t j = 0; j < D; ++j) {
+                    const float c = ix->fine_centroid[(size_t)f * D + j];
+                    if (!(std::fabs(c) <= 60000.f)) fail(LC_EINVAL, "fine centroids must be finite and |c| <= 6e4");
+                    fcent[fine_at(base, nu, i, j, D)] = c;
+                    f16[fine_at16(base, nu, i, j, D)] = __float2half_rn(c);
+                }
             }
             for (uint32_t j = 0; j < D; ++j) ucent[(size_t)j * a.cap_units + u] = ix->coarse_centroid[(size_t)u * D + j];
             urad[u] = ix->coarse_radius[u];
@@ -250,14 +255,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         up(a.urad + so * a.cap_units, urad.data(), urad.size() * 8);
         up(a.unit_off + so * (a.cap_units + 1), unit_off.data(), unit_off.size() * 4);
         up(a.fcent + so * a.cap_clusters * D, fcent.data(), fcent.size() * 4);
-        {  // fp16 copy for k_fine's filter; its error bound needs finite centroids inside fp16 range
-            std::vector<__half> f16(fcent.size());
-            for (size_t x = 0; x < fcent.size(); ++x) {
-                if (!(std::fabs(fcent[x]) <= 60000.f)) fail(LC_EINVAL, "fine centroids must be finite and |c| <= 6e4");
-                f16[x] = __float2half_rn(fcent[x]);
-            }
-            up(a.fcent16 + so * a.cap_clusters * D, f16.data(), f16.size() * 2);
-        }
+        up(a.fcent16 + so * a.cap_clusters * D, f16.data(), f16.size() * 2);
         up(a.frad + so * a.cap_clusters, frad.data(), frad.size() * 8);
         up(a.ftok + so * a.cap_clusters, ftok.data(), ftok.size() * 4);
         up(a.forig + so * a.cap_clusters, orig.data(), orig.size() * 4);

@@ -135,6 +135,12 @@ __host__ __device__ inline size_t fine_at(uint32_t base, uint32_t nu, uint32_t l
     return (size_t)base * d + ((size_t)(j >> 2) * nu + local) * 4 + (j & 3);
 }
 
+// the same element in the fp16 copy, octet-major ([d/8][nu][8] per unit
+// block): one 16-byte load per lane per row in k_fine
+__host__ __device__ inline size_t fine_at16(uint32_t base, uint32_t nu, uint32_t local, uint32_t j, uint32_t d) {
+    return (size_t)base * d + ((size_t)(j >> 3) * nu + local) * 8 + (j & 7);
+}
+
 __host__ __device__ inline size_t kv_off(const Arena& a, uint32_t slot) {
     return (size_t)slot * a.cap_tokens * a.d;
 }

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     __half* fcw16 = a.fcent16 + (size_t)slot * a.cap_clusters * d;
     for (uint32_t j = tid; j < d; j += blockDim.x) {
         fcw[fine_at(lo, nu, local, j, d)] = s_new[j];
-        fcw16[fine_at(lo, nu, local, j, d)] = __float2half_rn(s_new[j]);
+        fcw16[fine_at16(lo, nu, local, j, d)] = __float2half_rn(s_new[j]);
     }
     const uint32_t cid = M;
     if (a.keep_reps) {

@@ -486,13 +486,13 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
         sa = stage_a(next_tile());
         while (d.slot != ~0u) {
             // (C) this tile's centroids, radius and weight: one burst of loads
-            // fp16 centroid rows (4 dims = 8 bytes per lane per row)
-            const uint2* col = reinterpret_cast<const uint2*>(a.fcent16 + (size_t)d.slot * a.cap_clusters * D +
+            // fp16 centroid rows (8 dims = 16 bytes per lane per row, fine_at16)
+            const uint4* col = reinterpret_cast<const uint4*>(a.fcent16 + (size_t)d.slot * a.cap_clusters * D +
                                                              (size_t)d.base * D) + d.local;
-            uint2 v16[V];
+            uint4 v16[V / 2];
             if (d.valid) {
 #pragma unroll
-                for (uint32_t j = 0; j < V; ++j) v16[j] = __ldg(col + (size_t)j * d.nu);
+                for (uint32_t j = 0; j < V / 2; ++j) v16[j] = __ldg(col + (size_t)j * d.nu);
             }
             const uint32_t cid = d.base + d.local;
             const double r = d.valid ? __ldg(a.frad + (size_t)d.slot * a.cap_clusters + cid) : 0.0;
@@ -511,8 +511,9 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 for (int t = 0; t < 4; ++t) s4[g][t] = 0.f;
 #pragma unroll
             for (uint32_t j = 0; j < V; ++j) {
-                const float2 lo2 = __half22float2(*reinterpret_cast<const __half2*>(&v16[j].x));
-                const float2 hi2 = __half22float2(*reinterpret_cast<const __half2*>(&v16[j].y));
+                const uint32_t w0 = (j & 1) ? v16[j >> 1].z : v16[j >> 1].x, w1 = (j & 1) ? v16[j >> 1].w : v16[j >> 1].y;
+                const float2 lo2 = __half22float2(*reinterpret_cast<const __half2*>(&w0));
+                const float2 hi2 = __half22float2(*reinterpret_cast<const __half2*>(&w1));
                 const float4 vj = make_float4(lo2.x, lo2.y, hi2.x, hi2.y);
                 c2[0] = fmaf(vj.x, vj.x, c2[0]);  // ||c~||^2, shared by every head
                 c2[1] = fmaf(vj.y, vj.y, c2[1]);
@@ -674,7 +675,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
         const unsigned long long mn = pv.kmin()[g], mx = pv.kmax()[g];
         const unsigned long long diff = mn ^ mx;
         const int top = diff ? 63 - __clzll((long long)diff) : 0;
-        const int shift = (top / 8) * 8;
+        const int shift = top >= 7 ? top - 7 : 0;  // first digit: the 8 highest differing bits
         const unsigned long long mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
         s_prefix = mn & mask;
         s_mask = mask;
@@ -752,7 +753,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     // the first key (ascending = descending score) at which the running weight
     // exceeds the budget.  Keys ~0 (candidates ruled out by the filter) are skipped.
     auto radix_select = [&]() {
-    for (int shift = s_shift; shift >= 0; shift -= 8) {
+    for (int shift = s_shift; shift >= 0; shift = shift >= 8 ? shift - 8 : (shift > 0 ? 0 : -1)) {
         for (uint32_t b = tid; b < 256; b += blockDim.x) {
             hw[b] = 0;
             hc[b] = 0;
@@ -1039,7 +1040,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             const unsigned long long mn = s_rmin, mx = s_rmax;
             const unsigned long long diff = mn ^ mx;
             const int top = diff ? 63 - __clzll((long long)diff) : 0;
-            const int shift = (top / 8) * 8;
+            const int shift = top >= 7 ? top - 7 : 0;  // first digit: the 8 highest differing bits
             const unsigned long long mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
             s_prefix = mn & mask;
             s_mask = mask;
