@@ -453,7 +453,7 @@ static void ensure_streams(lc_index_t h, uint32_t groups) {
 
 static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
                           const uint32_t* buf_off, const uint32_t* buf_ids, float* out_dev,
-                          cudaStream_t st) {
+                          cudaStream_t st, const float* q_in = nullptr) {
     validate_budgets(b);
     if (!q_dev) fail(LC_EINVAL, "null q");
     if (flags > 2) fail(LC_EINVAL, "bad buffer flags");
@@ -482,7 +482,8 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     // one persistent k_attend over every slot (its grid barrier needs the whole GPU)
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs, uint32_t gi) {
         ck(launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, flags,
-                          buf_off, buf_ids, h->sel_scratch, a.max_cand, max_union, pmax, count, h->fine_ctr + 4 * gi, gs),
+                          buf_off, buf_ids, h->sel_scratch, a.max_cand, max_union, pmax, count, h->fine_ctr + 4 * gi, gs,
+                          q_in),
            "k_select3");
     };
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
@@ -661,19 +662,35 @@ int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uin
         }
         ck(cudaEventRecord(h->host_event, st), "order after caller");
         ck(cudaStreamWaitEvent(h->host_stream, h->host_event, 0), "order after caller");
-        ck(cudaMemcpyAsync(h->q_stage, q_host, bytes, cudaMemcpyHostToDevice, h->host_stream), "q H2D");
+        // page-locked, device-mapped host buffers (cudaHostAlloc / torch pin_memory):
+        // k_coarse reads q straight from host memory and k_attend writes the
+        // outputs straight into it, so no copy-engine transfer sits between the
+        // call and the kernels; other host memory goes through the staging copies
+        auto mapped = [](const void* ptr) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            return at.type == cudaMemoryTypeHost && at.devicePointer == ptr && !getenv("LC_HOST_STAGED");
+        };
+        const bool zc = mapped(q_host) && mapped(out_host);
+        if (!zc) ck(cudaMemcpyAsync(h->q_stage, q_host, bytes, cudaMemcpyHostToDevice, h->host_stream), "q H2D");
+        const float* q_in = zc ? q_host : nullptr;
+        float* out_k = zc ? out_host : h->out_stage;
         const bool same = h->host_exec && h->host_version == h->version && h->host_flags == flags &&
-                          std::memcmp(&h->host_budgets, b, sizeof *b) == 0;
+                          std::memcmp(&h->host_budgets, b, sizeof *b) == 0 && h->host_q == q_in &&
+                          h->host_out == out_k;
         if (!same) {
             if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
             h->host_exec = nullptr;
             // one eager run sizes every scratch buffer, then the capture
-            retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, h->out_stage, h->host_stream);
+            retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, out_k, h->host_stream, q_in);
             ck(cudaStreamSynchronize(h->host_stream), "warm-up");
             cudaGraph_t g = nullptr;
             ck(cudaStreamBeginCapture(h->host_stream, cudaStreamCaptureModeThreadLocal), "capture begin");
             try {
-                retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, h->out_stage, h->host_stream);
+                retrieve_impl(h, h->q_stage, b, flags, nullptr, nullptr, out_k, h->host_stream, q_in);
             } catch (...) {
                 cudaStreamEndCapture(h->host_stream, &g);
                 if (g) cudaGraphDestroy(g);
@@ -686,9 +703,11 @@ int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uin
             h->host_version = h->version;
             h->host_flags = flags;
             h->host_budgets = *b;
+            h->host_q = q_in;
+            h->host_out = out_k;
         }
         ck(cudaGraphLaunch(h->host_exec, h->host_stream), "graph launch");
-        ck(cudaMemcpyAsync(out_host, h->out_stage, bytes, cudaMemcpyDeviceToHost, h->host_stream), "out D2H");
+        if (!zc) ck(cudaMemcpyAsync(out_host, h->out_stage, bytes, cudaMemcpyDeviceToHost, h->host_stream), "out D2H");
         ck(cudaStreamSynchronize(h->host_stream), "stream sync");
         h->last_flags = flags;
         h->last_valid = 1;

@@ -14,7 +14,8 @@ size_t select3_pick_smem(const Arena& a);
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
-                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream);
+                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
+                           const float* q_in = nullptr);  // q_in: k_coarse reads q here and copies it to q
 uint32_t attend_grid(uint32_t d);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
@@ -116,6 +117,8 @@ struct lc_index_s {
     uint64_t host_version = 0;
     uint32_t host_flags = 0;
     lc_budgets host_budgets{};
+    const float* host_q = nullptr;  // the graph's q source (mapped host buffer) or nullptr (staged)
+    float* host_out = nullptr;      // the graph's output buffer (mapped host buffer or out_stage)
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
 
     ~lc_index_s() {

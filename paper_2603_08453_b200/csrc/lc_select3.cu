@@ -82,6 +82,7 @@ struct Sel3Params {
     Arena a;
     uint32_t keys_cap;  // per-head candidates staged in k_pickq's shared memory
     const float* q;  // [slot][G][d]
+    const float* q_in;  // k_coarse's source of q when it differs (host-mapped); k_coarse copies it to q
     uint32_t unit_topk, mode, cluster_topk, sink, flags;
     unsigned long long budget;
     const uint32_t* buf_off;
@@ -115,6 +116,9 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
     PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
     const bool degenerate = (p.mode == 1 && (unsigned long long)n <= p.budget) || st.n_chunks == 0;
     if (degenerate) {
+        if (p.q_in != p.q)  // k_attend still reads this slot's q (full attention)
+            for (uint32_t x = tid; x < G * D; x += kCoThreads)
+                const_cast<float*>(p.q)[(size_t)slot * G * D + x] = p.q_in[(size_t)slot * G * D + x];
         if (tid == 0) {
             pv.hdr()[0] = 1;
             pv.hdr()[1] = pv.hdr()[2] = 0;
@@ -144,7 +148,9 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
         }
     }
     for (uint32_t x = tid; x < G * D; x += kCoThreads) {
-        qd[x] = (double)p.q[(size_t)slot * G * D + x];
+        const float qv = p.q_in[(size_t)slot * G * D + x];
+        if (p.q_in != p.q) const_cast<float*>(p.q)[(size_t)slot * G * D + x] = qv;  // device copy for the rest
+        qd[x] = (double)qv;
         pv.qd()[x] = qd[x];  // k_fine reads q as f64 from the plan (L1-resident)
     }
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
@@ -1561,14 +1567,15 @@ size_t select3_pick_smem(const Arena& a) {
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
-                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream) {
+                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
+                           const float* q_in) {
     static unsigned long long *prof = nullptr, *prof_sp = nullptr;
     if (getenv("LC_PROF") && !prof) {
         cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
         cudaMalloc(&prof_sp, (size_t)a.n_slots * 8 * 8);
         cudaMemset(prof_sp, 0, (size_t)a.n_slots * 8 * 8);
     }
-    Sel3Params p{a, pick_keys_cap(a), q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
+    Sel3Params p{a, pick_keys_cap(a), q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
                  fine_ctr, prof_sp};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
                   : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)

@@ -134,6 +134,18 @@ def test_retrieve_host_matches_device():
     out = torch.zeros_like(q)
     eng.retrieve(q, b, out=out)
     assert np.array_equal(out.cpu().numpy(), oh)
+    # page-locked host buffers take the zero-copy path (k_coarse reads q from
+    # host memory, k_attend writes the outputs there): same bits; a second
+    # call with other buffers re-captures the graph
+    for _ in range(2):
+        qp = torch.from_numpy(qh.copy()).pin_memory()
+        op = torch.zeros_like(qp).pin_memory()
+        eng.retrieve_host(qp.numpy(), b, op.numpy())
+        assert np.array_equal(op.numpy(), oh)
+    # and the staged path again after the zero-copy graph
+    oh2 = np.zeros_like(qh)
+    eng.retrieve_host(qh, b, oh2)
+    assert np.array_equal(oh2, oh)
 
 
 def _stream_tokens(w, steps, seed):
