@@ -52,7 +52,9 @@ def parse():
     p.add_argument("--kv-heads", type=int, default=8)
     p.add_argument("--group", type=int, default=4)
     p.add_argument("--budget", type=int, default=2048)
-    p.add_argument("--batch", type=int, default=1)
+    p.add_argument("--batch", type=int, default=0,
+                   help="sequences per step; default: the number of GPUs (weak scaling: every GPU keeps "
+                        "one sequence's worth of slots, config 2's per-GPU load) -- 8 in --mode stream")
     p.add_argument("--splits", type=int, default=0)
     p.add_argument("--graph", type=int, default=1)
     p.add_argument("--slot-groups", type=int, default=1)
@@ -228,11 +230,12 @@ def run_reference(args):
         secs, _ = R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1)
         times.append(secs)
     step = sum(times) / len(times)
-    v = 1.0 / step
+    v = args.batch / step
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": getattr(args, "scaling", "strong"), "value_definition": VALUE_DEF, "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (reference gen_clustered_workload, seed %d)" % args.seed_base,
         "config": config_dict(args, 1),
         "cpu_baseline": {"value": v, "unit": "steps/s", "cores": base["threads"], "kind": "reference",
@@ -335,8 +338,24 @@ def run_stream_mode(args, api, torch):
     print(json.dumps(line))
 
 
+def resolve_batch(args):
+    """--batch 0 (default): batch = world size, so the per-GPU work stays one
+    sequence's 256 slots as N grows (weak scaling over KV-head x batch
+    sharding); an explicit --batch fixes the total work (strong scaling)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.batch == 0:
+        args.batch = world
+        return "weak"
+    return "strong"
+
+
+VALUE_DEF = "decode steps/s summed over the batch's sequences (batch x steps/s; batch 1 at N=1)"
+
+
 def main():
     args = parse()
+    if args.mode == "step":
+        args.scaling = resolve_batch(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -426,7 +445,7 @@ def main():
     d = 128
     att_bytes = step_bytes[2] * 2 * d * 2 + len(slots) * args.group * 2 * 4 * d
     att_gbs = att_bytes / (att_ms * 1e-3) / 1e9
-    step_gbs = step_bytes[0] / (ms * 1e-3) / 1e9
+    step_gbs = step_bytes_all[0] / (ms * 1e-3) / 1e9
 
     # end to end through the public host API (H2D q, retrieve + attention, D2H out)
     qh = torch.from_numpy(np.ascontiguousarray(qs)).pin_memory()
@@ -459,11 +478,11 @@ def main():
                              f"calls on {base['threads']} threads, 1 warm-up + 2 timed steps. Mode A (reference API "
                              f"as-is, serial calls, OpenMP kernels): {1.0 / base['step_mode_a_s']:.3f} steps/s"}
     if rank == 0:
-        value = 1000.0 / ms
+        value = args.batch * 1000.0 / ms
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": args.scaling, "value_definition": VALUE_DEF, "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (gen_clustered_workload streams on the GPU, seeds {args.seed_base}+slot; "
                     "indexes by GPU build_index, bit-exact to the reference)",
             "config": config_dict(args, world),
@@ -472,15 +491,16 @@ def main():
                          "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)",
                          "peak_source": peak_src,
                          "bytes_per_launch": att_bytes, "ms_per_launch": att_ms},
-            "step_roofline": {"achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
+            "step_roofline": {"achieved": step_gbs, "peak": peak * world, "unit": "GB/s",
+                              "frac": step_gbs / (peak * world),
                               "bytes_per_step_union": step_bytes_all[0],
                               "bytes_per_step_per_query": step_bytes_all[1],
                               "active_tokens_union": step_bytes_all[2],
                               "fine_candidates_union": step_bytes_all[3],
                               "select_ms": sel_ms, "attend_ms": att_ms},
             "cpu_baseline": cpu,
-            "e2e": {"value": 1000.0 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": io_bytes,
-                    "d2h_bytes_per_step": io_bytes},
+            "e2e": {"value": args.batch * 1000.0 / e2e_ms, "unit": "steps/s",
+                    "h2d_bytes_per_step": io_bytes * world, "d2h_bytes_per_step": io_bytes * world},
             "gpu_launches": args.steps * KERNELS_PER_STEP,
             "clocks": clocks,
             "setup": setup,
