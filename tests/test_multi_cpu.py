@@ -21,6 +21,19 @@ def test_slots_partition_all_heads():
             assert len(heads) == 8 // world
 
 
+def test_weak_scaling_keeps_per_gpu_load():
+    # bench.py's default at N GPUs: batch = N, so every rank keeps 256 slots
+    # (one sequence's worth), whole KV heads of every sequence
+    for world in (1, 2, 4, 8):
+        owned = [shard.slots_of_rank(r, world, 32, 8, batch=world) for r in range(world)]
+        assert all(len(o) == 256 for o in owned)
+        flat = sorted(s for o in owned for s in o)
+        assert flat == list(range(256 * world))
+        for o in owned:
+            seqs = {s // 256 for s in o}
+            assert seqs == set(range(world))
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
