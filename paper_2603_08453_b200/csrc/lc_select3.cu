@@ -148,9 +148,7 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
         }
     }
     for (uint32_t x = tid; x < G * D; x += kCoThreads) {
-        const float qv = p.q_in[(size_t)slot * G * D + x];
-        if (p.q_in != p.q) const_cast<float*>(p.q)[(size_t)slot * G * D + x] = qv;  // device copy for the rest
-        qd[x] = (double)qv;
+        qd[x] = (double)p.q_in[(size_t)slot * G * D + x];
         pv.qd()[x] = qd[x];  // k_fine reads q as f64 from the plan (L1-resident)
     }
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
@@ -318,6 +316,10 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
             pv.tiles()[t] = make_uint4(lo, mask, c0 - s_ucum[lo], 0u);
         }
     }
+    // q read from a host-mapped buffer: leave the device copy the later kernels
+    // read (stored last, so no load above waits behind a possibly aliasing store)
+    if (p.q_in != p.q)
+        for (uint32_t x = tid; x < G * D; x += kCoThreads) const_cast<float*>(p.q)[(size_t)slot * G * D + x] = (float)qd[x];
 }
 
 // ---------------------------------------------------------------------------

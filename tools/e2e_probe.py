@@ -15,6 +15,7 @@ from paper_2603_08453_b200 import _lib as L  # noqa: E402
 
 sys.argv = sys.argv[:1]
 args = bench.parse()
+bench.resolve_batch(args)
 slots = shard.slots_of_rank(0, 1, args.layers, args.kv_heads, args.batch)
 eng, qs, _ = bench.build_engine(api, torch, args, slots, 0)
 b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
