@@ -1510,7 +1510,35 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
                               cudaStream_t stream) {
     const size_t co_smem = (size_t)GQ * D * 8 + (size_t)D * ((pmax + 3) & ~3u) * 4 + (size_t)GQ * pmax * 8 +
                            (size_t)pmax * 16 + 4;  // urad, unit_off, union mask
-    const size_t pk_smem = select3_pick_smem(p.a);
+    // k_pickq stages up to keys_cap candidates per head in shared memory: the
+    // floor of 1024, raised when the grid leaves fewer CTAs per SM (long
+    // contexts over few slots), so the radix passes stay on chip
+    Sel3Params pp = p;
+    const size_t bw = (size_t)bit_words(p.a.cap_chunks) * 4;
+    {
+        static int sms = 0, smem_sm = 0, smem_blk = 0;
+        static size_t st_smem = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+            cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, k_pickq<D, GQ>);
+            st_smem = fa.sharedSizeBytes;
+            sms = std::max(1, sms);
+        }
+        const unsigned long long ctas = (unsigned long long)n_slots * GQ;
+        const unsigned long long per_sm = std::max(1ull, (ctas + sms - 1) / sms);
+        const long long avail = std::min<long long>((long long)smem_sm / (long long)per_sm - 1024, smem_blk) -
+                                (long long)st_smem - (long long)bw;
+        const unsigned long long cap = avail > 0 ? ((unsigned long long)avail / 12) & ~1ull : 0ull;
+        // only when it at least doubles the floor: a near-full SM keeps its CTA count
+        if (cap >= 2ull * p.keys_cap)
+            pp.keys_cap = (uint32_t)std::min<unsigned long long>(p.a.max_cand, cap);
+    }
+    const size_t pk_smem = (size_t)pp.keys_cap * 12 + bw;
     static size_t co_cfg = 0, pk_cfg = 0;
     if (co_smem > co_cfg) {
         cudaError_t e = cudaFuncSetAttribute(k_coarse<D, GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)co_smem);
@@ -1538,7 +1566,7 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
                                    std::min<uint32_t>(kMaxAttendSlots, n_slots - s0));
         if (e != cudaSuccess) return e;
     }
-    cudaError_t e2 = launch_pdl(k_pickq<D, GQ>, dim3(GQ, n_slots), dim3(kPqThreads), pk_smem, stream, p);
+    cudaError_t e2 = launch_pdl(k_pickq<D, GQ>, dim3(GQ, n_slots), dim3(kPqThreads), pk_smem, stream, pp);
     if (e2 != cudaSuccess) return e2;
     e2 = launch_pdl(k_spans<GQ>, dim3(n_slots), dim3(kSpThreads), 0, stream, p);
     if (e2 != cudaSuccess) return e2;
@@ -1608,8 +1636,16 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
         }
         double pre = 0;
         for (size_t r = (size_t)a.slot0 * a.G; r < (size_t)(a.slot0 + n_slots) * a.G; ++r) pre += (double)(t[r * 8 + 6] - t[r * 8 + 2]);
-        fprintf(stderr, "[LC_PROF] k_pickq refine set %.1f of %.1f candidates per head; x + R list %.2f us of refine\n", rs / nq,
-                ncs / nq, pre / nq / 1e3);
+        unsigned long long rmax = 0;
+        double tmax = 0;
+        for (size_t r = (size_t)a.slot0 * a.G; r < (size_t)(a.slot0 + n_slots) * a.G; ++r)
+            if ((double)(t[r * 8 + 5] - t[r * 8 + 0]) > tmax) {
+                tmax = (double)(t[r * 8 + 5] - t[r * 8 + 0]);
+                rmax = t[r * 8 + 7];
+            }
+        fprintf(stderr, "[LC_PROF] k_pickq refine set %.1f of %.1f candidates per head; x + R list %.2f us of refine; "
+                "slowest head: |R| %llu of %llu, %.1f us\n", rs / nq, ncs / nq, pre / nq / 1e3, rmax & 0xffffffffull,
+                rmax >> 32, tmax / 1e3);
         {
             std::vector<unsigned long long> u((size_t)a.n_slots * 8);
             cudaMemcpy(u.data(), prof_sp, u.size() * 8, cudaMemcpyDeviceToHost);
