@@ -675,9 +675,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             k2 += __popc(bal);
         }
         if (lane == 0) s_gpre[k2] = pv.hdr()[4 + g];
-    }
-    __syncthreads();
-    if (tid == 0) {
+    } else if (warp == 1 && lane == 0) {  // the plan header and key range, alongside warp 0's loads
         s_nc = pv.hdr()[4 + g];
         s_kU = pv.hdr()[3];
         const unsigned long long mn = pv.kmin()[g], mx = pv.kmax()[g];
