@@ -1536,6 +1536,8 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
         if (cap >= 2ull * p.keys_cap)
             pp.keys_cap = (uint32_t)std::min<unsigned long long>(p.a.max_cand, cap);
     }
+    if (const char* ev = getenv("LC_PICK_KEYS_CAP"))  // tests: force the unstaged (L2) key path
+        pp.keys_cap = std::min<uint32_t>(pp.keys_cap, (uint32_t)std::max(2, atoi(ev)) & ~1u);
     const size_t pk_smem = (size_t)pp.keys_cap * 12 + bw;
     static size_t co_cfg = 0, pk_cfg = 0;
     if (co_smem > co_cfg) {

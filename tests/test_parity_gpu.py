@@ -88,10 +88,14 @@ def test_degenerate_full_attention():
         assert rel_l2(got[g].output, full) < TOL
 
 
-@pytest.mark.parametrize("slot_groups", [0, 3])
-def test_batched_slots_match_per_head_reference(slot_groups):
+@pytest.mark.parametrize("slot_groups,keys_cap", [(0, None), (3, None), (0, 16)])
+def test_batched_slots_match_per_head_reference(slot_groups, keys_cap, monkeypatch):
     """8 slots (one layer of 8 KV heads), GQA 4: one batched call == 32 reference calls
-    (also with the slots split into groups on forked streams)."""
+    (also with the slots split into groups on forked streams, and with k_pickq's
+    shared-memory key cap forced below the heads' candidate counts, so the
+    selection runs its keys from L2 as the largest config-2 heads do)."""
+    if keys_cap is not None:
+        monkeypatch.setenv("LC_PICK_KEYS_CAP", str(keys_cap))
     S, G, n = 8, 4, 8192
     b = api.Budgets(token_budget=2048)
     eng = api.Engine(S, 128, G, cap_tokens=n + 64, cap_chunks=n // 8 + 64, cap_clusters=n // 8,
