@@ -55,7 +55,6 @@ def parse():
     p.add_argument("--batch", type=int, default=0,
                    help="sequences per step; default: the number of GPUs (weak scaling: every GPU keeps "
                         "one sequence's worth of slots, config 2's per-GPU load) -- 8 in --mode stream")
-    p.add_argument("--splits", type=int, default=0)
     p.add_argument("--graph", type=int, default=1)
     p.add_argument("--slot-groups", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
@@ -135,7 +134,7 @@ def build_engine(api, torch, args, slots, device):
     S = len(slots)
     cap_chunks = n // 8 + 64
     eng = api.Engine(S, 128, args.group, cap_tokens=n + 64, cap_chunks=cap_chunks,
-                     cap_clusters=(cap_chunks + 1) // 2, cap_units=64, splits=args.splits,
+                     cap_clusters=(cap_chunks + 1) // 2, cap_units=64,
                      keep_reps=False, device=device, slot_groups=args.slot_groups)
     seeds = np.array([args.seed_base + s for s in slots], np.uint64)
     t0 = time.time()

@@ -55,7 +55,6 @@ typedef struct {
     uint32_t cap_clusters;    /* per-slot fine clusters L (fixed after build) */
     uint32_t cap_units;       /* per-slot coarse units P (<= 1024) */
     uint32_t max_candidates;  /* bound on fine candidates per query (0 = auto) */
-    uint32_t splits;          /* unused: the attention grid is persistent and token-balanced */
     uint32_t structure_aware; /* StreamerConfig::structure_aware (host chunker) */
     uint32_t graft_full;      /* StreamerConfig::graft_search == full */
     uint32_t keep_reps;       /* keep chunk representatives on device (download parity) */
@@ -96,6 +95,18 @@ typedef struct {
     uint32_t* coarse_members;    /* fine ids, ascending within a unit */
     uint32_t* cluster_of_chunk;  /* [n_chunks] */
 } lc_host_index;
+
+/* tierkv::IndexConfig (index.hpp:13-22): recorded per slot (defaults at
+ * upload, the build's parameters after lc_index_build, the file's after
+ * lc_index_load) and serialized by index_to_bytes. */
+typedef struct {
+    double avg_chunks_per_cluster; /* 2.0 */
+    uint32_t max_coarse_units;     /* 64 */
+    uint32_t kmeans_iters;         /* 10 */
+    uint32_t pooling;              /* 0 mean, 1 max */
+    uint32_t elem_bytes;           /* 2 */
+    uint64_t seed;                 /* 0 */
+} lc_index_config;
 
 /* tierkv::GraftReport (streamer.hpp:27-35) */
 typedef struct {
@@ -224,6 +235,61 @@ int lc_step_bytes(lc_index_t h, uint64_t* out);
 /* Sticky device-side error bits (lc_common.cuh ErrBits) of every kernel since
  * the last clear; synchronous. */
 int lc_device_error(lc_index_t h, uint32_t* out, int clear);
+
+/* ---- TKIX <-> device (serialize.cpp:88-220) ------ */
+
+/* IndexConfig of a slot (serialized by index_to_bytes). */
+int lc_index_set_config(lc_index_t h, uint32_t slot, const lc_index_config* cfg);
+int lc_index_get_config(lc_index_t h, uint32_t slot, lc_index_config* cfg);
+
+/* index_to_bytes(state.index()) (serialize.cpp:88-125) of a slot's live index,
+ * every graft included (needs the chunk representatives: keep_reps or an
+ * upload that supplied them).  *size = full size; up to cap bytes copied to
+ * buf (NULL: size only).  Synchronous. */
+int lc_index_to_bytes(lc_index_t h, uint32_t slot, uint8_t* buf, uint64_t cap, uint64_t* size);
+
+/* save_index (serialize.cpp:127-148): a TKIX file of the slot's index plus
+ * its token store (texts packed as text_buf[text_offs[i], text_offs[i+1]),
+ * NULL = empty texts; K/V as fp32, bf16 stores widened exactly).  The
+ * reference's load_index reads it. */
+int lc_index_save(lc_index_t h, uint32_t slot, const char* path, const char* text_buf, const uint64_t* text_offs);
+
+/* load_index (serialize.cpp:150-220) into a slot: index + token store
+ * uploaded (bf16 engines round K/V to nearest even), IndexConfig recorded.
+ * Texts are returned packed when text_buf / text_offs are given (offs needs
+ * n_tokens + 1 entries; nothing past the caps is written); *n_tokens = the
+ * store size.  Reads files written by the reference's save_index. */
+int lc_index_load(lc_index_t h, uint32_t slot, const char* path, char* text_buf, uint64_t text_cap,
+                  uint64_t* text_offs, uint64_t offs_cap, uint64_t* n_tokens);
+
+/* Host-only codec of the index part (no device needed): index_to_bytes of a
+ * host index, its inverse, and the sizes to allocate for the inverse
+ * (dims as lc_index_slot_dims; dims[7] = bytes consumed). */
+int lc_tkix_encode(const lc_host_index* ix, const lc_index_config* cfg, uint8_t* buf, uint64_t cap,
+                   uint64_t* size);
+int lc_tkix_decode_dims(const uint8_t* buf, uint64_t size, uint64_t* dims);
+int lc_tkix_decode(const uint8_t* buf, uint64_t size, lc_host_index* out, lc_index_config* cfg);
+
+/* ---- evaluator on the device (evaluator.cpp) ------ */
+
+/* eval::audit_ub_soundness (evaluator.cpp:107-140) of one slot's live index
+ * for nq <= 64 host queries [nq][dim]: the number of (query, tier node,
+ * descendant chunk) triples whose exact rep dot exceeds the node's bound +
+ * tolerance -- the reference's count, bit for bit.  Needs keep_reps. */
+int lc_audit_ub(lc_index_t h, uint32_t slot, const float* queries_host, uint32_t nq, double tolerance,
+                uint64_t* violations);
+
+/* eval::oracle_topk_tokens (evaluator.cpp:43-64) over the slot's whole store
+ * for nq host queries: ids_out [nq][min(budget, n)] sorted ascending, ties
+ * toward the smaller id; *n_out = min(budget, n).  budget 0 is LC_EINVAL. */
+int lc_oracle_topk(lc_index_t h, uint32_t slot, const float* queries_host, uint32_t nq, uint64_t budget,
+                   uint32_t* ids_out, uint64_t* n_out);
+
+/* eval::full_attention (evaluator.cpp:11-41) over the slot's whole store for
+ * its `group` query heads: q_dev [group][dim] -> out_dev [group][dim]
+ * (bf16 store: fp32 accumulation; kv_f32: fp64).  Asynchronous; overwrites
+ * the slot's active row list like lc_sparse_attention_ids. */
+int lc_full_attention(lc_index_t h, uint32_t slot, const float* q_dev, float* out_dev, void* stream);
 
 /* ---- host chunk-boundary decision (streaming front end) ----------------- */
 

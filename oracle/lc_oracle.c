@@ -498,3 +498,12 @@ int lco_decode_step(lco_index* ix, const float* q, const float* key, const float
     free(rep);
     return rc;
 }
+
+uint64_t lco_fnv1a64(const uint8_t* buf, size_t n) {
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < n; ++i) {
+        h ^= buf[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}

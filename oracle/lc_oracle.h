@@ -78,6 +78,8 @@ typedef struct { /* tierkv::GraftReport (streamer.hpp:27-35) */
 } lco_graft_report;
 
 /* status: 0 ok, 1 invalid_argument, 2 runtime_error */
+/* FNV-1a-64 over raw bytes (the fixture fingerprint of SURVEY.md s8(d)) */
+uint64_t lco_fnv1a64(const uint8_t* buf, size_t n);
 double lco_dot(const float* a, const float* b, size_t d);     /* kernels.cpp:13-17 */
 double lco_l2_norm(const float* a, size_t d);                 /* kernels.cpp:19-23 */
 double lco_l2_dist(const float* a, const float* b, size_t d); /* kernels.cpp:25-32 */

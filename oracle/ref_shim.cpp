@@ -306,6 +306,36 @@ uint64_t tkr_engine_index_bytes(void* hv, uint8_t* buf, uint64_t cap) {
     return bytes.size();
 }
 
+// save_index (serialize.cpp:127-148) of the engine's index + store
+int tkr_save_index(void* hv, const char* path) {
+    return guard([&] { save_index(path, static_cast<EngineH*>(hv)->state->index()); });
+}
+
+// StreamState over load_index (serialize.cpp:150-220): a TKIX file written by
+// either side becomes a reference engine
+int tkr_engine_load(const char* path, uint32_t structure_aware, uint32_t graft_full, void** out) {
+    return guard([&] {
+        IndexFile f = load_index(path);
+        StreamerConfig scfg;
+        scfg.structure_aware = structure_aware != 0;
+        scfg.graft_search = graft_full ? GraftSearch::full : GraftSearch::scoped;
+        auto h = std::make_unique<EngineH>();
+        h->state = std::make_unique<StreamState>(std::move(f.store), std::move(f.index), scfg);
+        *out = h.release();
+    });
+}
+
+// eval::oracle_topk_tokens (evaluator.cpp:43-64)
+int tkr_oracle_topk(void* hv, const float* q, uint64_t d, uint64_t budget, uint32_t* out, uint64_t cap,
+                    uint64_t* n) {
+    return guard([&] {
+        auto ids = eval::oracle_topk_tokens(std::span<const float>(q, d), static_cast<EngineH*>(hv)->state->store(),
+                                            budget);
+        copy_ids(ids, out, cap);
+        *n = ids.size();
+    });
+}
+
 void tkr_engine_store_export(void* hv, float* keys, float* values) {
     const auto& st = static_cast<EngineH*>(hv)->state->store();
     if (keys) std::memcpy(keys, st.keys_flat().data(), st.keys_flat().size_bytes());

@@ -54,6 +54,10 @@ def lib():
         L.tkr_engine_index_bytes.argtypes = [vp, vp, C.c_uint64]
         L.tkr_engine_index_bytes.restype = C.c_uint64
         L.tkr_engine_store_export.argtypes = [vp, vp, vp]
+        L.tkr_save_index.argtypes = [vp, C.c_char_p]
+        L.tkr_engine_load.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(vp)]
+        L.tkr_oracle_topk.argtypes = [vp, f32p, C.c_uint64, C.c_uint64, u32p, C.c_uint64,
+                                      C.POINTER(C.c_uint64)]
         L.tkr_retrieve.argtypes = [vp, f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                    C.c_uint64, C.c_uint32, vp, C.c_uint64, C.c_int,
                                    u32p, C.c_uint64, u32p, C.c_uint64, u32p, C.c_uint64,
@@ -178,7 +182,11 @@ class RefEngine:
     """The reference StreamState (store + HierarchicalIndex) built by build_index."""
 
     def __init__(self, keys, values, text_code=None, spans=None, avg_chunks=2.0, max_units=64,
-                 iters=10, pooling=0, seed=0, structure_aware=True, graft_full=False):
+                 iters=10, pooling=0, seed=0, structure_aware=True, graft_full=False, _handle=None):
+        if _handle is not None:  # RefEngine.load
+            self.h = _handle
+            self.d = self.dims()[0]
+            return
         keys = np.ascontiguousarray(keys, np.float32)
         values = np.ascontiguousarray(values, np.float32)
         n, d = keys.shape
@@ -195,6 +203,26 @@ class RefEngine:
         if getattr(self, "h", None):
             lib().tkr_engine_free(self.h)
             self.h = None
+
+    @classmethod
+    def load(cls, path, structure_aware=True, graft_full=False) -> "RefEngine":
+        """StreamState over the reference's load_index (serialize.cpp:150-220)."""
+        h = vp()
+        _check(lib().tkr_engine_load(path.encode(), int(structure_aware), int(graft_full), C.byref(h)))
+        return cls(None, None, _handle=h)
+
+    def save(self, path):
+        """The reference's save_index (serialize.cpp:127-148)."""
+        _check(lib().tkr_save_index(self.h, path.encode()))
+
+    def oracle_topk(self, q, budget):
+        """eval::oracle_topk_tokens (evaluator.cpp:43-64)."""
+        q = np.ascontiguousarray(q, np.float32)
+        n = self.dims()[4]
+        out = np.empty(max(n, 1), np.uint32)
+        k = C.c_uint64()
+        _check(lib().tkr_oracle_topk(self.h, q, len(q), budget, out, len(out), C.byref(k)))
+        return out[: k.value].copy()
 
     def dims(self):
         out = np.zeros(8, np.uint64)
@@ -336,8 +364,9 @@ def threads():
 
 
 def fnv1a64(buf: bytes) -> int:
-    h = 1469598103934665603
-    for b in buf:
-        h ^= b
-        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
-    return h
+    """FNV-1a-64 (offset basis 1469598103934665603, prime 1099511628211) via the C oracle."""
+    from . import cpy
+    L = cpy.lib()
+    L.lco_fnv1a64.restype = C.c_uint64
+    L.lco_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
+    return int(L.lco_fnv1a64(buf, len(buf)))

@@ -22,7 +22,7 @@ u64 = C.c_uint64
 class IndexDesc(C.Structure):
     _fields_ = [("n_slots", u32), ("dim", u32), ("group", u32), ("cap_tokens", u32),
                 ("cap_chunks", u32), ("cap_clusters", u32), ("cap_units", u32),
-                ("max_candidates", u32), ("splits", u32), ("structure_aware", u32),
+                ("max_candidates", u32), ("structure_aware", u32),
                 ("graft_full", u32), ("keep_reps", u32), ("pooling", u32), ("slot_groups", u32),
                 ("device", C.c_int32), ("kv_f32", u32)]
 
@@ -38,6 +38,11 @@ class HostIndex_(C.Structure):
                 ("fine_token_count", vp), ("fine_parent", vp), ("fine_member_off", vp),
                 ("fine_members", vp), ("coarse_centroid", vp), ("coarse_radius", vp),
                 ("coarse_member_off", vp), ("coarse_members", vp), ("cluster_of_chunk", vp)]
+
+
+class IndexConfig_(C.Structure):
+    _fields_ = [("avg_chunks_per_cluster", C.c_double), ("max_coarse_units", u32),
+                ("kmeans_iters", u32), ("pooling", u32), ("elem_bytes", u32), ("seed", u64)]
 
 
 class GraftReport_(C.Structure):
@@ -59,6 +64,9 @@ EXPORTS = [
     "lc_retrieve", "lc_sparse_attention", "lc_graft", "lc_decode_step", "lc_retrieve_host",
     "lc_selection_download", "lc_step_bytes", "lc_device_error", "lc_segment", "lc_segment_packed", "lc_flush_take",
     "lc_index_build", "lc_gen_workload", "lc_graft_rep", "lc_sparse_attention_ids", "lc_chunk_rep",
+    "lc_index_set_config", "lc_index_get_config", "lc_index_to_bytes", "lc_index_save", "lc_index_load",
+    "lc_tkix_encode", "lc_tkix_decode_dims", "lc_tkix_decode",
+    "lc_audit_ub", "lc_oracle_topk", "lc_full_attention",
 ]
 
 _lib = None
@@ -111,6 +119,17 @@ def lib():
         L.lc_graft_rep.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.lc_sparse_attention_ids.argtypes = [vp, u32, vp, vp, u32, vp, vp]
         L.lc_chunk_rep.argtypes = [vp, u32, u32, u32, vp]
+        L.lc_index_set_config.argtypes = [vp, u32, C.POINTER(IndexConfig_)]
+        L.lc_index_get_config.argtypes = [vp, u32, C.POINTER(IndexConfig_)]
+        L.lc_index_to_bytes.argtypes = [vp, u32, vp, u64, C.POINTER(u64)]
+        L.lc_index_save.argtypes = [vp, u32, C.c_char_p, vp, vp]
+        L.lc_index_load.argtypes = [vp, u32, C.c_char_p, vp, u64, vp, u64, C.POINTER(u64)]
+        L.lc_tkix_encode.argtypes = [C.POINTER(HostIndex_), C.POINTER(IndexConfig_), vp, u64, C.POINTER(u64)]
+        L.lc_tkix_decode_dims.argtypes = [vp, u64, vp]
+        L.lc_tkix_decode.argtypes = [vp, u64, C.POINTER(HostIndex_), C.POINTER(IndexConfig_)]
+        L.lc_audit_ub.argtypes = [vp, u32, vp, u32, C.c_double, C.POINTER(u64)]
+        L.lc_oracle_topk.argtypes = [vp, u32, vp, u32, u64, vp, C.POINTER(u64)]
+        L.lc_full_attention.argtypes = [vp, u32, vp, vp, vp]
         _lib = L
     return _lib
 

@@ -96,6 +96,26 @@ class DecodeOutcome:
 
 
 @dataclass
+class IndexConfig:
+    """tierkv::IndexConfig (index.hpp:13-22) as index_to_bytes serializes it."""
+    avg_chunks_per_cluster: float = 2.0
+    max_coarse_units: int = 64
+    kmeans_iters: int = 10
+    pooling: int = 0
+    elem_bytes: int = 2
+    seed: int = 0
+
+    def c(self):
+        return L.IndexConfig_(self.avg_chunks_per_cluster, self.max_coarse_units, self.kmeans_iters,
+                              self.pooling, self.elem_bytes, self.seed)
+
+    @classmethod
+    def from_c(cls, c):
+        return cls(c.avg_chunks_per_cluster, c.max_coarse_units, c.kmeans_iters, c.pooling,
+                   c.elem_bytes, c.seed)
+
+
+@dataclass
 class HostIndex:
     """tierkv::HierarchicalIndex in SoA form, reference numbering (index.hpp:25-73)."""
     dim: int
@@ -155,6 +175,47 @@ class HostIndex:
                              "coarse_members", "cluster_of_chunk")])
         return s, arrs  # keep arrays alive while the struct is used
 
+    @classmethod
+    def empty(cls, dims) -> "HostIndex":
+        d, m, l, p, _, fm, cm, _ = [int(x) for x in dims]
+        return cls(d, np.zeros((m, 4), np.uint32), np.zeros((m, d), np.float32),
+                   np.zeros((l, d), np.float32), np.zeros(l, np.float64), np.zeros(l, np.uint64),
+                   np.zeros(l, np.uint32), np.zeros(l + 1, np.uint32), np.zeros(max(fm, 1), np.uint32),
+                   np.zeros((p, d), np.float32), np.zeros(p, np.float64), np.zeros(p + 1, np.uint32),
+                   np.zeros(max(cm, 1), np.uint32), np.zeros(m, np.uint32))
+
+    def _fill_from(self, keep, fm, cm):
+        for k, v in keep.items():
+            if v is not None:
+                setattr(self, k, v)
+        self.fine_members = self.fine_members[:fm]
+        self.coarse_members = self.coarse_members[:cm]
+        return self
+
+
+# ---- TKIX codec (serialize.cpp:88-220), host only ----------------------------
+def index_to_bytes(ix: HostIndex, cfg: Optional[IndexConfig] = None) -> bytes:
+    """index_to_bytes (serialize.cpp:88-125) of a host index."""
+    s, keep = ix._c()
+    c = (cfg or IndexConfig()).c()
+    n = L.u64()
+    L.check(L.lib().lc_tkix_encode(C.byref(s), C.byref(c), None, 0, C.byref(n)))
+    buf = np.zeros(n.value, np.uint8)
+    L.check(L.lib().lc_tkix_encode(C.byref(s), C.byref(c), buf.ctypes.data, n.value, C.byref(n)))
+    return buf.tobytes()
+
+
+def index_from_bytes(data: bytes):
+    """The index part of load_index (serialize.cpp:150-208) -> (HostIndex, IndexConfig)."""
+    buf = np.frombuffer(data, np.uint8).copy()
+    dims = np.zeros(8, np.uint64)
+    L.check(L.lib().lc_tkix_decode_dims(buf.ctypes.data, len(buf), dims.ctypes.data))
+    ix = HostIndex.empty(dims)
+    s, keep = ix._c()
+    c = L.IndexConfig_()
+    L.check(L.lib().lc_tkix_decode(buf.ctypes.data, len(buf), C.byref(s), C.byref(c)))
+    return ix._fill_from(keep, int(dims[5]), int(dims[6])), IndexConfig.from_c(c)
+
 
 # ---- bf16 helpers (the device KV cache is bf16) ------------------------------
 def bf16_bits(x: np.ndarray) -> np.ndarray:
@@ -198,13 +259,13 @@ class Engine:
 
     def __init__(self, n_slots: int, dim: int = 128, group: int = 4, cap_tokens: int = 1 << 16,
                  cap_chunks: int = 1 << 13, cap_clusters: int = 1 << 12, cap_units: int = 64,
-                 splits: int = 0, structure_aware: bool = True, graft_full: bool = False,
+                 structure_aware: bool = True, graft_full: bool = False,
                  keep_reps: bool = True, pooling: int = 0, device: int = 0, max_candidates: int = 0,
                  slot_groups: int = 0, kv_f32: bool = False):
         """kv_f32: keep K/V in fp32 exactly as given, attention in fp64 (the
         reference-exact mode; head dims 8/16/32 also allowed for group 1 or 4)."""
         self.desc = L.IndexDesc(n_slots, dim, group, cap_tokens, cap_chunks, cap_clusters,
-                                cap_units, max_candidates, splits, int(structure_aware),
+                                cap_units, max_candidates, int(structure_aware),
                                 int(graft_full), int(keep_reps), pooling, slot_groups, device, int(kv_f32))
         self.kv_f32 = bool(kv_f32)
         self.h = C.c_void_p()
@@ -286,20 +347,52 @@ class Engine:
         return [int(x) for x in out]
 
     def download_slot(self, slot: int) -> HostIndex:
-        d, m, l, p, n, fm, cm, ce = self.slot_dims(slot)
-        ix = HostIndex(d, np.zeros((m, 4), np.uint32), np.zeros((m, d), np.float32),
-                       np.zeros((l, d), np.float32), np.zeros(l, np.float64), np.zeros(l, np.uint64),
-                       np.zeros(l, np.uint32), np.zeros(l + 1, np.uint32), np.zeros(max(fm, 1), np.uint32),
-                       np.zeros((p, d), np.float32), np.zeros(p, np.float64), np.zeros(p + 1, np.uint32),
-                       np.zeros(max(cm, 1), np.uint32), np.zeros(m, np.uint32))
+        dims = self.slot_dims(slot)
+        ix = HostIndex.empty(dims)
         s, keep = ix._c()
         L.check(L.lib().lc_index_download_slot(self.h, slot, C.byref(s)))
-        ix.fine_members = keep["fine_members"][:fm]
-        ix.coarse_members = keep["coarse_members"][:cm]
-        for k, v in keep.items():
-            if v is not None and k not in ("fine_members", "coarse_members"):
-                setattr(ix, k, v)
-        return ix
+        return ix._fill_from(keep, dims[5], dims[6])
+
+    # ---- TKIX <-> device (serialize.cpp:88-220) ----
+    def set_config(self, slot: int, cfg: IndexConfig):
+        c = cfg.c()
+        L.check(L.lib().lc_index_set_config(self.h, slot, C.byref(c)))
+
+    def get_config(self, slot: int) -> IndexConfig:
+        c = L.IndexConfig_()
+        L.check(L.lib().lc_index_get_config(self.h, slot, C.byref(c)))
+        return IndexConfig.from_c(c)
+
+    def index_bytes(self, slot: int) -> bytes:
+        """index_to_bytes(state.index()) of the slot's live index (grafts included)."""
+        n = L.u64()
+        L.check(L.lib().lc_index_to_bytes(self.h, slot, None, 0, C.byref(n)))
+        buf = np.zeros(n.value, np.uint8)
+        L.check(L.lib().lc_index_to_bytes(self.h, slot, buf.ctypes.data, n.value, C.byref(n)))
+        return buf.tobytes()
+
+    def save_index(self, slot: int, path: str, texts: Optional[Sequence[str]] = None):
+        """save_index (serialize.cpp:127-148): TKIX file with the slot's token store."""
+        tb, offs = None, None
+        if texts is not None:
+            enc = [t.encode() for t in texts]
+            offs = np.zeros(len(enc) + 1, np.uint64)
+            offs[1:] = np.cumsum([len(e) for e in enc])
+            tb = np.frombuffer(b"".join(enc) + b"\0", np.uint8).copy()
+        L.check(L.lib().lc_index_save(self.h, slot, path.encode(), _ptr(tb), _ptr(offs)))
+
+    def load_index(self, slot: int, path: str):
+        """load_index (serialize.cpp:150-220) into a slot; returns the store's texts."""
+        n = L.u64()
+        L.check(L.lib().lc_index_load(self.h, slot, path.encode(), None, 0, None, 0, C.byref(n)))
+        offs = np.zeros(n.value + 1, np.uint64)
+        L.check(L.lib().lc_index_load(self.h, slot, path.encode(), None, 0, offs.ctypes.data, len(offs),
+                                      C.byref(n)))
+        tb = np.zeros(max(int(offs[-1]), 1), np.uint8)
+        L.check(L.lib().lc_index_load(self.h, slot, path.encode(), tb.ctypes.data, len(tb), offs.ctypes.data,
+                                      len(offs), C.byref(n)))
+        raw = tb.tobytes()
+        return [raw[int(offs[i]):int(offs[i + 1])].decode() for i in range(n.value)]
 
     # ---- decode-step operations ----
     def retrieve(self, q, budgets: Budgets, buffer: str = "none", out=None, buf_off=None,
@@ -376,6 +469,35 @@ class Engine:
                                        rb.data_ptr(), _stream_ptr(stream)))
         return out
 
+    # ---- evaluator (evaluator.cpp) on the device ----
+    def audit_ub(self, slot: int, queries: np.ndarray, tolerance: float = 1e-6) -> int:
+        """eval::audit_ub_soundness (evaluator.cpp:107-140) of the slot's live index."""
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
+        total = 0
+        for i in range(0, q.shape[0], 64):
+            part = np.ascontiguousarray(q[i:i + 64])
+            v = L.u64()
+            L.check(L.lib().lc_audit_ub(self.h, slot, part.ctypes.data, part.shape[0], tolerance, C.byref(v)))
+            total += v.value
+        return total
+
+    def oracle_topk(self, slot: int, queries: np.ndarray, budget: int) -> np.ndarray:
+        """eval::oracle_topk_tokens (evaluator.cpp:43-64) -> [nq, min(budget, n)] sorted ids."""
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
+        n = self.slot_dims(slot)[4]
+        out = np.zeros((q.shape[0], max(min(budget, n), 1)), np.uint32)
+        k = L.u64()
+        L.check(L.lib().lc_oracle_topk(self.h, slot, q.ctypes.data, q.shape[0], budget, out.ctypes.data,
+                                       C.byref(k)))
+        return out[:, : k.value]
+
+    def full_attention(self, slot: int, q, out=None, stream=None):
+        """eval::full_attention (evaluator.cpp:11-41) for the slot's query heads; q cuda [G, d]."""
+        if out is None:
+            out = torch.zeros_like(q)
+        L.check(L.lib().lc_full_attention(self.h, slot, _ptr(q), _ptr(out), _stream_ptr(stream)))
+        return out
+
     def step_bytes(self):
         out = np.zeros(4, np.uint64)
         L.check(L.lib().lc_step_bytes(self.h, out.ctypes.data))
@@ -450,11 +572,11 @@ class DeviceIndex:
 
     def __init__(self, ix: HostIndex, keys: np.ndarray, values: np.ndarray, group: int = 1,
                  extra_tokens: int = 0, extra_chunks: int = 0, structure_aware: bool = True,
-                 graft_full: bool = False, device: int = 0, splits: int = 0, kv_f32: bool = False):
+                 graft_full: bool = False, device: int = 0, kv_f32: bool = False):
         n = keys.shape[0]
         self.engine = Engine(1, ix.dim, group, cap_tokens=n + extra_tokens + 1,
                              cap_chunks=ix.n_chunks + extra_chunks + 1,
-                             cap_clusters=ix.n_clusters, cap_units=max(ix.n_units, 1), splits=splits,
+                             cap_clusters=ix.n_clusters, cap_units=max(ix.n_units, 1),
                              structure_aware=structure_aware, graft_full=graft_full, device=device,
                              kv_f32=kv_f32)
         self.engine.upload_slot(0, ix, keys, values)

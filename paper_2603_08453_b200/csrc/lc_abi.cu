@@ -124,7 +124,6 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         const size_t groups = std::max<uint32_t>(1, std::min(d.slot_groups, d.n_slots));
         h->fine_ctr = dalloc<uint32_t>(4 * groups, o);
         ck(cudaMemset(h->fine_ctr, 0, 4 * groups * 4), "memset k_fine counters");
-        a.counters = dalloc<uint32_t>(S, o);
         a.att_sync = dalloc<unsigned long long>(S, o);
         a.err = dalloc<uint32_t>(1, o);
         h->q_stage = dalloc<float>(S * G * D, o);
@@ -134,7 +133,6 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         h->reps_dev = dalloc<float>(S * D, o);
         ck(cudaMemset(a.state, 0, S * sizeof(SlotState)), "memset state");
         ck(cudaMemset(a.err, 0, 4), "memset err");
-        ck(cudaMemset(a.counters, 0, S * 4), "memset counters");
         ck(cudaMemset(a.att_sync, 0, S * 8), "memset attention sync");
         ck(cudaMemset(a.n_spans, 0, S * 4), "memset n_spans");
         ck(cudaMemset(a.slot_tok, 0, S * 4), "memset slot_tok");
@@ -265,6 +263,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         up(a.fmem + so * a.cap_chunks, mem.data(), mem.size() * 4);
         HostSlot& hs = h->hs[slot];
         hs = HostSlot{};
+        hs.cfg.pooling = h->desc.pooling;
         hs.kind.resize(M);
         hs.level.resize(M);
         for (uint32_t j = 0; j < M; ++j) {
@@ -586,6 +585,7 @@ int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev, const
             if (s.n_tokens >= h->a.cap_tokens) fail(LC_ENOMEM, "decode_step: token capacity exhausted");
         ck(launch_append(h->a, keys_dev, values_dev, st), "k_append");
         for (auto& s : h->hs) s.n_tokens += 1;
+        ++h->version;
         if (take) graft_impl(h, take, kind, level, nullptr, reports_dev, st);
     });
 }
@@ -637,7 +637,10 @@ int lc_sparse_attention_ids(lc_index_t h, uint32_t slot, const float* q_dev, con
            "rows H2D");
         ck(cudaMemcpyAsync(a.slot_tok + slot, &n_ids, 4, cudaMemcpyHostToDevice, st), "count H2D");
         a.slot0 = slot;
-        ck(launch_attend(a, q_dev, out_dev, h->att_part, 1, st), "k_attend");
+        // the attention kernels address q / out as [slot][G][d] arrays: shift the
+        // caller's [G][d] buffers so that row `slot` lands on them
+        const size_t off = (size_t)slot * a.G * a.d;
+        ck(launch_attend(a, q_dev - off, out_dev - off, h->att_part, 1, st), "k_attend");
         ck(cudaStreamSynchronize(st), "attention sync");  // host arrays above are pageable
         h->last_valid = 0;  // the slot's row list no longer matches its selection
     });
@@ -680,7 +683,7 @@ int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uin
         float* out_k = zc ? out_host : h->out_stage;
         const bool same = h->host_exec && h->host_version == h->version && h->host_flags == flags &&
                           std::memcmp(&h->host_budgets, b, sizeof *b) == 0 && h->host_q == q_in &&
-                          h->host_out == out_k;
+                          h->host_out == out_k && h->host_scratch == h->sel_scratch;
         if (!same) {
             if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
             h->host_exec = nullptr;
@@ -705,6 +708,7 @@ int lc_retrieve_host(lc_index_t h, const float* q_host, const lc_budgets* b, uin
             h->host_budgets = *b;
             h->host_q = q_in;
             h->host_out = out_k;
+            h->host_scratch = h->sel_scratch;  // a later reallocation invalidates the graph
         }
         ck(cudaGraphLaunch(h->host_exec, h->host_stream), "graph launch");
         if (!zc) ck(cudaMemcpyAsync(out_host, h->out_stage, bytes, cudaMemcpyDeviceToHost, h->host_stream), "out D2H");

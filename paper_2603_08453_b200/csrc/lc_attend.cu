@@ -131,19 +131,19 @@ struct GroupDesc {  // one 16-token group of one slot
 // static range w of slot s -> w + s, pool chunk k of slot s -> NW + n + k + s
 // (both injective because range and slot indices grow together).
 constexpr uint32_t kPoolPerWarp = 4;     // pool chunks per warp (upper bound; partial storage)
-// Measured on config 2 (profiles/run_attsweep.sh): a 1/8 tail in one chunk per
+// Measured on config 2 (round-1 sweep, LC_ATT_* knobs since removed): a 1/8 tail in one chunk per
 // warp balances the SMs with the fewest partials (tails 1/2..1/32 and 1..8
 // chunks per warp: 156.8 us best vs 166-181 us)
-__device__ uint32_t g_tail_div = 8;       // tail = t / g_tail_div of every slot's tokens (LC_ATT_TAIL_DIV)
-__device__ uint32_t g_pool_per_warp = 1;  // <= kPoolPerWarp (LC_ATT_POOL)
-__device__ __forceinline__ uint32_t head_of(uint32_t t) { return t - t / g_tail_div; }
+constexpr uint32_t kTailDiv = 8;      // tail = t / kTailDiv of every slot's tokens
+constexpr uint32_t kPoolUsed = 1;     // pool chunks per warp actually used (<= kPoolPerWarp)
+__device__ __forceinline__ uint32_t head_of(uint32_t t) { return t - t / kTailDiv; }
 struct PoolShape {
     uint32_t C;  // pool chunk length (multiple of 16)
     uint32_t K;  // pool chunks
 };
 __device__ __forceinline__ PoolShape pool_shape(uint32_t TP, uint32_t NW) {
     PoolShape ps;
-    const uint32_t kmax = g_pool_per_warp * NW;
+    const uint32_t kmax = kPoolUsed * NW;
     uint32_t C = (TP + kmax - 1) / kmax;
     C = (C + 15) & ~15u;
     ps.C = C ? C : 16;
@@ -222,6 +222,15 @@ __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G
 #pragma unroll
     for (int k = 0; k < PER; ++k) out[(size_t)g * D + lane + 32 * k] = L > 0.f ? o[k] / L : 0.f;
     if (!(L > 0.f) && lane == 0) atomicOr(err, kErrEmptyActive);
+}
+
+// Every head of slot s, merged by the warp that flushed the slot's last token
+// (kept out of line so the streaming loop's register allocation is unaffected).
+template <int D>
+__device__ __noinline__ void merge_slot(float* out, uint32_t* err, uint32_t G, uint32_t n, const float* part,
+                                        uint32_t zero_seg, uint32_t s, uint32_t NW, uint32_t TH, uint32_t h0,
+                                        uint32_t h1, uint32_t t0, uint32_t t1, uint32_t C) {
+    for (uint32_t g = 0; g < G; ++g) merge_head<D>(out, err, G, g, n, part, zero_seg, s, NW, TH, h0, h1, t0, t1, C);
 }
 
 template <int D>
@@ -406,9 +415,10 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     uint32_t cur = ~0u, cur_seg = ~0u, seg_tok = 0;
     const float scale = (float)(1.4426950408889634 / sqrt((double)D));
 
-    // partial (m, l, o) of this warp's segment of slot s; the warp completing
-    // the slot's token count merges all its partials
-    // partial (m, l, o) of this warp's current segment
+    // partial (m, l, o) of this warp's current segment of slot s.  Publishing
+    // adds the segment's token count to the slot's counter; the warp whose add
+    // completes the slot's total merges every head of the slot (no warp ever
+    // waits on another CTA, so the kernel needs no co-residency guarantee)
     auto flush = [&](uint32_t seg, uint32_t s, uint32_t ntok) {
         float l = l_run;
         l += __shfl_xor_sync(0xffffffffu, l, 1);
@@ -426,10 +436,19 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
                 o[D / 8 + j] = acc[j][1] + acc[j][3];
             }
         }
-        // publish: the slot's merge waits until every token has been flushed
         __threadfence();
         __syncwarp();
-        if (lane == 0) atomicAdd(a.att_sync + a.slot0 + s, (unsigned long long)ntok);
+        const uint32_t tok = s_hp[s + 1] - s_hp[s] + s_tp[s + 1] - s_tp[s];
+        unsigned long long* sync = a.att_sync + a.slot0 + s;
+        uint32_t last = 0;
+        if (lane == 0) last = (uint32_t)atomicAdd(sync, (unsigned long long)ntok) + ntok == tok;
+        if (__shfl_sync(0xffffffffu, last, 0)) {
+            __threadfence();
+            merge_slot<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, n, part,
+                          NW + n + kPoolPerWarp * NW + n, s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1],
+                          pool.C);
+            if (lane == 0) atomicExch(sync, 0ull);  // ready for the next launch
+        }
     };
 
     for (uint32_t it = 0;; ++it) {
@@ -570,25 +589,6 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     if (cur_seg != ~0u) flush(cur_seg, cur, seg_tok);
     const unsigned long long t_merge = p.prof ? gtime_a() : 0ull;
 
-    // ---- every warp merges (slot, head) pairs, each as soon as all of the
-    // slot's tokens have been flushed (the grid is co-resident, so waiting is
-    // safe): the slot's partials in a fixed order.  The last head to merge a
-    // slot resets its counter for the next launch ----
-    for (uint32_t x = w; x < n * G; x += NW) {
-        const uint32_t s = x / G, g = x % G;
-        const uint32_t tok = s_hp[s + 1] - s_hp[s] + s_tp[s + 1] - s_tp[s];
-        if (tok == 0) continue;  // written by block 0
-        unsigned long long* sync = a.att_sync + a.slot0 + s;
-        if (lane == 0)
-            while ((uint32_t)(*reinterpret_cast<volatile unsigned long long*>(sync)) != tok) __nanosleep(32);
-        __syncwarp();
-        __threadfence();
-        merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, part,
-                      NW + n + kPoolPerWarp * NW + n, s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1],
-                      pool.C);
-        __syncwarp();
-        if (lane == 0 && (atomicAdd(sync, 1ull << 32) >> 32) == G - 1) atomicExch(sync, 0ull);
-    }
     // the last CTA out resets the pool and the barrier for the next launch
     __syncthreads();
     if (tid == 0 && atomicAdd(pool_ctr + 2, 1u) == gridDim.x - 1) {
@@ -613,35 +613,22 @@ static constexpr size_t attend_smem() {
 }
 
 template <int D>
+static KernelCfg& attend_cfg() {
+    static KernelCfg c;
+    return c;
+}
+
+template <int D>
 static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_attend<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)attend_smem<D>());
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem(k_attend<D>, attend_cfg<D>(), attend_smem<D>());
+    if (e != cudaSuccess) return e;
     return launch_pdl(k_attend<D>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
 }
 
-// Persistent grid: every SM holds as many CTAs as fit.
+// Persistent grid: every SM of the current device holds as many CTAs as fit.
 uint32_t attend_grid(uint32_t d) {
-    static uint32_t cached[2] = {0, 0};
-    const int k = d == 128 ? 1 : 0;
-    if (cached[k]) return cached[k];
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (d == 128) {
-        cudaFuncSetAttribute(k_attend<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem<128>());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_attend<128>, kAttThreads, attend_smem<128>());
-    } else {
-        cudaFuncSetAttribute(k_attend<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem<64>());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_attend<64>, kAttThreads, attend_smem<64>());
-    }
-    cudaGetLastError();
-    cached[k] = (uint32_t)(sms > 0 ? sms : 1) * (uint32_t)(per > 0 ? per : 1);
-    return cached[k];
+    return d == 128 ? persistent_grid(k_attend<128>, attend_cfg<128>(), kAttThreads, attend_smem<128>())
+                    : persistent_grid(k_attend<64>, attend_cfg<64>(), kAttThreads, attend_smem<64>());
 }
 
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots) {
@@ -720,20 +707,10 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     uint32_t per = kMaxAttendSlots;
     const unsigned long long cap = a.cap_tokens ? a.cap_tokens : 1;
     if ((unsigned long long)per * cap > 0xffffffffull) per = (uint32_t)(0xffffffffull / cap);
-    static bool tuned = false;
-    if (!tuned) {  // experiment knobs: LC_ATT_TAIL_DIV (tail fraction 1/x), LC_ATT_POOL (chunks per warp)
-        tuned = true;
-        if (const char* e = getenv("LC_ATT_TAIL_DIV")) {
-            const uint32_t v = (uint32_t)atoi(e);
-            if (v >= 2) cudaMemcpyToSymbol(g_tail_div, &v, 4);
-        }
-        if (const char* e = getenv("LC_ATT_POOL")) {
-            const uint32_t v = (uint32_t)atoi(e);
-            if (v >= 1 && v <= kPoolPerWarp) cudaMemcpyToSymbol(g_pool_per_warp, &v, 4);
-        }
-    }
-    static unsigned long long* prof = nullptr;
+    // LC_PROF=1 (diagnostics only): per-warp timestamps, one buffer per device
+    static unsigned long long* prof_dev[kMaxDevices] = {};
     const bool want_prof = getenv("LC_PROF") != nullptr;
+    unsigned long long*& prof = prof_dev[current_device()];
     if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
         AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr};

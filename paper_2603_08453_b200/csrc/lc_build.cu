@@ -797,6 +797,7 @@ int lc_index_build(lc_index_t h, const uint32_t* n_tokens, const uint32_t* spans
             ix.cluster_of_chunk = coc.data();
             const int rc = lc_index_upload_slot(h, s, &ix, nullptr, nullptr, n_tokens[s]);
             if (rc != LC_OK) fail(rc, std::string("build upload: ") + lc_last_error());
+            h->hs[s].cfg = lc_index_config{avg, max_units, iters, h->desc.pooling, 2, seeds[s]};
             if (a.keep_reps)
                 ck(cudaMemcpy(a.chunk_rep + (size_t)s * a.cap_chunks * d, reps.p + (size_t)F.pt_off * d,
                               (size_t)m * d * 4, cudaMemcpyDeviceToDevice),

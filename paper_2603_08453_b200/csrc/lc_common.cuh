@@ -30,6 +30,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <utility>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -66,7 +67,6 @@ struct Arena {
     uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;
     uint32_t graft_full, keep_reps, cap_spans;
     uint32_t kv_f32;         // K/V stored as fp32 (Kf, Vf; reference-exact mode) instead of bf16 (K, V)
-    uint32_t smem_cand;      // candidates kept in shared memory by k_select
     uint32_t slot0;          // first slot of the launch (slot groups on several streams)
     // token store
     __nv_bfloat16* K;
@@ -95,7 +95,6 @@ struct Arena {
     uint32_t* sel_units;     // [slot][G][cap_units]
     uint32_t* sel_clusters;  // [slot][G][cap_clusters] reference ids, rank order
     uint32_t* sel_bits;      // [slot][G][words(cap_clusters)] internal-id bitmap
-    unsigned char* cand_scratch;  // [slot][G][max_cand * 12] overflow of k_select's smem
     unsigned char* plan;          // [slot][plan_bytes] coarse-tier plan of the 3-kernel selection
     uint32_t* chunk_bits;         // [slot][G][words(cap_chunks)] per-head active chunk bitmaps
     uint32_t plan_bytes;
@@ -106,8 +105,7 @@ struct Arena {
                              //   token row | head mask << 24 (k_spans -> k_attend)
     uint32_t* slot_tok;      // [slot] union active token count (length of the row list)
     unsigned long long* step_bytes;  // [slot][4]
-    uint32_t* counters;      // [slot] (unused)
-    unsigned long long* att_sync;  // [slot] k_attend: tokens flushed (low 32) | heads merged (high 32)
+    unsigned long long* att_sync;  // [slot] k_attend: tokens flushed so far (the completing warp merges and resets)
     uint32_t* err;           // [1]
 };
 
@@ -172,6 +170,88 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// ---- per-device launch configuration (host) --------------------------------
+// Device properties, dynamic shared-memory opt-ins and occupancy-derived grid
+// sizes are per device: cudaFuncSetAttribute applies to the calling thread's
+// current device, so every cache below is keyed by the device ordinal and
+// guarded by a mutex (several handles on several devices / threads).
+constexpr int kMaxDevices = 64;
+
+struct DevProps {
+    int sms = 0, smem_sm = 0, smem_blk = 0;
+};
+
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev);
+}
+
+inline DevProps dev_props() {
+    static std::mutex mu;
+    static DevProps props[kMaxDevices];
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    DevProps& p = props[dev];
+    if (!p.sms) {
+        cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&p.smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&p.smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (p.sms <= 0) p.sms = 1;
+    }
+    return p;
+}
+
+// One per kernel instantiation (a function-local static in its launcher).
+struct KernelCfg {
+    std::mutex mu;
+    size_t smem[kMaxDevices] = {};  // dynamic shared memory opted into so far
+    uint32_t grid[kMaxDevices] = {};  // persistent grid (SMs x resident CTAs)
+    size_t static_smem[kMaxDevices] = {};
+    bool have_static[kMaxDevices] = {};
+};
+
+// Raise the kernel's dynamic shared-memory limit on the current device to at
+// least `need` bytes (only ever raised, so a concurrent smaller request never
+// lowers what another launch relies on).
+template <typename F>
+inline cudaError_t ensure_smem(F* func, KernelCfg& c, size_t need) {
+    if (need <= 48 * 1024) return cudaSuccess;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (need <= c.smem[dev]) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+    if (e == cudaSuccess) c.smem[dev] = need;
+    return e;
+}
+
+// Persistent grid of the kernel on the current device: SMs x resident CTAs.
+template <typename F>
+inline uint32_t persistent_grid(F* func, KernelCfg& c, int threads, size_t smem) {
+    const int dev = current_device();
+    if (ensure_smem(func, c, smem) != cudaSuccess) cudaGetLastError();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.grid[dev]) {
+        int per = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, func, threads, smem) != cudaSuccess) cudaGetLastError();
+        c.grid[dev] = (uint32_t)dev_props().sms * (uint32_t)(per > 0 ? per : 1);
+    }
+    return c.grid[dev];
+}
+
+template <typename F>
+inline size_t static_smem_of(F* func, KernelCfg& c) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.have_static[dev]) {
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, func) != cudaSuccess) cudaGetLastError();
+        c.static_smem[dev] = fa.sharedSizeBytes;
+        c.have_static[dev] = true;
+    }
+    return c.static_smem[dev];
 }
 
 enum ErrBits : uint32_t {

@@ -84,6 +84,7 @@ struct HostSlot {
     std::vector<uint32_t> kind, level;   // per chunk (host-only fields of ChunkSpan)
     std::vector<float> rep;              // prefill reps when the device keeps none
     std::vector<uint32_t> fanout;        // n_u per unit (fixed after build)
+    lc_index_config cfg{2.0, 64, 10, 0, 2, 0};  // IndexConfig defaults (index.hpp:13-22)
 };
 
 struct lc_index_s {
@@ -119,6 +120,7 @@ struct lc_index_s {
     lc_budgets host_budgets{};
     const float* host_q = nullptr;  // the graph's q source (mapped host buffer) or nullptr (staged)
     float* host_out = nullptr;      // the graph's output buffer (mapped host buffer or out_stage)
+    unsigned char* host_scratch = nullptr;  // sel_scratch the graph was captured with
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
 
     ~lc_index_s() {

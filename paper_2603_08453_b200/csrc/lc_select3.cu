@@ -1514,19 +1514,10 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
     Sel3Params pp = p;
     const size_t bw = (size_t)bit_words(p.a.cap_chunks) * 4;
     {
-        static int sms = 0, smem_sm = 0, smem_blk = 0;
-        static size_t st_smem = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-            cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-            cudaFuncAttributes fa{};
-            cudaFuncGetAttributes(&fa, k_pickq<D, GQ>);
-            st_smem = fa.sharedSizeBytes;
-            sms = std::max(1, sms);
-        }
+        static KernelCfg pk_attr;
+        const DevProps dp = dev_props();
+        const int sms = dp.sms, smem_sm = dp.smem_sm, smem_blk = dp.smem_blk;
+        const size_t st_smem = static_smem_of(k_pickq<D, GQ>, pk_attr);
         const unsigned long long ctas = (unsigned long long)n_slots * GQ;
         const unsigned long long per_sm = std::max(1ull, (ctas + sms - 1) / sms);
         const long long avail = std::min<long long>((long long)smem_sm / (long long)per_sm - 1024, smem_blk) -
@@ -1539,26 +1530,13 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
     if (const char* ev = getenv("LC_PICK_KEYS_CAP"))  // tests: force the unstaged (L2) key path
         pp.keys_cap = std::min<uint32_t>(pp.keys_cap, (uint32_t)std::max(2, atoi(ev)) & ~1u);
     const size_t pk_smem = (size_t)pp.keys_cap * 12 + bw;
-    static size_t co_cfg = 0, pk_cfg = 0;
-    if (co_smem > co_cfg) {
-        cudaError_t e = cudaFuncSetAttribute(k_coarse<D, GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)co_smem);
-        if (e != cudaSuccess) return e;
-        co_cfg = co_smem;
-    }
-    if (pk_smem > pk_cfg) {
-        cudaError_t e = cudaFuncSetAttribute(k_pickq<D, GQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pk_smem);
-        if (e != cudaSuccess) return e;
-        pk_cfg = pk_smem;
-    }
+    static KernelCfg co_cfg, pk_cfg, fi_cfg;
+    cudaError_t e1 = ensure_smem(k_coarse<D, GQ>, co_cfg, co_smem);
+    if (e1 != cudaSuccess) return e1;
+    e1 = ensure_smem(k_pickq<D, GQ>, pk_cfg, pk_smem);
+    if (e1 != cudaSuccess) return e1;
     k_coarse<D, GQ><<<n_slots, kCoThreads, co_smem, stream>>>(p);
-    static uint32_t fine_grid = 0;
-    if (!fine_grid) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fine<D, GQ>, kFiThreads, 0);
-        fine_grid = (uint32_t)std::max(1, sms) * (uint32_t)std::max(1, per);
-    }
+    const uint32_t fine_grid = persistent_grid(k_fine<D, GQ>, fi_cfg, kFiThreads, 0);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += kMaxAttendSlots) {
         Sel3Params q = p;
         q.a.slot0 = p.a.slot0 + s0;
@@ -1599,7 +1577,11 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
                            uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
                            const float* q_in) {
-    static unsigned long long *prof = nullptr, *prof_sp = nullptr;
+    // LC_PROF=1 (diagnostics only): per-CTA timestamps, buffers per device
+    static unsigned long long *prof_dev[kMaxDevices] = {}, *prof_sp_dev[kMaxDevices] = {};
+    const int dev = current_device();
+    unsigned long long*& prof = prof_dev[dev];
+    unsigned long long*& prof_sp = prof_sp_dev[dev];
     if (getenv("LC_PROF") && !prof) {
         cudaMalloc(&prof, (size_t)a.n_slots * a.G * 8 * 8);
         cudaMalloc(&prof_sp, (size_t)a.n_slots * 8 * 8);

@@ -213,3 +213,35 @@ def test_reference_exact_fp32_mode(d):
             r = ref.retrieve(q, token_budget=budget)
             assert_same_selection(got[g], r, (d, budget, g))
             assert rel_l2(got[g].output, r["output"]) < 1e-6, (d, budget, g)
+
+
+def test_retrieve_host_graph_survives_scratch_reallocation():
+    """lc_retrieve_host replays a cached CUDA graph; a device call with a larger
+    unit_topk reallocates the selection scratch, so the next host call must
+    re-capture instead of replaying into freed memory."""
+    S, G, n = 2, 4, 4096
+    eng = api.Engine(S, 128, G, cap_tokens=n, cap_chunks=n // 8, cap_clusters=n // 8, cap_units=64)
+    ws, refs = [], []
+    for s in range(S):
+        w = rounded_workload(n, 128, seed=70 + s, query_count=G)
+        ref = ref_engine(w, seed=70 + s)
+        eng.upload_slot(s, host_index(ref), w.keys, w.values)
+        ws.append(w)
+        refs.append(ref)
+    qh = np.ascontiguousarray(np.stack([w.queries for w in ws]), np.float32)
+    b1 = api.Budgets(token_budget=512, unit_topk=1)
+    o1 = np.zeros_like(qh)
+    eng.retrieve_host(qh, b1, o1)
+    q = torch.from_numpy(qh).cuda()
+    out = torch.zeros_like(q)
+    eng.retrieve(q, api.Budgets(token_budget=512, unit_topk=64), out=out)  # grows the scratch
+    junk = torch.full((1 << 24,), 7, dtype=torch.int32, device="cuda")    # reuse of freed memory
+    o2 = np.zeros_like(qh)
+    eng.retrieve_host(qh, b1, o2)
+    torch.cuda.synchronize()
+    assert np.array_equal(o1, o2)
+    for s in range(S):
+        for g in range(G):
+            r = refs[s].retrieve(ws[s].queries[g], token_budget=512, unit_topk=1)
+            assert_same_selection(eng.selection(s, g), r, (s, g))
+    del junk
