@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--slot-groups", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
     p.add_argument("--seed-base", type=int, default=1000)
+    p.add_argument("--parity", type=int, default=1,
+                   help="re-check sampled slots' selections against the reference (oracle/_ref) after timing")
     return p.parse_args()
 
 
@@ -148,7 +150,7 @@ def build_engine(api, torch, args, slots, device):
     torch.cuda.synchronize()
     t3 = time.time()
     setup = {"gen_s": round(t1 - t0, 2), "segment_s": round(t2 - t1, 2), "build_s": round(t3 - t2, 2)}
-    return eng, qs, setup
+    return eng, qs, setup, codes
 
 
 def time_loop(torch, fn, steps, stream):
@@ -181,6 +183,47 @@ def verify_outputs(api, torch, eng, q, out, n_tokens, slots):
             err = float(np.linalg.norm(o[s, g] - ref) / max(np.linalg.norm(ref), 1e-30))
             worst = max(worst, err)
     return worst
+
+
+def parity_vs_reference(eng, codes, qs, out, slots, budgets):
+    """Selections of the timed step vs the reference's own retrieve()
+    (oracle/_ref, retriever.cpp:161-167) on the same indexes: each sampled
+    slot's GPU-built index and K/V go to the reference through a TKIX file
+    (lc_index_save -> load_index), then every head's units, clusters (rank
+    order), scanned count and active ids must be identical and the output
+    within 1e-3 relative."""
+    from oracle import refpy as R
+    if not R.available():
+        return {"ok": None, "why": "oracle/_ref not built"}
+    o = out.cpu().numpy()
+    heads, worst, bad = 0, 0.0, []
+    t0 = time.time()
+    for s in slots:
+        texts = ["\n" if c == 1 else ("}" if c == 2 else "") for c in codes[s]]
+        fd, path = tempfile.mkstemp(suffix=".tkix")
+        os.close(fd)
+        try:
+            eng.save_index(s, path, texts)
+            ref = R.RefEngine.load(path)
+        finally:
+            os.unlink(path)
+        for g in range(qs.shape[1]):
+            r = ref.retrieve(qs[s, g], token_budget=budgets.token_budget, unit_topk=budgets.unit_topk,
+                             sink=budgets.sink_size)
+            got = eng.selection(s, g)
+            same = (got.degenerate == r["degenerate"] and np.array_equal(got.selected_units, r["units"])
+                    and np.array_equal(got.selected_clusters, r["clusters"])
+                    and got.scanned_centroids == r["scanned"]
+                    and np.array_equal(got.active_token_ids, r["active"]))
+            err = float(np.linalg.norm(o[s, g] - r["output"]) / max(np.linalg.norm(r["output"]), 1e-30))
+            worst = max(worst, err)
+            heads += 1
+            if not same or err >= 1e-3:
+                bad.append([int(s), int(g)])
+    return {"ok": not bad, "heads_checked": heads, "slots": [int(s) for s in slots], "mismatches": bad,
+            "max_rel_err_vs_reference": worst, "tolerance": 1e-3, "seconds": round(time.time() - t0, 1),
+            "what": "selected units, clusters (rank order), scanned count and active ids bit-exact vs oracle/_ref "
+                    "retrieve() on the same GPU-built index (TKIX round trip); output within tolerance"}
 
 
 def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2):
@@ -378,7 +421,7 @@ def main():
     n_slots_total = args.layers * args.kv_heads * args.batch
     # KV-head sharding: rank r owns KV heads {h : h*world // kv_heads == r} of every layer/sequence
     slots = shard.slots_of_rank(rank, world, args.layers, args.kv_heads, args.batch)
-    eng, qs, setup = build_engine(api, torch, args, slots, local)
+    eng, qs, setup, codes = build_engine(api, torch, args, slots, local)
     stream = torch.cuda.current_stream()
     q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
     out = torch.zeros_like(q)
@@ -430,6 +473,7 @@ def main():
 
     check_slots = sorted({0, len(slots) // 2, len(slots) - 1})
     max_err = verify_outputs(api, torch, eng, q, out, args.tokens, check_slots)
+    parity = parity_vs_reference(eng, codes, qs, out, check_slots, b) if args.parity else None
 
     # dominant kernel (sparse attention) and selection timed on their own
     att_ms = time_loop(torch, lambda: eng.sparse_attention(q, out), args.steps, stream)
@@ -507,6 +551,7 @@ def main():
             "check": {"max_rel_err_vs_torch_fp64": max_err, "tolerance": 1e-3, "slots": check_slots,
                       "ok": max_err < 1e-3},
             "slot_groups": args.slot_groups,
+            "parity": parity,
         }
         print(json.dumps(line))
     if world > 1:

@@ -353,7 +353,7 @@ int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
         if (ix->chunk_rep) {
             if (a.keep_reps) down(ix->chunk_rep, a.chunk_rep + so * a.cap_chunks * D, (size_t)M * D * 4);
             else if (hs.rep.size() == (size_t)M * D) std::memcpy(ix->chunk_rep, hs.rep.data(), hs.rep.size() * 4);
-            else fail(LC_ERUNTIME, "chunk representatives not kept on device (keep_reps = 0)");
+            else recompute_slot_reps(h, slot, cs.data(), M, ix->chunk_rep);
         }
         for (uint32_t u = 0; u < P; ++u) {
             const uint32_t base = unit_off[u], nu = unit_off[u + 1] - base;
@@ -480,10 +480,11 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     // k_coarse -> k_fine -> k_pickq -> k_spans (selection, per slot group), then
     // one persistent k_attend over every slot (its grid barrier needs the whole GPU)
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs, uint32_t gi) {
-        ck(launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget, b->sink_size, flags,
-                          buf_off, buf_ids, h->sel_scratch, a.max_cand, max_union, pmax, count, h->fine_ctr + 4 * gi, gs,
-                          q_in),
-           "k_select3");
+        const cudaError_t e = launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
+                                             b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, a.max_cand,
+                                             max_union, pmax, count, h->fine_ctr + 4 * gi, gs, q_in);
+        if (e != cudaSuccess)
+            fail(LC_ECUDA, std::string("k_select3: ") + g_select3_where + ": " + cudaGetErrorString(e));
     };
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
     if (groups == 1) {

@@ -510,7 +510,7 @@ void run_kmeans(KMeans& km, const float* pts, float* cents, uint32_t* assign, do
     uint32_t max_k = 0;
     for (const auto& K : km.ks) max_k = std::max(max_k, K.k);
     const size_t scatter_smem = (size_t)max_k * 4;
-    if (scatter_smem > 48 * 1024)
+    if (scatter_smem + 1024 > 48 * 1024)  // the default limit covers static + dynamic
         ck(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem),
            "k_scatter smem");
     for (uint32_t it = 0; it <= iters; ++it) {
@@ -572,6 +572,31 @@ void run_kmeans(KMeans& km, const float* pts, float* cents, uint32_t* assign, do
 }
 
 }  // namespace
+
+// chunk_representative (index.cpp:20-41) of every chunk of one slot,
+// recomputed from the bf16 store (k_reps, the build's own kernel): what
+// index_to_bytes needs when the engine keeps no representatives.  Grafted
+// chunks' representatives come from the same rows by the same rule.
+void recompute_slot_reps(lc_index_t h, uint32_t slot, const uint32_t* chunk_bounds, uint32_t M, float* out) {
+    const Arena& a = h->a;
+    if (a.kv_f32) fail(LC_ERUNTIME, "chunk representatives not kept on device (keep_reps = 0, fp32 store)");
+    if (M == 0) return;
+    std::vector<uint32_t> cstart(M), clen(M), cslot(M, slot);
+    for (uint32_t j = 0; j < M; ++j) {
+        cstart[j] = chunk_bounds[j];
+        clen[j] = chunk_bounds[j + 1] - chunk_bounds[j];
+    }
+    DBuf<uint32_t> dcs(M), dcl(M), dcslot(M), err(1);
+    dcs.up(cstart);
+    dcl.up(clen);
+    dcslot.up(cslot);
+    ck(cudaMemset(err.p, 0, 4), "memset");
+    DBuf<float> reps((size_t)M * a.d);
+    k_reps<<<(M * 32 + 255) / 256, 256>>>(a, dcs.p, dcl.p, dcslot.p, M, h->desc.pooling, reps.p, err.p);
+    ck(cudaGetLastError(), "k_reps");
+    if (err.down(1)[0]) fail(LC_ERUNTIME, "chunk_representative: pooled key has zero norm");
+    ck(cudaMemcpy(out, reps.p, (size_t)M * a.d * 4, cudaMemcpyDeviceToHost), "reps D2H");
+}
 
 extern "C" {
 

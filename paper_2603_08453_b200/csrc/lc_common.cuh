@@ -215,10 +215,11 @@ struct KernelCfg {
 
 // Raise the kernel's dynamic shared-memory limit on the current device to at
 // least `need` bytes (only ever raised, so a concurrent smaller request never
-// lowers what another launch relies on).
+// lowers what another launch relies on).  The default limit is 48 KB for
+// static + dynamic together, so any dynamic request is opted into explicitly.
 template <typename F>
 inline cudaError_t ensure_smem(F* func, KernelCfg& c, size_t need) {
-    if (need <= 48 * 1024) return cudaSuccess;
+    if (need == 0) return cudaSuccess;
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(c.mu);
     if (need <= c.smem[dev]) return cudaSuccess;

@@ -16,6 +16,7 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
                            uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
                            const float* q_in = nullptr);  // q_in: k_coarse reads q here and copies it to q
+extern thread_local char g_select3_where[96];  // failing stage of the last launch_select3
 uint32_t attend_grid(uint32_t d);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
@@ -135,3 +136,7 @@ struct lc_index_s {
     void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
 };
 
+
+// chunk_representative of every chunk of a slot, recomputed on the device from
+// the bf16 store (lc_build.cu); chunk_bounds = chunk_start[0..M]
+void recompute_slot_reps(lc_index_t h, uint32_t slot, const uint32_t* chunk_bounds, uint32_t M, float* out);

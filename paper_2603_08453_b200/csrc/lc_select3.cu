@@ -1502,6 +1502,15 @@ __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
 
 size_t select3_pick_smem(const Arena& a);
 
+// The failing stage of the last launch_select3 (thread-local; the ABI appends
+// it to the error message).
+thread_local char g_select3_where[96];
+static cudaError_t select3_fail(cudaError_t e, const char* what, size_t arg) {
+    snprintf(g_select3_where, sizeof g_select3_where, "%s (%zu)", what, arg);
+    cudaGetLastError();  // a failed launch must not leak into the next call's error check
+    return e;
+}
+
 // ---------------------------------------------------------------------------
 template <int D, int GQ>
 static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t max_union, uint32_t pmax,
@@ -1532,22 +1541,24 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
     const size_t pk_smem = (size_t)pp.keys_cap * 12 + bw;
     static KernelCfg co_cfg, pk_cfg, fi_cfg;
     cudaError_t e1 = ensure_smem(k_coarse<D, GQ>, co_cfg, co_smem);
-    if (e1 != cudaSuccess) return e1;
+    if (e1 != cudaSuccess) return select3_fail(e1, "k_coarse smem opt-in", co_smem);
     e1 = ensure_smem(k_pickq<D, GQ>, pk_cfg, pk_smem);
-    if (e1 != cudaSuccess) return e1;
+    if (e1 != cudaSuccess) return select3_fail(e1, "k_pickq smem opt-in", pk_smem);
     k_coarse<D, GQ><<<n_slots, kCoThreads, co_smem, stream>>>(p);
+    e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) return select3_fail(e1, "k_coarse launch", co_smem);
     const uint32_t fine_grid = persistent_grid(k_fine<D, GQ>, fi_cfg, kFiThreads, 0);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += kMaxAttendSlots) {
         Sel3Params q = p;
         q.a.slot0 = p.a.slot0 + s0;
         cudaError_t e = launch_pdl(k_fine<D, GQ>, dim3(fine_grid), dim3(kFiThreads), 0, stream, q,
                                    std::min<uint32_t>(kMaxAttendSlots, n_slots - s0));
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) return select3_fail(e, "k_fine launch", fine_grid);
     }
     cudaError_t e2 = launch_pdl(k_pickq<D, GQ>, dim3(GQ, n_slots), dim3(kPqThreads), pk_smem, stream, pp);
-    if (e2 != cudaSuccess) return e2;
+    if (e2 != cudaSuccess) return select3_fail(e2, "k_pickq launch", pk_smem);
     e2 = launch_pdl(k_spans<GQ>, dim3(n_slots), dim3(kSpThreads), 0, stream, p);
-    if (e2 != cudaSuccess) return e2;
+    if (e2 != cudaSuccess) return select3_fail(e2, "k_spans launch", 0);
     return cudaGetLastError();
 }
 
@@ -1587,6 +1598,7 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
         cudaMalloc(&prof_sp, (size_t)a.n_slots * 8 * 8);
         cudaMemset(prof_sp, 0, (size_t)a.n_slots * 8 * 8);
     }
+    g_select3_where[0] = 0;
     Sel3Params p{a, pick_keys_cap(a), q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
                  fine_ctr, prof_sp};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
