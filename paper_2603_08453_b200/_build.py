@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "liblychee_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CU_SOURCES = ["lc_select3.cu", "lc_attend.cu", "lc_graft.cu", "lc_build.cu", "lc_abi.cu", "lc_tkix.cu", "lc_eval.cu"]
+CU_SOURCES = ["lc_select3.cu", "lc_attend.cu", "lc_graft.cu", "lc_build.cu", "lc_abi.cu", "lc_tkix.cu", "lc_eval.cu", "lc_fused.cu"]
 CPP_SOURCES = ["lc_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ccbin", "/usr/bin/g++",

@@ -95,7 +95,8 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.urad = dalloc<double>(S * a.cap_units, o);
         a.unit_off = dalloc<uint32_t>(S * (a.cap_units + 1), o);
         a.fcent = dalloc<float>(S * d.cap_clusters * D, o);
-        a.fcent16 = dalloc<__half>(S * d.cap_clusters * D, o);
+        a.frow16 = dalloc<__half>(S * d.cap_clusters * D, o);
+        a.fmeta = dalloc<uint4>(S * d.cap_clusters, o);
         a.frad = dalloc<double>(S * d.cap_clusters, o);
         a.ftok = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.forig = dalloc<uint32_t>(S * d.cap_clusters, o);
@@ -202,7 +203,8 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
                 ++nmem[f];
             }
         std::vector<float> fcent((size_t)L * D), ucent((size_t)a.cap_units * D, 0.f);
-        std::vector<__half> f16((size_t)L * D);  // k_fine's filter copy; its error bound needs |c| <= 6e4
+        std::vector<__half> f16((size_t)L * D);  // the filters' copy; their error bound needs |c| <= 6e4
+        std::vector<double> cn2(L, 0.0);
         std::vector<double> frad(L), urad(P);
         std::vector<uint32_t> ftok(L), fn(L), fu(L);
         for (uint32_t u = 0; u < P; ++u) {
@@ -213,19 +215,33 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
                     const float c = ix->fine_centroid[(size_t)f * D + j];
                     if (!(std::fabs(c) <= 60000.f)) fail(LC_EINVAL, "fine centroids must be finite and |c| <= 6e4");
                     fcent[fine_at(base, nu, i, j, D)] = c;
-                    f16[fine_at16(base, nu, i, j, D)] = __float2half_rn(c);
+                    f16[frow_at(base, i, j, D)] = __float2half_rn(c);
+                    cn2[base + i] += (double)c * (double)c;
                 }
             }
             for (uint32_t j = 0; j < D; ++j) ucent[(size_t)j * a.cap_units + u] = ix->coarse_centroid[(size_t)u * D + j];
             urad[u] = ix->coarse_radius[u];
         }
+        std::vector<uint4> meta(L);
+        float rmax = 0.f, cmax = 0.f;
         for (uint32_t i = 0; i < L; ++i) {
             const uint32_t f = orig[i];
             frad[i] = ix->fine_radius[f];
+            if (!(frad[i] >= 0.0 && frad[i] < 1e30)) fail(LC_EINVAL, "fine radii must be finite and >= 0");
             if (ix->fine_token_count[f] > 0xffffffffull) fail(LC_EINVAL, "token_count exceeds u32");
             ftok[i] = (uint32_t)ix->fine_token_count[f];
             fn[i] = nmem[f];
             fu[i] = ix->fine_parent[f];
+            uint64_t rb;
+            std::memcpy(&rb, &frad[i], 8);
+            const float cb = norm_bound(cn2[i]);
+            uint32_t cbits;
+            std::memcpy(&cbits, &cb, 4);
+            meta[i] = make_uint4((uint32_t)rb, (uint32_t)(rb >> 32), cbits, ftok[i]);
+            float rf = (float)frad[i];
+            if ((double)rf < frad[i]) rf = nextafterf(rf, 3.0e38f);
+            rmax = std::max(rmax, rf);
+            cmax = std::max(cmax, cb);
         }
         std::vector<uint32_t> cs(M + 1), cc(M);
         for (uint32_t j = 0; j < M; ++j) {
@@ -253,7 +269,8 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         up(a.urad + so * a.cap_units, urad.data(), urad.size() * 8);
         up(a.unit_off + so * (a.cap_units + 1), unit_off.data(), unit_off.size() * 4);
         up(a.fcent + so * a.cap_clusters * D, fcent.data(), fcent.size() * 4);
-        up(a.fcent16 + so * a.cap_clusters * D, f16.data(), f16.size() * 2);
+        up(a.frow16 + so * a.cap_clusters * D, f16.data(), f16.size() * 2);
+        up(a.fmeta + so * a.cap_clusters, meta.data(), meta.size() * 16);
         up(a.frad + so * a.cap_clusters, frad.data(), frad.size() * 8);
         up(a.ftok + so * a.cap_clusters, ftok.data(), ftok.size() * 4);
         up(a.forig + so * a.cap_clusters, orig.data(), orig.size() * 4);
@@ -281,6 +298,8 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
         st.m0 = M;
         st.L = L;
         st.P = P;
+        st.rmax = rmax;
+        st.cmax = cmax;
         up(a.state + slot, &st, sizeof st);
         hs.n_tokens = n_tokens;
         hs.chunked_end = chunked_end;
@@ -466,7 +485,9 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     for (auto& s : h->hs) pmax = std::max(pmax, s.P);
     if (select3_pick_smem(a) > 200 * 1024) fail(LC_EINVAL, "retrieve: chunk capacity too large for k_pickq");
     const uint32_t max_union = needed_candidates(h, std::min<uint32_t>(a.G * std::min<uint32_t>(b->unit_topk, 64), 4096));
-    const size_t need = (size_t)a.n_slots * a.G * a.max_cand * 20;  // lo key, weight, hi (k_fine)
+    const uint32_t kc8 = (a.max_cand + 7) & ~7u;  // k_select's per-head capacity
+    // k_fine -> k_pickq: lo key, weight, hi per candidate; k_select's large-R path: key, list
+    const size_t need = (size_t)a.n_slots * a.G * std::max<size_t>((size_t)a.max_cand * 20, (size_t)kc8 * 12);
     if (h->sel_scratch_bytes < need) {
         if (h->sel_scratch) cudaFree(h->sel_scratch);
         h->sel_scratch = nullptr;
@@ -479,7 +500,17 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     }
     // k_coarse -> k_fine -> k_pickq -> k_spans (selection, per slot group), then
     // one persistent k_attend over every slot (its grid barrier needs the whole GPU)
+    uint32_t max_fanout = 0;
+    for (auto& s : h->hs)
+        for (uint32_t f : s.fanout) max_fanout = std::max(max_fanout, f);
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs, uint32_t gi) {
+        // the fused per-slot kernel when the shape fits on chip, else the four-kernel chain
+        const cudaError_t ef = launch_fused(ag, q_dev, q_in, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
+                                            b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, kc8, max_union,
+                                            pmax, max_fanout, count, gs);
+        if (ef == cudaSuccess) return;
+        if (ef != cudaErrorNotSupported) fail(LC_ECUDA, std::string("k_select: ") + cudaGetErrorString(ef));
+        cudaGetLastError();
         const cudaError_t e = launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
                                              b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, a.max_cand,
                                              max_union, pmax, count, h->fine_ctr + 4 * gi, gs, q_in);

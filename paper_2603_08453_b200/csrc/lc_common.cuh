@@ -11,13 +11,19 @@
 //   urad        f64  [slot][cap_units]               CoarseUnit::radius
 //   unit_off    u32  [slot][cap_units+1]             CoarseUnit::members as a range of
 //                                                    internal fine ids
-//   fcent       f32  [slot][cap_clusters*d]          FineCluster::centroid; the members of
-//                                                    unit u form one block [d/4][n_u][4]
-//                                                    (dimension-quad-major: a warp reads a
-//                                                    float4 per cluster per step, 512 B
-//                                                    contiguous) at unit_off[u]*d
-//   fcent16     f16  [slot][cap_clusters*d]          fcent rounded to nearest fp16 (k_fine's
-//                                                    certified filter; the exact path reads fcent)
+//   fcent       f32  [slot][cap_clusters][d]         FineCluster::centroid, one row per internal
+//                                                    id (the exact fp64 refinement reads a
+//                                                    candidate's 512 B row)
+//   frow16      f16  [slot][cap_clusters][d]         fcent rounded to nearest fp16, one row per
+//                                                    internal id (the certified filters read
+//                                                    these; the exact path reads fcent).  The 16 B
+//                                                    chunks of a row are XOR-swizzled by the row's
+//                                                    position in its unit (swz16): a linear bulk
+//                                                    copy of a unit's rows lands in shared memory
+//                                                    already conflict-free for the MMA fragments
+//   fmeta       u32x4 [slot][cap_clusters]           {radius f64 (lo, hi word), norm bound f32,
+//                                                    token_count}: what the filter needs per row,
+//                                                    copied next to the rows
 //   frad        f64  [slot][cap_clusters]            FineCluster::radius
 //   ftok        u32  [slot][cap_clusters]            FineCluster::token_count
 //   forig       u32  [slot][cap_clusters]            reference cluster id of internal id
@@ -48,7 +54,8 @@ struct SlotState {
     uint32_t L;
     uint32_t P;
     uint32_t m0;      // chunks covered by the member CSR (prefill); later ones are grafts
-    uint32_t pad[2];
+    float rmax;       // upper bound of every fine radius (raised by grafts)
+    float cmax;       // upper bound of every fine centroid norm
 };
 
 struct Span {  // one contiguous run of active tokens and the query heads it serves
@@ -81,7 +88,8 @@ struct Arena {
     double* urad;
     uint32_t* unit_off;
     float* fcent;
-    __half* fcent16;         // fcent rounded to fp16, same layout: k_fine's filter reads these
+    __half* frow16;          // fcent rounded to fp16, one swizzled row per internal id (swz16)
+    uint4* fmeta;            // {radius lo, radius hi, norm bound (f32 bits), token_count} per internal id
     double* frad;
     uint32_t* ftok;
     uint32_t* forig;
@@ -127,16 +135,33 @@ __host__ __device__ inline uint32_t plan_layout(uint32_t cap_units, uint32_t G, 
     return t + ((cap_clusters + 31) / 32) * 16;
 }
 
-// element (member `local` of the unit block starting at internal id `base` with
-// `nu` members, dimension j) of the fine-centroid array
+// element (member `local` of the unit block starting at internal id `base`,
+// dimension j) of the fine-centroid array: one contiguous 4d-byte row per
+// internal id, so the exact refinement of one candidate reads whole lines
 __host__ __device__ inline size_t fine_at(uint32_t base, uint32_t nu, uint32_t local, uint32_t j, uint32_t d) {
-    return (size_t)base * d + ((size_t)(j >> 2) * nu + local) * 4 + (j & 3);
+    (void)nu;
+    return ((size_t)base + local) * d + j;
 }
 
-// the same element in the fp16 copy, octet-major ([d/8][nu][8] per unit
-// block): one 16-byte load per lane per row in k_fine
-__host__ __device__ inline size_t fine_at16(uint32_t base, uint32_t nu, uint32_t local, uint32_t j, uint32_t d) {
-    return (size_t)base * d + ((size_t)(j >> 3) * nu + local) * 8 + (j & 7);
+// Physical 16-byte chunk of logical chunk k (dims 8k..8k+7) of the fp16 row at
+// position `local` of its unit (d = 128: 16 chunks; other head dims are not
+// swizzled).  Bits 0-2 of k are XORed with a function of local mod 8 only, so
+// rows copied to any shared-memory row with the same residue mod 8 keep the
+// pattern: the MMA B-fragment reads (rows r = 0..7, chunks {w, 4+w, 8+w, 12+w})
+// then hit 8 distinct bank groups per quarter warp.
+__host__ __device__ inline uint32_t swz16(uint32_t local, uint32_t k, uint32_t d) {
+    return d == 128 ? (k ^ ((k >> 3) << 1) ^ (local & 7u) ^ ((local >> 1) & 1u)) : k;
+}
+// element j of internal id (base + local) in the fp16 row array
+__host__ __device__ inline size_t frow_at(uint32_t base, uint32_t local, uint32_t j, uint32_t d) {
+    return ((size_t)base + local) * d + swz16(local, j >> 3, d) * 8 + (j & 7);
+}
+// norm bound stored per fine centroid: >= ||c|| of the fp32 centroid
+__host__ __device__ inline float norm_bound(double n2) {
+    const double n = sqrt(n2) * (1.0 + 1.0 / 1048576.0);
+    float f = (float)n;
+    if ((double)f < n) f = nextafterf(f, 3.0e38f);
+    return f;
 }
 
 __host__ __device__ inline size_t kv_off(const Arena& a, uint32_t slot) {

@@ -17,6 +17,10 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                            uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
                            const float* q_in = nullptr);  // q_in: k_coarse reads q here and copies it to q
 extern thread_local char g_select3_where[96];  // failing stage of the last launch_select3
+cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint32_t unit_topk, uint32_t mode,
+                         uint32_t cluster_topk, unsigned long long budget, uint32_t sink, uint32_t flags,
+                         const uint32_t* buf_off, const uint32_t* buf_ids, unsigned char* scratch, uint32_t kc,
+                         uint32_t uc, uint32_t pmax, uint32_t max_fanout, uint32_t n_slots, cudaStream_t stream);
 uint32_t attend_grid(uint32_t d);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,

@@ -49,7 +49,7 @@ __global__ void k_audit_nodes(Arena a, uint32_t slot, const float* q, uint32_t n
     if (node >= st.L + st.P) return;
     const bool fine = node < st.L;
     const float* cen;
-    size_t stride;  // element j at cen[j * stride] (fine: per-unit quad-major block)
+    size_t stride;  // coarse element j at cen[j * stride] (fine: row `local` of the unit's block)
     uint32_t quad_nu = 0, local = 0;
     double rad;
     if (fine) {
@@ -71,7 +71,7 @@ __global__ void k_audit_nodes(Arena a, uint32_t slot, const float* q, uint32_t n
 #pragma unroll
         for (int k = 0; k < kAuditQ; ++k) acc[k] = 0.0;
         for (uint32_t j = 0; j < d; ++j) {
-            const float c = fine ? cen[((size_t)(j >> 2) * quad_nu + local) * 4 + (j & 3)] : cen[(size_t)j * stride];
+            const float c = fine ? cen[(size_t)local * d + j] : cen[(size_t)j * stride];
 #pragma unroll
             for (int k = 0; k < kAuditQ; ++k)
                 if (g0 + k < nq) acc[k] = __fma_rn((double)s_q[(g0 + k) * d + j], (double)c, acc[k]);

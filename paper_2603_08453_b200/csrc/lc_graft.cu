@@ -233,10 +233,10 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         else s_dg = r;
     }
     __syncthreads();
-    __half* fcw16 = a.fcent16 + (size_t)slot * a.cap_clusters * d;
+    __half* fcw16 = a.frow16 + (size_t)slot * a.cap_clusters * d;
     for (uint32_t j = tid; j < d; j += blockDim.x) {
         fcw[fine_at(lo, nu, local, j, d)] = s_new[j];
-        fcw16[fine_at16(lo, nu, local, j, d)] = __float2half_rn(s_new[j]);
+        fcw16[frow_at(lo, local, j, d)] = __float2half_rn(s_new[j]);
     }
     const uint32_t cid = M;
     if (a.keep_reps) {
@@ -249,6 +249,17 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         const double rr = r1 < s_tonew ? s_tonew : r1;  // std::max(r + delta, to_new)
         frad[best_c] = rr;
         a.ftok[(size_t)slot * a.cap_clusters + best_c] += take;
+        // the filters' per-row copy: radius, norm bound, token count; slot bounds raised
+        double cn2 = 0.0;
+        for (uint32_t j = 0; j < d; ++j) cn2 += (double)s_new[j] * (double)s_new[j];
+        const float cb = norm_bound(cn2);
+        const unsigned long long rb = (unsigned long long)__double_as_longlong(rr);
+        a.fmeta[(size_t)slot * a.cap_clusters + best_c] =
+            make_uint4((uint32_t)rb, (uint32_t)(rb >> 32), __float_as_uint(cb),
+                       a.ftok[(size_t)slot * a.cap_clusters + best_c]);
+        float rf = __double2float_ru(rr);
+        if (rf > stp->rmax) stp->rmax = rf;
+        if (cb > stp->cmax) stp->cmax = cb;
         double* ur = a.urad + (size_t)slot * a.cap_units;
         const double rg = ur[u] < s_dg ? s_dg : ur[u];  // std::max(radius, dist)
         ur[u] = rg;

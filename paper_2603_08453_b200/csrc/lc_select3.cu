@@ -494,13 +494,13 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
         sa = stage_a(next_tile());
         while (d.slot != ~0u) {
             // (C) this tile's centroids, radius and weight: one burst of loads
-            // fp16 centroid rows (8 dims = 16 bytes per lane per row, fine_at16)
-            const uint4* col = reinterpret_cast<const uint4*>(a.fcent16 + (size_t)d.slot * a.cap_clusters * D +
-                                                             (size_t)d.base * D) + d.local;
+            // the lane's fp16 centroid row (16-byte chunks in swz16 order, frow_at)
+            const uint4* row = reinterpret_cast<const uint4*>(a.frow16 + (size_t)d.slot * a.cap_clusters * D +
+                                                             ((size_t)d.base + d.local) * D);
             uint4 v16[V / 2];
             if (d.valid) {
 #pragma unroll
-                for (uint32_t j = 0; j < V / 2; ++j) v16[j] = __ldg(col + (size_t)j * d.nu);
+                for (uint32_t j = 0; j < V / 2; ++j) v16[j] = __ldg(row + swz16(d.local, j, D));
             }
             const uint32_t cid = d.base + d.local;
             const double r = d.valid ? __ldg(a.frad + (size_t)d.slot * a.cap_clusters + cid) : 0.0;
@@ -910,13 +910,13 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
             uint32_t k = 0;
             while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
             const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k], ci = s_gbase[k] + local;
-            const float4* col = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local;
+            const float4* col = reinterpret_cast<const float4*>(fcs + ((size_t)s_gbase[k] + local) * D);
             double sacc = 0.0;
             constexpr uint32_t B = D / 4 < 8 ? D / 4 : 8;  // rows per batch (head dims 8 / 16 have fewer)
             for (uint32_t j0 = 0; j0 < D / 4; j0 += B) {  // B loads in flight, then their chain steps
                 float4 v4[B];
 #pragma unroll
-                for (uint32_t t = 0; t < B; ++t) v4[t] = __ldg(col + (size_t)(j0 + t) * nu);
+                for (uint32_t t = 0; t < B; ++t) v4[t] = __ldg(col + j0 + t);
 #pragma unroll
                 for (uint32_t t = 0; t < B; ++t) {
                 const uint32_t jq = j0 + t;
@@ -952,7 +952,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
                     uint32_t k = 0;
                     while (k + 1 < kU && s_gpre[k + 1] <= i) ++k;
                     const uint32_t local = i - s_gpre[k], nu = s_gpre[k + 1] - s_gpre[k];
-                    const float4* src = reinterpret_cast<const float4*>(fcs + (size_t)s_gbase[k] * D) + local + (size_t)jq * nu;
+                    const float4* src = reinterpret_cast<const float4*>(fcs + ((size_t)s_gbase[k] + local) * D) + jq;
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
                                      (uint32_t)__cvta_generic_to_shared(slot_col(k0 + x / (D / 4)) + jq)),
                                  "l"(src));
