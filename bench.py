@@ -34,8 +34,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "retrieval+sparse-attn decode steps/s @128K (Llama-3-8B shape); % HBM roofline"
-# our kernels per decode step: k_coarse, k_fine, k_pickq, k_spans, k_attend
-KERNELS_PER_STEP = 5
 
 
 def parse():
@@ -463,6 +461,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    launches = eng.launch_count()  # k_select, k_attend, k_merge (or the 4-kernel selection chain)
     step_bytes = eng.step_bytes()  # [union bytes, per-query bytes, union tokens, union candidates]
     if world > 1:
         t = torch.tensor(step_bytes, dtype=torch.float64, device="cuda")
@@ -544,7 +543,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": args.batch * 1000.0 / e2e_ms, "unit": "steps/s",
                     "h2d_bytes_per_step": io_bytes * world, "d2h_bytes_per_step": io_bytes * world},
-            "gpu_launches": args.steps * KERNELS_PER_STEP,
+            "gpu_launches": args.steps * launches,
+            "kernels_per_step": launches,
             "clocks": clocks,
             "setup": setup,
             "cuda_graph": graph is not None,

@@ -232,6 +232,11 @@ int lc_selection_download(lc_index_t h, uint32_t slot, uint32_t g, lc_selection_
  * (union over each slot's group), out[3] = fine candidates (union). Synchronous. */
 int lc_step_bytes(lc_index_t h, uint64_t* out);
 
+/* Kernel launches the last lc_retrieve / lc_retrieve_host / lc_decode_step
+ * made for selection + attention (k_select or the four-kernel chain, then
+ * k_attend + k_merge); the bench's gpu_launches claim. */
+int lc_launch_count(lc_index_t h, uint32_t* out);
+
 /* Sticky device-side error bits (lc_common.cuh ErrBits) of every kernel since
  * the last clear; synchronous. */
 int lc_device_error(lc_index_t h, uint32_t* out, int clear);

@@ -503,6 +503,12 @@ class Engine:
         L.check(L.lib().lc_step_bytes(self.h, out.ctypes.data))
         return [int(x) for x in out]
 
+    def launch_count(self) -> int:
+        """Kernels the last retrieve launched (selection + attention)."""
+        out = np.zeros(1, np.uint32)
+        L.check(L.lib().lc_launch_count(self.h, out.ctypes.data))
+        return int(out[0])
+
     def device_error(self, clear: bool = True) -> int:
         out = np.zeros(1, np.uint32)
         L.check(L.lib().lc_device_error(self.h, out.ctypes.data, int(clear)))

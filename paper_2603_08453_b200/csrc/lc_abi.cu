@@ -125,7 +125,6 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         const size_t groups = std::max<uint32_t>(1, std::min(d.slot_groups, d.n_slots));
         h->fine_ctr = dalloc<uint32_t>(4 * groups, o);
         ck(cudaMemset(h->fine_ctr, 0, 4 * groups * 4), "memset k_fine counters");
-        a.att_sync = dalloc<unsigned long long>(S, o);
         a.err = dalloc<uint32_t>(1, o);
         h->q_stage = dalloc<float>(S * G * D, o);
         h->out_stage = dalloc<float>(S * G * D, o);
@@ -134,7 +133,6 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         h->reps_dev = dalloc<float>(S * D, o);
         ck(cudaMemset(a.state, 0, S * sizeof(SlotState)), "memset state");
         ck(cudaMemset(a.err, 0, 4), "memset err");
-        ck(cudaMemset(a.att_sync, 0, S * 8), "memset attention sync");
         ck(cudaMemset(a.n_spans, 0, S * 4), "memset n_spans");
         ck(cudaMemset(a.slot_tok, 0, S * 4), "memset slot_tok");
         ck(cudaMemset(a.span_off, 0, S * (a.cap_spans + 1) * 4), "memset span_off");
@@ -508,7 +506,10 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         const cudaError_t ef = launch_fused(ag, q_dev, q_in, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
                                             b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, kc8, max_union,
                                             pmax, max_fanout, count, gs);
-        if (ef == cudaSuccess) return;
+        if (ef == cudaSuccess) {
+            h->last_launches += 1;
+            return;
+        }
         if (ef != cudaErrorNotSupported) fail(LC_ECUDA, std::string("k_select: ") + cudaGetErrorString(ef));
         cudaGetLastError();
         const cudaError_t e = launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
@@ -516,7 +517,9 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
                                              max_union, pmax, count, h->fine_ctr + 4 * gi, gs, q_in);
         if (e != cudaSuccess)
             fail(LC_ECUDA, std::string("k_select3: ") + g_select3_where + ": " + cudaGetErrorString(e));
+        h->last_launches += 4;
     };
+    h->last_launches = 0;
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
     if (groups == 1) {
         a.slot0 = 0;
@@ -539,7 +542,10 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         }
     }
     a.slot0 = 0;
-    if (out_dev) ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, st), "k_attend");
+    if (out_dev) {
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, st), "k_attend");
+        h->last_launches += a.kv_f32 ? 1 : 2 * ((a.n_slots + kMaxAttendSlots - 1) / kMaxAttendSlots);
+    }
     h->last_flags = flags;
     h->last_valid = 1;
 }
@@ -811,6 +817,13 @@ int lc_step_bytes(lc_index_t h, uint64_t* out) {
         out[0] = out[1] = out[2] = out[3] = 0;
         for (uint32_t s = 0; s < h->a.n_slots; ++s)
             for (int k = 0; k < 4; ++k) out[k] += sb[(size_t)s * 4 + k];
+    });
+}
+
+int lc_launch_count(lc_index_t h, uint32_t* out) {
+    return guard([&] {
+        if (!h || !out) fail(LC_EINVAL, "null argument");
+        *out = h->last_launches;
     });
 }
 

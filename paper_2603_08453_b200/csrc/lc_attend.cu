@@ -224,13 +224,68 @@ __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G
     if (!(L > 0.f) && lane == 0) atomicOr(err, kErrEmptyActive);
 }
 
-// Every head of slot s, merged by the warp that flushed the slot's last token
-// (kept out of line so the streaming loop's register allocation is unaffected).
+// Prefix sums of the slots' head / tail token counts (head_of / the rest) over
+// the launch's n slots, into shared arrays of n + 1 entries (all threads).
+template <int NT>
+__device__ __forceinline__ void slot_prefixes(const Arena& a, uint32_t n, uint32_t* s_hp, uint32_t* s_tp,
+                                              uint32_t* s_wsum) {
+    constexpr int NWP = NT / 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t per = (n + NT - 1) / NT, i0 = tid * per;
+    uint32_t lh = 0, lt = 0;
+    for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
+        const uint32_t t = a.slot_tok[a.slot0 + i];
+        lh += head_of(t);
+        lt += t - head_of(t);
+    }
+    uint32_t xh = lh, xt = lt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yh = __shfl_up_sync(0xffffffffu, xh, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+        if (lane >= (uint32_t)o) {
+            xh += yh;
+            xt += yt;
+        }
+    }
+    if (lane == 31) {
+        s_wsum[warp] = xh;
+        s_wsum[NWP + warp] = xt;
+    }
+    __syncthreads();
+    uint32_t bh = 0, bt = 0;
+    for (uint32_t w = 0; w < warp; ++w) {
+        bh += s_wsum[w];
+        bt += s_wsum[NWP + w];
+    }
+    uint32_t rh = bh + xh - lh, rt = bt + xt - lt;
+    if (tid == 0) s_hp[0] = s_tp[0] = 0;
+    for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
+        const uint32_t t = a.slot_tok[a.slot0 + i];
+        rh += head_of(t);
+        rt += t - head_of(t);
+        s_hp[i + 1] = rh;
+        s_tp[i + 1] = rt;
+    }
+    __syncthreads();
+}
+
+// After k_attend: one warp per (slot, query head) combines that head's partials
+// (log-sum-exp, fixed contributor order -> deterministic); every partial row of
+// a batch of contributors is in flight at once.
 template <int D>
-__device__ __noinline__ void merge_slot(float* out, uint32_t* err, uint32_t G, uint32_t n, const float* part,
-                                        uint32_t zero_seg, uint32_t s, uint32_t NW, uint32_t TH, uint32_t h0,
-                                        uint32_t h1, uint32_t t0, uint32_t t1, uint32_t C) {
-    for (uint32_t g = 0; g < G; ++g) merge_head<D>(out, err, G, g, n, part, zero_seg, s, NW, TH, h0, h1, t0, t1, C);
+__global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
+    pdl_wait();
+    const Arena& a = p.a;
+    const uint32_t n = p.n, warp = threadIdx.x >> 5, G = a.G;
+    __shared__ uint32_t s_hp[kMaxAttendSlots + 1], s_tp[kMaxAttendSlots + 1], s_wsum[16];
+    slot_prefixes<256>(a, n, s_hp, s_tp, s_wsum);
+    const uint32_t x = blockIdx.x * 8 + warp, s = x / G, g = x % G;
+    if (s >= n) return;
+    if (s_hp[s + 1] == s_hp[s] && s_tp[s + 1] == s_tp[s]) return;  // empty: k_attend wrote zeros
+    const uint32_t TH = s_hp[n], TP = s_tp[n];
+    const PoolShape pool = pool_shape(TP, NW);
+    merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, p.part + 16, NW + n + kPoolPerWarp * NW + n,
+                  s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C);
 }
 
 template <int D>
@@ -256,44 +311,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     __shared__ uint32_t s_wsum[2 * kAttWarps];
 
     // ---- prefixes of the slots' head and tail lengths (k_spans wrote the totals) ----
-    {
-        const uint32_t per = (n + kAttThreads - 1) / kAttThreads, i0 = tid * per;
-        uint32_t lh = 0, lt = 0;
-        for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
-            const uint32_t t = a.slot_tok[a.slot0 + i];
-            lh += head_of(t);
-            lt += t - head_of(t);
-        }
-        uint32_t xh = lh, xt = lt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t yh = __shfl_up_sync(0xffffffffu, xh, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
-            if (lane >= o) {
-                xh += yh;
-                xt += yt;
-            }
-        }
-        if (lane == 31) {
-            s_wsum[warp] = xh;
-            s_wsum[kAttWarps + warp] = xt;
-        }
-        __syncthreads();
-        uint32_t bh = 0, bt = 0;
-        for (int w = 0; w < warp; ++w) {
-            bh += s_wsum[w];
-            bt += s_wsum[kAttWarps + w];
-        }
-        uint32_t rh = bh + xh - lh, rt = bt + xt - lt;
-        if (tid == 0) s_hp[0] = s_tp[0] = 0;
-        for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
-            const uint32_t t = a.slot_tok[a.slot0 + i];
-            rh += head_of(t);
-            rt += t - head_of(t);
-            s_hp[i + 1] = rh;
-            s_tp[i + 1] = rt;
-        }
-        __syncthreads();
-    }
+    slot_prefixes<kAttThreads>(a, n, s_hp, s_tp, s_wsum);
     const uint32_t TH = s_hp[n], TP = s_tp[n];
     // slots with no active token (reference: sparse_attention throws, retriever.cpp:43)
     if (blockIdx.x == 0) {
@@ -412,14 +430,13 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     uint32_t qf[KS][4];
     float acc[NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t cur = ~0u, cur_seg = ~0u, seg_tok = 0;
+    uint32_t cur = ~0u, cur_seg = ~0u;
     const float scale = (float)(1.4426950408889634 / sqrt((double)D));
 
-    // partial (m, l, o) of this warp's current segment of slot s.  Publishing
-    // adds the segment's token count to the slot's counter; the warp whose add
-    // completes the slot's total merges every head of the slot (no warp ever
-    // waits on another CTA, so the kernel needs no co-residency guarantee)
-    auto flush = [&](uint32_t seg, uint32_t s, uint32_t ntok) {
+    // partial (m, l, o) of this warp's current segment of slot s; k_merge
+    // combines a slot's partials after the kernel (no warp waits on another CTA,
+    // so the kernel needs no co-residency guarantee)
+    auto flush = [&](uint32_t seg) {
         float l = l_run;
         l += __shfl_xor_sync(0xffffffffu, l, 1);
         l += __shfl_xor_sync(0xffffffffu, l, 2);
@@ -436,19 +453,6 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
                 o[D / 8 + j] = acc[j][1] + acc[j][3];
             }
         }
-        __threadfence();
-        __syncwarp();
-        const uint32_t tok = s_hp[s + 1] - s_hp[s] + s_tp[s + 1] - s_tp[s];
-        unsigned long long* sync = a.att_sync + a.slot0 + s;
-        uint32_t last = 0;
-        if (lane == 0) last = (uint32_t)atomicAdd(sync, (unsigned long long)ntok) + ntok == tok;
-        if (__shfl_sync(0xffffffffu, last, 0)) {
-            __threadfence();
-            merge_slot<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, n, part,
-                          NW + n + kPoolPerWarp * NW + n, s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1],
-                          pool.C);
-            if (lane == 0) atomicExch(sync, 0ull);  // ready for the next launch
-        }
     };
 
     for (uint32_t it = 0;; ++it) {
@@ -464,15 +468,13 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         cp_wait<kStages - 1>();
         __syncwarp();
         if (gd.seg != cur_seg) {
-            if (cur_seg != ~0u) flush(cur_seg, cur, seg_tok);
+            if (cur_seg != ~0u) flush(cur_seg);
             cur_seg = gd.seg;
-            seg_tok = 0;
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
             m_run = -INFINITY;
             l_run = 0.f;
         }
-        seg_tok += gd.cnt;
         if (gd.slot != cur) {
             cur = gd.slot;
             // q fragments: softmax scale and log2(e) folded in, bf16 hi (row r) + lo (row r+8)
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
         __syncwarp();  // the stage is refilled by a later iteration's issue
     }
     cp_wait<0>();
-    if (cur_seg != ~0u) flush(cur_seg, cur, seg_tok);
+    if (cur_seg != ~0u) flush(cur_seg);
     const unsigned long long t_merge = p.prof ? gtime_a() : 0ull;
 
     // the last CTA out resets the pool and the barrier for the next launch
@@ -622,7 +624,9 @@ template <int D>
 static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStream_t stream) {
     cudaError_t e = ensure_smem(k_attend<D>, attend_cfg<D>(), attend_smem<D>());
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_attend<D>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
+    e = launch_pdl(k_attend<D>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(k_merge<D>, dim3((p.n * p.a.G + 7) / 8), dim3(256), 0, stream, p, grid * (uint32_t)kAttWarps);
 }
 
 // Persistent grid: every SM of the current device holds as many CTAs as fit.

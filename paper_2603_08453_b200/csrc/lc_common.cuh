@@ -113,7 +113,6 @@ struct Arena {
                              //   token row | head mask << 24 (k_spans -> k_attend)
     uint32_t* slot_tok;      // [slot] union active token count (length of the row list)
     unsigned long long* step_bytes;  // [slot][4]
-    unsigned long long* att_sync;  // [slot] k_attend: tokens flushed so far (the completing warp merges and resets)
     uint32_t* err;           // [1]
 };
 

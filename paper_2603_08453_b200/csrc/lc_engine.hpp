@@ -110,6 +110,7 @@ struct lc_index_s {
     }
     uint32_t last_flags = 0;
     uint32_t last_valid = 0;
+    uint32_t last_launches = 0;                // kernels of the last selection + attention
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
     unsigned char* sel_scratch = nullptr;      // per-head candidate keys + weights (k_fine -> k_pickq)
     size_t sel_scratch_bytes = 0;

@@ -126,6 +126,7 @@ struct FusedParams {
     uint32_t uc;             // union candidate capacity (shared-memory weights)
     uint32_t smem_a;         // bytes of region A
     uint32_t g8cap;          // entries of the 8-row group table
+    uint32_t pf;             // stages requested into L2 beyond the ring
     unsigned long long* prof;  // optional per-slot phase timestamps [slot][8] (LC_PROF=1)
 };
 
@@ -463,34 +464,61 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
     if (warp == kFuThreads / 32 - 1) {
         // producer: stage t holds groups [8t, 8t + 8) of the padded stream; each run of
         // groups of one unit is one bulk copy of its rows (and one of their meta)
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // region A was written generically in P1
-            for (uint32_t t = 0; t < nstage; ++t) {
-                const uint32_t s = t % kFuStages;
-                if (t >= kFuStages) mbar_wait(smem_u32(&s_bar[kFuStages + s]), ((t / kFuStages) - 1) & 1u);
-                uint32_t rk[8], rl[8], rn[8], rr[8], nrun = 0, bytes = 0;
-                const uint32_t ge = min(ng, 8 * t + 8);
-                for (uint32_t gi = 8 * t; gi < ge;) {
-                    const uint32_t e = g8[gi], k = e >> 16, l0 = e & 0xffffu, nu = s_uu[k][3];
-                    uint32_t gj = gi + 1;
-                    while (gj < ge && (g8[gj] >> 16) == k) ++gj;
-                    const uint32_t l1 = min(nu, (g8[gj - 1] & 0xffffu) + 8);
-                    rk[nrun] = k;
-                    rl[nrun] = l0;
-                    rn[nrun] = l1 - l0;
-                    rr[nrun] = 8 * (gi - 8 * t);
-                    bytes += (l1 - l0) * (D * 2 + 16);
-                    ++nrun;
-                    gi = gj;
-                }
+        // Warp-parallel: lane j < 8 looks at group 8t + j and, when a run of one unit's
+        // groups starts there, issues that run's copies.
+        if (lane == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P1 wrote region A
+        __syncwarp();
+        // one run per lane: (copy source row, rows, stage row); false when no run starts here
+        auto run_of = [&](uint32_t t, uint32_t& cid, uint32_t& rows, uint32_t& srow) -> bool {
+            const uint32_t gi = 8 * t + lane, ge = min(ng, 8 * t + 8);
+            const bool valid = lane < 8 && gi < ge;
+            const uint32_t e = valid ? g8[gi] : 0xffffffffu;
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, e, 1);
+            const bool start = valid && (lane == 0 || (prev >> 16) != (e >> 16));
+            const unsigned int sb = __ballot_sync(0xffffffffu, start);
+            // the run covers groups [gi, next start or the stage end)
+            const unsigned int later = sb & ~((2u << lane) - 1u);
+            const uint32_t gend = later ? 8 * t + (__ffs(later) - 1) : ge;
+            const uint32_t last = __shfl_sync(0xffffffffu, e, (gend - 8 * t - 1) & 31);
+            if (!start) return false;
+            const uint32_t k = e >> 16, l0 = e & 0xffffu;
+            const uint32_t l1 = min(s_uu[k][3], (last & 0xffffu) + 8);
+            cid = s_uu[k][2] + l0;
+            rows = l1 - l0;
+            srow = 8 * (gi - 8 * t);
+            return true;
+        };
+        // stages beyond the shared-memory ring are requested into L2 ahead of their copy
+        auto prefetch = [&](uint32_t t) {
+            if (t >= nstage) return;
+            uint32_t cid, rows, srow;
+            if (run_of(t, cid, rows, srow)) {
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(rows_g + (size_t)cid * D * 2),
+                             "r"(rows * D * 2)
+                             : "memory");
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(meta_g + cid), "r"(rows * 16)
+                             : "memory");
+            }
+        };
+        for (uint32_t t = 0; t < nstage; ++t) {
+            const uint32_t s = t % kFuStages;
+            if (p.pf) {  // keep stages [t + ring, t + ring + pf) requested into L2
+                if (t == 0)
+                    for (uint32_t f = kFuStages; f < kFuStages + p.pf; ++f) prefetch(f);
+                else
+                    prefetch(t + kFuStages + p.pf - 1);
+            }
+            if (t >= kFuStages) mbar_wait(smem_u32(&s_bar[kFuStages + s]), ((t / kFuStages) - 1) & 1u);
+            uint32_t cid = 0, rows = 0, srow = 0;
+            const bool mine = run_of(t, cid, rows, srow);
+            const uint32_t bytes = __reduce_add_sync(0xffffffffu, mine ? rows * (D * 2 + 16) : 0u);
+            const uint32_t fb = smem_u32(&s_bar[s]);
+            if (lane == 0) mbar_arrive_tx(fb, bytes);
+            __syncwarp();
+            if (mine) {
                 const uint32_t sbase = smem_u32(sm + s * kFuStageBytes);
-                const uint32_t fb = smem_u32(&s_bar[s]);
-                mbar_arrive_tx(fb, bytes);
-                for (uint32_t i = 0; i < nrun; ++i) {
-                    const uint32_t cid = s_uu[rk[i]][2] + rl[i];
-                    bulk_g2s(sbase + rr[i] * (D * 2), rows_g + (size_t)cid * D * 2, rn[i] * D * 2, fb);
-                    bulk_g2s(sbase + kFuRows * D * 2 + rr[i] * 16, meta_g + cid, rn[i] * 16, fb);
-                }
+                bulk_g2s(sbase + srow * (D * 2), rows_g + (size_t)cid * D * 2, rows * D * 2, fb);
+                bulk_g2s(sbase + kFuRows * D * 2 + srow * 16, meta_g + cid, rows * 16, fb);
             }
         }
     } else {
@@ -1371,7 +1399,8 @@ cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint
         cudaMemset(prof, 0, (size_t)a.n_slots * 16 * 8);
     }
     FusedParams fp{a, q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids,
-                   scratch, kc, uc, smem_a, fu_g8cap(uc), want_prof ? prof : nullptr};
+                   scratch, kc, uc, smem_a, fu_g8cap(uc), 0u, want_prof ? prof : nullptr};
+    if (const char* ev = getenv("LC_FUSED_PF")) fp.pf = (uint32_t)atoi(ev);  // experiments
     cudaError_t e;
     switch (a.G) {
         case 1: e = launch_fused_g<1>(fp, n_slots, lay.total, stream); break;
