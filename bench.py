@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--slot-groups", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
     p.add_argument("--seed-base", type=int, default=1000)
+    p.add_argument("--ref-slots", type=int, default=4,
+                   help="distinct reference-built slots the CPU reference timing spreads its calls over")
     p.add_argument("--parity", type=int, default=1,
                    help="re-check sampled slots' selections against the reference (oracle/_ref) after timing")
     return p.parse_args()
@@ -224,29 +226,57 @@ def parity_vs_reference(eng, codes, qs, out, slots, budgets):
                     "retrieve() on the same GPU-built index (TKIX round trip); output within tolerance"}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2):
-    """The reference's own CPU path (oracle/_ref) on a bounded sample: one
-    reference-built slot of the configured context, and per step all
-    n_query_heads retrieve() calls (ids + sparse attention) against it (its
-    queries cycled), OpenMP over calls with every host thread (mode B), after
-    one warm-up step.  Mode A (the reference API as-is: serial calls, OpenMP
-    inside the kernels) is timed on one slot's queries and scaled."""
+    """The reference's own CPU path (oracle/_ref) on a bounded sample:
+    args.ref_slots distinct reference-built slots of the configured context
+    (gen_clustered_workload seeds seed_base+s, build_index on the host), and per
+    step n_query_heads retrieve() calls (ids + sparse attention) spread evenly
+    over them (each slot's own queries cycled), OpenMP over calls with every
+    host thread (mode B), after one warm-up step.  Mode A (the reference API
+    as-is: serial calls, OpenMP inside the kernels) is timed on one slot's
+    queries and scaled."""
     from oracle import refpy as R
     if not R.available():
         return None
     t0 = time.time()
-    w = R.gen_workload(args.tokens, 128, seed=args.seed_base, query_count=args.group)
-    ref = R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base)
+    refs, qlist = [], []
+    for s in range(max(1, args.ref_slots)):
+        w = R.gen_workload(args.tokens, 128, seed=args.seed_base + s, query_count=args.group)
+        refs.append(R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base + s))
+        qlist.append(w.queries)
+        del w
     setup = time.time() - t0
     nthreads = R.threads() if threads == 0 else threads
-    qs = np.ascontiguousarray(np.tile(w.queries, (max(1, n_query_heads // args.group), 1)), np.float32)
-    R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1, threads=threads)  # warm-up
-    times = [R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1, threads=threads)[0]
+    per = max(1, n_query_heads // len(refs))
+    qs = np.ascontiguousarray(np.concatenate([np.tile(q, (-(-per // args.group), 1))[:per] for q in qlist]),
+                              np.float32)
+    R.time_retrieve(refs, qs, token_budget=args.budget, reps=1, mode=1, threads=threads)  # warm-up
+    times = [R.time_retrieve(refs, qs, token_budget=args.budget, reps=1, mode=1, threads=threads)[0]
              for _ in range(steps)]
-    step_b = sum(times) / len(times)
-    secs_a, _ = R.time_retrieve([ref], w.queries, token_budget=args.budget, reps=1, mode=0, threads=threads)
-    return {"threads": nthreads, "setup_s": setup, "ref": ref, "w": w, "step_s": step_b,
-            "step_mode_a_s": secs_a / args.group * n_query_heads, "calls": qs.shape[0] * steps}
+    step_b = sum(times) / len(times) * n_query_heads / qs.shape[0]
+    secs_a, _ = R.time_retrieve(refs[:1], qlist[0], token_budget=args.budget, reps=1, mode=0, threads=threads)
+    return {"threads": nthreads, "setup_s": setup, "refs": refs, "qs": qs, "step_s": step_b,
+            "step_mode_a_s": secs_a / args.group * n_query_heads, "calls": qs.shape[0] * steps,
+            "cpu": cpu_model()}
+
+
+def ref_sample_text(args, n_qh, base):
+    return (f"oracle/_ref (the reference built from /root/reference): {len(base['refs'])} distinct "
+            f"reference-built {args.tokens}-token slots (seeds {args.seed_base}..{args.seed_base + len(base['refs']) - 1}, "
+            f"build_index on the host, {base['setup_s']:.0f} s); each step = {n_qh} retrieve() calls (ids + sparse "
+            f"attention) spread evenly over them, each slot's {args.group} queries cycled; OpenMP over calls on "
+            f"{base['threads']} threads of a {base['cpu']}. Mode A (reference API as-is, serial calls, OpenMP "
+            f"kernels): {1.0 / base['step_mode_a_s']:.3f} steps/s")
 
 
 def run_reference(args):
@@ -259,16 +289,15 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     from oracle import refpy as R
-    ref, w = base["ref"], base["w"]
-    # each step: all 1024 query-head retrieve() calls of one decode step, run
-    # against the reference-built slot (its 4 queries cycled), OpenMP over calls
-    qs = np.ascontiguousarray(np.tile(w.queries, (n_qh // args.group, 1)), np.float32)
+    refs, qs = base["refs"], base["qs"]
+    # each step: all query-head retrieve() calls of one decode step over the
+    # distinct reference-built slots, OpenMP over calls
     for _ in range(args.warmup):
-        R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1)
+        R.time_retrieve(refs, qs, token_budget=args.budget, reps=1, mode=1)
     times = []
     for _ in range(args.steps):
-        secs, _ = R.time_retrieve([ref], qs, token_budget=args.budget, reps=1, mode=1)
-        times.append(secs)
+        secs, _ = R.time_retrieve(refs, qs, token_budget=args.budget, reps=1, mode=1)
+        times.append(secs * n_qh / qs.shape[0])
     step = sum(times) / len(times)
     v = args.batch / step
     line = {
@@ -276,12 +305,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": getattr(args, "scaling", "strong"), "value_definition": VALUE_DEF, "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (reference gen_clustered_workload, seed %d)" % args.seed_base,
+        "data": "synthetic (reference gen_clustered_workload, seeds %d+slot)" % args.seed_base,
         "config": config_dict(args, 1),
         "cpu_baseline": {"value": v, "unit": "steps/s", "cores": base["threads"], "kind": "reference",
-                         "sample": f"1 reference-built {args.tokens}-token slot (build_index on the host), "
-                                   f"{n_qh} retrieve() calls per step (its {args.group} queries cycled), "
-                                   f"OpenMP over calls with {base['threads']} threads"},
+                         "cpu": base["cpu"], "sample": ref_sample_text(args, n_qh, base)},
         "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -513,12 +540,8 @@ def main():
         base = cpu_baseline_ref(args, n_slots_total * args.group)
         if base:
             cpu = {"value": 1.0 / base["step_s"], "unit": "steps/s", "cores": base["threads"],
-                   "kind": "reference",
-                   "sample": f"oracle/_ref (the reference built from /root/reference): one reference-built "
-                             f"{args.tokens}-token slot; each step = {n_slots_total * args.group} retrieve() calls "
-                             f"(ids + sparse attention) against it, its {args.group} queries cycled, OpenMP over "
-                             f"calls on {base['threads']} threads, 1 warm-up + 2 timed steps. Mode A (reference API "
-                             f"as-is, serial calls, OpenMP kernels): {1.0 / base['step_mode_a_s']:.3f} steps/s"}
+                   "kind": "reference", "cpu": base["cpu"],
+                   "sample": ref_sample_text(args, n_slots_total * args.group, base)}
     if rank == 0:
         value = args.batch * 1000.0 / ms
         line = {

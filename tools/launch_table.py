@@ -3,10 +3,11 @@
 dram__bytes_write.sum --csv) -> the markdown launch table under profiles/."""
 import collections
 import csv
+import re
 import sys
 
 
-def main(src, dst, round_tag):
+def main(src, dst, round_tag, only=None):
     rows = list(csv.reader(open(src)))
     hdr = None
     per = {}
@@ -16,6 +17,8 @@ def main(src, dst, round_tag):
             continue
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
+            if only and not re.search(only, d["Kernel Name"]):
+                continue
             per.setdefault((d["ID"], d["Kernel Name"]), {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     agg = collections.OrderedDict()
     for (i, k), m in per.items():
@@ -36,4 +39,4 @@ def main(src, dst, round_tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "r01")
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "r01", sys.argv[4] if len(sys.argv) > 4 else None)
