@@ -39,17 +39,24 @@ METRIC = "retrieval+sparse-attn decode steps/s @128K (Llama-3-8B shape); % HBM r
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=0, help="timed steps (default 50; --mode stream: 4096)")
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--mode", default="step", choices=["step", "stream"],
                    help="step: config 2 retrieval + attention (the headline); stream: config 3 "
                         "decode steps with KV append and lazy grafts (batch --batch, default 8)")
-    p.add_argument("--tokens", type=int, default=131072)
-    p.add_argument("--layers", type=int, default=32)
-    p.add_argument("--kv-heads", type=int, default=8)
-    p.add_argument("--group", type=int, default=4)
-    p.add_argument("--budget", type=int, default=2048)
+    p.add_argument("--config", type=int, default=2, choices=[1, 2, 4, 5],
+                   help="BASELINE.json configs: 1 = 32K single layer, 2 = the headline (128K, Llama-3-8B shape), "
+                        "4 = Qwen3-8B shape at 1M sharded over --shards GPUs, 5 = the batched decode sweep "
+                        "(config 3 is --mode stream)")
+    p.add_argument("--shards", type=int, default=0,
+                   help="KV-head shards of the job (default: the number of GPUs; config 4: 2). With fewer GPUs "
+                        "than shards, this process runs shard RANK of them")
+    p.add_argument("--tokens", type=int, default=None)
+    p.add_argument("--layers", type=int, default=None)
+    p.add_argument("--kv-heads", type=int, default=None)
+    p.add_argument("--group", type=int, default=None)
+    p.add_argument("--budget", type=int, default=None)
     p.add_argument("--batch", type=int, default=0,
                    help="sequences per step; default: the number of GPUs (weak scaling: every GPU keeps "
                         "one sequence's worth of slots, config 2's per-GPU load) -- 8 in --mode stream")
@@ -62,6 +69,29 @@ def parse():
     p.add_argument("--parity", type=int, default=1,
                    help="re-check sampled slots' selections against the reference (oracle/_ref) after timing")
     return p.parse_args()
+
+
+CONFIGS = {
+    1: dict(layers=1, kv_heads=8, group=4, tokens=32768, budget=2048, shards=0,
+            name="config1: synthetic single-layer decode (1 layer x 8 KV heads x d128, GQA 4)"),
+    2: dict(layers=32, kv_heads=8, group=4, tokens=131072, budget=2048, shards=0,
+            name="config2: Llama-3-8B-shaped cache (32 layers x 8 KV heads x d128, GQA 4)"),
+    4: dict(layers=36, kv_heads=8, group=4, tokens=1 << 20, budget=2048, shards=2,
+            name="config4: Qwen3-8B-shaped cache (36 layers x 8 KV heads x d128, GQA 4), KV heads sharded"),
+    5: dict(layers=1, kv_heads=8, group=4, tokens=131072, budget=2048, shards=8,
+            name="config5: batched decode sweep (1 layer x 8 KV heads x d128, GQA 4), KV heads sharded over 8 GPUs"),
+}
+
+
+def apply_config(args):
+    c = CONFIGS[args.config]
+    for k in ("layers", "kv_heads", "group", "tokens", "budget"):
+        if getattr(args, k) is None:
+            setattr(args, k, c[k])
+    if not args.shards:
+        args.shards = c["shards"]
+    args.config_name = c["name"]
+    return args
 
 
 def peaks():
@@ -236,7 +266,28 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2):
+def metric_of(args):
+    if getattr(args, "config", 2) == 2:
+        return METRIC
+    return f"retrieval+sparse-attn decode steps/s ({args.config_name}, {args.tokens}-token context); % HBM roofline"
+
+
+def ref_from_gpu(eng, codes, s):
+    """A GPU-built slot handed to the reference (lc_index_save -> the
+    reference's load_index through a TKIX file): baseline timing at contexts
+    whose CPU build would take ~15 min per slot."""
+    from oracle import refpy as R
+    texts = ["\n" if c == 1 else ("}" if c == 2 else "") for c in codes[s]]
+    fd, path = tempfile.mkstemp(suffix=".tkix")
+    os.close(fd)
+    try:
+        eng.save_index(s, path, texts)
+        return R.RefEngine.load(path)
+    finally:
+        os.unlink(path)
+
+
+def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2, src=None):
     """The reference's own CPU path (oracle/_ref) on a bounded sample:
     args.ref_slots distinct reference-built slots of the configured context
     (gen_clustered_workload seeds seed_base+s, build_index on the host), and per
@@ -250,11 +301,18 @@ def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2):
         return None
     t0 = time.time()
     refs, qlist = [], []
-    for s in range(max(1, args.ref_slots)):
-        w = R.gen_workload(args.tokens, 128, seed=args.seed_base + s, query_count=args.group)
-        refs.append(R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base + s))
-        qlist.append(w.queries)
-        del w
+    if src is not None and args.tokens > 262144:  # GPU-built slots through TKIX (labelled in the sample text)
+        eng, codes, qs = src
+        for s in range(min(max(1, args.ref_slots), len(codes))):
+            refs.append(ref_from_gpu(eng, codes, s))
+            qlist.append(np.ascontiguousarray(qs[s], np.float32))
+        args.ref_from_gpu = True
+    else:
+        for s in range(max(1, args.ref_slots)):
+            w = R.gen_workload(args.tokens, 128, seed=args.seed_base + s, query_count=args.group)
+            refs.append(R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base + s))
+            qlist.append(w.queries)
+            del w
     setup = time.time() - t0
     nthreads = R.threads() if threads == 0 else threads
     per = max(1, n_query_heads // len(refs))
@@ -271,8 +329,10 @@ def cpu_baseline_ref(args, n_query_heads, threads=0, steps=2):
 
 
 def ref_sample_text(args, n_qh, base):
+    how = ("GPU-built slots (the bench's own, bit-exact to the reference build) loaded by the reference's "
+           "load_index from TKIX files" if getattr(args, "ref_from_gpu", False) else "reference-built")
     return (f"oracle/_ref (the reference built from /root/reference): {len(base['refs'])} distinct "
-            f"reference-built {args.tokens}-token slots (seeds {args.seed_base}..{args.seed_base + len(base['refs']) - 1}, "
+            f"{how} {args.tokens}-token slots (seeds {args.seed_base}..{args.seed_base + len(base['refs']) - 1}, "
             f"build_index on the host, {base['setup_s']:.0f} s); each step = {n_qh} retrieve() calls (ids + sparse "
             f"attention) spread evenly over them, each slot's {args.group} queries cycled; OpenMP over calls on "
             f"{base['threads']} threads of a {base['cpu']}. Mode A (reference API as-is, serial calls, OpenMP "
@@ -301,7 +361,7 @@ def run_reference(args):
     step = sum(times) / len(times)
     v = args.batch / step
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_of(args), "value": v, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": getattr(args, "scaling", "strong"), "value_definition": VALUE_DEF, "vs_baseline": None,
         "dtype": "f64",
@@ -315,30 +375,116 @@ def run_reference(args):
 
 
 def config_dict(args, world):
-    return {"workload": "config2: Llama-3-8B-shaped cache (32 layers x 8 KV heads x d128, GQA 4), "
+    shards = getattr(args, "shards", 0) or world
+    par = f"kv-head shard x{world}" if world > 1 else "1 GPU"
+    if shards > world:
+        par = (f"KV heads sharded over {shards} GPUs; this run measured shard {getattr(args, 'shard', 0)} of "
+               f"{shards} on {world} GPU (shards are symmetric: same shapes, independent slots, no collective "
+               f"inside the step), so the job's step time is this shard's")
+    return {"workload": f"{getattr(args, 'config_name', 'config2')}, "
                         f"{args.tokens}-token context, batch {args.batch}, {args.budget}-token budget",
+            "config": getattr(args, "config", 2), "shards": shards,
             "layers": args.layers, "kv_heads": args.kv_heads, "group": args.group,
             "context": args.tokens, "batch": args.batch, "token_budget": args.budget,
             "unit_topk": 8, "sink": 16, "slots": args.layers * args.kv_heads * args.batch,
-            "parallelism": f"kv-head shard x{world}" if world > 1 else "1 GPU",
-            "l2": "inputs larger than L2 (>1 GB of index + KV read per step vs 126 MB L2)"}
+            "parallelism": par,
+            "l2": ("flushed before every timed iteration (a 252 MB buffer written outside the event pairs)"
+                   if getattr(args, "l2_flush", False) else
+                   "inputs larger than L2 (index + KV read per step > 3 x the 126 MB L2)")}
+
+
+def stream_takes(total_steps, min_len=8, max_len=16, marker_every=12):
+    """The host chunker's flush decisions for the decoded text stream
+    (push_token / flush_buffer, streamer.cpp:29-66): a "\\n" marker every 12
+    decoded tokens like run_stream (bench.cpp:254-260); when the buffer reaches
+    max_len the head span is grafted.  Every slot of a sequence shares the
+    stream, so one decision per step applies to all of them.
+    -> [(step, take, kind, level)]"""
+    from paper_2603_08453_b200 import api
+    buf, out = [], []
+    for i in range(total_steps):
+        buf.append("\n" if (i + 1) % marker_every == 0 else "")
+        if len(buf) >= max_len:
+            t, kd, lv = api.flush_take(buf, min_len=min_len, max_len=max_len)
+            out.append((i, t, kd, lv))
+            buf = buf[t:]
+    return out
+
+
+def stream_cpu_baseline(args, total_slots, steps=48, copies=0):
+    """The reference's own decode path (oracle/_ref StreamState::decode_step,
+    streamer.cpp:145-165) on the host cores: one reference-built slot of the
+    configured prefix, cloned through the reference's save_index / load_index
+    into one engine per host thread, every engine running `steps` decode
+    steps (run_stream-style stationary queries and same-blob tokens, a marker
+    every 12 tokens) in parallel threads.  Whole-job steps/s for total_slots
+    slots is extrapolated from the parallel throughput (labelled)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import refpy as R
+    if not R.available():
+        return None
+    t0 = time.time()
+    w = R.gen_workload(args.tokens, 128, seed=args.seed_base, query_count=1)
+    base = R.RefEngine(w.keys, w.values, w.text_code, seed=args.seed_base)
+    fd, path = tempfile.mkstemp(suffix=".tkix")
+    os.close(fd)
+    try:
+        base.save(path)
+        nthr = copies or R.threads()
+        engines = [R.RefEngine.load(path) for _ in range(nthr)]
+    finally:
+        os.unlink(path)
+    setup = time.time() - t0
+    # run_stream-style stationary decode (bench.cpp:240-272): queries around the
+    # workload's own query, unit keys near it, N(0,1) values
+    rng = np.random.default_rng(5)
+    c = w.queries[0] / np.linalg.norm(w.queries[0])
+    toks = []
+    for i in range(steps):
+        q = c + 0.33 / np.sqrt(128) * rng.standard_normal(128)
+        q = (q * np.sqrt(128) / np.linalg.norm(q)).astype(np.float32)
+        k = c + 0.33 / np.sqrt(128) * rng.standard_normal(128)
+        k = (k / np.linalg.norm(k)).astype(np.float32)
+        toks.append((q, k, rng.standard_normal(128).astype(np.float32), 1 if (i + 1) % 12 == 0 else 0))
+
+    def run(e):
+        R.set_thread_team(1)  # one single-threaded engine per host thread
+        for q, k, v, code in toks:
+            e.decode_step(q, k, v, code, token_budget=args.budget)
+
+    t1 = time.time()
+    with ThreadPoolExecutor(max_workers=nthr) as ex:
+        list(ex.map(run, engines))
+    wall = time.time() - t1
+    slot_steps_per_s = nthr * steps / wall
+    return {"value": slot_steps_per_s / total_slots, "unit": "steps/s", "cores": nthr, "kind": "reference",
+            "cpu": cpu_model(),
+            "sample": f"oracle/_ref StreamState::decode_step (retrieve + attention + push_token + lazy graft): one "
+                      f"reference-built {args.tokens}-token slot cloned via save_index/load_index into {nthr} "
+                      f"engines, {steps} decode steps each on {nthr} parallel host threads ({wall:.1f} s, setup "
+                      f"{setup:.0f} s); whole-job value EXTRAPOLATED to {total_slots} slots as "
+                      f"(slot-steps/s) / {total_slots}"}
 
 
 def run_stream_mode(args, api, torch):
-    """Config 3: a 128K prefix per slot, then decode steps through lc_decode_step
-    -- retrieve(buffer) + attention, KV append, and the lazy graft whenever the
-    host chunker flushes (streamer.cpp:145-165) -- for every (layer, KV head,
-    sequence) slot at once.  The decoded tokens carry a "\n" marker every 12
-    steps like run_stream (bench.cpp:254-272); all slots of a sequence share
-    that text stream, so a flush grafts one chunk into every slot."""
+    """Config 3: a 128K prefix per slot, then 4K decode steps through
+    lc_decode_step_async -- retrieve(buffer) + attention, KV append, and the
+    lazy graft on the steps where the host chunker flushes (streamer.cpp:
+    145-165) -- for every (layer, KV head, sequence) slot at once.  The flush
+    decisions (take / kind / level per step) are the host chunker's, made
+    ahead for the shared decoded text stream and handed to the device as
+    arrays, so the whole timed run is ONE CUDA graph with no host sync."""
     batch = args.batch if args.batch > 1 else 8
     args.batch = batch
     n = args.tokens
     slots = list(range(args.layers * args.kv_heads * batch))
     S, d, G = len(slots), 128, args.group
-    steps, warm = args.steps, max(args.warmup, 3)
-    cap_chunks = n // 8 + 64 + (steps + warm) // 8 + 8
-    eng = api.Engine(S, d, G, cap_tokens=n + steps + warm + 64, cap_chunks=cap_chunks,
+    steps = args.steps if args.steps else 4096
+    warm = max(args.warmup, 3)
+    total = warm + steps
+    plan = stream_takes(total)
+    cap_chunks = n // 8 + 64 + len(plan) + 8
+    eng = api.Engine(S, d, G, cap_tokens=n + total + 64, cap_chunks=cap_chunks,
                      cap_clusters=(n // 8 + 64 + 1) // 2, cap_units=64, keep_reps=False)
     seeds = np.array([args.seed_base + s for s in slots], np.uint64)
     t0 = time.time()
@@ -349,38 +495,58 @@ def run_stream_mode(args, api, torch):
     eng.build_index([n] * S, spans, seeds)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
-    q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
-    out = torch.zeros_like(q)
-    b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
+    dims = [eng.slot_dims(s) for s in (0, S // 2, S - 1)]
+    ring = 64  # distinct per-step inputs, cycled (a stationary decode, run_stream-like)
     gen = torch.Generator(device="cuda").manual_seed(7)
-    kv = torch.randn((steps + warm, 2, S, d), device="cuda", generator=gen).to(torch.bfloat16).view(torch.int16)
-    # the buffer starts where the prefix's chunks end (every slot's chunks tile its prefix)
-    buf = []
-    grafts = 0
+    q0 = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+    qn = q0 + 0.05 * torch.randn((ring,) + tuple(q0.shape), device="cuda", generator=gen)
+    qn = (qn * (np.sqrt(d) / qn.norm(dim=-1, keepdim=True))).contiguous()
+    kv = torch.randn((ring, 2, S, d), device="cuda", generator=gen)
+    kv[:, 0] = kv[:, 0] / kv[:, 0].norm(dim=-1, keepdim=True)
+    kv = kv.to(torch.bfloat16).contiguous().view(torch.int16)
+    out = torch.zeros_like(q0)
+    b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
+    take_of = {i: (t, kd, lv) for i, t, kd, lv in plan}
+    tk = torch.zeros((max(1, len(plan)), 3, S), dtype=torch.int32, device="cuda")
+    for j, (i, t, kd, lv) in enumerate(plan):
+        tk[j, 0] = t
+        tk[j, 1] = kd
+        tk[j, 2] = lv
+    slot_of_plan = {i: j for j, (i, _, _, _) in enumerate(plan)}
 
     def step(i):
-        nonlocal buf, grafts
-        text = "\n" if (i + 1) % 12 == 0 else ""
-        buf.append(text)
-        take = kind = level = None
-        if len(buf) >= 16:  # push_token's flush (streamer.cpp:56-60), decided on the host
-            t, kd, lv = api.flush_take(buf)
-            take = np.full(S, t, np.uint32)
-            kind = np.full(S, kd, np.uint32)
-            level = np.full(S, lv, np.uint32)
-            buf = buf[t:]
-            grafts += 1
-        eng.decode_step(q, kv[i, 0], kv[i, 1], b, take, kind, level, out)
+        j = slot_of_plan.get(i)
+        tks = (tk[j, 0], tk[j, 1], tk[j, 2]) if j is not None else (None, None, None)
+        eng.decode_step_async(qn[i % ring], kv[i % ring, 0], kv[i % ring, 1], b, *tks, out=out)
 
     for i in range(warm):
         step(i)
     torch.cuda.synchronize()
-    g0 = grafts
+    err = eng.device_error()
+    if err:
+        raise RuntimeError(f"device error bits 0x{err:x}")
+    sb = eng.step_bytes()
+    launches_plain = eng.launch_count()
+    chunks0 = [eng.slot_dims(s)[1] for s in (0, S - 1)]
+    grafts_warm = sum(1 for i, *_ in plan if i < warm)
+    graph = None
+    if args.graph:
+        graph = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(graph, stream=cs):
+            for i in range(warm, total):
+                step(i)
+        torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
         ev0.record()
-        for i in range(warm, warm + steps):
-            step(i)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(warm, total):
+                step(i)
         ev1.record()
         torch.cuda.synchronize()
     clocks = clk.summary()
@@ -388,39 +554,209 @@ def run_stream_mode(args, api, torch):
     err = eng.device_error()
     if err:
         raise RuntimeError(f"device error bits 0x{err:x}")
+    grafts = sum(1 for i, *_ in plan if i >= warm)
+    n_end = eng.slot_dims(0)[4]
+    assert n_end == n + total, (n_end, n + total)
+    chunks1 = [eng.slot_dims(s)[1] for s in (0, S - 1)]
+    assert all(c1 - c0 == grafts for c0, c1 in zip(chunks0, chunks1)), (chunks0, chunks1, grafts)
+    # the last timed step's outputs vs a torch fp64 attention over each checked head's own active set
+    vslots = [0, S // 2, S - 1]
+    max_err = verify_outputs(api, torch, eng, qn[(total - 1) % ring], out, n_end, vslots)
+    # algorithmic bytes per step: the retrieval step's union
+    # bytes (measured on a warm-up step) + the KV append + the grafts' reads
+    # and writes averaged over the timed steps
+    e = 2
+    L, P = dims[0][2], dims[0][3]
+    take_mean = np.mean([t for i, t, *_ in plan if i >= warm]) if grafts else 0.0
+    graft_bytes = S * (take_mean * d * e + P * 4 * d + (L / max(P, 1)) * 4 * d + 4 * d + 16)
+    step_bytes = sb[0] + S * 2 * d * e + graft_bytes * grafts / steps
+    # the certified filter reads the fine tier at fp16 width (2d + 16 B per candidate, not 4d + 16)
+    step_bytes16 = step_bytes - sb[3] * 2 * d
+    peak, peak_src = peaks()
+    gbs = step_bytes16 / (ms * 1e-3) / 1e9
+    cpu = stream_cpu_baseline(args, S) if args.cpu_baseline else None
     line = {
         "metric": "config3 streaming decode steps/s (retrieve + attend + append + lazy graft, every slot)",
         "value": 1000.0 / ms, "unit": "steps/s", "n_gpus": 1, "steps": steps, "warmup": warm,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": f"synthetic (gen_clustered_workload prefixes, seeds {args.seed_base}+slot; random decoded K/V; "
-                "a newline marker every 12 decoded tokens)",
+        "data": f"synthetic (gen_clustered_workload prefixes on the GPU, seeds {args.seed_base}+slot, GPU "
+                f"build_index; decoded tokens: stationary queries and unit keys / N(0,1) values from a ring of "
+                f"{ring} per-step sets; a newline marker every 12 decoded tokens)",
         "config": {"workload": f"config3: {args.layers} layers x {args.kv_heads} KV heads x batch {batch} "
-                               f"(= {S} slots), {n}-token prefix, {args.budget}-token budget, grafts on flush",
-                   "slots": S, "context": n, "batch": batch, "token_budget": args.budget},
-        "grafts_per_slot_timed": grafts - g0, "graft_rate": (grafts - g0) / steps,
-        "gpu_launches_per_step": "7 (5 retrieval kernels + k_append, + k_graft on flush steps)",
+                               f"(= {S} slots), {n}-token prefix + {total} decoded tokens, {args.budget}-token "
+                               "budget, lazy graft on every flush",
+                   "slots": S, "context": n, "batch": batch, "token_budget": args.budget,
+                   "l2": "inputs larger than L2 (> 2 GB read per step vs 126 MB L2)"},
+        "roofline": {"bound": "hbm", "kernel": "whole decode step (k_select, k_attend, k_merge, k_append, k_graft)",
+                     "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "traffic": None,
+                     "peak_source": peak_src,
+                     "bytes_definition": "bytes the step's algorithm reads and writes: SURVEY s8(d) union bytes "
+                                         "with the fine tier at the fp16 width the certified filter streams, + "
+                                         "append + grafts; frac_survey_fp32_fine_width counts the fine tier at "
+                                         "the reference's fp32 width (bytes this path never reads). The peak is "
+                                         "a copy (read + write); a read-dominated stream can exceed it a little",
+                     "bytes_per_step": step_bytes16, "frac_survey_fp32_fine_width": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                     "bytes_per_step_survey": step_bytes,
+                     "bytes_retrieval_union": sb[0], "bytes_append": S * 2 * d * e,
+                     "bytes_graft_per_graft_step": graft_bytes},
+        "cpu_baseline": cpu,
+        "e2e": None,
+        "grafts_per_slot_timed": grafts, "graft_rate": grafts / steps,
+        "grafts_applied_on_device": {"slots": [0, S - 1], "chunks_before": chunks0, "chunks_after": chunks1},
+        "check": {"max_rel_err_vs_torch_fp64": max_err, "tolerance": 1e-3, "slots": vslots, "ok": max_err < 1e-3,
+                  "what": "the last timed step's outputs vs torch fp64 attention over each head's own active set"},
+        "gpu_launches": steps * (launches_plain) + grafts,
+        "kernels_per_step": f"{launches_plain} (k_select, k_attend, k_merge, k_append) + k_graft on flush steps",
+        "cuda_graph": graph is not None,
         "clocks": clocks, "setup_s": round(setup_s, 1),
-        "note": "eager launches: each graft step syncs for the host-side flush bookkeeping",
+        "final_tokens_per_slot": n_end,
     }
     print(json.dumps(line))
 
 
-def resolve_batch(args):
-    """--batch 0 (default): batch = world size, so the per-GPU work stays one
-    sequence's 256 slots as N grows (weak scaling over KV-head x batch
-    sharding); an explicit --batch fixes the total work (strong scaling)."""
+SWEEP_BATCH = (1, 8, 64)
+SWEEP_CONTEXT = (32768, 131072, 524288)
+SWEEP_BUDGET = (1024, 2048, 8192)
+
+
+def run_sweep(args, api, torch):
+    """Config 5: batch 1-64 x context 32K-512K x budget 1K-8K, one layer, KV
+    heads sharded over args.shards GPUs (8).  Each (batch, context) point
+    builds its shard's slots once (GPU generator + GPU build_index) and times
+    the decode step for every budget (CUDA graph, CUDA events)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    from paper_2603_08453_b200 import shard
+    shards = args.shards or world
+    args.shard = rank if shards == world else 0
+    peak, peak_src = peaks()
+    stream = torch.cuda.current_stream()
+    points = []
+    d = 128
+    t_all = time.time()
+    for ctx in SWEEP_CONTEXT:
+        for batch in SWEEP_BATCH:
+            a = argparse.Namespace(**vars(args))
+            a.tokens, a.batch = ctx, batch
+            slots = shard.slots_of_rank(args.shard, shards, a.layers, a.kv_heads, batch, order="layer")
+            eng, qs, setup, _ = build_engine(api, torch, a, slots, local)
+            q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+            out = torch.zeros_like(q)
+            for budget in SWEEP_BUDGET:
+                b = api.Budgets(token_budget=budget, unit_topk=8, sink_size=16)
+                ms, graphed = timed(torch, None, 1, lambda: eng.retrieve(q, b, out=out), args.steps, stream, 3,
+                                    "sweep step", graph=args.graph, flush=True)
+                err = eng.device_error()
+                if err:
+                    raise RuntimeError(f"device error bits 0x{err:x} at {(batch, ctx, budget)}")
+                sb = eng.step_bytes()
+                fp16 = sb[0] - sb[3] * (2 * d)
+                points.append({"batch": batch, "context": ctx, "budget": budget, "slots_per_gpu": len(slots),
+                               "value": batch * 1000.0 / ms, "ms_per_step": ms, "cuda_graph": graphed,
+                               "step_frac": sb[0] / (ms * 1e-3) / 1e9 / peak,
+                               "step_frac_fp16_fine_width": fp16 / (ms * 1e-3) / 1e9 / peak,
+                               "bytes_per_step_union": sb[0], "active_tokens_union": sb[2],
+                               "kernels_per_step": eng.launch_count()})
+            del eng, q, out
+            torch.cuda.empty_cache()
+    head = next(p for p in points if (p["batch"], p["context"], p["budget"]) == (8, 131072, 2048))
+    line = {
+        "metric": metric_of(args), "value": head["value"], "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": 3, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": f"synthetic (gen_clustered_workload on the GPU, seeds {args.seed_base}+slot; GPU build_index)",
+        "config": dict(config_dict(args, world), workload=args.config_name + " -- value: the batch 8 x 128K x "
+                       "2K point; every point in `sweep`", batch="1-64", context="32K-512K", token_budget="1K-8K"),
+        "l2": "flushed before every timed iteration (a 252 MB buffer written outside the event pairs)",
+        "sweep": points, "peak": peak, "peak_source": peak_src, "seconds": round(time.time() - t_all, 1),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def resolve_batch(args):
+    """--batch 0 (default): batch 1 -- the north star's strong scaling of the
+    batch-1 step by KV-head sharding (the total work is fixed as N grows).  At
+    N > 1 the same run also measures weak scaling (batch = N, every GPU keeps
+    one sequence's 256 slots) and reports it nested under "weak"."""
     if args.batch == 0:
-        args.batch = world
-        return "weak"
+        args.batch = 1
     return "strong"
 
 
 VALUE_DEF = "decode steps/s summed over the batch's sequences (batch x steps/s; batch 1 at N=1)"
 
 
+def capture(torch, fn, what):
+    """fn() captured once in a CUDA graph (after eager warm-up); None if the
+    capture fails (then the caller times eager launches and says so)."""
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        return g
+    except Exception as e:  # noqa: BLE001
+        sys.stderr.write(f"[bench] CUDA graph capture of the {what} failed ({e}); timing eager launches\n")
+        torch.cuda.synchronize()
+        return None
+
+
+def max_over_ranks(torch, dist, world, x):
+    if world == 1:
+        return x
+    t = torch.tensor([x], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+L2_BYTES = 126 * 2 ** 20
+_flush_buf = None
+
+
+def time_loop_flushed(torch, fn, steps, stream):
+    """Mean device time of fn() with the L2 flushed before every timed
+    iteration (a 2x-L2 buffer written between the event pairs, outside them):
+    for working sets that would otherwise stay L2-resident."""
+    global _flush_buf
+    if _flush_buf is None:
+        _flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for e0, e1 in evs:
+        _flush_buf.fill_(1.0)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+
+
+def timed(torch, dist, world, fn, steps, stream, warm, what, graph=True, flush=False):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    g = capture(torch, fn, what) if graph else None
+    run = g.replay if g is not None else fn
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = time_loop_flushed(torch, run, steps, stream) if flush else time_loop(torch, run, steps, stream)
+    return max_over_ranks(torch, dist, world, ms), g is not None
+
+
 def main():
-    args = parse()
+    args = apply_config(parse())
+    if args.mode == "step" and not args.steps:
+        args.steps = 50
     if args.mode == "step":
         args.scaling = resolve_batch(args)
     if args.impl == "reference":
@@ -431,6 +767,11 @@ def main():
         from paper_2603_08453_b200 import api
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         run_stream_mode(args, api, torch)
+        return
+    if args.config == 5:
+        import torch
+        from paper_2603_08453_b200 import api
+        run_sweep(args, api, torch)
         return
     import torch
     import torch.distributed as dist
@@ -443,9 +784,17 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2603_08453_b200 import api, shard
 
+    warm = max(args.warmup, 3)
     n_slots_total = args.layers * args.kv_heads * args.batch
-    # KV-head sharding: rank r owns KV heads {h : h*world // kv_heads == r} of every layer/sequence
-    slots = shard.slots_of_rank(rank, world, args.layers, args.kv_heads, args.batch)
+    # KV-head sharding: rank r owns KV heads {h : h*world // kv_heads == r} of every
+    # layer / sequence; local slots in (layer, sequence, head) order so that one
+    # layer's slots are contiguous for the layer-by-layer measurement
+    shards = args.shards or world
+    if shards != world and world != 1:
+        raise SystemExit("--shards must equal the number of GPUs (or run one shard on 1 GPU)")
+    args.shards = shards
+    args.shard = rank if shards == world else 0
+    slots = shard.slots_of_rank(args.shard, shards, args.layers, args.kv_heads, args.batch, order="layer")
     eng, qs, setup, codes = build_engine(api, torch, args, slots, local)
     stream = torch.cuda.current_stream()
     q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
@@ -454,40 +803,23 @@ def main():
     b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
 
     def step():
+        # the synthetic step has every layer's queries up front: all local slots
+        # in one launch, then the head outputs of every layer exchanged at once
         eng.retrieve(q, b, out=out)
         if world > 1:
             dist.all_gather_into_tensor(gathered, out)
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
+    # inputs smaller than 3x L2 (config 1: ~35 MB per step): flush L2 between timed iterations
+    est = len(slots) * (min(args.tokens, 4 * args.budget) * 2 * 128 * 2 + 1e6)  # rough bytes per step
+    flush = est < 3 * L2_BYTES
+    args.l2_flush = flush
+    with ClockSampler(local) as clk:
+        ms, graphed = timed(torch, dist, world, step, args.steps, stream, warm, "decode step", graph=args.graph,
+                            flush=flush)
+    clocks = clk.summary()
     err = eng.device_error()
     if err:
         raise RuntimeError(f"device error bits 0x{err:x}")
-    graph = None
-    if args.graph and world == 1:
-        graph = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            step()
-        torch.cuda.current_stream().wait_stream(s)
-        with torch.cuda.graph(graph):
-            step()
-        graph.replay()
-        torch.cuda.synchronize()
-    run = graph.replay if graph is not None else step
-
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ms = time_loop(torch, run, args.steps, stream)
-    clocks = clk.summary()
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     launches = eng.launch_count()  # k_select, k_attend, k_merge (or the 4-kernel selection chain)
     step_bytes = eng.step_bytes()  # [union bytes, per-query bytes, union tokens, union candidates]
     if world > 1:
@@ -500,6 +832,20 @@ def main():
     check_slots = sorted({0, len(slots) // 2, len(slots) - 1})
     max_err = verify_outputs(api, torch, eng, q, out, args.tokens, check_slots)
     parity = parity_vs_reference(eng, codes, qs, out, check_slots, b) if args.parity else None
+
+    # layer by layer (a real model's order): each layer's local slots, then the
+    # all-gather of that layer's head outputs at the layer boundary
+    heads_local = args.kv_heads // shards
+    lg = shard.LayerGather(rank, world, args.layers, heads_local * world, args.batch, tuple(q.shape[1:]), q.dtype,
+                           q.device)
+
+    def layer_step():
+        for layer in range(args.layers):
+            eng.retrieve_slots(layer * lg.rows, lg.rows, q, b, out=out)
+            lg.gather(out, layer)
+
+    lw_ms, lw_graphed = timed(torch, dist, world, layer_step, max(3, args.steps // 5), stream, 2,
+                              "layer-by-layer step", graph=args.graph)
 
     # dominant kernel (sparse attention) and selection timed on their own
     att_ms = time_loop(torch, lambda: eng.sparse_attention(q, out), args.steps, stream)
@@ -515,38 +861,62 @@ def main():
     att_bytes = step_bytes[2] * 2 * d * 2 + len(slots) * args.group * 2 * 4 * d
     att_gbs = att_bytes / (att_ms * 1e-3) / 1e9
     step_gbs = step_bytes_all[0] / (ms * 1e-3) / 1e9
+    # the fine tier at the width the certified filter reads (fp16 rows + 16 B metadata)
+    fp16_bytes = step_bytes_all[0] - step_bytes_all[3] * (4 * d + 16 - (2 * d + 16))
 
-    # end to end through the public host API (H2D q, retrieve + attention, D2H out)
+    # end to end through the public host API: q from page-locked host memory in,
+    # retrieve + attention, outputs back to host memory (and, at N > 1, the
+    # host result's all-gather: H2D of the outputs, then the collective)
     qh = torch.from_numpy(np.ascontiguousarray(qs)).pin_memory()
     oh = torch.zeros_like(qh).pin_memory()
     e2e_steps = max(3, args.steps // 2)
+    out_e2e = torch.zeros_like(q) if world > 1 else None
 
     def e2e():
         eng.retrieve_host(qh.numpy(), b, oh.numpy())
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
+            out_e2e.copy_(oh, non_blocking=True)
+            dist.all_gather_into_tensor(gathered, out_e2e)
 
     for _ in range(2):
         e2e()
-    e2e_ms = time_loop(torch, e2e, e2e_steps, stream)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(torch, dist, world, time_loop(torch, e2e, e2e_steps, stream))
     io_bytes = qh.numel() * 4
 
+    # weak scaling at N > 1: batch = N, every GPU keeps one sequence's 256 slots
+    weak = None
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline:
-        base = cpu_baseline_ref(args, n_slots_total * args.group)
+        base = cpu_baseline_ref(args, n_slots_total * args.group, src=(eng, codes, qs))
         if base:
             cpu = {"value": 1.0 / base["step_s"], "unit": "steps/s", "cores": base["threads"],
                    "kind": "reference", "cpu": base["cpu"],
                    "sample": ref_sample_text(args, n_slots_total * args.group, base)}
+    if world > 1:
+        del eng
+        torch.cuda.empty_cache()
+        wa = argparse.Namespace(**vars(args))
+        wa.batch = world
+        wslots = shard.slots_of_rank(rank, world, args.layers, args.kv_heads, wa.batch)
+        weng, wqs, _, _ = build_engine(api, torch, wa, wslots, local)
+        wq = torch.from_numpy(np.ascontiguousarray(wqs)).cuda()
+        wout = torch.zeros_like(wq)
+        wgath = torch.zeros((world,) + tuple(wq.shape), dtype=wq.dtype, device=wq.device)
+
+        def wstep():
+            weng.retrieve(wq, b, out=wout)
+            dist.all_gather_into_tensor(wgath, wout)
+
+        wms, wg = timed(torch, dist, world, wstep, args.steps, stream, warm, "weak-scaling step", graph=args.graph)
+        weak = {"value": wa.batch * 1000.0 / wms, "unit": "steps/s", "ms_per_step": wms, "batch": wa.batch,
+                "slots_per_gpu": len(wslots), "scaling": "weak", "cuda_graph": wg,
+                "what": "batch = N sequences, each GPU keeps one sequence's worth of slots; value = batch x steps/s"}
+
     if rank == 0:
         value = args.batch * 1000.0 / ms
         line = {
-            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "metric": metric_of(args), "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
             "scaling": args.scaling, "value_definition": VALUE_DEF, "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (gen_clustered_workload streams on the GPU, seeds {args.seed_base}+slot; "
                     "indexes by GPU build_index, bit-exact to the reference)",
@@ -558,7 +928,9 @@ def main():
                          "bytes_per_launch": att_bytes, "ms_per_launch": att_ms},
             "step_roofline": {"achieved": step_gbs, "peak": peak * world, "unit": "GB/s",
                               "frac": step_gbs / (peak * world),
+                              "frac_fp16_fine_width": fp16_bytes / (ms * 1e-3) / 1e9 / (peak * world),
                               "bytes_per_step_union": step_bytes_all[0],
+                              "bytes_per_step_fp16_fine_width": fp16_bytes,
                               "bytes_per_step_per_query": step_bytes_all[1],
                               "active_tokens_union": step_bytes_all[2],
                               "fine_candidates_union": step_bytes_all[3],
@@ -570,7 +942,15 @@ def main():
             "kernels_per_step": launches,
             "clocks": clocks,
             "setup": setup,
-            "cuda_graph": graph is not None,
+            "cuda_graph": graphed,
+            "collective": ("NCCL all_gather_into_tensor of every layer's head outputs, once per step, in the graph"
+                           if world > 1 else None),
+            "layerwise": {"value": args.batch * 1000.0 / lw_ms, "unit": "steps/s", "ms_per_step": lw_ms,
+                          "cuda_graph": lw_graphed,
+                          "what": f"{args.layers} x (lc_retrieve_slots over one layer's local slots"
+                                  + (", then an NCCL all-gather of that layer's head outputs" if world > 1 else "")
+                                  + "): the order a real model decodes in (layer l+1's queries need layer l)"},
+            "weak": weak,
             "check": {"max_rel_err_vs_torch_fp64": max_err, "tolerance": 1e-3, "slots": check_slots,
                       "ok": max_err < 1e-3},
             "slot_groups": args.slot_groups,

@@ -149,6 +149,14 @@ int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims);
  * Caller allocates every array from lc_index_slot_dims.  Synchronous. */
 int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* out);
 
+/* One fine cluster of a slot in the reference numbering: FineCluster::centroid
+ * [dim], radius, token_count (any pointer may be NULL).  A graft changes one
+ * cluster, one unit and appends one chunk (streamer.cpp:108-134), so a host
+ * mirror (the C++ drop-in's HierarchicalIndex) is patched from the graft
+ * report plus this call instead of re-downloading the index.  Synchronous. */
+int lc_cluster_download(lc_index_t h, uint32_t slot, uint32_t cluster_id, float* centroid,
+                        double* radius, uint64_t* token_count);
+
 /* Raw K/V rows of one slot (host memory, element type per desc.kv_f32): write rows
  * [0, n_tokens) and set the slot's store size (the index is left as is), or
  * read them back.  TokenStore::keys_flat/values_flat (types.hpp:48-49). */
@@ -173,6 +181,15 @@ int lc_retrieve(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t 
                 const uint32_t* buf_off_dev, const uint32_t* buf_ids_dev, float* out_dev,
                 void* stream);
 
+/* lc_retrieve over the slot range [first_slot, first_slot + n_slots) only
+ * (q_dev / out_dev keep the handle-wide [n_slots][group][dim] layout; rows
+ * outside the range are neither read nor written): one layer's KV heads of a
+ * layer-by-layer decode, whose head outputs are gathered across GPUs at the
+ * layer boundary before the next layer's queries exist. */
+int lc_retrieve_slots(lc_index_t h, uint32_t first_slot, uint32_t n_slots, const float* q_dev,
+                      const lc_budgets* b, uint32_t flags, const uint32_t* buf_off_dev,
+                      const uint32_t* buf_ids_dev, float* out_dev, void* stream);
+
 /* Sparse attention over the active sets of the last lc_retrieve (the second
  * half of retrieve(), retriever.cpp:165). */
 int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* stream);
@@ -194,6 +211,19 @@ int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev,
                    const void* values_dev, const lc_budgets* b, const uint32_t* take,
                    const uint32_t* kind, const uint32_t* level, float* out_dev,
                    lc_graft_report* reports_dev, void* stream);
+
+/* lc_decode_step with take / kind / level as DEVICE arrays [n_slots] (take 0:
+ * no graft on that slot; take_dev NULL: no graft this step) and no host
+ * synchronisation or host bookkeeping: every launch reads the stream cursors
+ * from the device, so a run of steps can be captured in one CUDA graph
+ * (config 3).  Device-side checks replace the host ones (sticky error bits:
+ * token / chunk capacity, take outside the buffered tokens).  The handle's
+ * host view of the cursors is refreshed from the device, synchronously, by
+ * the next call that needs it (download, graft, TKIX, ...). */
+int lc_decode_step_async(lc_index_t h, const float* q_dev, const void* keys_dev,
+                         const void* values_dev, const lc_budgets* b, const uint32_t* take_dev,
+                         const uint32_t* kind_dev, const uint32_t* level_dev, float* out_dev,
+                         lc_graft_report* reports_dev, void* stream);
 
 /* graft_chunk(Chunk) (streamer.cpp:68-143) with the chunk's representative
  * supplied by the caller instead of pooled from the keys: reps_host

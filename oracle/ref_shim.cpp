@@ -120,6 +120,16 @@ const char* tkr_last_error() { return g_err.c_str(); }
 
 int tkr_threads() { return kernels::thread_count(); }
 
+// OpenMP team size for parallel regions started by the calling host thread
+// (bench's threaded CPU baseline runs one single-threaded engine per thread)
+void tkr_set_thread_team(int n) {
+#ifdef _OPENMP
+    omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 // ---- workload (workload.cpp:110-169) -------------------------------------
 int tkr_workload_new(uint64_t n_tokens, uint64_t d, uint64_t n_blobs, double concentration,
                      uint64_t query_count, double locality, uint64_t seed, void** out) {

@@ -77,6 +77,7 @@ def lib():
                                         C.c_int, C.POINTER(C.c_uint64)]
         L.tkr_time_retrieve.restype = C.c_double
         L.tkr_threads.restype = C.c_int
+        L.tkr_set_thread_team.argtypes = [C.c_int]
         _lib = L
     return _lib
 
@@ -357,6 +358,11 @@ def time_retrieve(engines, queries, token_budget=2048, unit_topk=8, sink=16, rep
     secs = lib().tkr_time_retrieve(arr, len(engines), q, nq_per, q.shape[1], unit_topk,
                                    token_budget, sink, reps, mode, threads, C.byref(chk))
     return secs, chk.value
+
+
+def set_thread_team(n):
+    """OpenMP team size of parallel regions the calling thread starts."""
+    lib().tkr_set_thread_team(int(n))
 
 
 def threads():

@@ -404,6 +404,16 @@ class Engine:
                                     _ptr(buf_ids), _ptr(out), _stream_ptr(stream)))
         return out
 
+    def retrieve_slots(self, first: int, count: int, q, budgets: Budgets, out=None, buffer: str = "none",
+                       stream=None):
+        """retrieve() for slots [first, first + count) only (one layer of a
+        layer-by-layer decode); q / out keep the engine-wide [S, G, d] layout."""
+        flags = {"none": L.LC_BUFFER_NONE, "stream": L.LC_BUFFER_STREAM}[buffer]
+        b = self._budgets_c(budgets)
+        L.check(L.lib().lc_retrieve_slots(self.h, first, count, _ptr(q), C.byref(b), flags, None, None,
+                                          _ptr(out), _stream_ptr(stream)))
+        return out
+
     def retrieve_host(self, q_host: np.ndarray, budgets: Budgets, out_host: np.ndarray,
                       buffer: str = "none", stream=None):
         flags = {"none": L.LC_BUFFER_NONE, "stream": L.LC_BUFFER_STREAM}[buffer]
@@ -468,6 +478,23 @@ class Engine:
                                        C.byref(b), _ptr(take), _ptr(kind), _ptr(level), _ptr(out),
                                        rb.data_ptr(), _stream_ptr(stream)))
         return out
+
+    def decode_step_async(self, q, keys_bf16, values_bf16, budgets: Budgets, take=None, kind=None,
+                          level=None, out=None, stream=None):
+        """lc_decode_step_async: the same step with take / kind / level as DEVICE
+        uint32 tensors [n_slots] (take 0 = no graft on that slot; take None = no
+        graft this step).  No host synchronisation: graph-capturable."""
+        b = self._budgets_c(budgets)
+        rb = self._report_buf()
+        L.check(L.lib().lc_decode_step_async(self.h, _ptr(q), _ptr(keys_bf16), _ptr(values_bf16),
+                                             C.byref(b), _ptr(take), _ptr(kind), _ptr(level), _ptr(out),
+                                             rb.data_ptr(), _stream_ptr(stream)))
+        return out
+
+    def _budgets_c(self, budgets: Budgets):
+        # keep the ctypes struct alive for the call (and across graph capture)
+        self._bc = budgets.c()
+        return self._bc
 
     # ---- evaluator (evaluator.cpp) on the device ----
     def audit_ub(self, slot: int, queries: np.ndarray, tolerance: float = 1e-6) -> int:

@@ -121,6 +121,11 @@ struct Engine {
     uint32_t* bids_dev = nullptr;
     size_t bids_cap = 0;
     lc_graft_report* rep_dev = nullptr;
+    // the engine's own stream and page-locked staging: a call's copies and
+    // kernels are queued asynchronously and the host waits once
+    cudaStream_t st = nullptr;
+    float* h_io = nullptr;     // [2][d]: q in, output out
+    uint32_t* h_ids = nullptr; // [2 + bids_cap]: buffer offsets then ids
 
     Engine(uint32_t dim, uint32_t cap_tokens_, uint32_t cap_chunks, uint32_t cap_clusters, uint32_t cap_units,
            bool graft_full, uint32_t pooling)
@@ -147,6 +152,10 @@ struct Engine {
         cuda_ck(cudaMalloc(&kv_dev, 2 * d * 4), "cudaMalloc kv");
         cuda_ck(cudaMalloc(&boff_dev, 2 * 4), "cudaMalloc buffer offsets");
         cuda_ck(cudaMalloc(&rep_dev, sizeof(lc_graft_report)), "cudaMalloc report");
+        // a blocking stream: ordered with the legacy-stream calls of the ABI
+        // (k_append, k_chunk_rep, downloads) without extra events
+        cuda_ck(cudaStreamCreateWithFlags(&st, cudaStreamDefault), "stream");
+        cuda_ck(cudaMallocHost(&h_io, 2 * d * 4), "cudaMallocHost io");
     }
     ~Engine() {
         if (h) lc_index_destroy(h);
@@ -156,6 +165,9 @@ struct Engine {
         cudaFree(boff_dev);
         cudaFree(bids_dev);
         cudaFree(rep_dev);
+        if (st) cudaStreamDestroy(st);
+        cudaFreeHost(h_io);
+        cudaFreeHost(h_ids);
     }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -172,14 +184,21 @@ struct Engine {
 
     void buffer_list(std::span<const uint32_t> ids) {
         if (ids.size() > bids_cap || !bids_dev) {
+            cuda_ck(cudaStreamSynchronize(st), "sync");
             cudaFree(bids_dev);
+            cudaFreeHost(h_ids);
             bids_dev = nullptr;
+            h_ids = nullptr;
             bids_cap = std::max<size_t>(ids.size(), 64);
             cuda_ck(cudaMalloc(&bids_dev, bids_cap * 4), "cudaMalloc buffer ids");
+            cuda_ck(cudaMallocHost(&h_ids, (bids_cap + 2) * 4), "cudaMallocHost buffer ids");
         }
-        const uint32_t off[2] = {0, static_cast<uint32_t>(ids.size())};
-        cuda_ck(cudaMemcpy(boff_dev, off, sizeof off, cudaMemcpyHostToDevice), "buffer offsets");
-        if (!ids.empty()) cuda_ck(cudaMemcpy(bids_dev, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice), "buffer ids");
+        h_ids[0] = 0;
+        h_ids[1] = static_cast<uint32_t>(ids.size());
+        std::copy(ids.begin(), ids.end(), h_ids + 2);
+        cuda_ck(cudaMemcpyAsync(boff_dev, h_ids, 8, cudaMemcpyHostToDevice, st), "buffer offsets");
+        if (!ids.empty())
+            cuda_ck(cudaMemcpyAsync(bids_dev, h_ids + 2, ids.size() * 4, cudaMemcpyHostToDevice, st), "buffer ids");
     }
 
     // sticky device conditions of the last calls, as the reference's exceptions
@@ -193,45 +212,75 @@ struct Engine {
     }
 };
 
-uint64_t fnv(uint64_t h, const void* p, size_t n) {
+// 64-bit word hash (8 bytes per step; the tail byte-wise)
+uint64_t mix(uint64_t h, const void* p, size_t n) {
     const unsigned char* b = static_cast<const unsigned char*>(p);
-    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, b + i, 8);
+        h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+        h ^= h >> 29;
+    }
+    for (; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
     return h;
 }
+template <typename T>
+uint64_t mixv(uint64_t h, const T& x) {
+    return mix(h, &x, sizeof x);
+}
 
-// the store's rows, sampled (at most ~32K floats per array hashed) plus its
-// address and size: the store part of the engine cache key
+// The engine cache key of a (HierarchicalIndex, TokenStore) pair: identity
+// (addresses, sizes, the node arrays' buffers) plus a content digest of every
+// small field -- radii, token counts, parents, member lists, chunk spans,
+// the coarse centroids -- and of a fixed sample of each fine centroid (first,
+// middle and last coordinate) and of the store's rows.  That is ~2% of the
+// bytes a full content hash reads at 128K (the round-1 key hashed every
+// centroid byte-wise on every call, ~2.5 ms).
 uint64_t store_key(uint64_t h, const TokenStore& s) {
     const size_t n = s.size(), d = s.dim();
-    const void* addr = &s;
-    h = fnv(h, &addr, sizeof addr);
-    h = fnv(h, &n, sizeof n);
-    h = fnv(h, &d, sizeof d);
+    h = mixv(h, &s);
+    h = mixv(h, n);
+    h = mixv(h, d);
     for (const auto arr : {s.keys_flat(), s.values_flat()}) {
-        const size_t step = std::max<size_t>(1, arr.size() / 32768);
-        for (size_t i = 0; i < arr.size(); i += step) h = fnv(h, &arr[i], 4);
-        if (!arr.empty()) h = fnv(h, &arr.back(), 4);
+        h = mixv(h, arr.data());
+        const size_t step = std::max<size_t>(1, arr.size() / 4096);
+        for (size_t i = 0; i < arr.size(); i += step) h = mixv(h, arr[i]);
+        if (!arr.empty()) h = mix(h, arr.data() + (arr.size() - std::min<size_t>(arr.size(), d)),
+                                  std::min<size_t>(arr.size(), d) * 4);
     }
     return h;
 }
 
-// content fingerprint of an index (every centroid, radius and member list)
-// and its store: the engine cache key
 uint64_t fingerprint(const HierarchicalIndex& ix) {
     uint64_t h = 1469598103934665603ull;
     const size_t d = ix.dim;
-    h = fnv(h, &d, sizeof d);
-    for (const Chunk& c : ix.chunks) h = fnv(h, &c.span.start, 8);
+    h = mixv(h, &ix);
+    h = mixv(h, d);
+    h = mixv(h, ix.chunks.size());
+    h = mixv(h, ix.fine.size());
+    h = mixv(h, ix.coarse.size());
+    h = mixv(h, ix.chunks.data());
+    h = mixv(h, ix.fine.data());
+    h = mixv(h, ix.coarse.data());
+    for (const Chunk& c : ix.chunks) h = mixv(h, c.span.start), h = mixv(h, c.span.end);
+    h = mix(h, ix.cluster_of_chunk.data(), ix.cluster_of_chunk.size() * 4);
     for (const FineCluster& f : ix.fine) {
-        h = fnv(h, f.centroid.data(), f.centroid.size() * 4);
-        h = fnv(h, &f.radius, 8);
-        h = fnv(h, &f.token_count, sizeof f.token_count);
-        h = fnv(h, f.members.data(), f.members.size() * 4);
+        h = mixv(h, f.radius);
+        h = mixv(h, f.token_count);
+        h = mixv(h, f.parent_unit);
+        h = mixv(h, f.centroid.data());
+        if (!f.centroid.empty()) {
+            h = mixv(h, f.centroid.front());
+            h = mixv(h, f.centroid[f.centroid.size() / 2]);
+            h = mixv(h, f.centroid.back());
+        }
+        h = mix(h, f.members.data(), f.members.size() * 4);
     }
     for (const CoarseUnit& u : ix.coarse) {
-        h = fnv(h, u.centroid.data(), u.centroid.size() * 4);
-        h = fnv(h, &u.radius, 8);
-        h = fnv(h, u.members.data(), u.members.size() * 4);
+        h = mix(h, u.centroid.data(), u.centroid.size() * 4);
+        h = mixv(h, u.radius);
+        h = mix(h, u.members.data(), u.members.size() * 4);
     }
     return ix.store ? store_key(h, *ix.store) : h;
 }
@@ -289,12 +338,14 @@ RetrievalResult run_retrieve(Engine& e, const HierarchicalIndex& ix, const Token
         if (attend) res.output = sparse_attention(q, store, res.active_token_ids);
         return res;
     }
-    cuda_ck(cudaMemcpy(e.q_dev, q.data(), q.size() * 4, cudaMemcpyHostToDevice), "q H2D");
+    std::copy(q.begin(), q.end(), e.h_io);
+    cuda_ck(cudaMemcpyAsync(e.q_dev, e.h_io, q.size() * 4, cudaMemcpyHostToDevice, e.st), "q H2D");
     e.buffer_list(buf);
     const lc_budgets b = to_c(budgets);
-    ck(lc_retrieve(e.h, e.q_dev, &b, LC_BUFFER_LIST, e.boff_dev, e.bids_dev, attend ? e.out_dev : nullptr, nullptr));
-    cuda_ck(cudaDeviceSynchronize(), "retrieve");
-    e.device_errors();
+    ck(lc_retrieve(e.h, e.q_dev, &b, LC_BUFFER_LIST, e.boff_dev, e.bids_dev, attend ? e.out_dev : nullptr, e.st));
+    if (attend)
+        cuda_ck(cudaMemcpyAsync(e.h_io + e.d, e.out_dev, store.dim() * 4, cudaMemcpyDeviceToHost, e.st), "out D2H");
+    cuda_ck(cudaStreamSynchronize(e.st), "retrieve");
     lc_selection_info info{};
     res.selected_units.resize(ix.coarse.size());
     res.selected_clusters.resize(ix.fine.size());
@@ -302,15 +353,13 @@ RetrievalResult run_retrieve(Engine& e, const HierarchicalIndex& ix, const Token
     ck(lc_selection_download(e.h, 0, 0, &info, res.selected_units.data(), res.selected_units.size(),
                              res.selected_clusters.data(), res.selected_clusters.size(),
                              res.active_token_ids.data(), res.active_token_ids.size()));
+    if (info.error) e.device_errors();  // sticky bits: raise the reference's exception and clear them
     res.selected_units.resize(info.n_units);
     res.selected_clusters.resize(info.n_clusters);
     res.active_token_ids.resize(info.n_active);
     res.scanned_centroids = info.scanned_centroids;
     res.degenerate = info.degenerate != 0;
-    if (attend) {
-        res.output.resize(store.dim());
-        cuda_ck(cudaMemcpy(res.output.data(), e.out_dev, store.dim() * 4, cudaMemcpyDeviceToHost), "out D2H");
-    }
+    if (attend) res.output.assign(e.h_io + e.d, e.h_io + e.d + store.dim());
     return res;
 }
 
@@ -424,55 +473,6 @@ std::unique_ptr<StreamDevice> open_stream(const HierarchicalIndex& ix, const Tok
     return dev;
 }
 
-// host mirror <- device slot (after a graft): clusters, units, chunks
-void refresh_mirror(lc_index_t h, HierarchicalIndex& ix) {
-    uint64_t dims[8];
-    ck(lc_index_slot_dims(h, 0, dims));
-    const size_t d = dims[0], M = dims[1], L = dims[2], P = dims[3];
-    std::vector<uint32_t> span(M * 4), fparent(L), fmoff(L + 1), fmem(M), cmoff(P + 1), cmem(L), coc(M);
-    std::vector<float> rep(M * d), fcent(L * d), ccent(P * d);
-    std::vector<double> frad(L), crad(P);
-    std::vector<uint64_t> ftok(L);
-    lc_host_index v{};
-    v.chunk_span = span.data();
-    v.chunk_rep = rep.data();
-    v.fine_centroid = fcent.data();
-    v.fine_radius = frad.data();
-    v.fine_token_count = ftok.data();
-    v.fine_parent = fparent.data();
-    v.fine_member_off = fmoff.data();
-    v.fine_members = fmem.data();
-    v.coarse_centroid = ccent.data();
-    v.coarse_radius = crad.data();
-    v.coarse_member_off = cmoff.data();
-    v.coarse_members = cmem.data();
-    v.cluster_of_chunk = coc.data();
-    ck(lc_index_download_slot(h, 0, &v));
-    ix.chunks.resize(M);
-    for (size_t j = 0; j < M; ++j) {
-        Chunk& c = ix.chunks[j];
-        c.span.start = span[4 * j];
-        c.span.end = span[4 * j + 1];
-        c.span.kind = static_cast<BoundaryKind>(span[4 * j + 2]);
-        c.span.level = static_cast<int>(span[4 * j + 3]);
-        c.rep_key.assign(rep.begin() + j * d, rep.begin() + (j + 1) * d);
-    }
-    for (size_t c = 0; c < L; ++c) {
-        FineCluster& f = ix.fine[c];
-        f.centroid.assign(fcent.begin() + c * d, fcent.begin() + (c + 1) * d);
-        f.radius = frad[c];
-        f.token_count = ftok[c];
-        f.parent_unit = fparent[c];
-        f.members.assign(fmem.begin() + fmoff[c], fmem.begin() + fmoff[c + 1]);
-    }
-    for (size_t u = 0; u < P; ++u) {
-        CoarseUnit& cu = ix.coarse[u];
-        cu.centroid.assign(ccent.begin() + u * d, ccent.begin() + (u + 1) * d);
-        cu.radius = crad[u];
-        cu.members.assign(cmem.begin() + cmoff[u], cmem.begin() + cmoff[u + 1]);
-    }
-    ix.cluster_of_chunk = coc;
-}
 }  // namespace
 
 StreamState::StreamState(TokenStore store, HierarchicalIndex index, StreamerConfig cfg)
@@ -556,7 +556,19 @@ GraftReport StreamState::graft_chunk(Chunk chunk) {
     cuda_ck(cudaMemcpy(&r, dev_->e.rep_dev, sizeof r, cudaMemcpyDeviceToHost), "report D2H");
     dev_->dev_end += take;
     ++graft_count_;
-    refresh_mirror(dev_->e.h, index_);
+    // patch the host mirror the way the reference's graft mutates its index
+    // (streamer.cpp:108-134): one cluster (centroid, radius, token count,
+    // members), one unit (radius), one appended chunk
+    if (r.cluster_id >= index_.fine.size() || r.unit_id >= index_.coarse.size() || r.chunk_id != index_.chunks.size())
+        throw std::runtime_error("graft: device report does not match the host index");
+    FineCluster& fc = index_.fine[r.cluster_id];
+    uint64_t tok = 0;
+    ck(lc_cluster_download(dev_->e.h, 0, r.cluster_id, fc.centroid.data(), &fc.radius, &tok));
+    fc.token_count = static_cast<size_t>(tok);
+    fc.members.push_back(r.chunk_id);
+    index_.coarse[r.unit_id].radius = r.coarse_radius;
+    index_.cluster_of_chunk.push_back(r.cluster_id);
+    index_.chunks.push_back(std::move(chunk));
     GraftReport report;
     report.chunk_id = r.chunk_id;
     report.cluster_id = r.cluster_id;

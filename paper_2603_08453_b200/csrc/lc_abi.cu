@@ -34,6 +34,36 @@ static uint32_t needed_candidates(lc_index_s* h, uint32_t unit_topk) {
     return best;
 }
 
+// lc_decode_step_async leaves the host's per-slot cursors behind the device:
+// re-read them (and the grafted chunks' kind / level) before a host-side call
+void sync_host(lc_index_t h) {
+    if (!h || !h->dev_ahead) return;
+    h->set_device();
+    ck(cudaDeviceSynchronize(), "sync");
+    const Arena& a = h->a;
+    std::vector<SlotState> st(a.n_slots);
+    ck(cudaMemcpy(st.data(), a.state, st.size() * sizeof(SlotState), cudaMemcpyDeviceToHost), "state");
+    std::vector<uint32_t> kl;
+    for (uint32_t s = 0; s < a.n_slots; ++s) {
+        HostSlot& hs = h->hs[s];
+        if (!hs.loaded) continue;
+        if (st[s].n_chunks > hs.n_chunks) {
+            kl.resize(st[s].n_chunks - hs.n_chunks);
+            ck(cudaMemcpy(kl.data(), a.chunk_kl + (size_t)s * a.cap_chunks + hs.n_chunks, kl.size() * 4,
+                          cudaMemcpyDeviceToHost), "chunk kinds");
+            for (uint32_t v : kl) {
+                hs.kind.push_back(v & 0xffu);
+                hs.level.push_back(v >> 8);
+            }
+            if (!hs.rep.empty()) hs.rep.clear();  // prefill reps no longer complete
+        }
+        hs.n_tokens = st[s].n_tokens;
+        hs.chunked_end = st[s].chunked_end;
+        hs.n_chunks = st[s].n_chunks;
+    }
+    h->dev_ahead = false;
+}
+
 extern "C" {
 
 const char* lc_last_error(void) { return g_err.c_str(); }
@@ -104,6 +134,7 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         a.funit = dalloc<uint32_t>(S * d.cap_clusters, o);
         a.fmem_off = dalloc<uint32_t>(S * (d.cap_clusters + 1), o);
         a.fmem = dalloc<uint32_t>(S * d.cap_chunks, o);
+        a.chunk_kl = dalloc<uint32_t>(S * d.cap_chunks, o);
         a.plan_bytes = plan_layout(a.cap_units, d.group, d.dim, d.cap_clusters, nullptr, nullptr, nullptr);
         a.plan = dalloc<unsigned char>(S * a.plan_bytes, o);
         a.chunk_bits = dalloc<uint32_t>(S * G * bit_words(d.cap_chunks), o);
@@ -160,6 +191,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
                          const void* keys, const void* values, uint32_t n_tokens) {
     return guard([&] {
         if (!h || !ix) fail(LC_EINVAL, "lc_index_upload_slot: null argument");
+        sync_host(h);
         h->set_device();
         const Arena& a = h->a;
         if (slot >= a.n_slots) fail(LC_EINVAL, "slot out of range");
@@ -315,6 +347,7 @@ int lc_index_upload_slot(lc_index_t h, uint32_t slot, const lc_host_index* ix,
 int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims) {
     return guard([&] {
         if (!h || !dims || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_index_slot_dims: bad argument");
+        sync_host(h);
         const HostSlot& s = h->hs[slot];
         dims[0] = h->a.d;
         dims[1] = s.n_chunks;
@@ -330,6 +363,7 @@ int lc_index_slot_dims(lc_index_t h, uint32_t slot, uint64_t* dims) {
 int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
     return guard([&] {
         if (!h || !ix || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_index_download_slot: bad argument");
+        sync_host(h);
         h->set_device();
         ck(cudaDeviceSynchronize(), "sync");
         const Arena& a = h->a;
@@ -400,10 +434,39 @@ int lc_index_download_slot(lc_index_t h, uint32_t slot, lc_host_index* ix) {
     });
 }
 
+int lc_cluster_download(lc_index_t h, uint32_t slot, uint32_t cluster_id, float* centroid, double* radius,
+                        uint64_t* token_count) {
+    return guard([&] {
+        if (!h || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_cluster_download: bad argument");
+        sync_host(h);
+        HostSlot& hs = h->hs[slot];
+        if (!hs.loaded || cluster_id >= hs.L) fail(LC_EINVAL, "lc_cluster_download: no such cluster");
+        h->set_device();
+        const Arena& a = h->a;
+        if (hs.internal_of.size() != hs.L) {  // the renumbering is fixed once a slot is uploaded / built
+            std::vector<uint32_t> orig(hs.L);
+            ck(cudaMemcpy(orig.data(), a.forig + (size_t)slot * a.cap_clusters, hs.L * 4, cudaMemcpyDeviceToHost),
+               "forig");
+            hs.internal_of.assign(hs.L, 0);
+            for (uint32_t i = 0; i < hs.L; ++i) hs.internal_of[orig[i]] = i;
+        }
+        const size_t c = (size_t)slot * a.cap_clusters + hs.internal_of[cluster_id];
+        ck(cudaDeviceSynchronize(), "sync");
+        if (centroid) ck(cudaMemcpy(centroid, a.fcent + c * a.d, (size_t)a.d * 4, cudaMemcpyDeviceToHost), "centroid");
+        if (radius) ck(cudaMemcpy(radius, a.frad + c, 8, cudaMemcpyDeviceToHost), "radius");
+        if (token_count) {
+            uint32_t t = 0;
+            ck(cudaMemcpy(&t, a.ftok + c, 4, cudaMemcpyDeviceToHost), "token count");
+            *token_count = t;
+        }
+    });
+}
+
 int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const void* keys, const void* values,
                       uint32_t n_tokens) {
     return guard([&] {
         if (!h || !keys || !values || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_kv_upload_slot: bad argument");
+        sync_host(h);
         if (n_tokens > h->a.cap_tokens) fail(LC_EINVAL, "lc_kv_upload_slot: n_tokens exceeds capacity");
         h->set_device();
         const Arena& a = h->a;
@@ -421,6 +484,7 @@ int lc_kv_upload_slot(lc_index_t h, uint32_t slot, const void* keys, const void*
 int lc_kv_download_slot(lc_index_t h, uint32_t slot, void* keys, void* values, uint32_t n_tokens) {
     return guard([&] {
         if (!h || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_kv_download_slot: bad argument");
+        sync_host(h);
         if (n_tokens > h->hs[slot].n_tokens) fail(LC_EINVAL, "lc_kv_download_slot: beyond the store");
         h->set_device();
         ck(cudaDeviceSynchronize(), "sync");
@@ -433,6 +497,7 @@ int lc_kv_download_slot(lc_index_t h, uint32_t slot, void* keys, void* values, u
 int lc_kv_append(lc_index_t h, const void* keys_dev, const void* values_dev, void* stream) {
     return guard([&] {
         if (!h || !keys_dev || !values_dev) fail(LC_EINVAL, "lc_kv_append: null argument");
+        sync_host(h);
         h->set_device();
         for (auto& s : h->hs) {
             if (!s.loaded) fail(LC_EINVAL, "lc_kv_append: every slot must be uploaded or built");
@@ -469,7 +534,8 @@ static void ensure_streams(lc_index_t h, uint32_t groups) {
 
 static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t flags,
                           const uint32_t* buf_off, const uint32_t* buf_ids, float* out_dev,
-                          cudaStream_t st, const float* q_in = nullptr) {
+                          cudaStream_t st, const float* q_in = nullptr, uint32_t first = 0,
+                          uint32_t count = 0xffffffffu) {
     validate_budgets(b);
     if (!q_dev) fail(LC_EINVAL, "null q");
     if (flags > 2) fail(LC_EINVAL, "bad buffer flags");
@@ -520,17 +586,19 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         h->last_launches += 4;
     };
     h->last_launches = 0;
-    const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, a.n_slots));
+    if (count == 0xffffffffu) count = a.n_slots - std::min(first, a.n_slots);
+    if (first >= a.n_slots || count == 0 || count > a.n_slots - first) fail(LC_EINVAL, "retrieve: bad slot range");
+    const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, count));
     if (groups == 1) {
-        a.slot0 = 0;
-        run_group(a, a.n_slots, st, 0);
+        a.slot0 = first;
+        run_group(a, count, st, 0);
     } else {
         // fork: each slot group's selection runs on its own stream
         ensure_streams(h, groups);
         ck(cudaEventRecord(h->group_events[0], st), "fork");
         for (uint32_t gi = 0; gi < groups; ++gi) {
-            const uint32_t s0 = (uint32_t)((uint64_t)a.n_slots * gi / groups);
-            const uint32_t s1 = (uint32_t)((uint64_t)a.n_slots * (gi + 1) / groups);
+            const uint32_t s0 = first + (uint32_t)((uint64_t)count * gi / groups);
+            const uint32_t s1 = first + (uint32_t)((uint64_t)count * (gi + 1) / groups);
             if (s1 == s0) continue;
             cudaStream_t gs = h->group_streams[gi];
             ck(cudaStreamWaitEvent(gs, h->group_events[0], 0), "fork wait");
@@ -541,10 +609,10 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
             ck(cudaStreamWaitEvent(st, h->group_events[gi + 1], 0), "join");
         }
     }
-    a.slot0 = 0;
+    a.slot0 = first;
     if (out_dev) {
-        ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, st), "k_attend");
-        h->last_launches += a.kv_f32 ? 1 : 2 * ((a.n_slots + kMaxAttendSlots - 1) / kMaxAttendSlots);
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, count, st), "k_attend");
+        h->last_launches += a.kv_f32 ? 1 : 2 * ((count + kMaxAttendSlots - 1) / kMaxAttendSlots);
     }
     h->last_flags = flags;
     h->last_valid = 1;
@@ -555,6 +623,16 @@ int lc_retrieve(lc_index_t h, const float* q_dev, const lc_budgets* b, uint32_t 
     return guard([&] {
         if (!h) fail(LC_EINVAL, "null handle");
         retrieve_impl(h, q_dev, b, flags, buf_off_dev, buf_ids_dev, out_dev, (cudaStream_t)stream);
+    });
+}
+
+int lc_retrieve_slots(lc_index_t h, uint32_t first_slot, uint32_t n_slots, const float* q_dev,
+                      const lc_budgets* b, uint32_t flags, const uint32_t* buf_off_dev,
+                      const uint32_t* buf_ids_dev, float* out_dev, void* stream) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "null handle");
+        retrieve_impl(h, q_dev, b, flags, buf_off_dev, buf_ids_dev, out_dev, (cudaStream_t)stream, nullptr,
+                      first_slot, n_slots);
     });
 }
 
@@ -572,6 +650,7 @@ int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* 
 static void graft_impl(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
                        const float* reps_host, lc_graft_report* reports_dev, cudaStream_t st) {
     if (!take) fail(LC_EINVAL, "null take");
+    sync_host(h);
     bool any = false;
     for (uint32_t s = 0; s < h->a.n_slots; ++s) {
         const HostSlot& hs = h->hs[s];
@@ -618,6 +697,7 @@ int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev, const
     return guard([&] {
         if (!h || !keys_dev || !values_dev) fail(LC_EINVAL, "lc_decode_step: null argument");
         cudaStream_t st = (cudaStream_t)stream;
+        sync_host(h);
         retrieve_impl(h, q_dev, b, LC_BUFFER_STREAM, nullptr, nullptr, out_dev, st);
         for (auto& s : h->hs)
             if (s.n_tokens >= h->a.cap_tokens) fail(LC_ENOMEM, "decode_step: token capacity exhausted");
@@ -625,6 +705,28 @@ int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev, const
         for (auto& s : h->hs) s.n_tokens += 1;
         ++h->version;
         if (take) graft_impl(h, take, kind, level, nullptr, reports_dev, st);
+    });
+}
+
+int lc_decode_step_async(lc_index_t h, const float* q_dev, const void* keys_dev, const void* values_dev,
+                         const lc_budgets* b, const uint32_t* take_dev, const uint32_t* kind_dev,
+                         const uint32_t* level_dev, float* out_dev, lc_graft_report* reports_dev, void* stream) {
+    return guard([&] {
+        if (!h || !keys_dev || !values_dev) fail(LC_EINVAL, "lc_decode_step_async: null argument");
+        cudaStream_t st = (cudaStream_t)stream;
+        // no host reads or writes of the stream cursors: every launch below takes
+        // its slot state from the device, so the sequence is graph-capturable
+        retrieve_impl(h, q_dev, b, LC_BUFFER_STREAM, nullptr, nullptr, out_dev, st);
+        ck(launch_append(h->a, keys_dev, values_dev, st), "k_append");
+        h->last_launches += 1;
+        if (take_dev) {
+            ck(launch_graft(h->a, take_dev, h->desc.pooling, reports_dev ? (void*)reports_dev : (void*)h->rep_scratch,
+                            nullptr, st, kind_dev, level_dev),
+               "k_graft");
+            h->last_launches += 1;
+        }
+        h->dev_ahead = true;
+        ++h->version;
     });
 }
 
@@ -639,6 +741,7 @@ int lc_graft_rep(lc_index_t h, const uint32_t* take, const uint32_t* kind, const
 int lc_chunk_rep(lc_index_t h, uint32_t slot, uint32_t start, uint32_t take, float* rep_host) {
     return guard([&] {
         if (!h || !rep_host || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_chunk_rep: bad argument");
+        sync_host(h);
         if (take == 0 || start + take > h->hs[slot].n_tokens) fail(LC_EINVAL, "lc_chunk_rep: rows outside the store");
         h->set_device();
         uint32_t err0 = 0;
@@ -658,6 +761,7 @@ int lc_sparse_attention_ids(lc_index_t h, uint32_t slot, const float* q_dev, con
                             uint32_t n_ids, float* out_dev, void* stream) {
     return guard([&] {
         if (!h || !q_dev || !out_dev || slot >= h->a.n_slots) fail(LC_EINVAL, "lc_sparse_attention_ids: bad argument");
+        sync_host(h);
         if (n_ids == 0) fail(LC_EINVAL, "sparse_attention: empty active set");  // retriever.cpp:43
         if (!ids_host) fail(LC_EINVAL, "lc_sparse_attention_ids: null ids");
         const HostSlot& hs = h->hs[slot];
@@ -761,6 +865,7 @@ int lc_selection_download(lc_index_t h, uint32_t slot, uint32_t g, lc_selection_
                           uint64_t active_cap) {
     return guard([&] {
         if (!h || slot >= h->a.n_slots || g >= h->a.G) fail(LC_EINVAL, "lc_selection_download: bad argument");
+        sync_host(h);
         if (!h->last_valid) fail(LC_EINVAL, "no selection yet");
         h->set_device();
         ck(cudaDeviceSynchronize(), "sync");

@@ -83,6 +83,7 @@ struct Arena {
     // index
     uint32_t* chunk_start;
     uint32_t* chunk_clu;
+    uint32_t* chunk_kl;      // [slot][cap_chunks] kind | level << 8 of chunks grafted on the device
     float* chunk_rep;
     float* ucent;
     double* urad;
@@ -288,6 +289,7 @@ enum ErrBits : uint32_t {
     kErrChunkCap = 1u << 4,       // graft past cap_chunks
     kErrTokenCap = 1u << 5,       // append past cap_tokens
     kErrEmptyActive = 1u << 6,    // sparse_attention over an empty set (retriever.cpp:43)
+    kErrTake = 1u << 7,           // graft take outside the buffered tokens
 };
 
 }  // namespace lc

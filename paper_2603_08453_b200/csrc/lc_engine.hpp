@@ -29,7 +29,8 @@ cudaError_t launch_append(const Arena& a, const void* keys, const void* values, 
 cudaError_t launch_chunk_rep(const Arena& a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling,
                              float* rep_dev, cudaStream_t stream);
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
-                         const float* reps_dev, cudaStream_t stream);
+                         const float* reps_dev, cudaStream_t stream, const uint32_t* kind_dev = nullptr,
+                         const uint32_t* level_dev = nullptr);
 }  // namespace lc
 
 namespace lcx {
@@ -89,6 +90,7 @@ struct HostSlot {
     std::vector<uint32_t> kind, level;   // per chunk (host-only fields of ChunkSpan)
     std::vector<float> rep;              // prefill reps when the device keeps none
     std::vector<uint32_t> fanout;        // n_u per unit (fixed after build)
+    std::vector<uint32_t> internal_of;   // reference cluster id -> internal id (lazy; fixed after upload)
     lc_index_config cfg{2.0, 64, 10, 0, 2, 0};  // IndexConfig defaults (index.hpp:13-22)
 };
 
@@ -128,6 +130,10 @@ struct lc_index_s {
     float* host_out = nullptr;      // the graph's output buffer (mapped host buffer or out_stage)
     unsigned char* host_scratch = nullptr;  // sel_scratch the graph was captured with
     std::vector<cudaEvent_t> group_events;     // fork + one join per group
+    // lc_decode_step_async advances the per-slot stream cursors on the device
+    // only; the host copies in `hs` are re-read (sync_host) before any call that
+    // needs them
+    bool dev_ahead = false;
 
     ~lc_index_s() {
         for (void* p : owned) cudaFree(p);
@@ -141,6 +147,10 @@ struct lc_index_s {
     void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
 };
 
+
+// host mirror <- device after lc_decode_step_async steps: per-slot cursors
+// (n_tokens, chunked_end, n_chunks) and the grafted chunks' kind / level
+void sync_host(lc_index_t h);
 
 // chunk_representative of every chunk of a slot, recomputed on the device from
 // the bf16 store (lc_build.cu); chunk_bounds = chunk_start[0..M]

@@ -177,6 +177,7 @@ int lc_audit_ub(lc_index_t h, uint32_t slot, const float* queries_host, uint32_t
                 uint64_t* violations) {
     return lcx::guard([&] {
         if (!h || !queries_host || !violations || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_audit_ub: bad argument");
+        sync_host(h);
         if (!h->hs[slot].loaded) lcx::fail(LC_EINVAL, "lc_audit_ub: slot not loaded");
         if (!h->a.keep_reps) lcx::fail(LC_EINVAL, "lc_audit_ub: the audit reads the chunk representatives (keep_reps = 1)");
         h->set_device();
@@ -211,6 +212,7 @@ int lc_oracle_topk(lc_index_t h, uint32_t slot, const float* queries_host, uint3
     return lcx::guard([&] {
         if (!h || !queries_host || !ids_out || !n_out || slot >= h->a.n_slots)
             lcx::fail(LC_EINVAL, "lc_oracle_topk: bad argument");
+        sync_host(h);
         if (budget < 1) lcx::fail(LC_EINVAL, "oracle_topk_tokens: budget >= 1");  // evaluator.cpp:45
         h->set_device();
         const Arena& a = h->a;
@@ -241,6 +243,7 @@ int lc_oracle_topk(lc_index_t h, uint32_t slot, const float* queries_host, uint3
 int lc_full_attention(lc_index_t h, uint32_t slot, const float* q_dev, float* out_dev, void* stream) {
     return lcx::guard([&] {
         if (!h || !q_dev || !out_dev || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_full_attention: bad argument");
+        sync_host(h);
         const uint32_t n = h->hs[slot].n_tokens;
         if (n == 0) lcx::fail(LC_EINVAL, "full_attention: empty store");  // evaluator.cpp:14
         h->set_device();

@@ -42,6 +42,8 @@ struct GraftParams {
     uint32_t pooling;
     void* reports;          // lc_graft_report [n_slots]
     const float* reps;      // [n_slots][d] caller-supplied representatives (graft_chunk(Chunk)), or null
+    const uint32_t* kind;   // [n_slots] chunk kinds (device) or null (forced)
+    const uint32_t* level;  // [n_slots] chunk levels (device) or null (0)
 };
 
 struct GraftReportDev {  // layout of lc_graft_report
@@ -97,6 +99,10 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     const uint32_t start = stp->chunked_end, M = stp->n_chunks, P = stp->P, L = stp->L;
     if (M >= a.cap_chunks) {
         if (tid == 0) atomicOr(a.err, kErrChunkCap);
+        return;
+    }
+    if (take > stp->n_tokens - start) {  // the chunk must lie inside the buffered tokens
+        if (tid == 0) atomicOr(a.err, kErrTake);
         return;
     }
     if (p.reps) {  // graft_chunk(Chunk): the chunk arrives with its representative
@@ -267,6 +273,8 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         uint32_t* cs = a.chunk_start + (size_t)slot * (a.cap_chunks + 1);
         cs[cid + 1] = start + take;
         a.chunk_clu[(size_t)slot * a.cap_chunks + cid] = best_c;
+        a.chunk_kl[(size_t)slot * a.cap_chunks + cid] =
+            (p.kind ? (p.kind[slot] & 0xffu) : 1u) | ((p.level ? p.level[slot] : 0u) << 8);
         stp->n_chunks = M + 1;
         stp->chunked_end = start + take;
         GraftReportDev* rep = reinterpret_cast<GraftReportDev*>(p.reports) + slot;
@@ -327,8 +335,9 @@ cudaError_t launch_append(const Arena& a, const void* keys, const void* values, 
 }
 
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
-                         const float* reps_dev, cudaStream_t stream) {
-    GraftParams p{a, take_dev, pooling, reports, reps_dev};
+                         const float* reps_dev, cudaStream_t stream, const uint32_t* kind_dev,
+                         const uint32_t* level_dev) {
+    GraftParams p{a, take_dev, pooling, reports, reps_dev, kind_dev, level_dev};
     k_graft<<<a.n_slots, kGraftThreads, 0, stream>>>(p);
     return cudaGetLastError();
 }

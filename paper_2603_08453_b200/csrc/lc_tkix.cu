@@ -320,6 +320,7 @@ int lc_tkix_decode(const uint8_t* buf, uint64_t size, lc_host_index* out, lc_ind
 int lc_index_set_config(lc_index_t h, uint32_t slot, const lc_index_config* cfg) {
     return lcx::guard([&] {
         if (!h || !cfg || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_index_set_config: bad argument");
+        sync_host(h);
         h->hs[slot].cfg = *cfg;
     });
 }
@@ -327,6 +328,7 @@ int lc_index_set_config(lc_index_t h, uint32_t slot, const lc_index_config* cfg)
 int lc_index_get_config(lc_index_t h, uint32_t slot, lc_index_config* cfg) {
     return lcx::guard([&] {
         if (!h || !cfg || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_index_get_config: bad argument");
+        sync_host(h);
         *cfg = h->hs[slot].cfg;
     });
 }
@@ -334,6 +336,7 @@ int lc_index_get_config(lc_index_t h, uint32_t slot, lc_index_config* cfg) {
 int lc_index_to_bytes(lc_index_t h, uint32_t slot, uint8_t* buf, uint64_t cap, uint64_t* size) {
     return lcx::guard([&] {
         if (!h || !size || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_index_to_bytes: bad argument");
+        sync_host(h);
         if (!h->hs[slot].loaded) lcx::fail(LC_EINVAL, "lc_index_to_bytes: slot not loaded");
         IndexBuf b;
         download(h, slot, b);
@@ -347,6 +350,7 @@ int lc_index_to_bytes(lc_index_t h, uint32_t slot, uint8_t* buf, uint64_t cap, u
 int lc_index_save(lc_index_t h, uint32_t slot, const char* path, const char* text_buf, const uint64_t* text_offs) {
     return lcx::guard([&] {
         if (!h || !path || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_index_save: bad argument");
+        sync_host(h);
         if (!h->hs[slot].loaded) lcx::fail(LC_EINVAL, "lc_index_save: slot not loaded");
         IndexBuf b;
         download(h, slot, b);
@@ -391,6 +395,7 @@ int lc_index_load(lc_index_t h, uint32_t slot, const char* path, char* text_buf,
                   uint64_t* text_offs, uint64_t offs_cap, uint64_t* n_tokens) {
     return lcx::guard([&] {
         if (!h || !path || slot >= h->a.n_slots) lcx::fail(LC_EINVAL, "lc_index_load: bad argument");
+        sync_host(h);
         const std::vector<uint8_t> file = read_file(path);
         Reader r(file.data(), file.size());
         IndexBuf b;
