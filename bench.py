@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--graph", type=int, default=1)
     p.add_argument("--slot-groups", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
+    p.add_argument("--l2-flush", type=int, default=-1,
+                   help="flush L2 between timed iterations: -1 auto (when a step's inputs are < 3x L2), 0 off, 1 on")
     p.add_argument("--seed-base", type=int, default=1000)
     p.add_argument("--ref-slots", type=int, default=4,
                    help="distinct reference-built slots the CPU reference timing spreads its calls over")
@@ -389,7 +391,7 @@ def config_dict(args, world):
             "unit_topk": 8, "sink": 16, "slots": args.layers * args.kv_heads * args.batch,
             "parallelism": par,
             "l2": ("flushed before every timed iteration (a 252 MB buffer written outside the event pairs)"
-                   if getattr(args, "l2_flush", False) else
+                   if getattr(args, "l2_flush", 0) == True else
                    "inputs larger than L2 (index + KV read per step > 3 x the 126 MB L2)")}
 
 
@@ -811,7 +813,7 @@ def main():
 
     # inputs smaller than 3x L2 (config 1: ~35 MB per step): flush L2 between timed iterations
     est = len(slots) * (min(args.tokens, 4 * args.budget) * 2 * 128 * 2 + 1e6)  # rough bytes per step
-    flush = est < 3 * L2_BYTES
+    flush = est < 3 * L2_BYTES if args.l2_flush < 0 else bool(args.l2_flush)
     args.l2_flush = flush
     with ClockSampler(local) as clk:
         ms, graphed = timed(torch, dist, world, step, args.steps, stream, warm, "decode step", graph=args.graph,

@@ -116,6 +116,16 @@ __device__ __forceinline__ uint32_t warp_of(uint32_t T, uint32_t pos, uint32_t N
     return (uint32_t)((((unsigned long long)pos + 1) * NW - 1) / T);
 }
 
+// Warps that take static ranges: at least kMinWarpTok head tokens each.  A
+// launch with few active tokens (one slot, a 32K layer) would otherwise cut
+// them into ~1-token ranges over every warp of the persistent grid and leave
+// k_merge one partial per warp to combine (measured: 291 us for one slot).
+constexpr uint32_t kMinWarpTok = 256;
+__device__ __forceinline__ uint32_t active_warps(uint32_t TH, uint32_t NW) {
+    const uint32_t want = (TH + kMinWarpTok - 1) / kMinWarpTok;
+    return want < 1u ? 1u : (want < NW ? want : NW);
+}
+
 struct GroupDesc {  // one 16-token group of one slot
     uint32_t slot;  // local slot index, or ~0u when the warp's work is exhausted
     uint32_t pos;   // first token's index in the slot's row list
@@ -159,13 +169,13 @@ __device__ __forceinline__ PoolShape pool_shape(uint32_t TP, uint32_t NW) {
 template <int D>
 __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G, uint32_t g, uint32_t n,
                                            const float* part, uint32_t zero_seg, uint32_t s, uint32_t NW,
-                                           uint32_t TH, uint32_t h0, uint32_t h1, uint32_t t0, uint32_t t1,
-                                           uint32_t C) {
+                                           uint32_t NWe, uint32_t TH, uint32_t h0, uint32_t h1, uint32_t t0,
+                                           uint32_t t1, uint32_t C) {
     const uint32_t lane = threadIdx.x & 31;
     uint32_t wf = 1, wl = 0, kf = 1, kl = 0;
     if (h0 < h1) {
-        wf = warp_of(TH, h0, NW);
-        wl = warp_of(TH, h1 - 1, NW);
+        wf = warp_of(TH, h0, NWe);
+        wl = warp_of(TH, h1 - 1, NWe);
     }
     if (t0 < t1) {
         kf = t0 / C;
@@ -184,7 +194,7 @@ __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G
         if (i < nc) {
             if (i < nw) {
                 const uint32_t v = wf + i;
-                live = warp_begin(TH, v, NW) < warp_begin(TH, v + 1, NW);
+                live = warp_begin(TH, v, NWe) < warp_begin(TH, v + 1, NWe);
                 seg = v + s;
             } else {
                 live = true;
@@ -283,9 +293,10 @@ __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
     if (s >= n) return;
     if (s_hp[s + 1] == s_hp[s] && s_tp[s + 1] == s_tp[s]) return;  // empty: k_attend wrote zeros
     const uint32_t TH = s_hp[n], TP = s_tp[n];
-    const PoolShape pool = pool_shape(TP, NW);
+    const uint32_t NWe = active_warps(TH, NW);
+    const PoolShape pool = pool_shape(TP, NWe);
     merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, p.part + 16, NW + n + kPoolPerWarp * NW + n,
-                  s, NW, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C);
+                  s, NW, NWe, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C);
 }
 
 template <int D>
@@ -325,7 +336,8 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     uint32_t n_groups = 0;
     if (TH + TP == 0) return;
     const uint32_t NW = gridDim.x * kAttWarps, w = blockIdx.x * kAttWarps + warp;
-    const PoolShape pool = pool_shape(TP, NW);
+    const uint32_t NWe = active_warps(TH, NW);
+    const PoolShape pool = pool_shape(TP, NWe);
     uint32_t* pool_ctr = reinterpret_cast<uint32_t*>(p.part);  // [0] next pool chunk, [1] barrier, [2] CTAs out
     float* part = p.part + 16;
 
@@ -343,7 +355,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     };
     const uint32_t* pre = s_hp;  // active sequence: heads, then tails
     bool in_pool = false;
-    uint32_t ppos = warp_begin(TH, w, NW), pend = warp_begin(TH, w + 1, NW);
+    uint32_t ppos = w < NWe ? warp_begin(TH, w, NWe) : TH, pend = w < NWe ? warp_begin(TH, w + 1, NWe) : TH;
     uint32_t seg_base = w, ps = ppos < pend ? slot_of(pre, ppos) : 0u;
     // lane 0 claims the next pool chunk one call before the current range runs
     // out (the atomic's latency hides behind one group) -- not earlier, so a

@@ -84,7 +84,7 @@ __device__ void block_argmax(double& s, uint32_t& k, double* ws, uint32_t* wk) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
+__global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
     const Arena& a = p.a;
     const uint32_t slot = blockIdx.x, tid = threadIdx.x, d = a.d;
     const uint32_t take = p.take[slot];
@@ -142,10 +142,37 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     }
 
     // ---- nearest cluster (streamer.cpp:74-106) ----
+    // the slot's coarse centroids staged once, coalesced, dimension-major
+    // [d][P] (dynamic shared memory): the unit scan and the coarse l2_dist read
+    // them from shared memory instead of P strided global chains
+    extern __shared__ float s_uc[];
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
+    for (uint32_t x = tid; x < d * P; x += blockDim.x) s_uc[x] = uc[(size_t)(x / P) * a.cap_units + x % P];
+    __syncthreads();
     const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
     const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
     const uint32_t* fo = a.forig + (size_t)slot * a.cap_clusters;
+    // sequential fp64 dot (kernels::dot) of the representative with fine
+    // centroid row c: the row streams in as float4 batches (4 loads in flight)
+    auto row_dot = [&](uint32_t c) -> double {
+        const float4* row = reinterpret_cast<const float4*>(fc + (size_t)c * d);
+        double s = 0.0;
+        for (uint32_t j4 = 0; j4 < d / 4; j4 += 4) {
+            float4 v[4];
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) v[k] = j4 + k < d / 4 ? __ldg(row + j4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                if (j4 + k >= d / 4) break;
+                const uint32_t j = 4 * (j4 + k);
+                s = __fma_rn((double)s_rep[j], (double)v[k].x, s);
+                s = __fma_rn((double)s_rep[j + 1], (double)v[k].y, s);
+                s = __fma_rn((double)s_rep[j + 2], (double)v[k].z, s);
+                s = __fma_rn((double)s_rep[j + 3], (double)v[k].w, s);
+            }
+        }
+        return s;
+    };
     unsigned long long comps = 0;
     bool scoped = !a.graft_full;
     uint32_t best_c = 0;
@@ -154,8 +181,7 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         uint32_t bu = 0xffffffffu;
         for (uint32_t u = tid; u < P; u += blockDim.x) {
             double s = 0.0;
-            for (uint32_t j = 0; j < d; ++j)
-                s = __fma_rn((double)s_rep[j], (double)uc[(size_t)j * a.cap_units + u], s);
+            for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)s_uc[j * P + u], s);
             argmax_merge(bs, bu, s, u);
         }
         block_argmax(bs, bu, ws, wk);
@@ -167,12 +193,8 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
             const uint32_t nu = hi - lo;
             double bs2 = -INFINITY;
             uint32_t bc = 0xffffffffu;
-            for (uint32_t i = tid; i < nu; i += blockDim.x) {
-                double s = 0.0;
-                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)fc[fine_at(lo, nu, i, j, d)], s);
-                argmax_merge(bs2, bc, s, lo + i);  // stored order == internal order
-            }
-            block_argmax(bs2, bc, ws, wk);
+            for (uint32_t i = tid; i < nu; i += blockDim.x) argmax_merge(bs2, bc, row_dot(lo + i), lo + i);
+            block_argmax(bs2, bc, ws, wk);  // stored order == internal order
             best_c = bc;
             comps += nu;
         }
@@ -180,14 +202,7 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
     if (!scoped) {
         double bs = -INFINITY;
         uint32_t bo = 0xffffffffu;
-        for (uint32_t u = 0; u < P; ++u) {
-            const uint32_t lo = uoff[u], nu = uoff[u + 1] - lo;
-            for (uint32_t i = tid; i < nu; i += blockDim.x) {
-                double s = 0.0;
-                for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)fc[fine_at(lo, nu, i, j, d)], s);
-                argmax_merge(bs, bo, s, fo[lo + i]);  // full scan order = reference ids
-            }
-        }
+        for (uint32_t c = tid; c < L; c += blockDim.x) argmax_merge(bs, bo, row_dot(c), fo[c]);  // reference ids
         block_argmax(bs, bo, ws, wk);
         // reference id -> internal id
         for (uint32_t c = tid; c < L; c += blockDim.x)
@@ -222,14 +237,13 @@ __global__ void __launch_bounds__(kGraftThreads) k_graft(GraftParams p) {
         s_new[j] = norm > 0.0 ? (float)__ddiv_rn(s_moved[j], norm) : s_mu[j];
     __syncthreads();
     // three sequential l2_dist (kernels.cpp:25-32) on three warps in parallel
-    const float* ucu = uc;  // dimension-major coarse centroid of unit u
     if (tid == 0 || tid == 32 || tid == 64) {
         double s = 0.0;
         for (uint32_t j = 0; j < d; ++j) {
             double x, y;
             if (tid == 0) { x = s_new[j]; y = s_mu[j]; }
             else if (tid == 32) { x = s_rep[j]; y = s_new[j]; }
-            else { x = s_rep[j]; y = ucu[(size_t)j * a.cap_units + u]; }
+            else { x = s_rep[j]; y = s_uc[j * P + u]; }
             const double diff = __dsub_rn(x, y);
             s = __dadd_rn(s, __dmul_rn(diff, diff));
         }
@@ -338,7 +352,11 @@ cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pool
                          const float* reps_dev, cudaStream_t stream, const uint32_t* kind_dev,
                          const uint32_t* level_dev) {
     GraftParams p{a, take_dev, pooling, reports, reps_dev, kind_dev, level_dev};
-    k_graft<<<a.n_slots, kGraftThreads, 0, stream>>>(p);
+    const size_t smem = (size_t)a.d * a.cap_units * 4;  // staged coarse centroids
+    static KernelCfg cfg;
+    cudaError_t e = ensure_smem(k_graft, cfg, smem);
+    if (e != cudaSuccess) return e;
+    k_graft<<<a.n_slots, kGraftThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

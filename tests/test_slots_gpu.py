@@ -1,6 +1,9 @@
 """lc_retrieve_slots (one layer's slots of a layer-by-layer decode) gives the
-same selections and the same output bits as one lc_retrieve over every slot,
-and leaves the rows outside its range untouched."""
+same selections as one lc_retrieve over every slot (bit-exact) and the same
+outputs up to fp32 merge order (the persistent attention kernel cuts the
+launched slots' token sequence into different warp ranges, so the partials
+combine in a different order), and leaves the rows outside its range
+untouched."""
 import numpy as np
 import pytest
 
@@ -28,7 +31,8 @@ def test_retrieve_slots_equals_full_launch():
         eng.retrieve_slots(first, count, q, b, out=part)
         torch.cuda.synchronize()
         p = part.cpu().numpy()
-        assert np.array_equal(p[first:first + count], full.cpu().numpy()[first:first + count])
+        f = full.cpu().numpy()[first:first + count]
+        assert np.abs(p[first:first + count] - f).max() <= 1e-5 * np.abs(f).max()
         assert (p[first + count:] == 7.0).all()
         for s in range(first, first + count):
             for g in range(G):
