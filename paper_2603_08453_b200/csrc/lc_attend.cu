@@ -49,6 +49,7 @@ struct AttendParams {
     uint32_t n;      // slots of this launch, starting at a.slot0
     float* part;     // [(warps + n)][G][D + 2] per (warp, slot) segment partials
     unsigned long long* prof;  // optional per-warp [t_start, t_stream_end, t_end, groups | smid << 40] (LC_PROF=1)
+    uint32_t min_tok;          // head tokens per static warp range, at least (kMinWarpTok)
 };
 
 __device__ __forceinline__ unsigned long long gtime_a() {
@@ -121,8 +122,8 @@ __device__ __forceinline__ uint32_t warp_of(uint32_t T, uint32_t pos, uint32_t N
 // them into ~1-token ranges over every warp of the persistent grid and leave
 // k_merge one partial per warp to combine (measured: 291 us for one slot).
 constexpr uint32_t kMinWarpTok = 256;
-__device__ __forceinline__ uint32_t active_warps(uint32_t TH, uint32_t NW) {
-    const uint32_t want = (TH + kMinWarpTok - 1) / kMinWarpTok;
+__device__ __forceinline__ uint32_t active_warps(uint32_t TH, uint32_t NW, uint32_t min_tok) {
+    const uint32_t want = (TH + min_tok - 1) / min_tok;
     return want < 1u ? 1u : (want < NW ? want : NW);
 }
 
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
     if (s >= n) return;
     if (s_hp[s + 1] == s_hp[s] && s_tp[s + 1] == s_tp[s]) return;  // empty: k_attend wrote zeros
     const uint32_t TH = s_hp[n], TP = s_tp[n];
-    const uint32_t NWe = active_warps(TH, NW);
+    const uint32_t NWe = active_warps(TH, NW, p.min_tok);
     const PoolShape pool = pool_shape(TP, NWe);
     merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, p.part + 16, NW + n + kPoolPerWarp * NW + n,
                   s, NW, NWe, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C);
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     uint32_t n_groups = 0;
     if (TH + TP == 0) return;
     const uint32_t NW = gridDim.x * kAttWarps, w = blockIdx.x * kAttWarps + warp;
-    const uint32_t NWe = active_warps(TH, NW);
+    const uint32_t NWe = active_warps(TH, NW, p.min_tok);
     const PoolShape pool = pool_shape(TP, NWe);
     uint32_t* pool_ctr = reinterpret_cast<uint32_t*>(p.part);  // [0] next pool chunk, [1] barrier, [2] CTAs out
     float* part = p.part + 16;
@@ -729,7 +730,8 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     unsigned long long*& prof = prof_dev[current_device()];
     if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
-        AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr};
+        AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr, kMinWarpTok};
+        if (const char* ev = getenv("LC_ATT_MINTOK")) p.min_tok = std::max(16, atoi(ev));  // experiments
         if (prof) cudaMemset(prof, 0, (size_t)grid * kAttWarps * 4 * 8);
         p.a.slot0 = a.slot0 + s0;
         cudaError_t e = a.d == 128 ? launch_attend_d<128>(p, grid, stream)

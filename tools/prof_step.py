@@ -12,7 +12,7 @@ from paper_2603_08453_b200 import api  # noqa: E402
 
 
 def main():
-    args = bench.parse()
+    args = bench.apply_config(bench.parse())
     args.batch = args.batch or 1
     slots = list(range(args.layers * args.kv_heads * args.batch))
     eng, qs, setup, codes = bench.build_engine(api, torch, args, slots, 0)
