@@ -62,6 +62,9 @@ def parse():
                         "one sequence's worth of slots, config 2's per-GPU load) -- 8 in --mode stream")
     p.add_argument("--graph", type=int, default=1)
     p.add_argument("--slot-groups", type=int, default=1)
+    p.add_argument("--gather", default="nccl", choices=["nccl", "p2p"],
+                   help="N > 1: the layer-boundary all-gather of head outputs over NCCL, or fused into the "
+                        "attention merge as NVLink peer stores into symmetric-memory buffers (lc_set_gather)")
     p.add_argument("--cpu-baseline", type=int, default=1)
     p.add_argument("--l2-flush", type=int, default=-1,
                    help="flush L2 between timed iterations: -1 auto (when a step's inputs are < 3x L2), 0 off, 1 on")
@@ -712,6 +715,38 @@ def capture(torch, fn, what):
         return None
 
 
+class P2PGather:
+    """The fused all-gather at N > 1: every rank's gather buffer and arrival
+    counter live in torch symmetric memory (NVLink peer mappings), and the
+    engine's merge kernel stores each (slot, head) output row into all of
+    them (lc_set_gather); eng.gather_wait() releases a rank once every rank's
+    rows have landed.  Rows are global slot ids."""
+
+    FLAG_OFF = 512  # bytes into the signal pad, clear of torch's own barrier slots
+
+    def __init__(self, torch, dist, eng, rank, world, n_slots_total, group, slots):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.eng, self.dist = eng, dist
+        self.buf = symm_mem.empty((n_slots_total, group, 128), dtype=torch.float32, device="cuda")
+        self.hdl = symm_mem.rendezvous(self.buf, dist.group.WORLD.group_name)
+        self.peer_out = [int(p) for p in self.hdl.buffer_ptrs]
+        self.peer_flag = [int(p) + self.FLAG_OFF for p in self.hdl.signal_pad_ptrs]
+        self.rank, self.rows = rank, [int(s) for s in slots]
+        self.n_total = n_slots_total * group
+        self.configure(self.n_total)
+
+    def configure(self, rows_per_wait):
+        torch = __import__("torch")
+        torch.cuda.synchronize()
+        # this rank's counter restarts at 0 with the engine's wait count (set_gather resets it)
+        sig = self.hdl.get_signal_pad(self.rank, (1,), dtype=torch.int32, storage_offset=self.FLAG_OFF // 4)
+        sig.zero_()
+        torch.cuda.synchronize()
+        self.dist.barrier()
+        self.eng.set_gather(self.peer_out, self.peer_flag, self.rows, self.peer_flag[self.rank], rows_per_wait)
+        self.dist.barrier()
+
+
 def max_over_ranks(torch, dist, world, x):
     if world == 1:
         return x
@@ -804,11 +839,17 @@ def main():
     gathered = torch.zeros((world,) + tuple(q.shape), dtype=q.dtype, device=q.device) if world > 1 else None
     b = api.Budgets(token_budget=args.budget, unit_topk=8, sink_size=16)
 
+    p2p = None
+    if world > 1 and args.gather == "p2p":
+        p2p = P2PGather(torch, dist, eng, rank, world, n_slots_total, args.group, slots)
+
     def step():
         # the synthetic step has every layer's queries up front: all local slots
         # in one launch, then the head outputs of every layer exchanged at once
         eng.retrieve(q, b, out=out)
-        if world > 1:
+        if p2p is not None:
+            eng.gather_wait()  # the merge already stored every row into every rank's buffer
+        elif world > 1:
             dist.all_gather_into_tensor(gathered, out)
 
     # inputs smaller than 3x L2 (config 1: ~35 MB per step): flush L2 between timed iterations
@@ -841,10 +882,16 @@ def main():
     lg = shard.LayerGather(rank, world, args.layers, heads_local * world, args.batch, tuple(q.shape[1:]), q.dtype,
                            q.device)
 
+    if p2p is not None:  # one wait per layer: that layer's rows from every rank
+        p2p.configure(args.batch * args.kv_heads * args.group)
+
     def layer_step():
         for layer in range(args.layers):
             eng.retrieve_slots(layer * lg.rows, lg.rows, q, b, out=out)
-            lg.gather(out, layer)
+            if p2p is not None:
+                eng.gather_wait()
+            else:
+                lg.gather(out, layer)
 
     lw_ms, lw_graphed = timed(torch, dist, world, layer_step, max(3, args.steps // 5), stream, 2,
                               "layer-by-layer step", graph=args.graph)
@@ -869,6 +916,10 @@ def main():
     # end to end through the public host API: q from page-locked host memory in,
     # retrieve + attention, outputs back to host memory (and, at N > 1, the
     # host result's all-gather: H2D of the outputs, then the collective)
+    if p2p is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        eng.set_gather([], [], [], 0, 0)  # the host-API leg gathers with NCCL below
     qh = torch.from_numpy(np.ascontiguousarray(qs)).pin_memory()
     oh = torch.zeros_like(qh).pin_memory()
     e2e_steps = max(3, args.steps // 2)
@@ -945,8 +996,11 @@ def main():
             "clocks": clocks,
             "setup": setup,
             "cuda_graph": graphed,
-            "collective": ("NCCL all_gather_into_tensor of every layer's head outputs, once per step, in the graph"
-                           if world > 1 else None),
+            "collective": (None if world == 1 else
+                           "fused into k_merge: NVLink peer stores of every head output row into each rank's "
+                           "symmetric-memory gather buffer + system-scope arrival counters, k_gather_wait per "
+                           "step / layer" if p2p is not None else
+                           "NCCL all_gather_into_tensor of every layer's head outputs, once per step, in the graph"),
             "layerwise": {"value": args.batch * 1000.0 / lw_ms, "unit": "steps/s", "ms_per_step": lw_ms,
                           "cuda_graph": lw_graphed,
                           "what": f"{args.layers} x (lc_retrieve_slots over one layer's local slots"

@@ -190,6 +190,24 @@ int lc_retrieve_slots(lc_index_t h, uint32_t first_slot, uint32_t n_slots, const
                       const lc_budgets* b, uint32_t flags, const uint32_t* buf_off_dev,
                       const uint32_t* buf_ids_dev, float* out_dev, void* stream);
 
+/* Fused all-gather epilogue: the layer-boundary exchange
+ * of head outputs done by the attention merge itself.  After this call every
+ * merged (slot, head) output row of lc_retrieve / lc_retrieve_slots /
+ * lc_decode_step* is also stored into each of the n_peers gather buffers
+ * (peer_out[r]: a device pointer valid in this process -- NVLink peer memory
+ * of rank r, e.g. a symmetric-memory / IPC mapping -- laid out
+ * [rows][group][dim] fp32, this handle's slot s at row row_of_slot[s]), and
+ * each peer's uint32 arrival counter peer_flag[r] is incremented once per row
+ * (system-scope atomics after a system fence).  lc_gather_wait then blocks
+ * the stream until this rank's own counter (my_flag) has advanced by
+ * rows_per_wait since the previous wait -- every rank's rows of the step or
+ * layer have landed.  The wait count lives on the device, so the pair is
+ * CUDA-graph capturable.  n_peers = 0 turns the epilogue off.  peer_out /
+ * peer_flag / row_of_slot are host arrays (copied). */
+int lc_set_gather(lc_index_t h, uint32_t n_peers, const uint64_t* peer_out, const uint64_t* peer_flag,
+                  const uint32_t* row_of_slot, uint64_t my_flag, uint32_t rows_per_wait);
+int lc_gather_wait(lc_index_t h, void* stream);
+
 /* Sparse attention over the active sets of the last lc_retrieve (the second
  * half of retrieve(), retriever.cpp:165). */
 int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* stream);

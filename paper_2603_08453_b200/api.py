@@ -414,6 +414,22 @@ class Engine:
                                           _ptr(out), _stream_ptr(stream)))
         return out
 
+    def set_gather(self, peer_out, peer_flag, row_of_slot, my_flag, rows_per_wait):
+        """Fused all-gather epilogue (lc_set_gather): peer_out / peer_flag are
+        device pointers (ints) of every rank's gather buffer and arrival
+        counter, row_of_slot the gather-buffer row of each of this engine's
+        slots, my_flag this rank's counter.  Empty lists turn it off."""
+        n = len(peer_out)
+        po = np.ascontiguousarray(peer_out, np.uint64)
+        pf = np.ascontiguousarray(peer_flag, np.uint64)
+        rows = np.ascontiguousarray(row_of_slot, np.uint32)
+        L.check(L.lib().lc_set_gather(self.h, n, po.ctypes.data if n else None, pf.ctypes.data if n else None,
+                                      rows.ctypes.data if n else None, int(my_flag) if n else 0,
+                                      int(rows_per_wait)))
+
+    def gather_wait(self, stream=None):
+        L.check(L.lib().lc_gather_wait(self.h, _stream_ptr(stream)))
+
     def retrieve_host(self, q_host: np.ndarray, budgets: Budgets, out_host: np.ndarray,
                       buffer: str = "none", stream=None):
         flags = {"none": L.LC_BUFFER_NONE, "stream": L.LC_BUFFER_STREAM}[buffer]

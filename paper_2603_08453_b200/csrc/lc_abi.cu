@@ -611,7 +611,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     }
     a.slot0 = first;
     if (out_dev) {
-        ck(launch_attend(a, q_dev, out_dev, h->att_part, count, st), "k_attend");
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, count, st, h->pg.n ? &h->pg : nullptr), "k_attend");
         h->last_launches += a.kv_f32 ? 1 : 2 * ((count + kMaxAttendSlots - 1) / kMaxAttendSlots);
     }
     h->last_flags = flags;
@@ -633,6 +633,50 @@ int lc_retrieve_slots(lc_index_t h, uint32_t first_slot, uint32_t n_slots, const
         if (!h) fail(LC_EINVAL, "null handle");
         retrieve_impl(h, q_dev, b, flags, buf_off_dev, buf_ids_dev, out_dev, (cudaStream_t)stream, nullptr,
                       first_slot, n_slots);
+    });
+}
+
+int lc_set_gather(lc_index_t h, uint32_t n_peers, const uint64_t* peer_out, const uint64_t* peer_flag,
+                  const uint32_t* row_of_slot, uint64_t my_flag, uint32_t rows_per_wait) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "null handle");
+        h->set_device();
+        ck(cudaDeviceSynchronize(), "sync");
+        if (h->pg_mem) cudaFree(h->pg_mem);
+        h->pg_mem = nullptr;
+        h->pg = PeerGather{nullptr, nullptr, nullptr, 0u};
+        ++h->version;  // cached host-call graphs hold the old epilogue
+        if (n_peers == 0) return;
+        if (!peer_out || !peer_flag || !row_of_slot || !my_flag || rows_per_wait == 0)
+            fail(LC_EINVAL, "lc_set_gather: null argument");
+        const uint32_t S = h->a.n_slots;
+        // one allocation: [n] out pointers, [n] flag pointers, [S] rows, wait count
+        const size_t bytes = (size_t)n_peers * 16 + (size_t)S * 4 + 16;
+        void* m = nullptr;
+        if (cudaMalloc(&m, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            fail(LC_ENOMEM, "lc_set_gather: allocation failed");
+        }
+        h->pg_mem = m;
+        unsigned char* b = static_cast<unsigned char*>(m);
+        ck(cudaMemcpy(b, peer_out, (size_t)n_peers * 8, cudaMemcpyHostToDevice), "peer out");
+        ck(cudaMemcpy(b + (size_t)n_peers * 8, peer_flag, (size_t)n_peers * 8, cudaMemcpyHostToDevice), "peer flags");
+        ck(cudaMemcpy(b + (size_t)n_peers * 16, row_of_slot, (size_t)S * 4, cudaMemcpyHostToDevice), "rows");
+        h->pg_done = reinterpret_cast<unsigned int*>(b + (size_t)n_peers * 16 + (size_t)S * 4);
+        ck(cudaMemset(h->pg_done, 0, 16), "wait count");
+        h->pg = PeerGather{reinterpret_cast<float* const*>(b), reinterpret_cast<unsigned int* const*>(b + (size_t)n_peers * 8),
+                           reinterpret_cast<const uint32_t*>(b + (size_t)n_peers * 16), n_peers};
+        h->pg_myflag = reinterpret_cast<unsigned int*>(my_flag);
+        h->pg_expect = rows_per_wait;
+    });
+}
+
+int lc_gather_wait(lc_index_t h, void* stream) {
+    return guard([&] {
+        if (!h || !h->pg.n) fail(LC_EINVAL, "lc_gather_wait: no gather configured (lc_set_gather)");
+        h->set_device();
+        ck(launch_gather_wait(h->pg_myflag, h->pg_done, h->pg_expect, h->a.err, (cudaStream_t)stream),
+           "k_gather_wait");
     });
 }
 

@@ -50,6 +50,7 @@ struct AttendParams {
     float* part;     // [(warps + n)][G][D + 2] per (warp, slot) segment partials
     unsigned long long* prof;  // optional per-warp [t_start, t_stream_end, t_end, groups | smid << 40] (LC_PROF=1)
     uint32_t min_tok;          // head tokens per static warp range, at least (kMinWarpTok)
+    PeerGather pg;             // fused all-gather epilogue (pg.n == 0: off)
 };
 
 __device__ __forceinline__ unsigned long long gtime_a() {
@@ -171,7 +172,7 @@ template <int D>
 __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G, uint32_t g, uint32_t n,
                                            const float* part, uint32_t zero_seg, uint32_t s, uint32_t NW,
                                            uint32_t NWe, uint32_t TH, uint32_t h0, uint32_t h1, uint32_t t0,
-                                           uint32_t t1, uint32_t C) {
+                                           uint32_t t1, uint32_t C, const PeerGather& pg, uint32_t slot) {
     const uint32_t lane = threadIdx.x & 31;
     uint32_t wf = 1, wl = 0, kf = 1, kl = 0;
     if (h0 < h1) {
@@ -233,6 +234,38 @@ __device__ __forceinline__ void merge_head(float* out, uint32_t* err, uint32_t G
 #pragma unroll
     for (int k = 0; k < PER; ++k) out[(size_t)g * D + lane + 32 * k] = L > 0.f ? o[k] / L : 0.f;
     if (!(L > 0.f) && lane == 0) atomicOr(err, kErrEmptyActive);
+    if (pg.n) {  // the same row into every rank's gather buffer, then one arrival per rank
+        const size_t row = ((size_t)pg.row_of_slot[slot] * G + g) * D;
+        for (uint32_t r = 0; r < pg.n; ++r) {
+            float* dst = pg.out[r] + row;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) dst[lane + 32 * k] = L > 0.f ? o[k] / L : 0.f;
+        }
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t r = 0; r < pg.n; ++r) atomicAdd_system(pg.flag[r], 1u);
+    }
+}
+
+// One rank's side of the fused all-gather: wait until its arrival counter
+// shows `expect` more rows than at the previous wait (the count of waits done
+// lives on the device, so the launch replays unchanged in a CUDA graph).
+// Bounded: a peer that never writes raises an error bit instead of hanging.
+__global__ void k_gather_wait(unsigned int* flag, unsigned int* done, unsigned int expect, uint32_t* err) {
+    if (threadIdx.x != 0) return;
+    const unsigned int target = (*done + 1u) * expect;
+    for (uint32_t spin = 0;; ++spin) {
+        unsigned int cur;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(cur) : "l"(flag) : "memory");
+        if ((int)(cur - target) >= 0) break;
+        if (spin > (1u << 28)) {
+            atomicOr(err, kErrGatherTimeout);
+            break;
+        }
+        __nanosleep(64);
+    }
+    *done += 1u;
 }
 
 // Prefix sums of the slots' head / tail token counts (head_of / the rest) over
@@ -297,7 +330,7 @@ __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
     const uint32_t NWe = active_warps(TH, NW, p.min_tok);
     const PoolShape pool = pool_shape(TP, NWe);
     merge_head<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, n, p.part + 16, NW + n + kPoolPerWarp * NW + n,
-                  s, NW, NWe, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C);
+                  s, NW, NWe, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C, p.pg, a.slot0 + s);
 }
 
 template <int D>
@@ -714,8 +747,14 @@ __global__ void __launch_bounds__(256) k_attend_exact(Arena a, const float* q, f
 
 // Slots go in launches of at most kMaxAttendSlots whose total token capacity
 // fits the kernel's 32-bit global positions.
+cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned int expect, uint32_t* err,
+                               cudaStream_t stream) {
+    k_gather_wait<<<1, 32, 0, stream>>>(flag, done, expect, err);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const PeerGather* pg) {
     if (a.kv_f32) {
         k_attend_exact<<<n_slots, 32 * a.G, 0, stream>>>(a, q, out);
         return cudaGetLastError();
@@ -730,7 +769,8 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     unsigned long long*& prof = prof_dev[current_device()];
     if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
-        AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr, kMinWarpTok};
+        AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr, kMinWarpTok,
+                       pg ? *pg : PeerGather{nullptr, nullptr, nullptr, 0u}};
         if (const char* ev = getenv("LC_ATT_MINTOK")) p.min_tok = std::max(16, atoi(ev));  // experiments
         if (prof) cudaMemset(prof, 0, (size_t)grid * kAttWarps * 4 * 8);
         p.a.slot0 = a.slot0 + s0;

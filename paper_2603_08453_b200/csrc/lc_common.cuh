@@ -69,6 +69,18 @@ struct QInfo {  // per query head result summary (mirrors lc_selection_info)
     unsigned long long n_active;
 };
 
+// Fused all-gather epilogue: k_merge stores every merged
+// (slot, head) output row straight into each rank's gather buffer over
+// NVLink peer memory (and the local one), then bumps each rank's arrival
+// counter; k_gather_wait releases a rank once its counter shows every row of
+// the step.  n == 0: off (outputs go to `out` only).
+struct PeerGather {
+    float* const* out;            // [n] each rank's gather buffer [rows][G][D] (peer device pointers)
+    unsigned int* const* flag;    // [n] each rank's arrival counter
+    const uint32_t* row_of_slot;  // [handle slots] gather-buffer row of each slot
+    uint32_t n;
+};
+
 struct Arena {
     // shape
     uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;
@@ -290,6 +302,7 @@ enum ErrBits : uint32_t {
     kErrTokenCap = 1u << 5,       // append past cap_tokens
     kErrEmptyActive = 1u << 6,    // sparse_attention over an empty set (retriever.cpp:43)
     kErrTake = 1u << 7,           // graft take outside the buffered tokens
+    kErrGatherTimeout = 1u << 8,  // fused all-gather: a peer's rows never arrived (bounded wait gave up)
 };
 
 }  // namespace lc

@@ -24,7 +24,9 @@ cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint
 uint32_t attend_grid(uint32_t d);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
-                          cudaStream_t stream);
+                          cudaStream_t stream, const PeerGather* pg = nullptr);
+cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned int expect, uint32_t* err,
+                               cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
 cudaError_t launch_chunk_rep(const Arena& a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling,
                              float* rep_dev, cudaStream_t stream);
@@ -134,6 +136,12 @@ struct lc_index_s {
     // only; the host copies in `hs` are re-read (sync_host) before any call that
     // needs them
     bool dev_ahead = false;
+    // fused all-gather epilogue (lc_set_gather)
+    PeerGather pg{nullptr, nullptr, nullptr, 0u};
+    void* pg_mem = nullptr;            // device: peer out pointers, flag pointers, rows, wait count
+    unsigned int* pg_done = nullptr;
+    unsigned int* pg_myflag = nullptr;
+    uint32_t pg_expect = 0;
 
     ~lc_index_s() {
         for (void* p : owned) cudaFree(p);
@@ -143,6 +151,7 @@ struct lc_index_s {
         if (host_stream) cudaStreamDestroy(host_stream);
         if (host_event) cudaEventDestroy(host_event);
         for (auto e : group_events) cudaEventDestroy(e);
+        if (pg_mem) cudaFree(pg_mem);
     }
     void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
 };
