@@ -646,7 +646,7 @@ def run_sweep(args, api, torch):
             a = argparse.Namespace(**vars(args))
             a.tokens, a.batch = ctx, batch
             slots = shard.slots_of_rank(args.shard, shards, a.layers, a.kv_heads, batch, order="layer")
-            eng, qs, setup, _ = build_engine(api, torch, a, slots, local)
+            eng, qs, setup, codes = build_engine(api, torch, a, slots, local)
             q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
             out = torch.zeros_like(q)
             for budget in SWEEP_BUDGET:
@@ -658,7 +658,13 @@ def run_sweep(args, api, torch):
                     raise RuntimeError(f"device error bits 0x{err:x} at {(batch, ctx, budget)}")
                 sb = eng.step_bytes()
                 fp16 = sb[0] - sb[3] * (2 * d)
+                par = None
+                if args.parity and budget == SWEEP_BUDGET[-1]:  # the last slot vs the reference, largest budget
+                    par = parity_vs_reference(eng, codes, qs, out, [len(slots) - 1], b)
+                    par = {k: par[k] for k in ("ok", "heads_checked", "mismatches", "max_rel_err_vs_reference")
+                           if k in par}
                 points.append({"batch": batch, "context": ctx, "budget": budget, "slots_per_gpu": len(slots),
+                               "parity": par,
                                "value": batch * 1000.0 / ms, "ms_per_step": ms, "cuda_graph": graphed,
                                "step_frac": sb[0] / (ms * 1e-3) / 1e9 / peak,
                                "step_frac_fp16_fine_width": fp16 / (ms * 1e-3) / 1e9 / peak,

@@ -243,6 +243,14 @@ int lc_decode_step_async(lc_index_t h, const float* q_dev, const void* keys_dev,
                          const uint32_t* kind_dev, const uint32_t* level_dev, float* out_dev,
                          lc_graft_report* reports_dev, void* stream);
 
+/* Chunk-table compaction: fold every slot's grafted chunks (those appended
+ * since the last compaction) into the cluster member lists the selection
+ * reads, for slots with at least min_grafted of them.  lc_decode_step and
+ * lc_decode_step_async do it on their own every 128 steps; member order and
+ * every downloaded / serialized field are unchanged.  LC_EINVAL when the
+ * chunk table exceeds the kernel's shared-memory staging (~1M-token slots). */
+int lc_compact(lc_index_t h, uint32_t min_grafted, void* stream);
+
 /* graft_chunk(Chunk) (streamer.cpp:68-143) with the chunk's representative
  * supplied by the caller instead of pooled from the keys: reps_host
  * [n_slots][dim] fp32 (rows of slots without a graft are ignored). */

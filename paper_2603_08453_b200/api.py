@@ -507,6 +507,10 @@ class Engine:
                                              rb.data_ptr(), _stream_ptr(stream)))
         return out
 
+    def compact(self, min_grafted: int = 1, stream=None):
+        """lc_compact: grafted chunks into the member CSR (done every 128 decode steps anyway)."""
+        L.check(L.lib().lc_compact(self.h, int(min_grafted), _stream_ptr(stream)))
+
     def _budgets_c(self, budgets: Budgets):
         # keep the ctypes struct alive for the call (and across graph capture)
         self._bc = budgets.c()

@@ -735,6 +735,19 @@ int lc_graft(lc_index_t h, const uint32_t* take, const uint32_t* kind, const uin
     });
 }
 
+// Every kCompactEvery decode steps, fold the slots' grafted chunks into the
+// member CSR (k_compact; slots with >= kCompactMin grafts).  A fixed launch in
+// the step sequence, so a captured run of steps carries it too.  Skipped when
+// the chunk table does not fit the kernel's shared-memory staging (1M-token
+// contexts): the selection then keeps scanning the grafted tail.
+constexpr uint32_t kCompactEvery = 128, kCompactMin = 64;
+static void maybe_compact(lc_index_t h, cudaStream_t st) {
+    if (++h->steps_since_compact < kCompactEvery) return;
+    h->steps_since_compact = 0;
+    if (compact_smem(h->a) + 1024 > (size_t)dev_props().smem_blk) return;
+    ck(launch_compact(h->a, kCompactMin, st), "k_compact");
+}
+
 int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev, const void* values_dev,
                    const lc_budgets* b, const uint32_t* take, const uint32_t* kind, const uint32_t* level,
                    float* out_dev, lc_graft_report* reports_dev, void* stream) {
@@ -749,6 +762,18 @@ int lc_decode_step(lc_index_t h, const float* q_dev, const void* keys_dev, const
         for (auto& s : h->hs) s.n_tokens += 1;
         ++h->version;
         if (take) graft_impl(h, take, kind, level, nullptr, reports_dev, st);
+        maybe_compact(h, st);
+    });
+}
+
+int lc_compact(lc_index_t h, uint32_t min_grafted, void* stream) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "null handle");
+        h->set_device();
+        if (compact_smem(h->a) + 1024 > (size_t)dev_props().smem_blk)
+            fail(LC_EINVAL, "lc_compact: the chunk table is too large for the compaction kernel");
+        ck(launch_compact(h->a, min_grafted, (cudaStream_t)stream), "k_compact");
+        ++h->version;
     });
 }
 
@@ -769,6 +794,7 @@ int lc_decode_step_async(lc_index_t h, const float* q_dev, const void* keys_dev,
                "k_graft");
             h->last_launches += 1;
         }
+        maybe_compact(h, st);
         h->dev_ahead = true;
         ++h->version;
     });

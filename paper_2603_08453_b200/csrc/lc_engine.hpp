@@ -28,6 +28,8 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
 cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned int expect, uint32_t* err,
                                cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
+size_t compact_smem(const Arena& a);
+cudaError_t launch_compact(const Arena& a, uint32_t min_grafted, cudaStream_t stream);
 cudaError_t launch_chunk_rep(const Arena& a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling,
                              float* rep_dev, cudaStream_t stream);
 cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pooling, void* reports,
@@ -136,6 +138,7 @@ struct lc_index_s {
     // only; the host copies in `hs` are re-read (sync_host) before any call that
     // needs them
     bool dev_ahead = false;
+    uint32_t steps_since_compact = 0;  // decode steps since the last chunk-table compaction
     // fused all-gather epilogue (lc_set_gather)
     PeerGather pg{nullptr, nullptr, nullptr, 0u};
     void* pg_mem = nullptr;            // device: peer out pointers, flag pointers, rows, wait count

@@ -337,6 +337,96 @@ __global__ void k_chunk_rep(Arena a, uint32_t slot, uint32_t start, uint32_t tak
     for (uint32_t j = tid; j < d; j += blockDim.x) rep[j] = s_norm > 0.0 ? (float)__ddiv_rn(s_acc[j], s_norm) : 0.f;
 }
 
+// Chunk-table compaction: fold the grafted chunks [m0, M) of a slot into the
+// member CSR (fmem_off / fmem), so the selection reads every member of a
+// selected cluster from the CSR instead of scanning the grafted tail per head
+// and step (the scan grows with the stream).  Member lists stay ascending per
+// cluster (old members, then grafts in chunk order), exactly the reference's
+// FineCluster::members order.  One CTA per slot; the old CSR is staged in
+// shared memory first, so the rewrite is in place.  Slots with fewer than
+// `min_grafted` grafted chunks are left as they are.
+constexpr int kCompactThreads = 512;
+__global__ void __launch_bounds__(kCompactThreads) k_compact(Arena a, uint32_t min_grafted) {
+    extern __shared__ uint32_t s_c[];
+    const uint32_t slot = blockIdx.x, tid = threadIdx.x;
+    SlotState* stp = a.state + slot;
+    const uint32_t M = stp->n_chunks, m0 = stp->m0, L = stp->L;
+    if (M <= m0 || M - m0 < min_grafted) return;
+    const uint32_t G = M - m0;
+    uint32_t* s_wt = s_c;               // [32] scan scratch
+    uint32_t* off = s_wt + 32;          // [L + 1] old offsets
+    uint32_t* gpre = off + L + 1;       // [L + 1] grafted per cluster -> exclusive prefix
+    uint32_t* gcl = gpre + L + 1;       // [G] cluster of each grafted chunk
+    uint32_t* oldm = gcl + G;           // [off[L] = m0] old members
+    uint32_t* fo = a.fmem_off + (size_t)slot * (a.cap_clusters + 1);
+    uint32_t* fm = a.fmem + (size_t)slot * a.cap_chunks;
+    const uint32_t* cc = a.chunk_clu + (size_t)slot * a.cap_chunks;
+    for (uint32_t c = tid; c <= L; c += blockDim.x) {
+        off[c] = fo[c];
+        gpre[c] = 0u;
+    }
+    __syncthreads();
+    const uint32_t nold = off[L];
+    for (uint32_t k = tid; k < nold; k += blockDim.x) oldm[k] = fm[k];
+    for (uint32_t j = tid; j < G; j += blockDim.x) {
+        const uint32_t c = cc[m0 + j];
+        gcl[j] = c;
+        atomicAdd(&gpre[c], 1u);
+    }
+    __syncthreads();
+    // exclusive prefix of the grafted counts over the clusters (block scan in tiles)
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base <= L; base += blockDim.x) {
+        const uint32_t c = base + tid;
+        const uint32_t v = c <= L ? gpre[c] : 0u;
+        uint32_t x = v;
+        const uint32_t lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) s_wt[warp] = x;
+        __syncthreads();
+        uint32_t wb = 0, tot = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+            if (w < warp) wb += s_wt[w];
+            tot += s_wt[w];
+        }
+        if (c <= L) gpre[c] = carry + wb + x - v;
+        carry += tot;
+        __syncthreads();
+    }
+    // old members shift right by the grafts of every lower cluster
+    for (uint32_t k = tid; k < nold; k += blockDim.x) {
+        const uint32_t m = oldm[k];
+        fm[k + gpre[cc[m]]] = m;
+    }
+    // grafted chunk j: after its cluster's old members, in chunk order
+    for (uint32_t j = tid; j < G; j += blockDim.x) {
+        const uint32_t c = gcl[j];
+        uint32_t rank = 0;
+        for (uint32_t i = 0; i < j; ++i) rank += gcl[i] == c ? 1u : 0u;
+        fm[off[c + 1] + gpre[c] + rank] = m0 + j;
+    }
+    for (uint32_t c = tid; c <= L; c += blockDim.x) fo[c] = off[c] + gpre[c];
+    __syncthreads();
+    if (tid == 0) stp->m0 = M;
+}
+
+size_t compact_smem(const Arena& a) {
+    return ((size_t)2 * (a.cap_clusters + 1) + a.cap_chunks + 32) * 4;
+}
+
+cudaError_t launch_compact(const Arena& a, uint32_t min_grafted, cudaStream_t stream) {
+    const size_t smem = compact_smem(a);
+    static KernelCfg cfg;
+    cudaError_t e = ensure_smem(k_compact, cfg, smem);
+    if (e != cudaSuccess) return e;
+    k_compact<<<a.n_slots, kCompactThreads, smem, stream>>>(a, min_grafted ? min_grafted : 1u);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_chunk_rep(const Arena& a, uint32_t slot, uint32_t start, uint32_t take, uint32_t pooling,
                              float* rep_dev, cudaStream_t stream) {
     k_chunk_rep<<<1, 256, 0, stream>>>(a, slot, start, take, pooling, rep_dev);

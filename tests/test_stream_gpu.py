@@ -195,3 +195,36 @@ def test_config3_stream_parity_at_scale(tmp_path, seed):
     assert eng.device_error() == 0
     assert eng.slot_dims(0)[4] == n + steps
     assert eng.index_bytes(0) == ref.index_bytes()
+
+
+def test_compaction_keeps_selections_and_index():
+    """lc_compact folds the grafted chunks into the member CSR: the next
+    retrieve selects the same clusters and active ids, the index bytes are
+    unchanged, and further grafts keep matching the uncompacted twin."""
+    n, seeds, G, steps = 8192, [61, 62], 4, 200
+    engs = []
+    for _ in range(2):
+        eng, codes, qs = _gpu_engine(n, seeds, G, steps + 64)
+        engs.append(eng)
+    toks = _tokens(qs, steps, 3)
+    b = api.Budgets(token_budget=512)
+    ch = _Chunker()
+    S = len(seeds)
+    out = [torch.zeros((S, G, 128), device="cuda") for _ in engs]
+    for i, (q, k, v, code) in enumerate(toks):
+        plan = ch.push(code)
+        t = (None, None, None) if plan is None else tuple(_dev(np.full(S, x, np.uint32)) for x in plan)
+        for e, o in zip(engs, out):
+            e.decode_step_async(_dev(q), _bits(k), _bits(v), b, *t, out=o)
+        if i in (99, 150):
+            engs[0].compact(1)  # engine 0 compacts explicitly (engine 1 only by the every-128-steps rule)
+        if i % 25 == 24:
+            for s in range(S):
+                for g in range(G):
+                    a0, a1 = engs[0].selection(s, g), engs[1].selection(s, g)
+                    assert np.array_equal(a0.selected_clusters, a1.selected_clusters), (i, s, g)
+                    assert np.array_equal(a0.active_token_ids, a1.active_token_ids), (i, s, g)
+            assert np.array_equal(out[0].cpu().numpy(), out[1].cpu().numpy()), i
+    for s in range(S):
+        assert engs[0].index_bytes(s) == engs[1].index_bytes(s)
+    assert all(e.device_error() == 0 for e in engs)
