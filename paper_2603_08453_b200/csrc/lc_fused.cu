@@ -40,8 +40,7 @@ constexpr int kFuThreads = 288;   // 8 consumer warps + 1 producer warp
 constexpr int kFuCons = 256;      // threads of the consumer warps
 constexpr int kFuD = 128;
 constexpr uint32_t kFuRows = 64;  // candidate rows per stage
-constexpr uint32_t kFuStages = 3;       // ring depth when two CTAs share an SM
-constexpr uint32_t kFuMaxStages = 12;   // ring depth bound (one CTA per SM: the ring takes the freed shared memory)
+constexpr uint32_t kFuStages = 3;
 constexpr uint32_t kFuStageBytes = kFuRows * kFuD * 2 + kFuRows * 16;  // rows + per-row meta
 constexpr uint32_t kFuMaxUnion = 128;
 constexpr uint32_t kFuMaxKU = 64;
@@ -129,7 +128,6 @@ struct FusedParams {
     uint32_t g8cap;          // entries of the 8-row group table
     uint32_t pf;             // stages requested into L2 beyond the ring
     unsigned long long* prof;  // optional per-slot phase timestamps [slot][8] (LC_PROF=1)
-    uint32_t nst;            // fine-tier ring stages (kFuStages .. kFuMaxStages)
 };
 
 // dynamic shared memory: region A (phase-dependent: coarse tier / stage ring /
@@ -215,8 +213,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
     __shared__ uint32_t s_nc[GQ];                       // candidates per head
     __shared__ double s_qn[GQ], s_glo[GQ], s_gstep[GQ];
     __shared__ uint32_t s_emax[GQ];
-    __shared__ unsigned long long s_bar[2 * kFuMaxStages + 1];  // full[], empty[], coarse tier
-    const uint32_t NST = p.nst;  // fine-tier ring stages of this launch
+    __shared__ unsigned long long s_bar[2 * kFuStages + 1];  // full[], empty[], coarse tier
     __shared__ uint32_t s_nuu, s_kU, s_ng, s_deg, s_ncu;
     // P3 per head
     __shared__ unsigned long long s_wbefore[GQ];
@@ -269,11 +266,10 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
         uint32_t* s_uoff = reinterpret_cast<uint32_t*>(ukey + (size_t)G * P);
         uint32_t* s_umask = s_uoff + P + 1;
         if (tid == 0) {
-            for (uint32_t k = 0; k < 2 * NST; ++k)
-                mbar_init(smem_u32(&s_bar[k]), k < NST ? 1u : (uint32_t)(kFuCons / 32));
-            mbar_init(smem_u32(&s_bar[2 * kFuMaxStages]), 1u);
+            for (uint32_t k = 0; k < 2 * kFuStages + 1; ++k)
+                mbar_init(smem_u32(&s_bar[k]), k < kFuStages ? 1u : (k < 2 * kFuStages ? (uint32_t)(kFuCons / 32) : 1u));
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-            const uint32_t cb = smem_u32(&s_bar[2 * kFuMaxStages]);
+            const uint32_t cb = smem_u32(&s_bar[2 * kFuStages]);
             mbar_arrive_tx(cb, D * CU * 4 + CU * 8);
             bulk_g2s(smem_u32(ucs), a.ucent + (size_t)slot * CU * D, D * CU * 4, cb);
             bulk_g2s(smem_u32(s_urad), a.urad + (size_t)slot * CU, CU * 8, cb);
@@ -302,7 +298,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
         for (uint32_t x = tid; x < G * 256; x += kFuThreads) hist1[x] = 0u;
         if (tid < G) s_emax[tid] = 0u;
         __syncthreads();  // barrier inits, q, offsets
-        mbar_wait(smem_u32(&s_bar[2 * kFuMaxStages]), 0);
+        mbar_wait(smem_u32(&s_bar[2 * kFuStages]), 0);
         FU_MARK(8)
         // ||q_g|| (kernels.cpp:19-23) on the last warp; one thread per unit runs the
         // G coarse dots as independent exact chains
@@ -505,14 +501,14 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
             }
         };
         for (uint32_t t = 0; t < nstage; ++t) {
-            const uint32_t s = t % NST;
+            const uint32_t s = t % kFuStages;
             if (p.pf) {  // keep stages [t + ring, t + ring + pf) requested into L2
                 if (t == 0)
-                    for (uint32_t f = NST; f < NST + p.pf; ++f) prefetch(f);
+                    for (uint32_t f = kFuStages; f < kFuStages + p.pf; ++f) prefetch(f);
                 else
-                    prefetch(t + NST + p.pf - 1);
+                    prefetch(t + kFuStages + p.pf - 1);
             }
-            if (t >= NST) mbar_wait(smem_u32(&s_bar[NST + s]), ((t / NST) - 1) & 1u);
+            if (t >= kFuStages) mbar_wait(smem_u32(&s_bar[kFuStages + s]), ((t / kFuStages) - 1) & 1u);
             uint32_t cid = 0, rows = 0, srow = 0;
             const bool mine = run_of(t, cid, rows, srow);
             const uint32_t bytes = __reduce_add_sync(0xffffffffu, mine ? rows * (D * 2 + 16) : 0u);
@@ -560,8 +556,8 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
         uint32_t* hist_h = hist1 + (ehead ? eh : 0) * 256;
         double emax = 0.0;
         for (uint32_t t = 0; t < nstage; ++t) {
-            const uint32_t s = t % NST;
-            mbar_wait(smem_u32(&s_bar[s]), (t / NST) & 1u);
+            const uint32_t s = t % kFuStages;
+            mbar_wait(smem_u32(&s_bar[s]), (t / kFuStages) & 1u);
             const uint32_t gi = 8 * t + warp;
             if (gi < ng) {
                 const uint32_t e8 = g8[gi], k = e8 >> 16, l0 = e8 & 0xffffu;
@@ -606,7 +602,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&s_bar[NST + s]));
+            if (lane == 0) mbar_arrive(smem_u32(&s_bar[kFuStages + s]));
         }
         if (ehead) atomicMax(&s_emax[eh], __float_as_uint(__double2float_ru(emax)));
     }
@@ -1350,9 +1346,9 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
 // ---------------------------------------------------------------------------
 // Host: shape check, shared-memory sizing, launch.  Returns cudaErrorNotSupported
 // when the shape does not fit (the caller then runs the four-kernel chain).
-static uint32_t fu_region_a(uint32_t G, uint32_t cap_units, uint32_t pmax, uint32_t nst = kFuStages) {
+static uint32_t fu_region_a(uint32_t G, uint32_t cap_units, uint32_t pmax) {
     const uint32_t p1 = kFuD * cap_units * 4 + cap_units * 8 + G * pmax * 8 + (pmax + 1) * 4 + pmax * 4 + 64;
-    const uint32_t ring = nst * kFuStageBytes;
+    const uint32_t ring = kFuStages * kFuStageBytes;
     const uint32_t p3 = G * kFuLC * kFuRBytes + 16 * kFuColBytes;
     const uint32_t p4 = 33 * kFuThreads * 4 + 3 * kFuSpCache * 4;
     return (std::max(std::max(p1, ring), std::max(p3, p4)) + 127) & ~127u;
@@ -1377,26 +1373,11 @@ cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint
     if (std::min<uint64_t>((uint64_t)a.G * std::min(unit_topk, pmax), pmax) > kFuMaxUnion) return cudaErrorNotSupported;
     kc = (kc + 7) & ~7u;
     uc = (uc + 7) & ~7u;
-    uint32_t smem_a = fu_region_a(a.G, a.cap_units, pmax);
-    FuLayout lay = fu_layout(smem_a, a.G, kc, uc, bit_words(a.cap_chunks));
+    const uint32_t smem_a = fu_region_a(a.G, a.cap_units, pmax);
+    const FuLayout lay = fu_layout(smem_a, a.G, kc, uc, bit_words(a.cap_chunks));
     const DevProps dp = dev_props();
     // static shared memory of the instantiation is below 24 KB; keep the total within the opt-in limit
     if ((size_t)lay.total + 24 * 1024 > (size_t)dp.smem_blk) return cudaErrorNotSupported;
-    // A launch of at most one CTA per SM (few slots: a strong-scaling shard, one
-    // layer of a layer-by-layer decode) gives its fine-tier ring the shared memory
-    // a second CTA would have used: a lone CTA's streaming rate is bounded by the
-    // bytes its ring keeps in flight.
-    uint32_t nst = kFuStages;
-    if (n_slots <= (uint32_t)dp.sms && !getenv("LC_FUSED_SHALLOW")) {
-        const size_t rest = lay.total - smem_a, room = (size_t)dp.smem_blk - 24 * 1024 - rest;
-        nst = (uint32_t)std::min<size_t>(kFuMaxStages, room / kFuStageBytes);
-        if (nst > kFuStages) {
-            smem_a = fu_region_a(a.G, a.cap_units, pmax, nst);
-            lay = fu_layout(smem_a, a.G, kc, uc, bit_words(a.cap_chunks));
-        } else {
-            nst = kFuStages;
-        }
-    }
     if (getenv("LC_FUSED_DEBUG")) {
         static int once = 0;
         if (!once++) {
@@ -1418,7 +1399,7 @@ cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint
         cudaMemset(prof, 0, (size_t)a.n_slots * 16 * 8);
     }
     FusedParams fp{a, q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids,
-                   scratch, kc, uc, smem_a, fu_g8cap(uc), 0u, want_prof ? prof : nullptr, nst};
+                   scratch, kc, uc, smem_a, fu_g8cap(uc), 0u, want_prof ? prof : nullptr};
     if (const char* ev = getenv("LC_FUSED_PF")) fp.pf = (uint32_t)atoi(ev);  // experiments
     cudaError_t e;
     switch (a.G) {
