@@ -78,6 +78,29 @@ __device__ __forceinline__ void bar_g(uint32_t id, uint32_t n) {
 
 }  // namespace
 
+// 1D TMA (cp.async.bulk) into shared memory with mbarrier completion
+__device__ __forceinline__ void bulk_g2s3(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init3(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect3(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait3(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+
 struct Sel3Params {
     Arena a;
     uint32_t keys_cap;  // per-head candidates staged in k_pickq's shared memory
@@ -330,7 +353,11 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
 // Each warp scores a contiguous static range of tiles, then claims single
 // tiles from a pool (the last kFinePoolPct % of the list) as it finishes, so
 // SMs that see less bandwidth do less work.  In a tile each lane owns one
-// candidate: its 512-byte centroid is loaded into registers in one burst.
+// candidate.  A tile's fp16 rows are contiguous within each coarse unit, so
+// the lane that starts a unit's run moves the whole run with one 1D TMA bulk
+// copy into the warp's 3-stage shared-memory ring (mbarrier completion); two
+// tiles are in flight while the warp scores the third, and no row sits in
+// registers.
 //
 // The reference upper bound UB = fl64(sequential fp64 q.c) + qn*r
 // (kernels.cpp:155-159) is enclosed, not computed, from the fp16 copy of the
@@ -356,7 +383,12 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
     constexpr uint32_t G = GQ, V = D / 4;  // float4s per centroid
     __shared__ uint32_t s_tp[kMaxAttendSlots + 1];  // prefix of the slots' tile counts
     __shared__ uint32_t s_ws[kFiWarps];
-    __shared__ __align__(16) float s_q[kFiWarps][2][GQ * D];  // q of the warp's slots (double buffer)
+    __shared__ __align__(8) unsigned long long s_fbar[kFiWarps][3];  // the warps' ring barriers
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < 3; ++st) mbar_init3((uint32_t)__cvta_generic_to_shared(&s_fbar[warp][st]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     {
         const uint32_t per = (n + kFiThreads - 1) / kFiThreads, i0 = tid * per;
         uint32_t loc = 0;
@@ -403,19 +435,21 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             return t;
         };
         uint32_t lo = 0;  // slot (local index) of the last looked-up tile
-        // A tile goes through three stages, one loop iteration apart, so no
+        // A tile goes through four steps, one loop iteration apart, so no
         // dependent load sits on the critical path: (A) slot lookup + tile-table
-        // entry load, (B) the lane's unit row loads, (C) the centroid burst and
-        // the fp32 scoring.  The slot's q rides a cp.async into one of two
-        // per-warp buffers one tile ahead of its first use.
+        // entry load, (B) the lane's unit row loads, (I) the bulk copy of the
+        // tile's rows (issued by the lanes that start a unit run) + the lane's
+        // radius / weight loads, (C) scoring from shared memory.
         struct StA {
             uint32_t slot, ti;  // slot ~0u: no tile
             uint4 te;           // {first unit, unit starts, first local, -}
             uint32_t ncu;
         };
         struct StB {
-            uint32_t slot, valid, local, base, nu, mask, qb;
+            uint32_t slot, valid, local, base, mask, vc, starts;
             uint32_t qoff[GQ];
+            double r;
+            uint32_t wt;
         };
         auto stage_a = [&](uint32_t t) -> StA {
             StA x;
@@ -438,35 +472,58 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             x.ncu = __ldg(pv.hdr() + 2);
             return x;
         };
-        uint32_t qslot_next = ~0u, qb_next = 1;  // slot whose q was staged last, its buffer
         auto stage_b = [&](const StA& x) -> StB {
             StB y;
             y.slot = x.slot;
             y.valid = 0;
             y.mask = 0;
+            y.vc = 0;
+            y.r = 0.0;
+            y.wt = 0;
             if (x.slot == ~0u) return y;
             const PlanView pv(a.plan + (size_t)x.slot * a.plan_bytes, a);
-            y.valid = x.ti * 32 + lane < x.ncu;
+            y.vc = min(32u, x.ncu - x.ti * 32);
+            y.valid = lane < y.vc;
+            y.starts = x.te.y;
             const uint32_t below = x.te.y & ((2u << lane) - 1u);  // unit starts at positions <= lane
             const uint32_t nb = __popc(below);
             const uint32_t k = x.te.x + nb;
             y.local = y.valid ? (nb ? lane - (31 - __clz(below)) : x.te.z + lane) : 0u;
             const uint32_t* u = pv.units() + (size_t)k * (4 + G);
             y.base = __ldg(u + 2);
-            y.nu = __ldg(u + 3);
             y.mask = y.valid ? __ldg(u + 1) : 0u;
 #pragma unroll
             for (int g = 0; g < GQ; ++g) y.qoff[g] = __ldg(u + 4 + g);
-            if (x.slot != qslot_next) {  // stage the slot's q into the other buffer
-                qslot_next = x.slot;
-                qb_next ^= 1u;
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_q[warp][qb_next][0]);
-                const unsigned char* src = reinterpret_cast<const unsigned char*>(p.q + (size_t)x.slot * G * D);
-                for (uint32_t c = lane; c < G * D / 4; c += 32)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst + c * 16), "l"(src + c * 16));
-            }
-            y.qb = qb_next;
             return y;
+        };
+        // the warp's ring: 3 stages of 32 rows; barrier per stage
+        constexpr uint32_t ROWB = D * 2, STG = 32 * ROWB, NSTG = 3;
+        extern __shared__ __align__(128) unsigned char fsm[];
+        const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(fsm + (size_t)warp * NSTG * STG);
+        const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&s_fbar[warp][0]);
+        float* qs = reinterpret_cast<float*>(fsm + (size_t)kFiWarps * NSTG * STG) + (size_t)warp * GQ * D;
+        uint32_t qslot = ~0u;
+        // (I): the lanes that start a unit run copy the run; every lane requests its radius / weight
+        auto issue = [&](StB& y, uint32_t st) {
+            if (y.slot == ~0u) return;
+            const uint32_t bar = bar_s + 8u * st;
+            if (lane == 0) mbar_expect3(bar, y.vc * ROWB);
+            __syncwarp();
+            const bool start = y.valid && (lane == 0 || ((y.starts >> lane) & 1u));
+            if (start) {
+                const uint32_t later = y.starts & ~((2u << lane) - 1u);
+                const uint32_t end = min(later ? (uint32_t)(__ffs(later) - 1) : 32u, y.vc);
+                // the ring stage was read (generic proxy) before the warp's last __syncwarp
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                bulk_g2s3(ring_s + st * STG + lane * ROWB,
+                          a.frow16 + (size_t)y.slot * a.cap_clusters * D + ((size_t)y.base + y.local) * D,
+                          (end - lane) * ROWB, bar);
+            }
+            if (y.valid) {
+                const uint32_t cid = y.base + y.local;
+                y.r = __ldg(a.frad + (size_t)y.slot * a.cap_clusters + cid);
+                y.wt = p.mode == 1 ? __ldg(a.ftok + (size_t)y.slot * a.cap_clusters + cid) : 1u;
+            }
         };
         uint32_t mslot = ~0u;  // slot whose per-head key range the warp is tracking
         unsigned long long wmin[GQ], wmax[GQ];
@@ -488,52 +545,62 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             }
         };
 
+        // prologue: B of tiles 0..2, tiles 0 and 1 issued, A of tile 3
         StA sa = stage_a(next_tile());
         StB d = stage_b(sa);
-        asm volatile("cp.async.commit_group;\n" ::);
         sa = stage_a(next_tile());
-        while (d.slot != ~0u) {
-            // (C) this tile's centroids, radius and weight: one burst of loads
-            // the lane's fp16 centroid row (16-byte chunks in swz16 order, frow_at)
-            const uint4* row = reinterpret_cast<const uint4*>(a.frow16 + (size_t)d.slot * a.cap_clusters * D +
-                                                             ((size_t)d.base + d.local) * D);
-            uint4 v16[V / 2];
-            if (d.valid) {
-#pragma unroll
-                for (uint32_t j = 0; j < V / 2; ++j) v16[j] = __ldg(row + swz16(d.local, j, D));
+        StB n1 = stage_b(sa);
+        issue(d, 0);
+        sa = stage_a(next_tile());
+        StB n2 = stage_b(sa);
+        issue(n1, 1);
+        sa = stage_a(next_tile());
+        for (uint32_t it = 0; d.slot != ~0u; ++it) {
+            issue(n2, (it + 2) % NSTG);       // (I) tile it + 2
+            const StB nb = stage_b(sa);       // (B) tile it + 3
+            sa = stage_a(next_tile());        // (A) tile it + 4
+            if (d.slot != qslot) {  // the tile's q (fp32) into the warp's buffer
+                __syncwarp();
+                const float4* src = reinterpret_cast<const float4*>(p.q + (size_t)d.slot * G * D);
+                for (uint32_t c = lane; c < G * D / 4; c += 32) reinterpret_cast<float4*>(qs)[c] = __ldg(src + c);
+                qslot = d.slot;
+                __syncwarp();
             }
-            const uint32_t cid = d.base + d.local;
-            const double r = d.valid ? __ldg(a.frad + (size_t)d.slot * a.cap_clusters + cid) : 0.0;
-            const uint32_t wt = d.valid ? (p.mode == 1 ? __ldg(a.ftok + (size_t)d.slot * a.cap_clusters + cid) : 1u) : 0u;
-            // (B) next tile, (A) the one after
-            const StB dn = stage_b(sa);
-            asm volatile("cp.async.commit_group;\n" ::);
-            sa = stage_a(next_tile());
-            asm volatile("cp.async.wait_group 1;\n" ::);  // this tile's q (staged last iteration)
-            __syncwarp();
-            const float* qs = s_q[warp][d.qb];
+            mbar_wait3(bar_s + 8u * (it % NSTG), (it / NSTG) & 1u);  // (C) this tile's rows
+            const uint32_t rowp = ring_s + (it % NSTG) * STG + lane * ROWB;
+            const double r = d.r;
+            const uint32_t wt = d.wt;
             float s4[GQ][4], c2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int g = 0; g < GQ; ++g)
 #pragma unroll
                 for (int t = 0; t < 4; ++t) s4[g][t] = 0.f;
 #pragma unroll
-            for (uint32_t j = 0; j < V; ++j) {
-                const uint32_t w0 = (j & 1) ? v16[j >> 1].z : v16[j >> 1].x, w1 = (j & 1) ? v16[j >> 1].w : v16[j >> 1].y;
-                const float2 lo2 = __half22float2(*reinterpret_cast<const __half2*>(&w0));
-                const float2 hi2 = __half22float2(*reinterpret_cast<const __half2*>(&w1));
-                const float4 vj = make_float4(lo2.x, lo2.y, hi2.x, hi2.y);
-                c2[0] = fmaf(vj.x, vj.x, c2[0]);  // ||c~||^2, shared by every head
-                c2[1] = fmaf(vj.y, vj.y, c2[1]);
-                c2[2] = fmaf(vj.z, vj.z, c2[2]);
-                c2[3] = fmaf(vj.w, vj.w, c2[3]);
+            for (uint32_t j2 = 0; j2 < V / 2; ++j2) {
+                uint4 v16 = make_uint4(0u, 0u, 0u, 0u);
+                if (d.valid)
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                                 : "=r"(v16.x), "=r"(v16.y), "=r"(v16.z), "=r"(v16.w)
+                                 : "r"(rowp + swz16(d.local, j2, D) * 16u));
 #pragma unroll
-                for (int g = 0; g < GQ; ++g) {
-                    const float4 q4 = reinterpret_cast<const float4*>(qs + g * D)[j];
-                    s4[g][0] = fmaf(q4.x, vj.x, s4[g][0]);
-                    s4[g][1] = fmaf(q4.y, vj.y, s4[g][1]);
-                    s4[g][2] = fmaf(q4.z, vj.z, s4[g][2]);
-                    s4[g][3] = fmaf(q4.w, vj.w, s4[g][3]);
+                for (uint32_t h2 = 0; h2 < 2; ++h2) {
+                    const uint32_t j = 2 * j2 + h2;
+                    const uint32_t w0 = h2 ? v16.z : v16.x, w1 = h2 ? v16.w : v16.y;
+                    const float2 lo2 = __half22float2(*reinterpret_cast<const __half2*>(&w0));
+                    const float2 hi2 = __half22float2(*reinterpret_cast<const __half2*>(&w1));
+                    const float4 vj = make_float4(lo2.x, lo2.y, hi2.x, hi2.y);
+                    c2[0] = fmaf(vj.x, vj.x, c2[0]);  // ||c~||^2, shared by every head
+                    c2[1] = fmaf(vj.y, vj.y, c2[1]);
+                    c2[2] = fmaf(vj.z, vj.z, c2[2]);
+                    c2[3] = fmaf(vj.w, vj.w, c2[3]);
+#pragma unroll
+                    for (int g = 0; g < GQ; ++g) {
+                        const float4 q4 = reinterpret_cast<const float4*>(qs + g * D)[j];
+                        s4[g][0] = fmaf(q4.x, vj.x, s4[g][0]);
+                        s4[g][1] = fmaf(q4.y, vj.y, s4[g][1]);
+                        s4[g][2] = fmaf(q4.z, vj.z, s4[g][2]);
+                        s4[g][3] = fmaf(q4.w, vj.w, s4[g][3]);
+                    }
                 }
             }
             // the filter reads c~ = fp16(c): |c_j - c~_j| <= 2^-11 |c_j| + 2^-25.  ||c~|| from
@@ -574,10 +641,11 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                     wmax[g] = max(wmax[g], key);
                 }
             }
-            __syncwarp();  // the q buffer may be restaged two tiles later
-            d = dn;
+            __syncwarp();  // the stage is refilled two iterations later
+            d = n1;
+            n1 = n2;
+            n2 = nb;
         }
-        asm volatile("cp.async.wait_group 0;\n" ::);
         flush_minmax();
     }
     // the last CTA out resets the pool for the next launch
@@ -1547,11 +1615,13 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
     k_coarse<D, GQ><<<n_slots, kCoThreads, co_smem, stream>>>(p);
     e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return select3_fail(e1, "k_coarse launch", co_smem);
-    const uint32_t fine_grid = persistent_grid(k_fine<D, GQ>, fi_cfg, kFiThreads, 0);
+    // k_fine: each warp's 3-stage row ring, then its q buffer
+    const size_t fi_smem = (size_t)kFiWarps * (3 * 32 * D * 2 + (size_t)GQ * D * 4);
+    const uint32_t fine_grid = persistent_grid(k_fine<D, GQ>, fi_cfg, kFiThreads, fi_smem);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += kMaxAttendSlots) {
         Sel3Params q = p;
         q.a.slot0 = p.a.slot0 + s0;
-        cudaError_t e = launch_pdl(k_fine<D, GQ>, dim3(fine_grid), dim3(kFiThreads), 0, stream, q,
+        cudaError_t e = launch_pdl(k_fine<D, GQ>, dim3(fine_grid), dim3(kFiThreads), fi_smem, stream, q,
                                    std::min<uint32_t>(kMaxAttendSlots, n_slots - s0));
         if (e != cudaSuccess) return select3_fail(e, "k_fine launch", fine_grid);
     }
