@@ -19,6 +19,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -231,12 +234,14 @@ uint64_t mixv(uint64_t h, const T& x) {
 }
 
 // The engine cache key of a (HierarchicalIndex, TokenStore) pair: identity
-// (addresses, sizes, the node arrays' buffers) plus a content digest of every
-// small field -- radii, token counts, parents, member lists, chunk spans,
-// the coarse centroids -- and of a fixed sample of each fine centroid (first,
-// middle and last coordinate) and of the store's rows.  That is ~2% of the
-// bytes a full content hash reads at 128K (the round-1 key hashed every
-// centroid byte-wise on every call, ~2.5 ms).
+// (addresses, sizes, the node arrays' buffers) plus a digest of every
+// cluster's and unit's radius, token count, parent and member count, one
+// coordinate of each fine centroid, a strided sample of the coarse centroids,
+// chunk spans and chunk -> cluster map, and a sample of the store's rows
+// (~30 K words at 128K, ~0.1 ms; the round-1 key hashed every centroid
+// byte-wise on every call, ~2.5 ms).  An in-place edit of a field outside
+// the digest on the same index object between calls is not seen; build a new
+// index or touch a digested field (e.g. a radius) after such an edit.
 uint64_t store_key(uint64_t h, const TokenStore& s) {
     const size_t n = s.size(), d = s.dim();
     h = mixv(h, &s);
@@ -244,7 +249,7 @@ uint64_t store_key(uint64_t h, const TokenStore& s) {
     h = mixv(h, d);
     for (const auto arr : {s.keys_flat(), s.values_flat()}) {
         h = mixv(h, arr.data());
-        const size_t step = std::max<size_t>(1, arr.size() / 4096);
+        const size_t step = std::max<size_t>(1, arr.size() / 1024);
         for (size_t i = 0; i < arr.size(); i += step) h = mixv(h, arr[i]);
         if (!arr.empty()) h = mix(h, arr.data() + (arr.size() - std::min<size_t>(arr.size(), d)),
                                   std::min<size_t>(arr.size(), d) * 4);
@@ -263,24 +268,21 @@ uint64_t fingerprint(const HierarchicalIndex& ix) {
     h = mixv(h, ix.chunks.data());
     h = mixv(h, ix.fine.data());
     h = mixv(h, ix.coarse.data());
-    for (const Chunk& c : ix.chunks) h = mixv(h, c.span.start), h = mixv(h, c.span.end);
-    h = mix(h, ix.cluster_of_chunk.data(), ix.cluster_of_chunk.size() * 4);
+    // chunk spans and chunk -> cluster: a fixed stride (they only change by
+    // appending, which changes the sizes above)
+    for (size_t c = 0; c < ix.chunks.size(); c += 16) h = mixv(h, ix.chunks[c].span.start);
+    if (!ix.chunks.empty()) h = mixv(h, ix.chunks.back().span.end);
+    for (size_t c = 0; c < ix.cluster_of_chunk.size(); c += 16) h = mixv(h, ix.cluster_of_chunk[c]);
+    // every cluster's scalar fields and member count, one centroid coordinate
     for (const FineCluster& f : ix.fine) {
         h = mixv(h, f.radius);
-        h = mixv(h, f.token_count);
-        h = mixv(h, f.parent_unit);
-        h = mixv(h, f.centroid.data());
-        if (!f.centroid.empty()) {
-            h = mixv(h, f.centroid.front());
-            h = mixv(h, f.centroid[f.centroid.size() / 2]);
-            h = mixv(h, f.centroid.back());
-        }
-        h = mix(h, f.members.data(), f.members.size() * 4);
+        h = mixv(h, (uint64_t)f.token_count ^ ((uint64_t)f.parent_unit << 40) ^ ((uint64_t)f.members.size() << 52));
+        if (!f.centroid.empty()) h = mixv(h, f.centroid[f.centroid.size() / 2]);
     }
     for (const CoarseUnit& u : ix.coarse) {
-        h = mix(h, u.centroid.data(), u.centroid.size() * 4);
         h = mixv(h, u.radius);
-        h = mix(h, u.members.data(), u.members.size() * 4);
+        h = mixv(h, u.members.size());
+        for (size_t j = 0; j < u.centroid.size(); j += 16) h = mixv(h, u.centroid[j]);
     }
     return ix.store ? store_key(h, *ix.store) : h;
 }
@@ -338,14 +340,20 @@ RetrievalResult run_retrieve(Engine& e, const HierarchicalIndex& ix, const Token
         if (attend) res.output = sparse_attention(q, store, res.active_token_ids);
         return res;
     }
+    static const bool prof = getenv("TIERKV_DROPIN_PROF") != nullptr;  // diagnostics: per-phase host times
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
     std::copy(q.begin(), q.end(), e.h_io);
     cuda_ck(cudaMemcpyAsync(e.q_dev, e.h_io, q.size() * 4, cudaMemcpyHostToDevice, e.st), "q H2D");
     e.buffer_list(buf);
     const lc_budgets b = to_c(budgets);
+    const auto t1 = now();
     ck(lc_retrieve(e.h, e.q_dev, &b, LC_BUFFER_LIST, e.boff_dev, e.bids_dev, attend ? e.out_dev : nullptr, e.st));
     if (attend)
         cuda_ck(cudaMemcpyAsync(e.h_io + e.d, e.out_dev, store.dim() * 4, cudaMemcpyDeviceToHost, e.st), "out D2H");
+    const auto t2 = now();
     cuda_ck(cudaStreamSynchronize(e.st), "retrieve");
+    const auto t3 = now();
     lc_selection_info info{};
     res.selected_units.resize(ix.coarse.size());
     res.selected_clusters.resize(ix.fine.size());
@@ -353,6 +361,12 @@ RetrievalResult run_retrieve(Engine& e, const HierarchicalIndex& ix, const Token
     ck(lc_selection_download(e.h, 0, 0, &info, res.selected_units.data(), res.selected_units.size(),
                              res.selected_clusters.data(), res.selected_clusters.size(),
                              res.active_token_ids.data(), res.active_token_ids.size()));
+    if (prof) {
+        const auto t4 = now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "[dropin] stage %.1f launch %.1f device %.1f download %.1f us\n", us(t0, t1), us(t1, t2),
+                     us(t2, t3), us(t3, t4));
+    }
     if (info.error) e.device_errors();  // sticky bits: raise the reference's exception and clear them
     res.selected_units.resize(info.n_units);
     res.selected_clusters.resize(info.n_clusters);

@@ -690,58 +690,119 @@ size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots) {
 // (kernels.cpp:108-144) in fp64 -- logits q.k / sqrt(d), max-subtracted
 // softmax, weighted value sum -- one warp per query head over the slot's row
 // list: per token the lanes split the dims, the logit is a warp sum.
-__global__ void __launch_bounds__(256) k_attend_exact(Arena a, const float* q, float* out) {
-    const uint32_t slot = a.slot0 + blockIdx.x, lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-    const uint32_t d = a.d, G = a.G;
-    if (g >= G) return;
+// Reference-exact mode (fp32 K/V): kernels::attention (kernels.cpp:108-144)
+// in fp64, split over the row list: CTA (g, slot, z) takes entries
+// [z*C, (z+1)*C) of the slot's row list, one token per thread (sequential
+// fp64 dot over the fp32 key row), its max, the weights through shared
+// memory, and (dim, half) threads accumulating the fp64 value sums; it leaves
+// (m, z, o[d]) in fp64.  k_attend_exact_merge combines a head's splits.
+__global__ void __launch_bounds__(256) k_attend_exact(Arena a, const float* q, double* part, uint32_t S) {
+    const uint32_t g = blockIdx.x, sl = blockIdx.y, zi = blockIdx.z, tid = threadIdx.x;
+    const uint32_t slot = a.slot0 + sl, d = a.d, G = a.G;
     const uint32_t n = a.slot_tok[slot];
+    const uint32_t C = (n + S - 1) / S, b0 = min(n, zi * C), b1 = min(n, b0 + C);
     const uint32_t* rows = a.rows + (size_t)slot * a.cap_tokens;
     const float* K = a.Kf + kv_off(a, slot);
     const float* V = a.Vf + kv_off(a, slot);
     const float* qg = q + ((size_t)slot * G + g) * d;
     const double scale = 1.0 / sqrt((double)d);
-    auto logit = [&](uint32_t row) -> double {
-        double s = 0.0;
-        for (uint32_t j = lane; j < d; j += 32) s += (double)qg[j] * (double)K[(size_t)row * d + j];
+    __shared__ double s_q[256];
+    __shared__ double s_w[256], s_acc[256];
+    __shared__ uint32_t s_row[256];
+    __shared__ double s_mx[8];
+    for (uint32_t j = tid; j < d; j += blockDim.x) s_q[j] = (double)qg[j];
+    __syncthreads();
+    double* pp = part + (((size_t)sl * G + g) * S + zi) * (d + 2);
+    // the range's entries in chunks of one per thread: logit, then the chunk max
+    double m = -INFINITY, z = 0.0, acc0 = 0.0, acc1 = 0.0;
+    const uint32_t j = tid & 127u, h = tid >> 7;
+    for (uint32_t base = b0; base < b1; base += blockDim.x) {
+        const uint32_t t = base + tid;
+        double l = -INFINITY;
+        uint32_t row = 0;
+        if (t < b1) {
+            const uint32_t e = rows[t];
+            if ((e >> (24 + g)) & 1u) {
+                row = e & 0x00ffffffu;
+                const float4* kr = reinterpret_cast<const float4*>(K + (size_t)row * d);
+                double s = 0.0;
+                for (uint32_t j4 = 0; j4 < d / 4; ++j4) {
+                    const float4 kv = __ldg(kr + j4);
+                    s = __fma_rn(s_q[4 * j4], (double)kv.x, s);
+                    s = __fma_rn(s_q[4 * j4 + 1], (double)kv.y, s);
+                    s = __fma_rn(s_q[4 * j4 + 2], (double)kv.z, s);
+                    s = __fma_rn(s_q[4 * j4 + 3], (double)kv.w, s);
+                }
+                l = s * scale;
+            }
+        }
+        double cm = l;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        return s * scale;
-    };
-    double mx = -INFINITY;
-    uint32_t cnt = 0;
-    for (uint32_t t = 0; t < n; ++t) {
-        const uint32_t e = rows[t];
-        if (!((e >> (24 + g)) & 1u)) continue;
-        mx = fmax(mx, logit(e & 0x00ffffffu));
-        ++cnt;
+        for (int o = 16; o > 0; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+        if ((tid & 31) == 0) s_mx[tid >> 5] = cm;
+        __syncthreads();
+        cm = -INFINITY;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) cm = fmax(cm, s_mx[w]);
+        const double mn = fmax(m, cm);
+        if (mn != -INFINITY) {  // rescale what the earlier chunks accumulated
+            const double f = m == -INFINITY ? 0.0 : exp(m - mn);
+            z *= f;
+            acc0 *= f;
+            acc1 *= f;
+            m = mn;
+        }
+        s_w[tid] = l == -INFINITY ? 0.0 : exp(l - m);
+        s_row[tid] = row;
+        __syncthreads();
+        const uint32_t cnt = min(blockDim.x, b1 - base), half = (cnt + 1) / 2;
+        const uint32_t i0 = h ? half : 0u, i1 = h ? cnt : half;
+        for (uint32_t i = i0; i < i1; ++i) {
+            const double wi = s_w[i];
+            if (wi == 0.0) continue;
+            const float* vr = V + (size_t)s_row[i] * d;
+            if (j < d) acc0 += wi * (double)vr[j];
+            if (j + 128 < d) acc1 += wi * (double)vr[j + 128];
+            z += wi;
+        }
+        __syncthreads();
     }
-    float* og = out + ((size_t)slot * G + g) * d;
-    if (cnt == 0) {  // sparse_attention over an empty set throws (retriever.cpp:43)
-        for (uint32_t j = lane; j < d; j += 32) og[j] = 0.f;
-        if (lane == 0) atomicOr(a.err, kErrEmptyActive);
-        return;
+    if (h == 1) {
+        s_acc[j] = acc0;
+        s_acc[128 + j] = acc1;
+        if (j == 0) s_w[0] = z;
     }
-    constexpr int kMaxPer = 8;  // d <= 256
-    double acc[kMaxPer];
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) acc[k] = 0.0;
-    double z = 0.0;
-    for (uint32_t t = 0; t < n; ++t) {
-        const uint32_t e = rows[t];
-        if (!((e >> (24 + g)) & 1u)) continue;
-        const uint32_t row = e & 0x00ffffffu;
-        const double w = exp(logit(row) - mx);
-        z += w;
-#pragma unroll
-        for (int k = 0; k < kMaxPer; ++k) {
-            const uint32_t j = lane + 32 * k;
-            if (j < d) acc[k] += w * (double)V[(size_t)row * d + j];
+    __syncthreads();
+    if (h == 0) {
+        if (j < d) pp[2 + j] = acc0 + s_acc[j];
+        if (j + 128 < d) pp[2 + j + 128] = acc1 + s_acc[128 + j];
+        if (j == 0) {
+            pp[0] = m;
+            pp[1] = z + s_w[0];
         }
     }
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-        const uint32_t j = lane + 32 * k;
-        if (j < d) og[j] = (float)(acc[k] / z);
+}
+
+__global__ void __launch_bounds__(256) k_attend_exact_merge(Arena a, const double* part, uint32_t S, float* out) {
+    const uint32_t g = blockIdx.x, sl = blockIdx.y, tid = threadIdx.x, slot = a.slot0 + sl, d = a.d, G = a.G;
+    const double* pp = part + ((size_t)sl * G + g) * S * (d + 2);
+    double M = -INFINITY;
+    for (uint32_t z = 0; z < S; ++z) M = fmax(M, pp[(size_t)z * (d + 2)]);
+    float* og = out + ((size_t)slot * G + g) * d;
+    if (M == -INFINITY) {  // sparse_attention over an empty set throws (retriever.cpp:43)
+        for (uint32_t j = tid; j < d; j += blockDim.x) og[j] = 0.f;
+        if (tid == 0) atomicOr(a.err, kErrEmptyActive);
+        return;
+    }
+    for (uint32_t j = tid; j < d; j += blockDim.x) {
+        double num = 0.0, den = 0.0;
+        for (uint32_t z = 0; z < S; ++z) {
+            const double* pz = pp + (size_t)z * (d + 2);
+            if (pz[0] == -INFINITY) continue;
+            const double f = exp(pz[0] - M);
+            num += f * pz[2 + j];
+            den += f * pz[1];
+        }
+        og[j] = (float)(num / den);
     }
 }
 
@@ -756,7 +817,13 @@ cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned 
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
                           cudaStream_t stream, const PeerGather* pg) {
     if (a.kv_f32) {
-        k_attend_exact<<<n_slots, 32 * a.G, 0, stream>>>(a, q, out);
+        // splits per (slot, head): as many as the partials buffer holds, at most 16
+        const size_t cap = (attend_partials_floats(a.d, a.G, n_slots) - 16) * 4;
+        const size_t per = (size_t)n_slots * a.G * (a.d + 2) * 8;
+        const uint32_t S = (uint32_t)std::max<size_t>(1, std::min<size_t>(16, cap / std::max<size_t>(per, 1)));
+        double* dp = reinterpret_cast<double*>(part + 16);
+        k_attend_exact<<<dim3(a.G, n_slots, S), 256, 0, stream>>>(a, q, dp, S);
+        k_attend_exact_merge<<<dim3(a.G, n_slots), 128, 0, stream>>>(a, dp, S, out);
         return cudaGetLastError();
     }
     const uint32_t grid = attend_grid(a.d);

@@ -1446,6 +1446,28 @@ cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint
                     "spans %.2f | max %.2f | first start->last end %.1f us | stages %.1f R %.1f per slot\n",
                     ph[0] / cnt / 1e3, ph[1] / cnt / 1e3, ph[2] / cnt / 1e3, ph[3] / cnt / 1e3, ph[4] / cnt / 1e3,
                     mx / 1e3, (double)(t1 - t0) / 1e3, st / cnt, rr / cnt);
+        if (cnt > 0) {  // the slowest decile of CTAs: where their time goes and how big their slots are
+            std::vector<std::pair<double, uint32_t>> dur;
+            for (uint32_t s = a.slot0; s < a.slot0 + n_slots; ++s) {
+                const unsigned long long* x = &t[(size_t)s * 16];
+                if (x[5] && x[5] >= x[0]) dur.push_back({(double)(x[5] - x[0]), s});
+            }
+            std::sort(dur.begin(), dur.end());
+            const size_t k0 = dur.size() - std::max<size_t>(1, dur.size() / 10);
+            double sp[5] = {0, 0, 0, 0, 0}, sst = 0, srr = 0, c2 = 0, start = 0;
+            for (size_t i = k0; i < dur.size(); ++i) {
+                const unsigned long long* x = &t[(size_t)dur[i].second * 16];
+                for (int k = 0; k < 5; ++k) sp[k] += (double)(x[k + 1] - x[k]);
+                sst += (double)(x[6] & 0xffffffffull);
+                srr += (double)(x[6] >> 32);
+                start += (double)(x[0] - t0);
+                c2 += 1;
+            }
+            fprintf(stderr, "[LC_PROF] k_select slowest 10%%: coarse %.2f fine %.2f select %.2f rank+members %.2f spans "
+                    "%.2f us | start offset %.2f us | stages %.1f R %.1f | median CTA %.2f us\n",
+                    sp[0] / c2 / 1e3, sp[1] / c2 / 1e3, sp[2] / c2 / 1e3, sp[3] / c2 / 1e3, sp[4] / c2 / 1e3,
+                    start / c2 / 1e3, sst / c2, srr / c2, dur[dur.size() / 2].first / 1e3);
+        }
     }
     return e;
 }

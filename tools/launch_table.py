@@ -7,7 +7,7 @@ import re
 import sys
 
 
-def main(src, dst, round_tag, only=None):
+def main(src, dst, round_tag, only=None, max_id=None):
     rows = list(csv.reader(open(src)))
     hdr = None
     per = {}
@@ -18,6 +18,8 @@ def main(src, dst, round_tag, only=None):
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
             if only and not re.search(only, d["Kernel Name"]):
+                continue
+            if max_id is not None and int(d["ID"]) > max_id:
                 continue
             per.setdefault((d["ID"], d["Kernel Name"]), {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     agg = collections.OrderedDict()
@@ -39,4 +41,5 @@ def main(src, dst, round_tag, only=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "r01", sys.argv[4] if len(sys.argv) > 4 else None)
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "r01", sys.argv[4] if len(sys.argv) > 4 else None,
+         int(sys.argv[5]) if len(sys.argv) > 5 else None)
