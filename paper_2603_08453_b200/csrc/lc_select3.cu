@@ -101,6 +101,26 @@ __device__ __forceinline__ void mbar_wait3(uint32_t bar, uint32_t parity) {
     }
 }
 
+__device__ __forceinline__ void mma_f16x(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2x(float lo, float hi) {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+// the tensor-core filter's error constants (the same computation and bound as
+// k_select, lc_fused.cu): fp16 rounding of c (2^-11), q's fp16 hi + lo split
+// (2^-22), fp32 MMA accumulation over <= 16 k-steps (2^-15, generous), the
+// final hi + lo add (2^-24), subnormal terms 2^-25 sqrt(d); 2^-44 for the
+// reference's fp64 dot and our fp64 adds
+constexpr double kFiK1 = 5.25e-4;
+constexpr double kFiK2 = 3.5e-7;
+constexpr double kFiK3 = 5.7e-14;
+
 struct Sel3Params {
     Arena a;
     uint32_t keys_cap;  // per-head candidates staged in k_pickq's shared memory
@@ -384,6 +404,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
     __shared__ uint32_t s_tp[kMaxAttendSlots + 1];  // prefix of the slots' tile counts
     __shared__ uint32_t s_ws[kFiWarps];
     __shared__ __align__(8) unsigned long long s_fbar[kFiWarps][3];  // the warps' ring barriers
+    __shared__ float s_sco[kFiWarps][GQ][32];                       // a tile's scores, (head, candidate)
     if (lane == 0) {
 #pragma unroll
         for (int st = 0; st < 3; ++st) mbar_init3((uint32_t)__cvta_generic_to_shared(&s_fbar[warp][st]), 1u);
@@ -449,7 +470,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             uint32_t slot, valid, local, base, mask, vc, starts;
             uint32_t qoff[GQ];
             double r;
-            uint32_t wt;
+            uint32_t wt, cnb;  // token count (mode 1) or 1; the row's norm bound (f32 bits)
         };
         auto stage_a = [&](uint32_t t) -> StA {
             StA x;
@@ -480,6 +501,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             y.vc = 0;
             y.r = 0.0;
             y.wt = 0;
+            y.cnb = 0;
             if (x.slot == ~0u) return y;
             const PlanView pv(a.plan + (size_t)x.slot * a.plan_bytes, a);
             y.vc = min(32u, x.ncu - x.ti * 32);
@@ -502,8 +524,11 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
         const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(fsm + (size_t)warp * NSTG * STG);
         const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&s_fbar[warp][0]);
         float* qs = reinterpret_cast<float*>(fsm + (size_t)kFiWarps * NSTG * STG) + (size_t)warp * GQ * D;
-        uint32_t qslot = ~0u;
-        // (I): the lanes that start a unit run copy the run; every lane requests its radius / weight
+        uint32_t qslot = ~0u, fslot = ~0u;
+        constexpr int KSF = D >= 32 ? D / 16 : 2;  // MMA k-steps (D >= 32; smaller dims use fp32 FMAs)
+        const uint32_t r = lane >> 2, c = lane & 3;
+        uint32_t qf[KSF][4];
+        // (I): the lanes that start a unit run copy the run; every lane requests its row's metadata
         auto issue = [&](StB& y, uint32_t st) {
             if (y.slot == ~0u) return;
             const uint32_t bar = bar_s + 8u * st;
@@ -519,10 +544,11 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                           a.frow16 + (size_t)y.slot * a.cap_clusters * D + ((size_t)y.base + y.local) * D,
                           (end - lane) * ROWB, bar);
             }
-            if (y.valid) {
-                const uint32_t cid = y.base + y.local;
-                y.r = __ldg(a.frad + (size_t)y.slot * a.cap_clusters + cid);
-                y.wt = p.mode == 1 ? __ldg(a.ftok + (size_t)y.slot * a.cap_clusters + cid) : 1u;
+            if (y.valid) {  // the row's filter metadata: radius, norm bound, token count
+                const uint4 mt = __ldg(a.fmeta + (size_t)y.slot * a.cap_clusters + y.base + y.local);
+                y.r = __hiloint2double((int)mt.y, (int)mt.x);
+                y.cnb = mt.z;
+                y.wt = p.mode == 1 ? mt.w : 1u;
             }
         };
         uint32_t mslot = ~0u;  // slot whose per-head key range the warp is tracking
@@ -567,10 +593,52 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 __syncwarp();
             }
             mbar_wait3(bar_s + 8u * (it % NSTG), (it / NSTG) & 1u);  // (C) this tile's rows
+            if constexpr (D >= 32) {
+            if (d.slot != fslot) {  // q as fp16 hi + lo rows of the MMA A operand (heads r, r + 8)
+                fslot = d.slot;
+                const uint32_t gr = r < G ? r : 0u;
+#pragma unroll
+                for (int s2 = 0; s2 < KSF; ++s2) {
+                    const float* qq = qs + gr * D + c * (D / 4) + 4 * s2;
+                    float hh[4], ll[4];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        hh[x] = __half2float(__float2half_rn(qq[x]));
+                        ll[x] = qq[x] - hh[x];
+                    }
+                    const bool on = r < G;
+                    qf[s2][0] = on ? pack_h2x(hh[0], hh[1]) : 0u;
+                    qf[s2][2] = on ? pack_h2x(hh[2], hh[3]) : 0u;
+                    qf[s2][1] = on ? pack_h2x(ll[0], ll[1]) : 0u;
+                    qf[s2][3] = on ? pack_h2x(ll[2], ll[3]) : 0u;
+                }
+            }
+            // S = Q C~^T on the tensor cores, n-tile by n-tile (8 candidates each);
+            // thread (r, c) holds head r's scores of candidates 8 nt + 2c, + 1
+            const uint32_t stg = ring_s + (it % NSTG) * STG;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const uint32_t row = 8 * nt + r;
+                const uint32_t loc = __shfl_sync(0xffffffffu, d.local, row);
+                float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int w2 = 0; w2 < KSF / 2; ++w2) {
+                    uint4 kv;
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                                 : "=r"(kv.x), "=r"(kv.y), "=r"(kv.z), "=r"(kv.w)
+                                 : "r"(stg + row * ROWB + swz16(loc, c * (KSF / 2) + w2, D) * 16u));
+                    mma_f16x(sc, qf[2 * w2], kv.x, kv.y);
+                    mma_f16x(sd, qf[2 * w2 + 1], kv.z, kv.w);
+                }
+                if (r < G) {
+                    s_sco[warp][r][8 * nt + 2 * c] = (sc[0] + sd[0]) + (sc[2] + sd[2]);
+                    s_sco[warp][r][8 * nt + 2 * c + 1] = (sc[1] + sd[1]) + (sc[3] + sd[3]);
+                }
+            }
+            } else {
+            // small head dims: fp32 FMA per lane over its own row (c~ from shared memory)
             const uint32_t rowp = ring_s + (it % NSTG) * STG + lane * ROWB;
-            const double r = d.r;
-            const uint32_t wt = d.wt;
-            float s4[GQ][4], c2[4] = {0.f, 0.f, 0.f, 0.f};
+            float s4[GQ][4];
 #pragma unroll
             for (int g = 0; g < GQ; ++g)
 #pragma unroll
@@ -588,28 +656,21 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                     const uint32_t w0 = h2 ? v16.z : v16.x, w1 = h2 ? v16.w : v16.y;
                     const float2 lo2 = __half22float2(*reinterpret_cast<const __half2*>(&w0));
                     const float2 hi2 = __half22float2(*reinterpret_cast<const __half2*>(&w1));
-                    const float4 vj = make_float4(lo2.x, lo2.y, hi2.x, hi2.y);
-                    c2[0] = fmaf(vj.x, vj.x, c2[0]);  // ||c~||^2, shared by every head
-                    c2[1] = fmaf(vj.y, vj.y, c2[1]);
-                    c2[2] = fmaf(vj.z, vj.z, c2[2]);
-                    c2[3] = fmaf(vj.w, vj.w, c2[3]);
 #pragma unroll
                     for (int g = 0; g < GQ; ++g) {
                         const float4 q4 = reinterpret_cast<const float4*>(qs + g * D)[j];
-                        s4[g][0] = fmaf(q4.x, vj.x, s4[g][0]);
-                        s4[g][1] = fmaf(q4.y, vj.y, s4[g][1]);
-                        s4[g][2] = fmaf(q4.z, vj.z, s4[g][2]);
-                        s4[g][3] = fmaf(q4.w, vj.w, s4[g][3]);
+                        s4[g][0] = fmaf(q4.x, lo2.x, s4[g][0]);
+                        s4[g][1] = fmaf(q4.y, lo2.y, s4[g][1]);
+                        s4[g][2] = fmaf(q4.z, hi2.x, s4[g][2]);
+                        s4[g][3] = fmaf(q4.w, hi2.y, s4[g][3]);
                     }
                 }
             }
-            // the filter reads c~ = fp16(c): |c_j - c~_j| <= 2^-11 |c_j| + 2^-25.  ||c~|| from
-            // an fp32 sum of squares (relative error < 132 * 2^-24, inside the 1.0001 factor);
-            // ||c|| <= (||c~|| + 2^-25 sqrt(d)) / (1 - 2^-11)
-            const double cn16 = sqrt((double)((c2[0] + c2[1]) + (c2[2] + c2[3]))) * 1.0001;
-            const double cn = (cn16 + 2.9802322387695312e-08 * sqrt((double)D)) / (1.0 - 4.8828125e-04);
-            // |q.c - q.c~| <= 2^-11 ||q|| ||c|| + 2^-25 ||q||_1 and ||q||_1 <= sqrt(d) ||q||
-            const double e16 = 4.8828125e-04 * cn + 2.9802322387695312e-08 * sqrt((double)D);
+#pragma unroll
+            for (int g = 0; g < GQ; ++g) s_sco[warp][g][lane] = (s4[g][0] + s4[g][1]) + (s4[g][2] + s4[g][3]);
+            }
+            __syncwarp();
+            // the enclosure, per candidate on its own lane (k_select's bound, norm bound from fmeta)
             if (d.slot != mslot) {
                 flush_minmax();
                 mslot = d.slot;
@@ -620,22 +681,23 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 }
             }
             const PlanView pv(a.plan + (size_t)d.slot * a.plan_bytes, a);
-            unsigned char* sc = p.scratch + (size_t)d.slot * G * p.qcap * kScratchEntry;
-            unsigned long long* keys = reinterpret_cast<unsigned long long*>(sc);
+            unsigned char* sc8 = p.scratch + (size_t)d.slot * G * p.qcap * kScratchEntry;
+            unsigned long long* keys = reinterpret_cast<unsigned long long*>(sc8);
             uint32_t* wts = reinterpret_cast<uint32_t*>(keys + (size_t)G * p.qcap);
             double* his = reinterpret_cast<double*>(wts + (size_t)G * p.qcap);
+            const double rad = d.r;
+            const double cn = (double)__uint_as_float(d.cnb);
 #pragma unroll
             for (int g = 0; g < GQ; ++g) {
                 if ((d.mask >> g) & 1u) {
-                    const float sv = (s4[g][0] + s4[g][1]) + (s4[g][2] + s4[g][3]);
                     const double qn = __ldg(pv.qnorm() + g);
-                    const double ub = __dadd_rn((double)sv, __dmul_rn(qn, r));
-                    const double e = qn * (cn * (1.01 * 132.0 / 16777216.0) + e16) * 1.0001 +
-                                     fabs(ub) * (1.0 / 562949953421312.0) + 1e-300;
+                    const double ub = __dadd_rn((double)s_sco[warp][g][lane], __dmul_rn(qn, rad));
+                    const double e = (qn * kFiK1 * cn + qn * kFiK2 + kFiK2 * cn +
+                                      (fabs(ub) * kFiK3 + qn * kFiK3 * (cn + rad))) * (1.0 + 1e-9) + 1e-300;
                     const unsigned long long key = desc_key(ub - e);
                     const size_t at = (size_t)g * p.qcap + d.qoff[g] + d.local;
                     keys[at] = key;
-                    wts[at] = wt;
+                    wts[at] = d.wt;
                     his[at] = ub + e;
                     wmin[g] = min(wmin[g], key);
                     wmax[g] = max(wmax[g], key);

@@ -198,7 +198,7 @@ def test_decode_stream_parity(graft_full):
     assert_same_index(st.engine.download_slot(0), ref.export())
 
 
-@pytest.mark.parametrize("d", [32, 128])
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
 def test_reference_exact_fp32_mode(d):
     """kv_f32 engines keep the reference's own fp32 K/V (no bf16 rounding) and
     attend in fp64: selections bit-exact and outputs at fp64 round-off (the
