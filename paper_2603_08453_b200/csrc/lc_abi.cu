@@ -567,12 +567,45 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     uint32_t max_fanout = 0;
     for (auto& s : h->hs)
         for (uint32_t f : s.fanout) max_fanout = std::max(max_fanout, f);
+    // streamed attention: the selection publishes each slot's tasks as it
+    // finishes and the attention grid starts on them without waiting for the
+    // slowest slot (one selection launch, one attention launch)
+    const AttQueueDev* aq_use = nullptr;
+    bool fused_ok = false;
+    const uint32_t ncount = count == 0xffffffffu ? a.n_slots - std::min(first, a.n_slots) : count;
+    if (out_dev && !a.kv_f32 && std::min<uint32_t>(h->desc.slot_groups, ncount) <= 1 && ncount <= kMaxAttendSlots &&
+        getenv("LC_ATT_QUEUE")) {
+        if (!h->aq_mem) {
+            const uint32_t cap = attend_queue_cap(a.d, a.G, a.n_slots);
+            const size_t words = 8 + 2 * (size_t)a.n_slots + 4 * (size_t)cap;
+            void* m = nullptr;
+            if (cudaMalloc(&m, words * 4) != cudaSuccess) {
+                cudaGetLastError();
+                fail(LC_ENOMEM, "streamed attention queue allocation failed");
+            }
+            h->aq_mem = m;
+            uint32_t* w = static_cast<uint32_t*>(m);
+            h->aq.ctl = w;
+            h->aq.sbase = w + 8;
+            h->aq.scnt = h->aq.sbase + a.n_slots;
+            h->aq.t_slot = h->aq.scnt + a.n_slots;
+            h->aq.t_pos = h->aq.t_slot + cap;
+            h->aq.t_cnt = h->aq.t_pos + cap;
+            h->aq.tag = h->aq.t_cnt + cap;
+            h->aq.cap = cap;
+            ck(cudaMemset(w, 0, (8 + 2 * (size_t)a.n_slots + 3 * (size_t)cap) * 4), "queue init");
+            ck(cudaMemset(h->aq.tag, 0xff, (size_t)cap * 4), "queue tags");
+        }
+        h->aq.n = ncount;
+        aq_use = &h->aq;
+    }
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs, uint32_t gi) {
         // the fused per-slot kernel when the shape fits on chip, else the four-kernel chain
         const cudaError_t ef = launch_fused(ag, q_dev, q_in, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
                                             b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, kc8, max_union,
-                                            pmax, max_fanout, count, gs);
+                                            pmax, max_fanout, count, gs, aq_use);
         if (ef == cudaSuccess) {
+            fused_ok = true;
             h->last_launches += 1;
             return;
         }
@@ -589,6 +622,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     if (count == 0xffffffffu) count = a.n_slots - std::min(first, a.n_slots);
     if (first >= a.n_slots || count == 0 || count > a.n_slots - first) fail(LC_EINVAL, "retrieve: bad slot range");
     const uint32_t groups = std::max<uint32_t>(1, std::min<uint32_t>(h->desc.slot_groups, count));
+
     if (groups == 1) {
         a.slot0 = first;
         run_group(a, count, st, 0);
@@ -611,7 +645,9 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     }
     a.slot0 = first;
     if (out_dev) {
-        ck(launch_attend(a, q_dev, out_dev, h->att_part, count, st, h->pg.n ? &h->pg : nullptr), "k_attend");
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, count, st, h->pg.n ? &h->pg : nullptr,
+                         fused_ok ? aq_use : nullptr),
+           "k_attend");
         h->last_launches += a.kv_f32 ? 1 : 2 * ((count + kMaxAttendSlots - 1) / kMaxAttendSlots);
     }
     h->last_flags = flags;

@@ -51,6 +51,7 @@ struct AttendParams {
     unsigned long long* prof;  // optional per-warp [t_start, t_stream_end, t_end, groups | smid << 40] (LC_PROF=1)
     uint32_t min_tok;          // head tokens per static warp range, at least (kMinWarpTok)
     PeerGather pg;             // fused all-gather epilogue (pg.n == 0: off)
+    AttQueueDev aq;            // streamed mode: tasks published by the selection (k_attend<D, true>)
 };
 
 __device__ __forceinline__ unsigned long long gtime_a() {
@@ -316,11 +317,91 @@ __device__ __forceinline__ void slot_prefixes(const Arena& a, uint32_t n, uint32
 // After k_attend: one warp per (slot, query head) combines that head's partials
 // (log-sum-exp, fixed contributor order -> deterministic); every partial row of
 // a batch of contributors is in flight at once.
+// Streamed mode: head g of slot s from the partials of the slot's tasks
+// [base, base + cnt), in task (= row-list) order -- deterministic.
 template <int D>
+__device__ __forceinline__ void merge_tasks(float* out, uint32_t* err, uint32_t G, uint32_t g, const float* part,
+                                            uint32_t zero_seg, uint32_t base, uint32_t cnt, const PeerGather& pg,
+                                            uint32_t slot) {
+    const uint32_t lane = threadIdx.x & 31;
+    constexpr int PER = D / 32;
+    float M = -INFINITY, L = 0.f, o[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) o[k] = 0.f;
+    for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        uint32_t seg = i < cnt ? base + i : zero_seg;
+        const float* ps = part + ((size_t)seg * G + g) * (D + 2);
+        const float ms = i < cnt ? __ldcg(ps) : -INFINITY;
+        const float ls = i < cnt ? __ldcg(ps + 1) : 0.f;
+        float bm = ms;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+        const float Mn = fmaxf(M, bm);
+        if (Mn == -INFINITY) continue;
+        const float fo = exp2f(M - Mn);
+        L *= fo;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) o[k] *= fo;
+        M = Mn;
+        const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+        if (f == 0.f) seg = zero_seg;
+        L += f * ls;
+        const uint32_t m = min(32u, cnt - b0);
+#pragma unroll 8
+        for (uint32_t j = 0; j < m; ++j) {
+            const float fj = __shfl_sync(0xffffffffu, f, j);
+            const uint32_t sj = __shfl_sync(0xffffffffu, seg, j);
+            const float* pj = part + ((size_t)sj * G + g) * (D + 2) + 2 + lane;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) o[k] += fj * __ldcg(pj + 32 * k);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) out[(size_t)g * D + lane + 32 * k] = L > 0.f ? o[k] / L : 0.f;
+    if (!(L > 0.f) && lane == 0) atomicOr(err, kErrEmptyActive);
+    if (pg.n) {
+        const size_t row = ((size_t)pg.row_of_slot[slot] * G + g) * D;
+        for (uint32_t r = 0; r < pg.n; ++r) {
+            float* dst = pg.out[r] + row;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) dst[lane + 32 * k] = L > 0.f ? o[k] / L : 0.f;
+        }
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t r = 0; r < pg.n; ++r) atomicAdd_system(pg.flag[r], 1u);
+    }
+}
+
+template <int D, bool QUEUE>
 __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
     pdl_wait();
     const Arena& a = p.a;
     const uint32_t n = p.n, warp = threadIdx.x >> 5, G = a.G;
+    if constexpr (QUEUE) {
+        const uint32_t x = blockIdx.x * 8 + warp, s = x / G, g = x % G;
+        if (s < n)
+            merge_tasks<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, p.part + 16,
+                           NW + n + kPoolPerWarp * NW + n, __ldcg(p.aq.sbase + s), __ldcg(p.aq.scnt + s), p.pg,
+                           a.slot0 + s);
+        // the last block out resets the queue and advances the epoch for the next step
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(p.aq.ctl + 4, 1u) == gridDim.x - 1) {
+                p.aq.ctl[0] = 0;
+                p.aq.ctl[1] = 0;
+                p.aq.ctl[2] = 0;
+                p.aq.ctl[4] = 0;
+                p.aq.ctl[3] = p.aq.ctl[3] + 1u;
+                __threadfence();
+            }
+        }
+        return;
+    }
     __shared__ uint32_t s_hp[kMaxAttendSlots + 1], s_tp[kMaxAttendSlots + 1], s_wsum[16];
     slot_prefixes<256>(a, n, s_hp, s_tp, s_wsum);
     const uint32_t x = blockIdx.x * 8 + warp, s = x / G, g = x % G;
@@ -333,9 +414,11 @@ __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
                   s, NW, NWe, TH, s_hp[s], s_hp[s + 1], s_tp[s], s_tp[s + 1], pool.C, p.pg, a.slot0 + s);
 }
 
-template <int D>
+template <int D, bool QUEUE>
 __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
-    pdl_wait();
+    // streamed mode: no grid-wide wait on the selection -- each claimed task is
+    // acquired from its publication tag instead
+    if constexpr (!QUEUE) pdl_wait();
     static_assert(D == 64 || D == 128, "D must be 64 or 128");
     constexpr int KS = D / 16;             // k-steps of QK
     constexpr int KW = D / 32;             // 16-byte chunks per thread per K row
@@ -356,10 +439,10 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     __shared__ uint32_t s_wsum[2 * kAttWarps];
 
     // ---- prefixes of the slots' head and tail lengths (k_spans wrote the totals) ----
-    slot_prefixes<kAttThreads>(a, n, s_hp, s_tp, s_wsum);
-    const uint32_t TH = s_hp[n], TP = s_tp[n];
+    if constexpr (!QUEUE) slot_prefixes<kAttThreads>(a, n, s_hp, s_tp, s_wsum);
+    const uint32_t TH = QUEUE ? 1u : s_hp[n], TP = QUEUE ? 0u : s_tp[n];
     // slots with no active token (reference: sparse_attention throws, retriever.cpp:43)
-    if (blockIdx.x == 0) {
+    if (!QUEUE && blockIdx.x == 0) {
         for (uint32_t s = warp; s < n; s += kAttWarps) {
             if (s_hp[s + 1] != s_hp[s] || s_tp[s + 1] != s_tp[s]) continue;
             for (uint32_t x = lane; x < G * D; x += 32) p.out[(size_t)(a.slot0 + s) * G * D + x] = 0.f;
@@ -389,17 +472,65 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     };
     const uint32_t* pre = s_hp;  // active sequence: heads, then tails
     bool in_pool = false;
-    uint32_t ppos = w < NWe ? warp_begin(TH, w, NWe) : TH, pend = w < NWe ? warp_begin(TH, w + 1, NWe) : TH;
-    uint32_t seg_base = w, ps = ppos < pend ? slot_of(pre, ppos) : 0u;
+    uint32_t ppos = (!QUEUE && w < NWe) ? warp_begin(TH, w, NWe) : TH;
+    uint32_t pend = (!QUEUE && w < NWe) ? warp_begin(TH, w + 1, NWe) : TH;
+    uint32_t seg_base = w, ps = (!QUEUE && ppos < pend) ? slot_of(pre, ppos) : 0u;
     // lane 0 claims the next pool chunk one call before the current range runs
     // out (the atomic's latency hides behind one group) -- not earlier, so a
     // slow warp never sits on a chunk a faster one could take
     uint32_t k_next = 0;
-    if (ppos >= pend && lane == 0) k_next = atomicAdd(pool_ctr, 1u);
+    if (!QUEUE && ppos >= pend && lane == 0) k_next = atomicAdd(pool_ctr, 1u);
     bool done = false;
+    // streamed mode: the warp's current task (warp-uniform)
+    uint32_t q_idx = ~0u, q_pos = 0, q_end = 0, q_slot = 0;
+    const uint32_t q_epoch = QUEUE ? __ldcg(p.aq.ctl + 3) : 0u;
+    auto claim = [&]() -> bool {  // the next task in publication order; false when none will come
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(p.aq.ctl + 0, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        for (uint32_t spin = 0;; ++spin) {
+            uint32_t tg = ~0u, pub = 0, tail = 0;
+            if (lane == 0) {
+                if (idx < p.aq.cap)
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(tg) : "l"(p.aq.tag + idx) : "memory");
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(pub) : "l"(p.aq.ctl + 2) : "memory");
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(tail) : "l"(p.aq.ctl + 1) : "memory");
+            }
+            tg = __shfl_sync(0xffffffffu, tg, 0);
+            pub = __shfl_sync(0xffffffffu, pub, 0);
+            tail = __shfl_sync(0xffffffffu, tail, 0);
+            if (idx < p.aq.cap && tg == q_epoch) break;
+            if (pub >= n && idx >= min(tail, p.aq.cap)) return false;
+            if (spin > (1u << 26)) {  // bounded: a selection that never publishes raises an error bit
+                if (lane == 0) atomicOr(a.err, 1u << 10);
+                return false;
+            }
+            __nanosleep(128);
+        }
+        __syncwarp();
+        q_idx = idx;
+        q_slot = __ldcg(p.aq.t_slot + idx);
+        q_pos = __ldcg(p.aq.t_pos + idx);
+        q_end = q_pos + __ldcg(p.aq.t_cnt + idx);
+        return true;
+    };
     auto next_group = [&]() -> GroupDesc {
         GroupDesc gd{~0u, 0u, 0u, 0u};
         if (done) return gd;
+        if constexpr (QUEUE) {
+            while (q_idx == ~0u || q_pos >= q_end) {
+                if (!claim()) {
+                    done = true;
+                    return gd;
+                }
+            }
+            gd.slot = q_slot;
+            gd.pos = q_pos;
+            gd.cnt = min(16u, q_end - q_pos);
+            gd.seg = q_idx;
+            q_pos += gd.cnt;
+            return gd;
+        }
         if (ppos >= pend) {  // range exhausted: take the claimed pool chunk
             const uint32_t k = __shfl_sync(0xffffffffu, k_next, 0);
             if (k >= pool.K) {
@@ -639,7 +770,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
 
     // the last CTA out resets the pool and the barrier for the next launch
     __syncthreads();
-    if (tid == 0 && atomicAdd(pool_ctr + 2, 1u) == gridDim.x - 1) {
+    if (!QUEUE && tid == 0 && atomicAdd(pool_ctr + 2, 1u) == gridDim.x - 1) {
         pool_ctr[0] = 0;
         pool_ctr[1] = 0;
         pool_ctr[2] = 0;
@@ -666,19 +797,28 @@ static KernelCfg& attend_cfg() {
     return c;
 }
 
-template <int D>
+template <int D, bool QUEUE>
 static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStream_t stream) {
-    cudaError_t e = ensure_smem(k_attend<D>, attend_cfg<D>(), attend_smem<D>());
+    static KernelCfg qcfg;
+    cudaError_t e = QUEUE ? ensure_smem(k_attend<D, true>, qcfg, attend_smem<D>())
+                          : ensure_smem(k_attend<D, false>, attend_cfg<D>(), attend_smem<D>());
     if (e != cudaSuccess) return e;
-    e = launch_pdl(k_attend<D>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
+    e = launch_pdl(k_attend<D, QUEUE>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_merge<D>, dim3((p.n * p.a.G + 7) / 8), dim3(256), 0, stream, p, grid * (uint32_t)kAttWarps);
+    return launch_pdl(k_merge<D, QUEUE>, dim3((p.n * p.a.G + 7) / 8), dim3(256), 0, stream, p,
+                      grid * (uint32_t)kAttWarps);
 }
 
 // Persistent grid: every SM of the current device holds as many CTAs as fit.
 uint32_t attend_grid(uint32_t d) {
-    return d == 128 ? persistent_grid(k_attend<128>, attend_cfg<128>(), kAttThreads, attend_smem<128>())
-                    : persistent_grid(k_attend<64>, attend_cfg<64>(), kAttThreads, attend_smem<64>());
+    return d == 128 ? persistent_grid(k_attend<128, false>, attend_cfg<128>(), kAttThreads, attend_smem<128>())
+                    : persistent_grid(k_attend<64, false>, attend_cfg<64>(), kAttThreads, attend_smem<64>());
+}
+
+// Task capacity of the streamed mode: every partial row but the zero row
+uint32_t attend_queue_cap(uint32_t d, uint32_t G, uint32_t n_slots) {
+    const size_t warps = (size_t)attend_grid(d) * kAttWarps, n = std::min<uint32_t>(n_slots, kMaxAttendSlots);
+    return (uint32_t)(warps + n + kPoolPerWarp * warps + n);
 }
 
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots) {
@@ -815,7 +955,7 @@ cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned 
 }
 
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
-                          cudaStream_t stream, const PeerGather* pg) {
+                          cudaStream_t stream, const PeerGather* pg, const AttQueueDev* aq) {
     if (a.kv_f32) {
         // splits per (slot, head): as many as the partials buffer holds, at most 16
         const size_t cap = (attend_partials_floats(a.d, a.G, n_slots) - 16) * 4;
@@ -837,12 +977,15 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
         AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr, kMinWarpTok,
-                       pg ? *pg : PeerGather{nullptr, nullptr, nullptr, 0u}};
+                       pg ? *pg : PeerGather{nullptr, nullptr, nullptr, 0u}, aq ? *aq : AttQueueDev{}};
+        const bool queued = aq && aq->ctl && n_slots <= per;  // streamed: one launch covers the selection's slots
         if (const char* ev = getenv("LC_ATT_MINTOK")) p.min_tok = std::max(16, atoi(ev));  // experiments
         if (prof) cudaMemset(prof, 0, (size_t)grid * kAttWarps * 4 * 8);
         p.a.slot0 = a.slot0 + s0;
-        cudaError_t e = a.d == 128 ? launch_attend_d<128>(p, grid, stream)
-                      : a.d == 64  ? launch_attend_d<64>(p, grid, stream)
+        cudaError_t e = a.d == 128 ? (queued ? launch_attend_d<128, true>(p, grid, stream)
+                                              : launch_attend_d<128, false>(p, grid, stream))
+                      : a.d == 64  ? (queued ? launch_attend_d<64, true>(p, grid, stream)
+                                              : launch_attend_d<64, false>(p, grid, stream))
                                    : cudaErrorInvalidValue;
         if (e != cudaSuccess) return e;
         if (want_prof) {

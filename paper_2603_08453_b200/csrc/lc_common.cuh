@@ -81,6 +81,52 @@ struct PeerGather {
     uint32_t n;
 };
 
+// Streamed attention work queue (selection -> attention without a grid-wide
+// barrier): each selection CTA publishes its slot's row list as tasks of at
+// most C tokens once the slot is done; attention warps claim tasks in order
+// and wait only for the tasks they claimed.  Tags carry the step's epoch, so
+// nothing needs clearing between steps; k_merge's last block resets the
+// counters and advances the epoch.  ctl: [0] next task to claim, [1] tasks
+// reserved, [2] slots published, [3] epoch, [4] merge blocks out.
+struct AttQueueDev {
+    uint32_t* ctl;
+    uint32_t* t_slot;  // [cap] slot (local to the attention launch)
+    uint32_t* t_pos;   // [cap] first row-list entry
+    uint32_t* t_cnt;   // [cap] entries
+    uint32_t* tag;     // [cap] epoch of the step that published the task
+    uint32_t* sbase;   // [n] the slot's first task
+    uint32_t* scnt;    // [n] the slot's task count
+    uint32_t cap, n;   // task capacity, slots of the launch
+};
+
+// One selection CTA's thread publishes its slot's tasks (after every thread's
+// row-list writes were fenced and the CTA synchronised).
+__device__ __forceinline__ void publish_tasks(const AttQueueDev& q, uint32_t lslot, uint32_t tok, uint32_t epoch,
+                                              uint32_t* err) {
+    const uint32_t nt_max = q.cap / (q.n ? q.n : 1u) > 0 ? q.cap / (q.n ? q.n : 1u) : 1u;
+    uint32_t C = (tok + nt_max - 1) / nt_max;
+    C = C < 512u ? 512u : ((C + 15u) & ~15u);
+    const uint32_t nt = tok ? (tok + C - 1) / C : 0u;
+    const uint32_t base = atomicAdd(q.ctl + 1, nt);
+    const bool fits = base + nt <= q.cap;
+    if (!fits) atomicOr(err, 1u << 9);  // sized so that it cannot happen; the slot's output is then zero
+    q.sbase[lslot] = base;
+    q.scnt[lslot] = fits ? nt : 0u;
+    // every reserved index below the capacity gets a task (empty on overflow),
+    // so no attention warp waits on an index that never comes
+    const uint32_t lim = base < q.cap ? min(nt, q.cap - base) : 0u;
+    for (uint32_t i = 0; i < lim; ++i) {
+        q.t_slot[base + i] = lslot;
+        q.t_pos[base + i] = i * C;
+        q.t_cnt[base + i] = fits ? min(C, tok - i * C) : 0u;
+    }
+    __threadfence();
+    for (uint32_t i = 0; i < lim; ++i)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(q.tag + base + i), "r"(epoch) : "memory");
+    __threadfence();
+    atomicAdd(q.ctl + 2, 1u);
+}
+
 struct Arena {
     // shape
     uint32_t n_slots, d, G, cap_tokens, cap_chunks, cap_clusters, cap_units, max_cand;

@@ -20,11 +20,13 @@ extern thread_local char g_select3_where[96];  // failing stage of the last laun
 cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint32_t unit_topk, uint32_t mode,
                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink, uint32_t flags,
                          const uint32_t* buf_off, const uint32_t* buf_ids, unsigned char* scratch, uint32_t kc,
-                         uint32_t uc, uint32_t pmax, uint32_t max_fanout, uint32_t n_slots, cudaStream_t stream);
+                         uint32_t uc, uint32_t pmax, uint32_t max_fanout, uint32_t n_slots, cudaStream_t stream,
+                         const AttQueueDev* aq = nullptr);
 uint32_t attend_grid(uint32_t d);
+uint32_t attend_queue_cap(uint32_t d, uint32_t G, uint32_t n_slots);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
-                          cudaStream_t stream, const PeerGather* pg = nullptr);
+                          cudaStream_t stream, const PeerGather* pg = nullptr, const AttQueueDev* aq = nullptr);
 cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned int expect, uint32_t* err,
                                cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
@@ -139,6 +141,9 @@ struct lc_index_s {
     // needs them
     bool dev_ahead = false;
     uint32_t steps_since_compact = 0;  // decode steps since the last chunk-table compaction
+    // streamed attention (selection publishes tasks, attention claims them)
+    void* aq_mem = nullptr;
+    AttQueueDev aq{};
     // fused all-gather epilogue (lc_set_gather)
     PeerGather pg{nullptr, nullptr, nullptr, 0u};
     void* pg_mem = nullptr;            // device: peer out pointers, flag pointers, rows, wait count
@@ -155,6 +160,7 @@ struct lc_index_s {
         if (host_event) cudaEventDestroy(host_event);
         for (auto e : group_events) cudaEventDestroy(e);
         if (pg_mem) cudaFree(pg_mem);
+        if (aq_mem) cudaFree(aq_mem);
     }
     void set_device() { ck(cudaSetDevice(desc.device), "cudaSetDevice"); }
 };

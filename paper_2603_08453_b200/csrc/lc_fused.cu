@@ -128,6 +128,7 @@ struct FusedParams {
     uint32_t g8cap;          // entries of the 8-row group table
     uint32_t pf;             // stages requested into L2 beyond the ring
     unsigned long long* prof;  // optional per-slot phase timestamps [slot][8] (LC_PROF=1)
+    AttQueueDev aq;            // streamed attention: publish the slot's tasks at the end (aq.ctl null: off)
 };
 
 // dynamic shared memory: region A (phase-dependent: coarse tier / stage ring /
@@ -190,6 +191,10 @@ __device__ __forceinline__ unsigned long long fu_time() {
 template <int GQ>
 __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
     pdl_wait();
+    // streamed attention: let the attention grid launch as SMs free up; it takes
+    // each slot's tasks once this CTA publishes them
+    if (p.aq.ctl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t aq_epoch = p.aq.ctl ? __ldcg(p.aq.ctl + 3) : 0u;
     FU_MARK(0)
     constexpr uint32_t G = GQ, D = kFuD;
     constexpr uint32_t GT = kFuCons / GQ;  // threads per head in P3
@@ -254,6 +259,11 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
         }
         uint32_t* rows = a.rows + (size_t)slot * a.cap_tokens;
         for (uint32_t t = tid; t < n; t += kFuThreads) rows[t] = t | (all << 24);
+        if (p.aq.ctl) {
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) publish_tasks(p.aq, blockIdx.x, n, aq_epoch, a.err);
+        }
         return;
     }
     const uint32_t CU = a.cap_units;
@@ -452,6 +462,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
             a.n_spans[slot] = 0;
             a.span_off[(size_t)slot * (a.cap_spans + 1)] = 0;
             a.slot_tok[slot] = 0;
+            if (p.aq.ctl) publish_tasks(p.aq, blockIdx.x, 0u, aq_epoch, a.err);
         }
         return;
     }
@@ -1313,6 +1324,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
                 tok += (uint32_t)(total & 0xffffffffffull);
             }
         }
+        if (p.aq.ctl) __threadfence();  // every thread's row-list writes, before the publication
         __syncthreads();
         if (tid == 0) {
             if (out > a.cap_spans) {
@@ -1337,6 +1349,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
             sb[1] = per_q;
             sb[2] = tok;
             sb[3] = ncu;
+            if (p.aq.ctl) publish_tasks(p.aq, blockIdx.x, tok, aq_epoch, a.err);
         }
     }
     FU_MARK(5)
@@ -1365,7 +1378,8 @@ static cudaError_t launch_fused_g(const FusedParams& p, uint32_t n_slots, size_t
 cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint32_t unit_topk, uint32_t mode,
                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink, uint32_t flags,
                          const uint32_t* buf_off, const uint32_t* buf_ids, unsigned char* scratch, uint32_t kc,
-                         uint32_t uc, uint32_t pmax, uint32_t max_fanout, uint32_t n_slots, cudaStream_t stream) {
+                         uint32_t uc, uint32_t pmax, uint32_t max_fanout, uint32_t n_slots, cudaStream_t stream,
+                         const AttQueueDev* aq) {
     if (a.d != (uint32_t)kFuD || getenv("LC_NO_FUSED")) return cudaErrorNotSupported;
     if (max_fanout >= 16384) return cudaErrorNotSupported;  // stage descriptors hold 14-bit unit offsets
     if (a.G != 1 && a.G != 2 && a.G != 4 && a.G != 8) return cudaErrorNotSupported;
@@ -1399,7 +1413,8 @@ cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint
         cudaMemset(prof, 0, (size_t)a.n_slots * 16 * 8);
     }
     FusedParams fp{a, q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids,
-                   scratch, kc, uc, smem_a, fu_g8cap(uc), 0u, want_prof ? prof : nullptr};
+                   scratch, kc, uc, smem_a, fu_g8cap(uc), 0u, want_prof ? prof : nullptr,
+                   aq ? *aq : AttQueueDev{}};
     if (const char* ev = getenv("LC_FUSED_PF")) fp.pf = (uint32_t)atoi(ev);  // experiments
     cudaError_t e;
     switch (a.G) {

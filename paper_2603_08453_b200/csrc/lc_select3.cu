@@ -755,7 +755,7 @@ __device__ __forceinline__ T pk_scan(T v, T* wt, T& total) {
 // k_pickq: one CTA per query head (128 threads).  Dynamic smem:
 //   keys u64 [kPickKeysCap], weights / selection u32 [kPickKeysCap] (staged),
 //   cbits u32 [words(cap_chunks)] this head's active-chunk bitmap.
-constexpr int kPqThreads = 256;
+constexpr int kPqThreads = 512;
 constexpr int kPqWarps = kPqThreads / 32;
 
 template <int DQ, int GQ>
