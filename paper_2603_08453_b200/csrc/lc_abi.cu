@@ -574,7 +574,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     bool fused_ok = false;
     const uint32_t ncount = count == 0xffffffffu ? a.n_slots - std::min(first, a.n_slots) : count;
     if (out_dev && !a.kv_f32 && std::min<uint32_t>(h->desc.slot_groups, ncount) <= 1 && ncount <= kMaxAttendSlots &&
-        getenv("LC_ATT_QUEUE")) {
+        !(getenv("LC_ATT_QUEUE") && atoi(getenv("LC_ATT_QUEUE")) == 0)) {
         if (!h->aq_mem) {
             const uint32_t cap = attend_queue_cap(a.d, a.G, a.n_slots);
             const size_t words = 8 + 2 * (size_t)a.n_slots + 4 * (size_t)cap;
@@ -597,6 +597,10 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
             ck(cudaMemset(h->aq.tag, 0xff, (size_t)cap * 4), "queue tags");
         }
         h->aq.n = ncount;
+        // tasks of >= 512 tokens when the launch fills the GPU; few slots (one
+        // layer of a layer-by-layer decode) cut finer so more warps share them
+        h->aq.cmin = ncount >= 128 ? 512u : 128u;
+        if (const char* ev = getenv("LC_ATT_QC")) h->aq.cmin = (uint32_t)std::max(16, atoi(ev)) & ~15u;  // experiments
         aq_use = &h->aq;
     }
     auto run_group = [&](Arena ag, uint32_t count, cudaStream_t gs, uint32_t gi) {

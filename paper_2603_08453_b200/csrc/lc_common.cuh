@@ -97,34 +97,42 @@ struct AttQueueDev {
     uint32_t* sbase;   // [n] the slot's first task
     uint32_t* scnt;    // [n] the slot's task count
     uint32_t cap, n;   // task capacity, slots of the launch
+    uint32_t cmin;     // minimum tokens per task
 };
 
-// One selection CTA's thread publishes its slot's tasks (after every thread's
-// row-list writes were fenced and the CTA synchronised).
+// One selection CTA's warp publishes its slot's tasks (after every thread's
+// row-list writes were fenced and the CTA synchronised): lane 0 reserves the
+// task range, the lanes write the tasks, fence, then tag them with the epoch
+// (consumers acquire the tag); the published-slot count goes last.
 __device__ __forceinline__ void publish_tasks(const AttQueueDev& q, uint32_t lslot, uint32_t tok, uint32_t epoch,
                                               uint32_t* err) {
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t nt_max = q.cap / (q.n ? q.n : 1u) > 0 ? q.cap / (q.n ? q.n : 1u) : 1u;
     uint32_t C = (tok + nt_max - 1) / nt_max;
-    C = C < 512u ? 512u : ((C + 15u) & ~15u);
+    C = C < q.cmin ? q.cmin : ((C + 15u) & ~15u);
     const uint32_t nt = tok ? (tok + C - 1) / C : 0u;
-    const uint32_t base = atomicAdd(q.ctl + 1, nt);
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(q.ctl + 1, nt);
+    base = __shfl_sync(0xffffffffu, base, 0);
     const bool fits = base + nt <= q.cap;
-    if (!fits) atomicOr(err, 1u << 9);  // sized so that it cannot happen; the slot's output is then zero
-    q.sbase[lslot] = base;
-    q.scnt[lslot] = fits ? nt : 0u;
+    if (lane == 0) {
+        if (!fits) atomicOr(err, 1u << 9);  // sized so that it cannot happen; the slot's output is then zero
+        q.sbase[lslot] = base;
+        q.scnt[lslot] = fits ? nt : 0u;
+    }
     // every reserved index below the capacity gets a task (empty on overflow),
     // so no attention warp waits on an index that never comes
     const uint32_t lim = base < q.cap ? min(nt, q.cap - base) : 0u;
-    for (uint32_t i = 0; i < lim; ++i) {
+    for (uint32_t i = lane; i < lim; i += 32) {
         q.t_slot[base + i] = lslot;
         q.t_pos[base + i] = i * C;
         q.t_cnt[base + i] = fits ? min(C, tok - i * C) : 0u;
     }
     __threadfence();
-    for (uint32_t i = 0; i < lim; ++i)
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(q.tag + base + i), "r"(epoch) : "memory");
+    for (uint32_t i = lane; i < lim; i += 32) *reinterpret_cast<volatile uint32_t*>(q.tag + base + i) = epoch;
     __threadfence();
-    atomicAdd(q.ctl + 2, 1u);
+    __syncwarp();
+    if (lane == 0) atomicAdd(q.ctl + 2, 1u);
 }
 
 struct Arena {

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
         if (p.aq.ctl) {
             __threadfence();
             __syncthreads();
-            if (tid == 0) publish_tasks(p.aq, blockIdx.x, n, aq_epoch, a.err);
+            if (warp == 0) publish_tasks(p.aq, blockIdx.x, n, aq_epoch, a.err);
         }
         return;
     }
@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
             a.n_spans[slot] = 0;
             a.span_off[(size_t)slot * (a.cap_spans + 1)] = 0;
             a.slot_tok[slot] = 0;
-            if (p.aq.ctl) publish_tasks(p.aq, blockIdx.x, 0u, aq_epoch, a.err);
         }
+        if (p.aq.ctl && warp == 0) publish_tasks(p.aq, blockIdx.x, 0u, aq_epoch, a.err);
         return;
     }
     const uint32_t kU = s_kU, ng = s_ng, nstage = (ng + 7) / 8;
@@ -1349,8 +1349,8 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
             sb[1] = per_q;
             sb[2] = tok;
             sb[3] = ncu;
-            if (p.aq.ctl) publish_tasks(p.aq, blockIdx.x, tok, aq_epoch, a.err);
         }
+        if (p.aq.ctl && warp == 0) publish_tasks(p.aq, blockIdx.x, tok, aq_epoch, a.err);
     }
     FU_MARK(5)
     if (p.prof && tid == 0) p.prof[(size_t)slot * 16 + 6] = nstage | ((unsigned long long)s_rbase[G] << 32);
