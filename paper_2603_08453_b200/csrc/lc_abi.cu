@@ -573,7 +573,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
     const AttQueueDev* aq_use = nullptr;
     bool fused_ok = false;
     const uint32_t ncount = count == 0xffffffffu ? a.n_slots - std::min(first, a.n_slots) : count;
-    if (out_dev && !a.kv_f32 && std::min<uint32_t>(h->desc.slot_groups, ncount) <= 1 && ncount <= kMaxAttendSlots &&
+    if (out_dev && !a.kv_f32 && std::min<uint32_t>(h->desc.slot_groups, ncount) <= 1 &&
         !(getenv("LC_ATT_QUEUE") && atoi(getenv("LC_ATT_QUEUE")) == 0)) {
         if (!h->aq_mem) {
             const uint32_t cap = attend_queue_cap(a.d, a.G, a.n_slots);
@@ -652,7 +652,7 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         ck(launch_attend(a, q_dev, out_dev, h->att_part, count, st, h->pg.n ? &h->pg : nullptr,
                          fused_ok ? aq_use : nullptr),
            "k_attend");
-        h->last_launches += a.kv_f32 ? 1 : 2 * ((count + kMaxAttendSlots - 1) / kMaxAttendSlots);
+        h->last_launches += a.kv_f32 ? 2 : (fused_ok && aq_use) ? 2 : 2 * ((count + kMaxAttendSlots - 1) / kMaxAttendSlots);
     }
     h->last_flags = flags;
     h->last_valid = 1;

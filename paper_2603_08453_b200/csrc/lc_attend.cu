@@ -975,10 +975,14 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     const bool want_prof = getenv("LC_PROF") != nullptr;
     unsigned long long*& prof = prof_dev[current_device()];
     if (want_prof && !prof) cudaMalloc(&prof, (size_t)grid * kAttWarps * 4 * 8);
+    // streamed: one launch covers every slot of the selection (tasks carry
+    // their own positions, so neither the per-launch slot table nor the 32-bit
+    // global positions of the static partition apply)
+    const bool queued = aq && aq->ctl;
+    if (queued) per = n_slots;
     for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
         AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr, kMinWarpTok,
                        pg ? *pg : PeerGather{nullptr, nullptr, nullptr, 0u}, aq ? *aq : AttQueueDev{}};
-        const bool queued = aq && aq->ctl && n_slots <= per;  // streamed: one launch covers the selection's slots
         if (const char* ev = getenv("LC_ATT_MINTOK")) p.min_tok = std::max(16, atoi(ev));  // experiments
         if (prof) cudaMemset(prof, 0, (size_t)grid * kAttWarps * 4 * 8);
         p.a.slot0 = a.slot0 + s0;
