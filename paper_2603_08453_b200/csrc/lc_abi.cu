@@ -617,10 +617,9 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         cudaGetLastError();
         const cudaError_t e = launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
                                              b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, a.max_cand,
-                                             max_union, pmax, count, h->fine_ctr + 4 * gi, gs, q_in, aq_use);
+                                             max_union, pmax, count, h->fine_ctr + 4 * gi, gs, q_in);
         if (e != cudaSuccess)
             fail(LC_ECUDA, std::string("k_select3: ") + g_select3_where + ": " + cudaGetErrorString(e));
-        fused_ok = true;  // (the chain's k_spans publishes the tasks)
         h->last_launches += 4;
     };
     h->last_launches = 0;

@@ -15,8 +15,7 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
                            uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
-                           const float* q_in = nullptr,  // q_in: k_coarse reads q here and copies it to q
-                           const AttQueueDev* aq = nullptr);
+                           const float* q_in = nullptr);  // q_in: k_coarse reads q here and copies it to q
 extern thread_local char g_select3_where[96];  // failing stage of the last launch_select3
 cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint32_t unit_topk, uint32_t mode,
                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink, uint32_t flags,

@@ -135,7 +135,6 @@ struct Sel3Params {
     unsigned long long* prof;  // optional k_pick phase timestamps [slot][8] (LC_PROF=1)
     uint32_t* fine_ctr;        // k_fine pool / exit counters (zeroed; reset by k_fine)
     unsigned long long* prof_sp;  // optional k_spans phase timestamps [slot][8] (LC_PROF=1)
-    AttQueueDev aq;               // streamed attention: k_spans publishes each slot's tasks (aq.ctl null: off)
 };
 
 __device__ __forceinline__ unsigned long long gtime3() {
@@ -1366,7 +1365,7 @@ __device__ __forceinline__ T sp_scan(T v, T* wt, T& total) {
 template <int GQ>
 #define LC_SMARK(ph) \
     if (p.prof_sp && threadIdx.x == 0) p.prof_sp[(size_t)slot * 8 + (ph)] = gtime3();
-__device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot, uint32_t aq_epoch) {
+__device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) {
     LC_SMARK(0)
     const Arena& a = p.a;
     const uint32_t tid = threadIdx.x, lane = tid & 31, kSpWarps = blockDim.x >> 5;
@@ -1403,11 +1402,6 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot, 
             a.slot_tok[slot] = n;
         }
         for (uint32_t t = tid; t < n; t += blockDim.x) rows[t] = t | (all << 24);
-        if (p.aq.ctl) {
-            __threadfence();
-            __syncthreads();
-            if ((tid >> 5) == 0) publish_tasks(p.aq, slot - p.a.slot0, n, aq_epoch, a.err);
-        }
         return;
     }
     __shared__ unsigned long long wtot[kSpMaxWarps];
@@ -1430,7 +1424,6 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot, 
             so[0] = 0;
             a.slot_tok[slot] = 0;
         }
-        if (p.aq.ctl && (tid >> 5) == 0) publish_tasks(p.aq, slot - p.a.slot0, 0u, aq_epoch, a.err);
         return;
     }
     const uint32_t mwcap = bit_words(a.cap_chunks), mw = bit_words(M);
@@ -1596,7 +1589,6 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot, 
             tok += (uint32_t)(total & 0xffffffffffull);
         }
     }
-    if (p.aq.ctl) __threadfence();  // every thread's row-list writes, before the publication
     __syncthreads();
     if (tid == 0) {
         if (out > a.cap_spans) {
@@ -1622,7 +1614,6 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot, 
         sb[2] = tok;
         sb[3] = ncu;
     }
-    if (p.aq.ctl && (tid >> 5) == 0) publish_tasks(p.aq, slot - p.a.slot0, tok, aq_epoch, a.err);
     LC_SMARK(4)
 }
 
@@ -1636,10 +1627,7 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
 template <int GQ>
 __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     pdl_wait();
-    // streamed attention: the attention grid may launch now and take each
-    // slot's tasks as this kernel publishes them
-    if (p.aq.ctl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    build_spans<GQ>(p, p.a.slot0 + blockIdx.x, p.aq.ctl ? __ldcg(p.aq.ctl + 3) : 0u);
+    build_spans<GQ>(p, p.a.slot0 + blockIdx.x);
 }
 
 size_t select3_pick_smem(const Arena& a);
@@ -1731,7 +1719,7 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
                            uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
-                           const float* q_in, const AttQueueDev* aq) {
+                           const float* q_in) {
     // LC_PROF=1 (diagnostics only): per-CTA timestamps, buffers per device
     static unsigned long long *prof_dev[kMaxDevices] = {}, *prof_sp_dev[kMaxDevices] = {};
     const int dev = current_device();
@@ -1744,7 +1732,7 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
     }
     g_select3_where[0] = 0;
     Sel3Params p{a, pick_keys_cap(a), q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
-                 fine_ctr, prof_sp, aq ? *aq : AttQueueDev{}};
+                 fine_ctr, prof_sp};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
                   : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)
                   : a.d == 32  ? launch3_d<32>(p, n_slots, max_union, pmax, stream)
