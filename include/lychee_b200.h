@@ -294,7 +294,12 @@ int lc_step_bytes(lc_index_t h, uint64_t* out);
 int lc_launch_count(lc_index_t h, uint32_t* out);
 
 /* Sticky device-side error bits (lc_common.cuh ErrBits) of every kernel since
- * the last clear; synchronous. */
+ * the last clear; synchronous.  Bit 0 candidates over capacity, 1 empty
+ * candidate set (select_topk k = 0), 2 spans over capacity, 3 zero-norm
+ * chunk representative, 4 chunk capacity, 5 token capacity, 6 empty active
+ * set, 7 graft take outside the buffered tokens, 8 fused all-gather: a peer's
+ * rows never arrived, 9 streamed-attention task queue overflow, 10
+ * streamed attention: a slot's tasks never published (bounded wait). */
 int lc_device_error(lc_index_t h, uint32_t* out, int clear);
 
 /* ---- TKIX <-> device (serialize.cpp:88-220) ------ */

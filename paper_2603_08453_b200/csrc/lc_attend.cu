@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
             if (idx < p.aq.cap && tg == q_epoch) break;
             if (pub >= n && idx >= min(tail, p.aq.cap)) return false;
             if (spin > (1u << 26)) {  // bounded: a selection that never publishes raises an error bit
-                if (lane == 0) atomicOr(a.err, 1u << 10);
+                if (lane == 0) atomicOr(a.err, kErrQueueTimeout);
                 return false;
             }
             __nanosleep(128);

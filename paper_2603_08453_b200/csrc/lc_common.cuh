@@ -116,7 +116,7 @@ __device__ __forceinline__ void publish_tasks(const AttQueueDev& q, uint32_t lsl
     base = __shfl_sync(0xffffffffu, base, 0);
     const bool fits = base + nt <= q.cap;
     if (lane == 0) {
-        if (!fits) atomicOr(err, 1u << 9);  // sized so that it cannot happen; the slot's output is then zero
+        if (!fits) atomicOr(err, 1u << 9);  // kErrQueueOverflow: sized so it cannot happen; the slot's output is then zero
         q.sbase[lslot] = base;
         q.scnt[lslot] = fits ? nt : 0u;
     }
@@ -357,6 +357,8 @@ enum ErrBits : uint32_t {
     kErrEmptyActive = 1u << 6,    // sparse_attention over an empty set (retriever.cpp:43)
     kErrTake = 1u << 7,           // graft take outside the buffered tokens
     kErrGatherTimeout = 1u << 8,  // fused all-gather: a peer's rows never arrived (bounded wait gave up)
+    kErrQueueOverflow = 1u << 9,  // streamed attention: task queue full (sized so it cannot happen)
+    kErrQueueTimeout = 1u << 10,  // streamed attention: a slot's tasks never published (bounded wait gave up)
 };
 
 }  // namespace lc
