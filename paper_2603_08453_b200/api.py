@@ -246,9 +246,14 @@ def _ptr(t):
     return t.ctypes.data
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None) if torch is not None else None
+
+
 def _stream_ptr(stream):
     if stream is None:
         if torch is not None and torch.cuda.is_available():
+            if _raw_stream is not None:  # the current stream's handle without a Stream object (hot loops)
+                return _raw_stream(torch.cuda.current_device())
             return torch.cuda.current_stream().cuda_stream
         return None
     return getattr(stream, "cuda_stream", stream)
@@ -432,10 +437,21 @@ class Engine:
 
     def retrieve_host(self, q_host: np.ndarray, budgets: Budgets, out_host: np.ndarray,
                       buffer: str = "none", stream=None):
-        flags = {"none": L.LC_BUFFER_NONE, "stream": L.LC_BUFFER_STREAM}[buffer]
-        b = budgets.c()
-        L.check(L.lib().lc_retrieve_host(self.h, _ptr(q_host), C.byref(b), flags, _ptr(out_host),
-                                         _stream_ptr(stream)))
+        """retrieve() for every (slot, head) with q and the outputs in host memory
+        (page-locked buffers are read and written in place by the kernels)."""
+        flags = L.LC_BUFFER_STREAM if buffer == "stream" else L.LC_BUFFER_NONE
+        if buffer not in ("none", "stream"):
+            raise ValueError("buffer must be 'none' or 'stream'")
+        key = (budgets.unit_topk, int(budgets.mode), budgets.cluster_topk, budgets.token_budget, budgets.sink_size)
+        bc = self._host_budgets.get(key) if hasattr(self, "_host_budgets") else None
+        if bc is None:  # one ctypes struct per distinct budgets (the call is on the decode hot loop)
+            if not hasattr(self, "_host_budgets"):
+                self._host_budgets = {}
+            bc = self._host_budgets[key] = budgets.c()
+        rc = L.lib().lc_retrieve_host(self.h, q_host.ctypes.data, C.byref(bc), flags, out_host.ctypes.data,
+                                      _stream_ptr(stream))
+        if rc:
+            L.check(rc)
         return out_host
 
     def sparse_attention(self, q, out, stream=None):
