@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
             }
             uint32_t mask = 0;
             for (uint32_t k = lo + 1; k < nuu && s_ucum[k] < c0 + 32; ++k) mask |= 1u << (s_ucum[k] - c0);
-            pv.tiles()[t] = make_uint4(lo, mask, c0 - s_ucum[lo], 0u);
+            pv.tiles()[t] = make_uint4(lo, mask, c0 - s_ucum[lo], min(32u, ncu - c0));
         }
     }
     // q read from a host-mapped buffer: leave the device copy the later kernels
@@ -459,18 +459,15 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
         // A tile goes through four steps, one loop iteration apart, so no
         // dependent load sits on the critical path: (A) slot lookup + tile-table
         // entry load, (B) the lane's unit row loads, (I) the bulk copy of the
-        // tile's rows (issued by the lanes that start a unit run) + the lane's
-        // radius / weight loads, (C) scoring from shared memory.
+        // tile's rows and their filter metadata (issued by the lanes that start
+        // a unit run), (C) scoring from shared memory.
         struct StA {
             uint32_t slot, ti;  // slot ~0u: no tile
-            uint4 te;           // {first unit, unit starts, first local, -}
-            uint32_t ncu;
+            uint4 te;           // {first unit, unit starts, first local, candidates in the tile}
         };
         struct StB {
             uint32_t slot, valid, local, base, mask, vc, starts;
             uint32_t qoff[GQ];
-            double r;
-            uint32_t wt, cnb;  // token count (mode 1) or 1; the row's norm bound (f32 bits)
         };
         auto stage_a = [&](uint32_t t) -> StA {
             StA x;
@@ -490,7 +487,6 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             x.ti = t - s_tp[lo];
             const PlanView pv(a.plan + (size_t)x.slot * a.plan_bytes, a);
             x.te = __ldg(pv.tiles() + x.ti);
-            x.ncu = __ldg(pv.hdr() + 2);
             return x;
         };
         auto stage_b = [&](const StA& x) -> StB {
@@ -499,12 +495,9 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             y.valid = 0;
             y.mask = 0;
             y.vc = 0;
-            y.r = 0.0;
-            y.wt = 0;
-            y.cnb = 0;
             if (x.slot == ~0u) return y;
             const PlanView pv(a.plan + (size_t)x.slot * a.plan_bytes, a);
-            y.vc = min(32u, x.ncu - x.ti * 32);
+            y.vc = x.te.w;
             y.valid = lane < y.vc;
             y.starts = x.te.y;
             const uint32_t below = x.te.y & ((2u << lane) - 1u);  // unit starts at positions <= lane
@@ -518,21 +511,24 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             for (int g = 0; g < GQ; ++g) y.qoff[g] = __ldg(u + 4 + g);
             return y;
         };
-        // the warp's ring: 3 stages of 32 rows; barrier per stage
-        constexpr uint32_t ROWB = D * 2, STG = 32 * ROWB, NSTG = 3;
+        // the warp's ring: 3 stages of 32 rows + their 16-byte filter metadata
+        // (radius, norm bound, token count); one barrier per stage
+        constexpr uint32_t ROWB = D * 2, STG = 32 * ROWB, NSTG = 3, MSTG = 32 * 16;
         extern __shared__ __align__(128) unsigned char fsm[];
         const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(fsm + (size_t)warp * NSTG * STG);
+        const uint32_t meta_s =
+            (uint32_t)__cvta_generic_to_shared(fsm + (size_t)kFiWarps * NSTG * STG + (size_t)warp * NSTG * MSTG);
         const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&s_fbar[warp][0]);
-        float* qs = reinterpret_cast<float*>(fsm + (size_t)kFiWarps * NSTG * STG) + (size_t)warp * GQ * D;
+        float* qs = reinterpret_cast<float*>(fsm + (size_t)kFiWarps * NSTG * (STG + MSTG)) + (size_t)warp * GQ * D;
         uint32_t qslot = ~0u, fslot = ~0u;
         constexpr int KSF = D >= 32 ? D / 16 : 2;  // MMA k-steps (D >= 32; smaller dims use fp32 FMAs)
         const uint32_t r = lane >> 2, c = lane & 3;
         uint32_t qf[KSF][4];
-        // (I): the lanes that start a unit run copy the run; every lane requests its row's metadata
+        // (I): the lanes that start a unit run copy the run's rows and metadata
         auto issue = [&](StB& y, uint32_t st) {
             if (y.slot == ~0u) return;
             const uint32_t bar = bar_s + 8u * st;
-            if (lane == 0) mbar_expect3(bar, y.vc * ROWB);
+            if (lane == 0) mbar_expect3(bar, y.vc * (ROWB + 16u));
             __syncwarp();
             const bool start = y.valid && (lane == 0 || ((y.starts >> lane) & 1u));
             if (start) {
@@ -543,12 +539,8 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 bulk_g2s3(ring_s + st * STG + lane * ROWB,
                           a.frow16 + (size_t)y.slot * a.cap_clusters * D + ((size_t)y.base + y.local) * D,
                           (end - lane) * ROWB, bar);
-            }
-            if (y.valid) {  // the row's filter metadata: radius, norm bound, token count
-                const uint4 mt = __ldg(a.fmeta + (size_t)y.slot * a.cap_clusters + y.base + y.local);
-                y.r = __hiloint2double((int)mt.y, (int)mt.x);
-                y.cnb = mt.z;
-                y.wt = p.mode == 1 ? mt.w : 1u;
+                bulk_g2s3(meta_s + st * MSTG + lane * 16u,
+                          a.fmeta + (size_t)y.slot * a.cap_clusters + y.base + y.local, (end - lane) * 16u, bar);
             }
         };
         uint32_t mslot = ~0u;  // slot whose per-head key range the warp is tracking
@@ -585,7 +577,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             issue(n2, (it + 2) % NSTG);       // (I) tile it + 2
             const StB nb = stage_b(sa);       // (B) tile it + 3
             sa = stage_a(next_tile());        // (A) tile it + 4
-            if (d.slot != qslot) {  // the tile's q (fp32) into the warp's buffer
+            if (D < 32 && d.slot != qslot) {  // the tile's q (fp32) into the warp's buffer
                 __syncwarp();
                 const float4* src = reinterpret_cast<const float4*>(p.q + (size_t)d.slot * G * D);
                 for (uint32_t c = lane; c < G * D / 4; c += 32) reinterpret_cast<float4*>(qs)[c] = __ldg(src + c);
@@ -599,7 +591,9 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                 const uint32_t gr = r < G ? r : 0u;
 #pragma unroll
                 for (int s2 = 0; s2 < KSF; ++s2) {
-                    const float* qq = qs + gr * D + c * (D / 4) + 4 * s2;
+                    const float4 q4 =
+                        __ldg(reinterpret_cast<const float4*>(p.q + ((size_t)d.slot * G + gr) * D + c * (D / 4) + 4 * s2));
+                    const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
                     float hh[4], ll[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
@@ -685,8 +679,14 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
             unsigned long long* keys = reinterpret_cast<unsigned long long*>(sc8);
             uint32_t* wts = reinterpret_cast<uint32_t*>(keys + (size_t)G * p.qcap);
             double* his = reinterpret_cast<double*>(wts + (size_t)G * p.qcap);
-            const double rad = d.r;
-            const double cn = (double)__uint_as_float(d.cnb);
+            uint4 mt = make_uint4(0u, 0u, 0u, 0u);
+            if (d.valid)
+                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                             : "=r"(mt.x), "=r"(mt.y), "=r"(mt.z), "=r"(mt.w)
+                             : "r"(meta_s + (it % NSTG) * MSTG + lane * 16u));
+            const double rad = __hiloint2double((int)mt.y, (int)mt.x);
+            const double cn = (double)__uint_as_float(mt.z);
+            const uint32_t wt = p.mode == 1 ? mt.w : 1u;
 #pragma unroll
             for (int g = 0; g < GQ; ++g) {
                 if ((d.mask >> g) & 1u) {
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kFiThreads, 2) k_fine(Sel3Params p, uint32_t n
                     const unsigned long long key = desc_key(ub - e);
                     const size_t at = (size_t)g * p.qcap + d.qoff[g] + d.local;
                     keys[at] = key;
-                    wts[at] = d.wt;
+                    wts[at] = wt;
                     his[at] = ub + e;
                     wmin[g] = min(wmin[g], key);
                     wmax[g] = max(wmax[g], key);
@@ -1445,13 +1445,17 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
 #pragma unroll
     for (int g = 0; g < GQ; ++g) my_cnt[g] = my_nsp[g] = 0;
     LC_SMARK(1)
+    uint32_t nx[GQ];  // the next round's bitmap words, loaded one round ahead
+#pragma unroll
+    for (int g = 0; g < GQ; ++g) nx[g] = tid < mw ? __ldcg(cbg + g * mwcap + tid) : 0u;
     for (uint32_t w0 = 0; w0 < mw; w0 += blockDim.x) {
-        const uint32_t w = w0 + tid;
+        const uint32_t w = w0 + tid, wn = w + blockDim.x;
         uint32_t wg[GQ], any = 0;
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
-            wg[g] = w < mw ? __ldcg(cbg + g * mwcap + w) : 0u;
+            wg[g] = nx[g];
             any |= wg[g];
+            nx[g] = wn < mw ? __ldcg(cbg + g * mwcap + wn) : 0u;
         }
         // the bounds of the word's set chunks: one batch of independent loads,
         // parked in the thread's own shared column so the loops below visit
@@ -1677,8 +1681,8 @@ static cudaError_t launch3_dg(const Sel3Params& p, uint32_t n_slots, uint32_t ma
     k_coarse<D, GQ><<<n_slots, kCoThreads, co_smem, stream>>>(p);
     e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return select3_fail(e1, "k_coarse launch", co_smem);
-    // k_fine: each warp's 3-stage row ring, then its q buffer
-    const size_t fi_smem = (size_t)kFiWarps * (3 * 32 * D * 2 + (size_t)GQ * D * 4);
+    // k_fine: each warp's 3-stage row + metadata ring, then (D < 32) its q buffer
+    const size_t fi_smem = (size_t)kFiWarps * (3 * 32 * (D * 2 + 16) + (D < 32 ? (size_t)GQ * D * 4 : 0));
     const uint32_t fine_grid = persistent_grid(k_fine<D, GQ>, fi_cfg, kFiThreads, fi_smem);
     for (uint32_t s0 = 0; s0 < n_slots; s0 += kMaxAttendSlots) {
         Sel3Params q = p;
