@@ -1445,30 +1445,46 @@ __device__ __forceinline__ void build_spans(const Sel3Params& p, uint32_t slot) 
 #pragma unroll
     for (int g = 0; g < GQ; ++g) my_cnt[g] = my_nsp[g] = 0;
     LC_SMARK(1)
-    uint32_t nx[GQ];  // the next round's bitmap words, loaded one round ahead
+    // software pipeline over rounds of blockDim words: round r + 1's bounds and
+    // round r + 2's bitmap words are requested while round r is counted and
+    // written, so only the prologue waits on memory
+    const uint32_t W = blockDim.x;
+    auto words = [&](uint32_t w, uint32_t* x) {
 #pragma unroll
-    for (int g = 0; g < GQ; ++g) nx[g] = tid < mw ? __ldcg(cbg + g * mwcap + tid) : 0u;
-    for (uint32_t w0 = 0; w0 < mw; w0 += blockDim.x) {
-        const uint32_t w = w0 + tid, wn = w + blockDim.x;
+        for (int g = 0; g < GQ; ++g) x[g] = w < mw ? __ldcg(cbg + g * mwcap + w) : 0u;
+    };
+    // the bounds of the word's set chunks (chunk b's start and end), one batch of
+    // independent loads
+    auto bounds = [&](uint32_t w, const uint32_t* x, uint32_t* bnd) {
+        uint32_t any = 0;
+#pragma unroll
+        for (int g = 0; g < GQ; ++g) any |= x[g];
+#pragma unroll
+        for (int b = 0; b <= 32; ++b) {
+            const bool need = (b < 32 && ((any >> b) & 1u)) || (b > 0 && ((any >> (b - 1)) & 1u));
+            bnd[b] = need ? __ldg(cs + w * 32 + b) : 0u;
+        }
+    };
+    uint32_t cw[GQ], nx[GQ], nb[33];
+    words(tid, cw);
+    bounds(tid, cw, nb);
+    words(tid + W, nx);
+    for (uint32_t w0 = 0; w0 < mw; w0 += W) {
+        const uint32_t w = w0 + tid;
         uint32_t wg[GQ], any = 0;
+        // round r's bounds, parked in the thread's own shared column so the
+        // loops below visit only the set bits
+#pragma unroll
+        for (int b = 0; b <= 32; ++b) s_bnd[b][tid] = nb[b];
 #pragma unroll
         for (int g = 0; g < GQ; ++g) {
-            wg[g] = nx[g];
+            wg[g] = cw[g];
             any |= wg[g];
-            nx[g] = wn < mw ? __ldcg(cbg + g * mwcap + wn) : 0u;
+            cw[g] = nx[g];
         }
-        // the bounds of the word's set chunks: one batch of independent loads,
-        // parked in the thread's own shared column so the loops below visit
-        // only the set bits
-        {
-            uint32_t bnd[33];
-#pragma unroll
-            for (int b = 0; b <= 32; ++b) {
-                const bool need = (b < 32 && ((any >> b) & 1u)) || (b > 0 && ((any >> (b - 1)) & 1u));
-                bnd[b] = need ? __ldg(cs + w * 32 + b) : 0u;
-            }
-#pragma unroll
-            for (int b = 0; b <= 32; ++b) s_bnd[b][tid] = bnd[b];
+        if (w0 + W < mw) {
+            bounds(w + W, cw, nb);
+            words(w + 2 * W, nx);
         }
         uint32_t cnt = 0, toks = 0;
         for (uint32_t bits = any; bits; bits &= bits - 1u) {

@@ -1,4 +1,4 @@
-"""Config-2 engine, a few eager retrieve() calls: with LC_PROF=1 the kernels
+"""A config's engine (its rank-0 shard), a few eager retrieve() calls: with LC_PROF=1 the kernels
 print their per-phase timestamps (diagnostics; not a bench number)."""
 import os
 import sys
@@ -14,7 +14,9 @@ from paper_2603_08453_b200 import api  # noqa: E402
 def main():
     args = bench.apply_config(bench.parse())
     args.batch = args.batch or 1
-    slots = list(range(args.layers * args.kv_heads * args.batch))
+    from paper_2603_08453_b200 import shard
+    slots = shard.slots_of_rank(0, max(1, args.shards), args.layers, args.kv_heads, args.batch,
+                                order="layer")
     eng, qs, setup, codes = bench.build_engine(api, torch, args, slots, 0)
     q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
     out = torch.zeros_like(q)
