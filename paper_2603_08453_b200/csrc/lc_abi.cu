@@ -154,8 +154,9 @@ int lc_index_create(const lc_index_desc* desc, lc_index_t* out) {
         h->att_part = dalloc<float>(part_floats, o);
         ck(cudaMemset(h->att_part, 0, part_floats * 4), "memset attention partials");
         const size_t groups = std::max<uint32_t>(1, std::min(d.slot_groups, d.n_slots));
-        h->fine_ctr = dalloc<uint32_t>(4 * groups, o);
-        ck(cudaMemset(h->fine_ctr, 0, 4 * groups * 4), "memset k_fine counters");
+        h->fine_ctr = dalloc<uint32_t>(32 * groups, o);
+        ck(cudaMemset(h->fine_ctr, 0, 32 * groups * 4), "memset k_fine / k_pickq counters");
+        h->pick_ord = dalloc<uint32_t>((size_t)16 * S * G, o);
         a.err = dalloc<uint32_t>(1, o);
         h->q_stage = dalloc<float>(S * G * D, o);
         h->out_stage = dalloc<float>(S * G * D, o);
@@ -617,7 +618,8 @@ static void retrieve_impl(lc_index_t h, const float* q_dev, const lc_budgets* b,
         cudaGetLastError();
         const cudaError_t e = launch_select3(ag, q_dev, b->unit_topk, b->mode, b->cluster_topk, b->token_budget,
                                              b->sink_size, flags, buf_off, buf_ids, h->sel_scratch, a.max_cand,
-                                             max_union, pmax, count, h->fine_ctr + 4 * gi, gs, q_in);
+                                             max_union, pmax, count, h->fine_ctr + 32 * gi,
+                                             h->pick_ord + (size_t)16 * ag.G * ag.slot0, gs, q_in);
         if (e != cudaSuccess)
             fail(LC_ECUDA, std::string("k_select3: ") + g_select3_where + ": " + cudaGetErrorString(e));
         h->last_launches += 4;

@@ -14,8 +14,8 @@ size_t select3_pick_smem(const Arena& a);
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
-                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
-                           const float* q_in = nullptr);  // q_in: k_coarse reads q here and copies it to q
+                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, uint32_t* pick_ord,
+                           cudaStream_t stream, const float* q_in = nullptr);  // q_in: k_coarse reads q here and copies it to q
 extern thread_local char g_select3_where[96];  // failing stage of the last launch_select3
 cudaError_t launch_fused(const Arena& a, const float* q, const float* q_in, uint32_t unit_topk, uint32_t mode,
                          uint32_t cluster_topk, unsigned long long budget, uint32_t sink, uint32_t flags,
@@ -123,7 +123,8 @@ struct lc_index_s {
     unsigned char* sel_scratch = nullptr;      // per-head candidate keys + weights (k_fine -> k_pickq)
     size_t sel_scratch_bytes = 0;
     float* att_part = nullptr;                 // k_attend per-(warp, slot) segment partials + counters
-    uint32_t* fine_ctr = nullptr;              // k_fine pool counters, 4 per slot group (zeroed)
+    uint32_t* fine_ctr = nullptr;              // k_fine / k_pickq counters, 32 per slot group (zeroed)
+    uint32_t* pick_ord = nullptr;              // k_pickq's size-class lists, 16 x G per slot
     std::vector<cudaStream_t> group_streams;   // one per slot group
     uint64_t version = 0;                      // bumped by every upload / append / graft
     cudaStream_t host_stream = nullptr;        // lc_retrieve_host's graph replay stream

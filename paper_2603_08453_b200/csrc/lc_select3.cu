@@ -133,7 +133,9 @@ struct Sel3Params {
     unsigned char* scratch;  // per slot: keys u64 [G][qcap] + weights/selection u32 [G][qcap]
     uint32_t qcap;
     unsigned long long* prof;  // optional k_pick phase timestamps [slot][8] (LC_PROF=1)
-    uint32_t* fine_ctr;        // k_fine pool / exit counters (zeroed; reset by k_fine)
+    uint32_t* fine_ctr;        // k_fine pool / exit counters [0, 2) (reset by k_fine); k_pickq's
+                               // size-class counters [16, 32) (reset by k_spans); zeroed
+    uint32_t* pick_ord;        // k_pickq's heads by size class: [class][n_slots * G] (this group)
     unsigned long long* prof_sp;  // optional k_spans phase timestamps [slot][8] (LC_PROF=1)
 };
 
@@ -143,10 +145,25 @@ __device__ __forceinline__ unsigned long long gtime3() {
     return t;
 }
 #define LC_PMARK(ph) \
-    if (p.prof && threadIdx.x == 0) p.prof[((size_t)slot * GQ + blockIdx.x) * 8 + (ph)] = gtime3();
+    if (p.prof && threadIdx.x == 0) p.prof[((size_t)slot * GQ + g) * 8 + (ph)] = gtime3();
 
 // ---------------------------------------------------------------------------
 constexpr int kCoThreads = 256;
+
+// k_pickq's launch order: k_coarse files every (slot, head) under the log2 size
+// class of its candidate count, and k_pickq's CTAs take the heads largest class
+// first, so the few long heads start in the first wave instead of ending the
+// kernel (longest-processing-time-first list scheduling).
+constexpr uint32_t kPickClasses = 16;
+__device__ __forceinline__ uint32_t pick_class(uint32_t nc) {
+    const uint32_t c = nc ? 31u - __clz(nc) : 0u;
+    return kPickClasses - 1u - min(c, kPickClasses - 1u);  // class 0: the largest heads
+}
+__device__ __forceinline__ void pick_push(const Sel3Params& p, uint32_t h, uint32_t nc) {
+    const uint32_t c = pick_class(nc), nh = gridDim.x * p.a.G;  // k_coarse: one CTA per slot
+    const uint32_t at = atomicAdd(p.fine_ctr + 16 + c, 1u);
+    if (at < nh) p.pick_ord[(size_t)c * nh + at] = h;  // (a miscount falls back to launch order)
+}
 
 template <int D, int GQ>
 __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
@@ -166,6 +183,7 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
             pv.hdr()[0] = 1;
             pv.hdr()[1] = pv.hdr()[2] = 0;
         }
+        if (tid < G) pick_push(p, blockIdx.x * G + tid, 0u);
         return;
     }
     const uint32_t Pp = (P + 3) & ~3u;
@@ -337,6 +355,7 @@ __global__ void __launch_bounds__(kCoThreads) k_coarse(Sel3Params p) {
         }
         if (lane < G) {
             pv.hdr()[4 + lane] = qacc[lane];
+            pick_push(p, blockIdx.x * G + lane, qacc[lane]);
             pv.kmin()[lane] = ~0ull;
             pv.kmax()[lane] = 0ull;
             pv.qnorm()[lane] = s_qn[lane];
@@ -763,8 +782,34 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
     constexpr uint32_t D = DQ;
     extern __shared__ __align__(16) unsigned char qsm[];
     const Arena& a = p.a;
-    const uint32_t g = blockIdx.x, slot = a.slot0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t G = GQ;
+    uint32_t g, slot;
+    {  // this CTA's head: rank blockIdx in the size-class order k_coarse filed
+        __shared__ uint32_t s_h;
+        const uint32_t nh = gridDim.x * gridDim.y, b = blockIdx.y * gridDim.x + blockIdx.x;
+        if (warp == 0) {
+            const uint32_t cnt = lane < kPickClasses ? __ldcg(p.fine_ctr + 16 + lane) : 0u;
+            uint32_t x = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+            const unsigned int in = __ballot_sync(0xffffffffu, lane < kPickClasses && b < x);
+            const uint32_t c = in ? (uint32_t)(__ffs(in) - 1) : 0u;
+            const uint32_t before = __shfl_sync(0xffffffffu, x - cnt, c);
+            if (lane == 0) {
+                uint32_t h = b;  // identity if the filing is incomplete (never expected)
+                if (total == nh && in) h = __ldcg(p.pick_ord + (size_t)c * nh + (b - before));
+                s_h = h;
+            }
+        }
+        __syncthreads();
+        g = s_h % G;
+        slot = a.slot0 + s_h / G;
+    }
     const SlotState st = a.state[slot];
     const uint32_t M = st.n_chunks, P = st.P, L = st.L;
     PlanView pv(a.plan + (size_t)slot * a.plan_bytes, a);
@@ -1032,7 +1077,7 @@ __device__ __forceinline__ void pick_head(const Sel3Params& p) {
         }
         __syncthreads();
         const uint32_t nr = s_rn;
-        if (p.prof && tid == 0) p.prof[((size_t)slot * GQ + blockIdx.x) * 8 + 7] = nr | ((unsigned long long)nc << 32);
+        if (p.prof && tid == 0) p.prof[((size_t)slot * GQ + g) * 8 + 7] = nr | ((unsigned long long)nc << 32);
         LC_PMARK(6)
         const float* fcs = a.fcent + (size_t)slot * a.cap_clusters * D;
         const double qn = pv.qnorm()[g];
@@ -1647,6 +1692,7 @@ __global__ void __launch_bounds__(kPqThreads) k_pickq(Sel3Params p) {
 template <int GQ>
 __global__ void __launch_bounds__(kSpThreads) k_spans(Sel3Params p) {
     pdl_wait();
+    if (blockIdx.x == 0 && threadIdx.x < kPickClasses) p.fine_ctr[16 + threadIdx.x] = 0;  // k_pickq is done
     build_spans<GQ>(p, p.a.slot0 + blockIdx.x);
 }
 
@@ -1738,8 +1784,8 @@ size_t select3_pick_smem(const Arena& a) {
 cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, uint32_t mode, uint32_t cluster_topk,
                            unsigned long long budget, uint32_t sink, uint32_t flags, const uint32_t* buf_off,
                            const uint32_t* buf_ids, unsigned char* scratch, uint32_t qcap, uint32_t max_union,
-                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, cudaStream_t stream,
-                           const float* q_in) {
+                           uint32_t pmax, uint32_t n_slots, uint32_t* fine_ctr, uint32_t* pick_ord,
+                           cudaStream_t stream, const float* q_in) {
     // LC_PROF=1 (diagnostics only): per-CTA timestamps, buffers per device
     static unsigned long long *prof_dev[kMaxDevices] = {}, *prof_sp_dev[kMaxDevices] = {};
     const int dev = current_device();
@@ -1752,7 +1798,7 @@ cudaError_t launch_select3(const Arena& a, const float* q, uint32_t unit_topk, u
     }
     g_select3_where[0] = 0;
     Sel3Params p{a, pick_keys_cap(a), q, q_in ? q_in : q, unit_topk, mode, cluster_topk, sink, flags, budget, buf_off, buf_ids, scratch, qcap, prof,
-                 fine_ctr, prof_sp};
+                 fine_ctr, pick_ord, prof_sp};
     cudaError_t e = a.d == 128 ? launch3_d<128>(p, n_slots, max_union, pmax, stream)
                   : a.d == 64  ? launch3_d<64>(p, n_slots, max_union, pmax, stream)
                   : a.d == 32  ? launch3_d<32>(p, n_slots, max_union, pmax, stream)
