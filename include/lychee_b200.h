@@ -293,6 +293,14 @@ int lc_step_bytes(lc_index_t h, uint64_t* out);
  * k_attend + k_merge); the bench's gpu_launches claim. */
 int lc_launch_count(lc_index_t h, uint32_t* out);
 
+/* Measurement hook for the bench's per-kernel roofline: reports the summed
+ * CUDA-event time (ms) and count of the k_attend launches timed since the
+ * previous call (ms_sum / timed may be null), then arms n_launches event
+ * pairs: each following single-launch lc_sparse_attention records one pair
+ * on its stream around k_attend alone (k_merge follows the second record).
+ * n_launches = 0 disarms.  Synchronous when reporting. */
+int lc_attend_timing(lc_index_t h, uint32_t n_launches, float* ms_sum, uint32_t* timed);
+
 /* Sticky device-side error bits (lc_common.cuh ErrBits) of every kernel since
  * the last clear; synchronous.  Bit 0 candidates over capacity, 1 empty
  * candidate set (select_topk k = 0), 2 spans over capacity, 3 zero-norm

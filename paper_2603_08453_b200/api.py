@@ -572,6 +572,14 @@ class Engine:
         L.check(L.lib().lc_launch_count(self.h, out.ctypes.data))
         return int(out[0])
 
+    def attend_timing(self, arm: int = 0):
+        """(summed ms, launches) of the k_attend launches timed since the last
+        call (CUDA events around k_attend alone), then arm `arm` more."""
+        ms = np.zeros(1, np.float32)
+        n = np.zeros(1, np.uint32)
+        L.check(L.lib().lc_attend_timing(self.h, arm, ms.ctypes.data, n.ctypes.data))
+        return float(ms[0]), int(n[0])
+
     def device_error(self, clear: bool = True) -> int:
         out = np.zeros(1, np.uint32)
         L.check(L.lib().lc_device_error(self.h, out.ctypes.data, int(clear)))
@@ -641,13 +649,13 @@ class DeviceIndex:
 
     def __init__(self, ix: HostIndex, keys: np.ndarray, values: np.ndarray, group: int = 1,
                  extra_tokens: int = 0, extra_chunks: int = 0, structure_aware: bool = True,
-                 graft_full: bool = False, device: int = 0, kv_f32: bool = False):
+                 graft_full: bool = False, device: int = 0, kv_f32: bool = False, pooling: int = 0):
         n = keys.shape[0]
         self.engine = Engine(1, ix.dim, group, cap_tokens=n + extra_tokens + 1,
                              cap_chunks=ix.n_chunks + extra_chunks + 1,
                              cap_clusters=ix.n_clusters, cap_units=max(ix.n_units, 1),
                              structure_aware=structure_aware, graft_full=graft_full, device=device,
-                             kv_f32=kv_f32)
+                             kv_f32=kv_f32, pooling=pooling)
         self.engine.upload_slot(0, ix, keys, values)
         self.dim = ix.dim
         self.group = group
@@ -702,10 +710,10 @@ class StreamState:
 
     def __init__(self, ix: HostIndex, keys: np.ndarray, values: np.ndarray, texts: Sequence[str],
                  structure_aware=True, graft_full=False, extra_tokens=4096, extra_chunks=512,
-                 history_capacity=32, min_len=8, max_len=16, device=0, group=1):
+                 history_capacity=32, min_len=8, max_len=16, device=0, group=1, pooling=0):
         self.index = DeviceIndex(ix, keys, values, group=group, extra_tokens=extra_tokens,
                                  extra_chunks=extra_chunks, structure_aware=structure_aware,
-                                 graft_full=graft_full, device=device)
+                                 graft_full=graft_full, device=device, pooling=pooling)
         self.engine = self.index.engine
         self.texts = list(texts)
         self.structure_aware = structure_aware

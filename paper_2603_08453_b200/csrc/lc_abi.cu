@@ -729,7 +729,38 @@ int lc_sparse_attention(lc_index_t h, const float* q_dev, float* out_dev, void* 
         h->set_device();
         Arena a = h->a;
         a.slot0 = 0;
-        ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, (cudaStream_t)stream), "k_attend");
+        cudaEvent_t* ev = nullptr;
+        if (h->att_ev_used * 2 + 2 <= h->att_ev.size()) ev = &h->att_ev[2 * h->att_ev_used++];
+        ck(launch_attend(a, q_dev, out_dev, h->att_part, a.n_slots, (cudaStream_t)stream, nullptr, nullptr, ev),
+           "k_attend");
+    });
+}
+
+int lc_attend_timing(lc_index_t h, uint32_t n_launches, float* ms_sum, uint32_t* timed) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "lc_attend_timing: null handle");
+        h->set_device();
+        if (ms_sum || timed) {
+            float sum = 0.f;
+            uint32_t n = 0;
+            if (!h->att_ev.empty()) ck(cudaEventSynchronize(h->att_ev[2 * (h->att_ev_used ? h->att_ev_used - 1 : 0) + 1]), "sync");
+            for (size_t i = 0; i < h->att_ev_used; ++i) {
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, h->att_ev[2 * i], h->att_ev[2 * i + 1]) != cudaSuccess) continue;
+                sum += ms;
+                ++n;
+            }
+            if (ms_sum) *ms_sum = sum;
+            if (timed) *timed = n;
+        }
+        for (cudaEvent_t e : h->att_ev) cudaEventDestroy(e);
+        h->att_ev.clear();
+        h->att_ev_used = 0;
+        for (uint32_t i = 0; i < 2 * n_launches; ++i) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "event");
+            h->att_ev.push_back(e);
+        }
     });
 }
 

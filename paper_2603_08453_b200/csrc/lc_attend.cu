@@ -279,7 +279,7 @@ __device__ __forceinline__ void slot_prefixes(const Arena& a, uint32_t n, uint32
     const uint32_t per = (n + NT - 1) / NT, i0 = tid * per;
     uint32_t lh = 0, lt = 0;
     for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
-        const uint32_t t = a.slot_tok[a.slot0 + i];
+        const uint32_t t = __ldcg(a.slot_tok + a.slot0 + i);
         lh += head_of(t);
         lt += t - head_of(t);
     }
@@ -305,7 +305,7 @@ __device__ __forceinline__ void slot_prefixes(const Arena& a, uint32_t n, uint32
     uint32_t rh = bh + xh - lh, rt = bt + xt - lt;
     if (tid == 0) s_hp[0] = s_tp[0] = 0;
     for (uint32_t i = i0; i < i0 + per && i < n; ++i) {
-        const uint32_t t = a.slot_tok[a.slot0 + i];
+        const uint32_t t = __ldcg(a.slot_tok + a.slot0 + i);
         rh += head_of(t);
         rt += t - head_of(t);
         s_hp[i + 1] = rh;
@@ -378,10 +378,10 @@ __device__ __forceinline__ void merge_tasks(float* out, uint32_t* err, uint32_t 
 
 template <int D, bool QUEUE>
 __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
-    pdl_wait();
     const Arena& a = p.a;
     const uint32_t n = p.n, warp = threadIdx.x >> 5, G = a.G;
     if constexpr (QUEUE) {
+        pdl_wait();
         const uint32_t x = blockIdx.x * 8 + warp, s = x / G, g = x % G;
         if (s < n)
             merge_tasks<D>(p.out + (size_t)(a.slot0 + s) * G * D, a.err, G, g, p.part + 16,
@@ -402,8 +402,13 @@ __global__ void __launch_bounds__(256) k_merge(AttendParams p, uint32_t NW) {
         }
         return;
     }
+    // static partition: k_attend triggers this launch once all its CTAs are past
+    // their own griddepcontrol.wait, so the slot totals (written by the
+    // selection, before k_attend) are final; the prefixes are computed while
+    // k_attend drains, its partials only after the wait
     __shared__ uint32_t s_hp[kMaxAttendSlots + 1], s_tp[kMaxAttendSlots + 1], s_wsum[16];
     slot_prefixes<256>(a, n, s_hp, s_tp, s_wsum);
+    pdl_wait();
     const uint32_t x = blockIdx.x * 8 + warp, s = x / G, g = x % G;
     if (s >= n) return;
     if (s_hp[s + 1] == s_hp[s] && s_tp[s + 1] == s_tp[s]) return;  // empty: k_attend wrote zeros
@@ -418,7 +423,12 @@ template <int D, bool QUEUE>
 __global__ void __launch_bounds__(kAttThreads, 2) k_attend(AttendParams p) {
     // streamed mode: no grid-wide wait on the selection -- each claimed task is
     // acquired from its publication tag instead
+    // k_merge may launch once every CTA of this grid is resident: its CTAs take
+    // SMs as this grid drains (static partition: its slot prefixes are computed
+    // there before its own wait).  Static partition: only after this grid's own
+    // wait, so the selection's slot totals are final when k_merge reads them.
     if constexpr (!QUEUE) pdl_wait();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     static_assert(D == 64 || D == 128, "D must be 64 or 128");
     constexpr int KS = D / 16;             // k-steps of QK
     constexpr int KW = D / 32;             // 16-byte chunks per thread per K row
@@ -798,13 +808,18 @@ static KernelCfg& attend_cfg() {
 }
 
 template <int D, bool QUEUE>
-static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStream_t stream) {
+static cudaError_t launch_attend_d(const AttendParams& p, uint32_t grid, cudaStream_t stream,
+                                   cudaEvent_t* ev) {
     static KernelCfg qcfg;
     cudaError_t e = QUEUE ? ensure_smem(k_attend<D, true>, qcfg, attend_smem<D>())
                           : ensure_smem(k_attend<D, false>, attend_cfg<D>(), attend_smem<D>());
     if (e != cudaSuccess) return e;
+    // lc_attend_timing: an event pair on the launching stream around k_attend
+    // alone (k_merge then starts after the second record, without PDL overlap)
+    if (ev && (e = cudaEventRecord(ev[0], stream)) != cudaSuccess) return e;
     e = launch_pdl(k_attend<D, QUEUE>, dim3(grid), dim3(kAttThreads), attend_smem<D>(), stream, p);
     if (e != cudaSuccess) return e;
+    if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) return e;
     return launch_pdl(k_merge<D, QUEUE>, dim3((p.n * p.a.G + 7) / 8), dim3(256), 0, stream, p,
                       grid * (uint32_t)kAttWarps);
 }
@@ -955,7 +970,7 @@ cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned 
 }
 
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
-                          cudaStream_t stream, const PeerGather* pg, const AttQueueDev* aq) {
+                          cudaStream_t stream, const PeerGather* pg, const AttQueueDev* aq, cudaEvent_t* att_ev) {
     if (a.kv_f32) {
         // splits per (slot, head): as many as the partials buffer holds, at most 16
         const size_t cap = (attend_partials_floats(a.d, a.G, n_slots) - 16) * 4;
@@ -980,16 +995,17 @@ cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* par
     // global positions of the static partition apply)
     const bool queued = aq && aq->ctl;
     if (queued) per = n_slots;
+    const bool one = n_slots <= per;  // lc_attend_timing times single-launch calls only
     for (uint32_t s0 = 0; s0 < n_slots; s0 += per) {
         AttendParams p{a, q, out, std::min(per, n_slots - s0), part, want_prof ? prof : nullptr, kMinWarpTok,
                        pg ? *pg : PeerGather{nullptr, nullptr, nullptr, 0u}, aq ? *aq : AttQueueDev{}};
         if (const char* ev = getenv("LC_ATT_MINTOK")) p.min_tok = std::max(16, atoi(ev));  // experiments
         if (prof) cudaMemset(prof, 0, (size_t)grid * kAttWarps * 4 * 8);
         p.a.slot0 = a.slot0 + s0;
-        cudaError_t e = a.d == 128 ? (queued ? launch_attend_d<128, true>(p, grid, stream)
-                                              : launch_attend_d<128, false>(p, grid, stream))
-                      : a.d == 64  ? (queued ? launch_attend_d<64, true>(p, grid, stream)
-                                              : launch_attend_d<64, false>(p, grid, stream))
+        cudaError_t e = a.d == 128 ? (queued ? launch_attend_d<128, true>(p, grid, stream, one ? att_ev : nullptr)
+                                              : launch_attend_d<128, false>(p, grid, stream, one ? att_ev : nullptr))
+                      : a.d == 64  ? (queued ? launch_attend_d<64, true>(p, grid, stream, one ? att_ev : nullptr)
+                                              : launch_attend_d<64, false>(p, grid, stream, one ? att_ev : nullptr))
                                    : cudaErrorInvalidValue;
         if (e != cudaSuccess) return e;
         if (want_prof) {

@@ -26,7 +26,8 @@ uint32_t attend_grid(uint32_t d);
 uint32_t attend_queue_cap(uint32_t d, uint32_t G, uint32_t n_slots);
 size_t attend_partials_floats(uint32_t d, uint32_t G, uint32_t n_slots);
 cudaError_t launch_attend(const Arena& a, const float* q, float* out, float* part, uint32_t n_slots,
-                          cudaStream_t stream, const PeerGather* pg = nullptr, const AttQueueDev* aq = nullptr);
+                          cudaStream_t stream, const PeerGather* pg = nullptr, const AttQueueDev* aq = nullptr,
+                          cudaEvent_t* att_ev = nullptr);
 cudaError_t launch_gather_wait(unsigned int* flag, unsigned int* done, unsigned int expect, uint32_t* err,
                                cudaStream_t stream);
 cudaError_t launch_append(const Arena& a, const void* keys, const void* values, cudaStream_t stream);
@@ -119,6 +120,8 @@ struct lc_index_s {
     uint32_t last_flags = 0;
     uint32_t last_valid = 0;
     uint32_t last_launches = 0;                // kernels of the last selection + attention
+    std::vector<cudaEvent_t> att_ev;           // lc_attend_timing: event pairs around k_attend launches
+    size_t att_ev_used = 0;
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
     unsigned char* sel_scratch = nullptr;      // per-head candidate keys + weights (k_fine -> k_pickq)
     size_t sel_scratch_bytes = 0;
@@ -160,6 +163,7 @@ struct lc_index_s {
         if (host_stream) cudaStreamDestroy(host_stream);
         if (host_event) cudaEventDestroy(host_event);
         for (auto e : group_events) cudaEventDestroy(e);
+        for (auto e : att_ev) cudaEventDestroy(e);
         if (pg_mem) cudaFree(pg_mem);
         if (aq_mem) cudaFree(aq_mem);
     }

@@ -8,6 +8,8 @@
 // ties keep the first candidate in the reference's scan order.
 #include "lc_common.cuh"
 
+#include <algorithm>
+
 namespace lc {
 
 __global__ void k_append(Arena a, const void* keys, const void* values) {
@@ -84,6 +86,108 @@ __device__ void block_argmax(double& s, uint32_t& k, double* ws, uint32_t* wk) {
     __syncthreads();
 }
 
+constexpr uint32_t kKeyTile = 32;     // chunk key rows staged per round
+constexpr uint32_t kMemberTile = 64;  // unit member centroid rows staged per round
+
+// n contiguous floats from global into shared memory, element x at
+// dst[(x / d) * pitch + x % d]; float4 loads, up to 4 per thread in flight
+__device__ __forceinline__ void stage_rows(float* dst, const float* src, uint32_t n, uint32_t d, uint32_t pitch) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    const uint32_t n4 = n / 4;
+    for (uint32_t b = threadIdx.x; b < n4; b += 4 * blockDim.x) {
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = b + k * blockDim.x;
+            if (x < n4) v[k] = __ldg(s4 + x);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = b + k * blockDim.x;
+            if (x < n4) {
+                const uint32_t e = 4 * x, r = e / d, j = e % d;
+                float* o = dst + r * pitch + j;
+                o[0] = v[k].x;
+                o[1] = v[k].y;
+                o[2] = v[k].z;
+                o[3] = v[k].w;
+            }
+        }
+    }
+}
+// n contiguous bf16 (n % 8 == 0 when d % 8 == 0) as floats into dst[x]
+__device__ __forceinline__ void stage_rows_bf16(float* dst, const __nv_bfloat16* src, uint32_t n) {
+    const uint4* s8 = reinterpret_cast<const uint4*>(src);
+    const uint32_t n8 = n / 8;
+    for (uint32_t b = threadIdx.x; b < n8; b += 2 * blockDim.x) {
+        uint4 v[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t x = b + k * blockDim.x;
+            if (x < n8) v[k] = __ldg(s8 + x);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t x = b + k * blockDim.x;
+            if (x < n8) {
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 f = __bfloat1622float2(h[t]);
+                    dst[8 * x + 2 * t] = f.x;
+                    dst[8 * x + 2 * t + 1] = f.y;
+                }
+            }
+        }
+    }
+}
+
+// Sequential fp64 chains in the reference's index order, with each group of
+// 8 terms loaded (and its independent products formed) before the group is
+// folded in, so only the dependent add / FMA stays on the chain.  Every
+// supported head dim is a multiple of 8.
+__device__ __forceinline__ double seq_sumsq(const double* v, uint32_t d) {  // std::inner_product(v, v)
+    double s = 0.0;
+    for (uint32_t j = 0; j < d; j += 8) {
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = __dmul_rn(v[j + k], v[j + k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, t[k]);
+    }
+    return s;
+}
+// kernels::l2_dist (kernels.cpp:25-32): diff = (double)x - y, s += diff * diff
+__device__ __forceinline__ double seq_l2(const float* x, const float* y, uint32_t ys, uint32_t d) {
+    double s = 0.0;
+    for (uint32_t j = 0; j < d; j += 8) {
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double diff = __dsub_rn((double)x[j + k], (double)y[(size_t)(j + k) * ys]);
+            t[k] = __dmul_rn(diff, diff);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = __dadd_rn(s, t[k]);
+    }
+    return __dsqrt_rn(s);
+}
+// kernels::dot (sequential FMA chain) of x with y[j * ys]
+__device__ __forceinline__ double seq_dot(const float* x, const float* y, uint32_t ys, uint32_t d) {
+    double s = 0.0;
+    for (uint32_t j = 0; j < d; j += 8) {
+        float a[8], b[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a[k] = x[j + k];
+            b[k] = y[(size_t)(j + k) * ys];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = __fma_rn((double)a[k], (double)b[k], s);
+    }
+    return s;
+}
+
 __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
     const Arena& a = p.a;
     const uint32_t slot = blockIdx.x, tid = threadIdx.x, d = a.d;
@@ -95,6 +199,8 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
     __shared__ double s_norm, s_delta, s_tonew, s_dg;
     __shared__ double ws[kGraftThreads / 32];
     __shared__ uint32_t wk[kGraftThreads / 32];
+    __shared__ float s_ucol[256];  // the chosen unit's coarse centroid (dimension j)
+    extern __shared__ float s_dyn[];
     SlotState* stp = a.state + slot;
     const uint32_t start = stp->chunked_end, M = stp->n_chunks, P = stp->P, L = stp->L;
     if (M >= a.cap_chunks) {
@@ -110,27 +216,33 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
         __syncthreads();
     } else {
     // ---- chunk_representative (index.cpp:20-41) over keys [start, start+take) ----
-    auto key = [&](uint32_t i, uint32_t j) -> double {
-        return a.kv_f32 ? (double)a.Kf[kv_off(a, slot) + (size_t)(start + i) * d + j]
-                        : (double)__bfloat162float(a.K[kv_off(a, slot) + (size_t)(start + i) * d + j]);
-    };
-    for (uint32_t j = tid; j < d; j += blockDim.x) {
-        double acc;
-        if (p.pooling == 0) {
-            acc = 0.0;
-            for (uint32_t i = 0; i < take; ++i) acc = __dadd_rn(acc, key(i, j));
-            acc = __ddiv_rn(acc, (double)take);
-        } else {
-            acc = key(0, j);
-            for (uint32_t i = 1; i < take; ++i) acc = fmax(acc, key(i, j));
+    // the chunk's key rows stream through shared memory kKeyTile rows at a
+    // time (coalesced 16-byte loads, all in flight together); thread j then
+    // folds dimension j of the tile in row order, so the sequential fp64
+    // chain reads shared memory instead of one dependent global load per row
+    double acc = p.pooling == 0 ? 0.0 : -INFINITY;
+    const size_t kbase = kv_off(a, slot) + (size_t)start * d;
+    for (uint32_t i0 = 0; i0 < take; i0 += kKeyTile) {
+        const uint32_t nr = min(kKeyTile, take - i0);
+        if (a.kv_f32) stage_rows(s_dyn, a.Kf + kbase + (size_t)i0 * d, nr * d, d, d);
+        else stage_rows_bf16(s_dyn, a.K + kbase + (size_t)i0 * d, nr * d);
+        __syncthreads();
+        if (tid < d) {
+            if (p.pooling == 0) {
+#pragma unroll 8
+                for (uint32_t i = 0; i < nr; ++i) acc = __dadd_rn(acc, (double)s_dyn[i * d + tid]);
+            } else {
+                uint32_t i = 0;
+                if (i0 == 0) acc = (double)s_dyn[tid], i = 1;
+                for (; i < nr; ++i) acc = fmax(acc, (double)s_dyn[i * d + tid]);
+            }
         }
-        s_acc[j] = acc;
+        __syncthreads();
     }
+    if (tid < d) s_acc[tid] = p.pooling == 0 ? __ddiv_rn(acc, (double)take) : acc;
     __syncthreads();
     if (tid == 0) {
-        double n2 = 0.0;  // std::inner_product: n2 + a*a, rounded product
-        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(s_acc[j], s_acc[j]));
-        s_norm = __dsqrt_rn(n2);
+        s_norm = __dsqrt_rn(seq_sumsq(s_acc, d));  // std::inner_product: n2 + a*a, rounded product
     }
     __syncthreads();
     if (s_norm == 0.0) {
@@ -145,9 +257,23 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
     // the slot's coarse centroids staged once, coalesced, dimension-major
     // [d][P] (dynamic shared memory): the unit scan and the coarse l2_dist read
     // them from shared memory instead of P strided global chains
-    extern __shared__ float s_uc[];
+    float* s_uc = s_dyn;
     const float* uc = a.ucent + (size_t)slot * a.cap_units * d;
-    for (uint32_t x = tid; x < d * P; x += blockDim.x) s_uc[x] = uc[(size_t)(x / P) * a.cap_units + x % P];
+    // (8 independent loads per thread in flight per round: the store of each
+    // waits on its load, so a one-at-a-time loop paid a round trip per element)
+    for (uint32_t b = tid; b < d * P; b += 8 * blockDim.x) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t x = b + k * blockDim.x;
+            if (x < d * P) v[k] = __ldg(uc + (size_t)(x / P) * a.cap_units + x % P);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t x = b + k * blockDim.x;
+            if (x < d * P) s_uc[x] = v[k];
+        }
+    }
     __syncthreads();
     const uint32_t* uoff = a.unit_off + (size_t)slot * (a.cap_units + 1);
     const float* fc = a.fcent + (size_t)slot * a.cap_clusters * d;
@@ -180,9 +306,7 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
         double bs = -INFINITY;
         uint32_t bu = 0xffffffffu;
         for (uint32_t u = tid; u < P; u += blockDim.x) {
-            double s = 0.0;
-            for (uint32_t j = 0; j < d; ++j) s = __fma_rn((double)s_rep[j], (double)s_uc[j * P + u], s);
-            argmax_merge(bs, bu, s, u);
+            argmax_merge(bs, bu, seq_dot(s_rep, s_uc + u, P, d), u);
         }
         block_argmax(bs, bu, ws, wk);
         const uint32_t lo = uoff[bu], hi = uoff[bu + 1];
@@ -193,7 +317,20 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
             const uint32_t nu = hi - lo;
             double bs2 = -INFINITY;
             uint32_t bc = 0xffffffffu;
-            for (uint32_t i = tid; i < nu; i += blockDim.x) argmax_merge(bs2, bc, row_dot(lo + i), lo + i);
+            // the unit's member rows are contiguous: stage them kMemberTile rows
+            // at a time (pitch d + 1: thread t's row walk is conflict free) over
+            // the coarse centroids, whose one needed column is kept in s_ucol
+            for (uint32_t j = tid; j < d; j += blockDim.x) s_ucol[j] = s_uc[j * P + bu];
+            __syncthreads();
+            for (uint32_t t0 = 0; t0 < nu; t0 += kMemberTile) {
+                const uint32_t nr = min(kMemberTile, nu - t0);
+                stage_rows(s_dyn, fc + (size_t)(lo + t0) * d, nr * d, d, d + 1);
+                __syncthreads();
+                if (tid < nr) {
+                    argmax_merge(bs2, bc, seq_dot(s_rep, s_dyn + tid * (d + 1), 1, d), lo + t0 + tid);
+                }
+                __syncthreads();
+            }
             block_argmax(bs2, bc, ws, wk);  // stored order == internal order
             best_c = bc;
             comps += nu;
@@ -227,9 +364,7 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
     }
     __syncthreads();
     if (tid == 0) {
-        double n2 = 0.0;
-        for (uint32_t j = 0; j < d; ++j) n2 = __dadd_rn(n2, __dmul_rn(s_moved[j], s_moved[j]));
-        s_norm = __dsqrt_rn(n2);
+        s_norm = __dsqrt_rn(seq_sumsq(s_moved, d));
     }
     __syncthreads();
     const double norm = s_norm;
@@ -237,20 +372,10 @@ __global__ void __launch_bounds__(kGraftThreads, 4) k_graft(GraftParams p) {
         s_new[j] = norm > 0.0 ? (float)__ddiv_rn(s_moved[j], norm) : s_mu[j];
     __syncthreads();
     // three sequential l2_dist (kernels.cpp:25-32) on three warps in parallel
-    if (tid == 0 || tid == 32 || tid == 64) {
-        double s = 0.0;
-        for (uint32_t j = 0; j < d; ++j) {
-            double x, y;
-            if (tid == 0) { x = s_new[j]; y = s_mu[j]; }
-            else if (tid == 32) { x = s_rep[j]; y = s_new[j]; }
-            else { x = s_rep[j]; y = s_uc[j * P + u]; }
-            const double diff = __dsub_rn(x, y);
-            s = __dadd_rn(s, __dmul_rn(diff, diff));
-        }
-        const double r = __dsqrt_rn(s);
-        if (tid == 0) s_delta = r;
-        else if (tid == 32) s_tonew = r;
-        else s_dg = r;
+    if (tid == 0) s_delta = seq_l2(s_new, s_mu, 1, d);
+    else if (tid == 32) s_tonew = seq_l2(s_rep, s_new, 1, d);
+    else if (tid == 64) {
+        s_dg = scoped ? seq_l2(s_rep, s_ucol, 1, d) : seq_l2(s_rep, s_uc + u, P, d);
     }
     __syncthreads();
     __half* fcw16 = a.frow16 + (size_t)slot * a.cap_clusters * d;
@@ -442,7 +567,9 @@ cudaError_t launch_graft(const Arena& a, const uint32_t* take_dev, uint32_t pool
                          const float* reps_dev, cudaStream_t stream, const uint32_t* kind_dev,
                          const uint32_t* level_dev) {
     GraftParams p{a, take_dev, pooling, reports, reps_dev, kind_dev, level_dev};
-    const size_t smem = (size_t)a.d * a.cap_units * 4;  // staged coarse centroids
+    // staged coarse centroids, then (aliased) unit member tiles; chunk key tiles before both
+    const size_t smem = std::max<size_t>((size_t)a.d * a.cap_units * 4,
+                                         std::max<size_t>((size_t)kKeyTile * a.d * 4, (size_t)kMemberTile * (a.d + 1) * 4));
     static KernelCfg cfg;
     cudaError_t e = ensure_smem(k_graft, cfg, smem);
     if (e != cudaSuccess) return e;

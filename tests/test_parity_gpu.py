@@ -120,6 +120,19 @@ def test_batched_slots_match_per_head_reference(slot_groups, keys_cap, monkeypat
     assert eng.device_error() == 0
     bytes_ = eng.step_bytes()
     assert bytes_[0] > 0 and bytes_[1] >= bytes_[0]
+    # the bench's per-kernel timing hook: k_attend alone, same outputs
+    # (sparse_attention uses the static partition: same values as the streamed
+    # step within rounding, bit-equal with and without the event pairs)
+    out3 = torch.zeros_like(q)
+    eng.sparse_attention(q, out3)
+    eng.attend_timing(arm=3)
+    out2 = torch.zeros_like(q)
+    for _ in range(4):
+        eng.sparse_attention(q, out2)
+    ms, n_timed = eng.attend_timing(arm=0)
+    assert n_timed == 3 and ms > 0
+    assert torch.equal(out3, out2)
+    assert rel_l2(out2.cpu().numpy(), o) < 1e-5
 
 
 def test_retrieve_host_matches_device():
@@ -166,14 +179,15 @@ def _stream_tokens(w, steps, seed):
     return toks
 
 
-@pytest.mark.parametrize("graft_full", [False, True])
-def test_decode_stream_parity(graft_full):
+@pytest.mark.parametrize("graft_full,pooling", [(False, 0), (True, 0), (False, 1)])
+def test_decode_stream_parity(graft_full, pooling):
     """decode_step over 300 steps: selections, outputs, graft reports and the
-    final index (index_to_bytes fields) match the reference."""
+    final index (index_to_bytes fields) match the reference (mean and max
+    chunk pooling)."""
     w = rounded_workload(3000, 128, seed=4, n_blobs=3, query_count=2)
-    ref = R.RefEngine(w.keys, w.values, w.text_code, seed=4, graft_full=graft_full)
+    ref = R.RefEngine(w.keys, w.values, w.text_code, seed=4, graft_full=graft_full, pooling=pooling)
     texts = ["\n" if c == 1 else ("}" if c == 2 else "") for c in w.text_code]
-    st = api.StreamState(host_index(ref), w.keys, w.values, texts, graft_full=graft_full)
+    st = api.StreamState(host_index(ref), w.keys, w.values, texts, graft_full=graft_full, pooling=pooling)
     b = api.Budgets(token_budget=256)
     code_text = {0: "", 1: "\n", 2: "}"}
     n0 = w.keys.shape[0]
