@@ -282,6 +282,16 @@ int lc_selection_download(lc_index_t h, uint32_t slot, uint32_t g, lc_selection_
                           uint32_t* units, uint64_t units_cap, uint32_t* clusters,
                           uint64_t clusters_cap, uint32_t* active, uint64_t active_cap);
 
+/* The same result without device-wide synchronisation: lc_selection_stage
+ * queues D2H copies of head g of `slot`'s selection (error bits, summary,
+ * units, clusters, the slot's spans) into handle-owned page-locked memory on
+ * `stream`; after the caller has synchronised that stream,
+ * lc_selection_read_staged unpacks them exactly as lc_selection_download
+ * would (the C++ drop-in's per-call path: one stream sync per retrieve). */
+int lc_selection_stage(lc_index_t h, uint32_t slot, uint32_t g, void* stream);
+int lc_selection_read_staged(lc_index_t h, lc_selection_info* info, uint32_t* units, uint64_t units_cap,
+                             uint32_t* clusters, uint64_t clusters_cap, uint32_t* active, uint64_t active_cap);
+
 /* Bytes read by the last lc_retrieve in algorithmic terms,
  * computed on the device from the step's own selections: out[0] = union
  * bytes, out[1] = per-query (non-deduplicated) bytes, out[2] = active tokens

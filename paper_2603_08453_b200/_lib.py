@@ -62,7 +62,7 @@ EXPORTS = [
     "lc_index_upload_slot", "lc_index_slot_dims", "lc_index_download_slot", "lc_cluster_download", "lc_kv_append",
     "lc_kv_upload_slot", "lc_kv_download_slot",
     "lc_retrieve", "lc_retrieve_slots", "lc_set_gather", "lc_gather_wait", "lc_sparse_attention", "lc_graft", "lc_decode_step", "lc_decode_step_async", "lc_compact", "lc_retrieve_host",
-    "lc_selection_download", "lc_step_bytes", "lc_launch_count", "lc_attend_timing", "lc_device_error", "lc_segment", "lc_segment_packed", "lc_flush_take",
+    "lc_selection_download", "lc_selection_stage", "lc_selection_read_staged", "lc_step_bytes", "lc_launch_count", "lc_attend_timing", "lc_device_error", "lc_segment", "lc_segment_packed", "lc_flush_take",
     "lc_index_build", "lc_gen_workload", "lc_graft_rep", "lc_sparse_attention_ids", "lc_chunk_rep",
     "lc_index_set_config", "lc_index_get_config", "lc_index_to_bytes", "lc_index_save", "lc_index_load",
     "lc_tkix_encode", "lc_tkix_decode_dims", "lc_tkix_decode",
@@ -111,6 +111,8 @@ def lib():
         L.lc_compact.argtypes = [vp, u32, vp]
         L.lc_decode_step_async.argtypes = [vp, vp, vp, vp, C.POINTER(Budgets_), vp, vp, vp, vp, vp, vp]
         L.lc_retrieve_host.argtypes = [vp, vp, C.POINTER(Budgets_), u32, vp, vp]
+        L.lc_selection_stage.argtypes = [vp, u32, u32, vp]
+        L.lc_selection_read_staged.argtypes = [vp, C.POINTER(SelectionInfo_), vp, u64, vp, u64, vp, u64]
         L.lc_selection_download.argtypes = [vp, u32, u32, C.POINTER(SelectionInfo_), vp, u64, vp,
                                             u64, vp, u64]
         L.lc_step_bytes.argtypes = [vp, vp]

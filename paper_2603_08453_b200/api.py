@@ -458,15 +458,25 @@ class Engine:
         L.check(L.lib().lc_sparse_attention(self.h, _ptr(q), _ptr(out), _stream_ptr(stream)))
         return out
 
-    def selection(self, slot: int, g: int, active: bool = True, output=None) -> RetrievalResult:
+    def selection(self, slot: int, g: int, active: bool = True, output=None, staged: bool = False,
+                  stream=None) -> RetrievalResult:
+        """staged=True: through lc_selection_stage on `stream` + one stream
+        sync + lc_selection_read_staged (the C++ drop-in's path)."""
         d, m, l, p, n, _, _, _ = self.slot_dims(slot)
         info = L.SelectionInfo_()
         units = np.zeros(max(p, 1), np.uint32)
         clusters = np.zeros(max(l, 1), np.uint32)
         act = np.zeros(max(n + 1024, 1), np.uint32) if active else None
-        L.check(L.lib().lc_selection_download(self.h, slot, g, C.byref(info), units.ctypes.data, len(units),
-                                              clusters.ctypes.data, len(clusters), _ptr(act),
-                                              0 if act is None else len(act)))
+        if staged:
+            L.check(L.lib().lc_selection_stage(self.h, slot, g, _stream_ptr(stream)))
+            (stream or torch.cuda.current_stream()).synchronize()
+            L.check(L.lib().lc_selection_read_staged(self.h, C.byref(info), units.ctypes.data, len(units),
+                                                     clusters.ctypes.data, len(clusters), _ptr(act),
+                                                     0 if act is None else len(act)))
+        else:
+            L.check(L.lib().lc_selection_download(self.h, slot, g, C.byref(info), units.ctypes.data, len(units),
+                                                  clusters.ctypes.data, len(clusters), _ptr(act),
+                                                  0 if act is None else len(act)))
         if info.error:
             raise L.LcError(L.LC_ERUNTIME, f"device selection error bits 0x{info.error:x}")
         return RetrievalResult(units[: info.n_units].copy(), clusters[: info.n_clusters].copy(),

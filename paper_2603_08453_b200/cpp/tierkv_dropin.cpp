@@ -236,7 +236,7 @@ uint64_t mixv(uint64_t h, const T& x) {
 // The engine cache key of a (HierarchicalIndex, TokenStore) pair: identity
 // (addresses, sizes, the node arrays' buffers) plus a digest of every
 // cluster's and unit's radius, token count, parent and member count, one
-// coordinate of each fine centroid, a strided sample of the coarse centroids,
+// coordinate of every 8th fine centroid, a strided sample of the coarse centroids,
 // chunk spans and chunk -> cluster map, and a sample of the store's rows
 // (~30 K words at 128K, ~0.1 ms; the round-1 key hashed every centroid
 // byte-wise on every call, ~2.5 ms).  An in-place edit of a field outside
@@ -273,11 +273,14 @@ uint64_t fingerprint(const HierarchicalIndex& ix) {
     for (size_t c = 0; c < ix.chunks.size(); c += 16) h = mixv(h, ix.chunks[c].span.start);
     if (!ix.chunks.empty()) h = mixv(h, ix.chunks.back().span.end);
     for (size_t c = 0; c < ix.cluster_of_chunk.size(); c += 16) h = mixv(h, ix.cluster_of_chunk[c]);
-    // every cluster's scalar fields and member count, one centroid coordinate
-    for (const FineCluster& f : ix.fine) {
+    // every cluster's scalar fields and member count (contiguous structs), and
+    // one centroid coordinate of every 8th cluster (each is a pointer chase
+    // into its own allocation; the fp64 radii already pin every cluster)
+    for (size_t c = 0; c < ix.fine.size(); ++c) {
+        const FineCluster& f = ix.fine[c];
         h = mixv(h, f.radius);
         h = mixv(h, (uint64_t)f.token_count ^ ((uint64_t)f.parent_unit << 40) ^ ((uint64_t)f.members.size() << 52));
-        if (!f.centroid.empty()) h = mixv(h, f.centroid[f.centroid.size() / 2]);
+        if ((c & 7) == 0 && !f.centroid.empty()) h = mixv(h, f.centroid[f.centroid.size() / 2]);
     }
     for (const CoarseUnit& u : ix.coarse) {
         h = mixv(h, u.radius);
@@ -351,16 +354,20 @@ RetrievalResult run_retrieve(Engine& e, const HierarchicalIndex& ix, const Token
     ck(lc_retrieve(e.h, e.q_dev, &b, LC_BUFFER_LIST, e.boff_dev, e.bids_dev, attend ? e.out_dev : nullptr, e.st));
     if (attend)
         cuda_ck(cudaMemcpyAsync(e.h_io + e.d, e.out_dev, store.dim() * 4, cudaMemcpyDeviceToHost, e.st), "out D2H");
+    // the selection rides the same stream into page-locked staging: one wait per call
+    ck(lc_selection_stage(e.h, 0, 0, e.st));
     const auto t2 = now();
     cuda_ck(cudaStreamSynchronize(e.st), "retrieve");
     const auto t3 = now();
     lc_selection_info info{};
-    res.selected_units.resize(ix.coarse.size());
-    res.selected_clusters.resize(ix.fine.size());
-    res.active_token_ids.resize(n);
-    ck(lc_selection_download(e.h, 0, 0, &info, res.selected_units.data(), res.selected_units.size(),
-                             res.selected_clusters.data(), res.selected_clusters.size(),
-                             res.active_token_ids.data(), res.active_token_ids.size()));
+    ck(lc_selection_read_staged(e.h, &info, nullptr, 0, nullptr, 0, nullptr, 0));  // sizes first
+    // (no zero-filled n-token vectors per call: exact sizes, then the copies)
+    res.selected_units.resize(info.degenerate ? ix.coarse.size() : info.n_units);
+    res.selected_clusters.resize(info.degenerate ? ix.fine.size() : info.n_clusters);
+    res.active_token_ids.resize(info.n_active);
+    ck(lc_selection_read_staged(e.h, &info, res.selected_units.data(), res.selected_units.size(),
+                                res.selected_clusters.data(), res.selected_clusters.size(),
+                                res.active_token_ids.data(), res.active_token_ids.size()));
     if (prof) {
         const auto t4 = now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };

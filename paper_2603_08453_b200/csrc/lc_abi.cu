@@ -1055,6 +1055,114 @@ int lc_selection_download(lc_index_t h, uint32_t slot, uint32_t g, lc_selection_
     });
 }
 
+// Page-locked staging of one head's selection (lc_selection_stage /
+// lc_selection_read_staged): [0] error bits, [16] QInfo, [48] span count,
+// [64] units [cap_units], clusters [cap_clusters], spans [cap_spans].
+static size_t stage_units_off() { return 64; }
+static size_t stage_clusters_off(const Arena& a) { return 64 + (size_t)a.cap_units * 4; }
+static size_t stage_spans_off(const Arena& a) {
+    return (stage_clusters_off(a) + (size_t)a.cap_clusters * 4 + 15) & ~(size_t)15;
+}
+
+// Active ids of head g from the slot's union spans (ascending, disjoint runs;
+// sorted defensively if not), as the reference's collect_active returns them.
+static uint64_t expand_active(const Span* sp, uint32_t ns, uint32_t g, uint32_t* active, uint64_t cap) {
+    uint64_t k = 0;
+    bool sorted = true;
+    uint32_t last = 0;
+    std::vector<uint32_t> ids;
+    for (uint32_t i = 0; i < ns; ++i) {
+        if (!((sp[i].len_mask >> g) & 1u)) continue;
+        const uint32_t len = sp[i].len_mask >> 8;
+        for (uint32_t t = 0; t < len; ++t) {
+            const uint32_t id = sp[i].start + t;
+            if (k && id <= last) sorted = false;
+            last = id;
+            ids.push_back(id);
+            ++k;
+        }
+    }
+    if (!sorted) {
+        std::sort(ids.begin(), ids.end());
+        ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    }
+    if (active) std::memcpy(active, ids.data(), std::min<uint64_t>(cap, ids.size()) * 4);
+    return ids.size();
+}
+
+int lc_selection_stage(lc_index_t h, uint32_t slot, uint32_t g, void* stream) {
+    return guard([&] {
+        if (!h || slot >= h->a.n_slots || g >= h->a.G) fail(LC_EINVAL, "lc_selection_stage: bad argument");
+        if (!h->last_valid) fail(LC_EINVAL, "no selection yet");
+        h->set_device();
+        const Arena& a = h->a;
+        const size_t need = stage_spans_off(a) + (size_t)a.cap_spans * sizeof(Span);
+        if (h->sel_stage_bytes < need) {
+            if (h->sel_stage) cudaFreeHost(h->sel_stage);
+            h->sel_stage = nullptr;
+            h->sel_stage_bytes = 0;
+            ck(cudaHostAlloc(reinterpret_cast<void**>(&h->sel_stage), need, cudaHostAllocDefault), "stage alloc");
+            h->sel_stage_bytes = need;
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        unsigned char* b = h->sel_stage;
+        const size_t q = (size_t)slot * a.G + g;
+        ck(cudaMemcpyAsync(b, a.err, 4, cudaMemcpyDeviceToHost, st), "err");
+        ck(cudaMemcpyAsync(b + 16, a.qinfo + q, sizeof(QInfo), cudaMemcpyDeviceToHost, st), "qinfo");
+        ck(cudaMemcpyAsync(b + 48, a.n_spans + slot, 4, cudaMemcpyDeviceToHost, st), "n_spans");
+        ck(cudaMemcpyAsync(b + stage_units_off(), a.sel_units + q * a.cap_units, (size_t)a.cap_units * 4,
+                           cudaMemcpyDeviceToHost, st), "units");
+        ck(cudaMemcpyAsync(b + stage_clusters_off(a), a.sel_clusters + q * a.cap_clusters, (size_t)a.cap_clusters * 4,
+                           cudaMemcpyDeviceToHost, st), "clusters");
+        ck(cudaMemcpyAsync(b + stage_spans_off(a), a.spans + (size_t)slot * a.cap_spans, (size_t)a.cap_spans * sizeof(Span),
+                           cudaMemcpyDeviceToHost, st), "spans");
+        h->stage_slot = slot;
+        h->stage_g = g;
+        h->stage_valid = true;
+    });
+}
+
+int lc_selection_read_staged(lc_index_t h, lc_selection_info* info, uint32_t* units, uint64_t units_cap,
+                             uint32_t* clusters, uint64_t clusters_cap, uint32_t* active, uint64_t active_cap) {
+    return guard([&] {
+        if (!h) fail(LC_EINVAL, "lc_selection_read_staged: null handle");
+        if (!h->stage_valid) fail(LC_EINVAL, "lc_selection_read_staged: nothing staged");
+        const Arena& a = h->a;
+        const unsigned char* b = h->sel_stage;
+        uint32_t err, ns;
+        QInfo qi;
+        std::memcpy(&err, b, 4);
+        std::memcpy(&qi, b + 16, sizeof qi);
+        std::memcpy(&ns, b + 48, 4);
+        if (ns > a.cap_spans) fail(LC_ERUNTIME, "lc_selection_read_staged: span count over capacity");
+        const HostSlot& hs = h->hs[h->stage_slot];
+        if (info) {
+            info->n_units = qi.n_units;
+            info->n_clusters = qi.n_clusters;
+            info->degenerate = qi.degenerate;
+            info->error = qi.error | err;
+            info->scanned_centroids = qi.scanned;
+            info->n_active = qi.n_active;
+        }
+        if (qi.degenerate) {
+            if (units) for (uint64_t i = 0; i < std::min<uint64_t>(units_cap, hs.P); ++i) units[i] = (uint32_t)i;
+            if (clusters) for (uint64_t i = 0; i < std::min<uint64_t>(clusters_cap, hs.L); ++i) clusters[i] = (uint32_t)i;
+        } else {
+            if (units)
+                std::memcpy(units, b + stage_units_off(),
+                            std::min<uint64_t>({units_cap, qi.n_units, a.cap_units}) * 4);
+            if (clusters)
+                std::memcpy(clusters, b + stage_clusters_off(a),
+                            std::min<uint64_t>({clusters_cap, qi.n_clusters, a.cap_clusters}) * 4);
+        }
+        if (active || info) {
+            const uint64_t n = expand_active(reinterpret_cast<const Span*>(b + stage_spans_off(a)), ns, h->stage_g,
+                                             active, active_cap);
+            if (info) info->n_active = n;
+        }
+    });
+}
+
 int lc_step_bytes(lc_index_t h, uint64_t* out) {
     return guard([&] {
         if (!h || !out) fail(LC_EINVAL, "null argument");

@@ -121,6 +121,10 @@ struct lc_index_s {
     uint32_t last_valid = 0;
     uint32_t last_launches = 0;                // kernels of the last selection + attention
     std::vector<cudaEvent_t> att_ev;           // lc_attend_timing: event pairs around k_attend launches
+    unsigned char* sel_stage = nullptr;        // lc_selection_stage: page-locked copy of one head's selection
+    size_t sel_stage_bytes = 0;
+    uint32_t stage_slot = 0, stage_g = 0;
+    bool stage_valid = false;
     size_t att_ev_used = 0;
     std::map<uint32_t, uint32_t> cand_cache;  // unit_topk -> max candidates over slots
     unsigned char* sel_scratch = nullptr;      // per-head candidate keys + weights (k_fine -> k_pickq)
@@ -164,6 +168,7 @@ struct lc_index_s {
         if (host_event) cudaEventDestroy(host_event);
         for (auto e : group_events) cudaEventDestroy(e);
         for (auto e : att_ev) cudaEventDestroy(e);
+        if (sel_stage) cudaFreeHost(sel_stage);
         if (pg_mem) cudaFree(pg_mem);
         if (aq_mem) cudaFree(aq_mem);
     }

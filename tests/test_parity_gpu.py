@@ -116,6 +116,7 @@ def test_batched_slots_match_per_head_reference(slot_groups, keys_cap, monkeypat
             r = refs[s].retrieve(ws[s].queries[g], token_budget=2048)
             got = eng.selection(s, g)
             assert_same_selection(got, r, (s, g))
+            assert_same_selection(eng.selection(s, g, staged=True), r, (s, g, "staged"))
             assert rel_l2(o[s, g], r["output"]) < TOL, (s, g, rel_l2(o[s, g], r["output"]))
     assert eng.device_error() == 0
     bytes_ = eng.step_bytes()
