@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblychee_b200.so")
+LIB_PATH = os.environ.get("LC_LIB_PATH") or os.path.join(PKG, "liblychee_b200.so")  # override: A/B runs only
 
 LC_OK, LC_EINVAL, LC_ERUNTIME, LC_ECUDA, LC_ENOMEM = 0, 1, 2, 3, 4
 LC_BUFFER_NONE, LC_BUFFER_STREAM, LC_BUFFER_LIST = 0, 1, 2
