@@ -910,17 +910,41 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
         bar_named(hbar, GT);
         // selected clusters in rank order; member chunks over the lanes of a warp (their
         // span bounds prefetched into L2 for the span phase)
+        // One lane per selected cluster (the warp's clusters x2 = hw_ + k * GT/32),
+        // so every cluster's member-list loads are in flight together instead
+        // of one dependent round trip per cluster; clusters with long member
+        // lists (grafted runs) go over the warp's lanes afterwards.
         const uint32_t nsel = s_nsel[g], hw_ = gt >> 5;
-        for (uint32_t x2 = hw_; x2 < nsel; x2 += GT / 32) {
-            const uint32_t* e = ent(g, ent(g, x2)[7]);
-            if (lane == 0) {
+        constexpr uint32_t kLaneMembers = 8;
+        for (uint32_t base = hw_; base < nsel; base += 32 * (GT / 32)) {
+            const uint32_t x2 = base + lane * (GT / 32);
+            const uint32_t* e = x2 < nsel ? ent(g, ent(g, x2)[7]) : nullptr;
+            bool longl = false;
+            if (e) {
                 out_cl[x2] = e[2];
                 if (grafted) atomicOr(&clb[e[4] >> 5], 1u << (e[4] & 31));
+                const uint32_t t0 = e[5], t1 = e[6];
+                longl = t1 - t0 > kLaneMembers;
+                if (!longl) {
+                    uint32_t j[kLaneMembers];
+#pragma unroll
+                    for (uint32_t k = 0; k < kLaneMembers; ++k)
+                        if (t0 + k < t1) j[k] = mem[t0 + k];
+#pragma unroll
+                    for (uint32_t k = 0; k < kLaneMembers; ++k)
+                        if (t0 + k < t1) {
+                            atomicOr(&cb[j[k] >> 5], 1u << (j[k] & 31));
+                            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(cs_g + j[k]));
+                        }
+                }
             }
-            for (uint32_t t = e[5] + lane; t < e[6]; t += 32) {
-                const uint32_t j = mem[t];
-                atomicOr(&cb[j >> 5], 1u << (j & 31));
-                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(cs_g + j));
+            for (unsigned int lb = __ballot_sync(0xffffffffu, longl); lb; lb &= lb - 1u) {
+                const uint32_t* el = ent(g, ent(g, base + (uint32_t)(__ffs(lb) - 1) * (GT / 32))[7]);
+                for (uint32_t t = el[5] + lane; t < el[6]; t += 32) {
+                    const uint32_t jj = mem[t];
+                    atomicOr(&cb[jj >> 5], 1u << (jj & 31));
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(cs_g + jj));
+                }
             }
         }
     } else if (in_head) {
