@@ -840,6 +840,8 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
                 uint32_t h;
                 uint32_t* e = rent(r0 + t, h);
                 const float4* cv = reinterpret_cast<const float4*>(col(t));
+                // the radius load is issued before the dot chain, so its latency overlaps it
+                const double rad = __ldg(a.frad + (size_t)slot * a.cap_clusters + e[4]);
                 double sacc = 0.0;
 #pragma unroll 8
                 for (uint32_t jq = 0; jq < D / 4; ++jq) {
@@ -849,7 +851,6 @@ __global__ void __launch_bounds__(kFuThreads, 2) k_select(FusedParams p) {
                     sacc = __fma_rn(s_qd[h * D + 4 * jq + 2], (double)v.z, sacc);
                     sacc = __fma_rn(s_qd[h * D + 4 * jq + 3], (double)v.w, sacc);
                 }
-                const double rad = __ldg(a.frad + (size_t)slot * a.cap_clusters + e[4]);
                 const unsigned long long kx = desc_key(__dadd_rn(sacc, __dmul_rn(s_qn[h], rad)));
                 e[0] = (uint32_t)kx;
                 e[1] = (uint32_t)(kx >> 32);
